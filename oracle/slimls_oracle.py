@@ -1,0 +1,327 @@
+"""CPU oracle for the slimLS hot path -- TEST INFRASTRUCTURE ONLY.
+
+This module is the *checker*, never the product: only ``tests/``,
+``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import it.  The product package
+``paper_1912_07962_b200`` must never import anything under ``oracle/``.
+
+It restates, in plain NumPy/SciPy, the reference algorithm of
+``arxiv/paper_1912_07962`` (package ``slimsolve``) for exactly the path
+the B200 build accelerates: ``solvers.run("slimls", ...)`` with identity
+regularizer, ``lam = 0`` and ``inner = "auto"``.  Every function cites the
+reference file:line it follows (paths relative to the reference's
+``pkg/src/slimsolve/``).  The arithmetic is the reference's own: dense
+block fetch, ``vstack`` of the window, full Gram recompute every step,
+``scipy.linalg.solve(assume_a="pos")`` for the dual system and
+``np.linalg.inv`` for the single-block route.  That keeps the oracle's
+cost structure equal to the reference's, so it doubles as the CPU
+baseline ("port") that ``bench.py --impl reference`` times.
+
+Pinning: ``tests/test_oracle_golden.py`` checks this restatement against
+vectors produced by the reference itself (``tests/golden/make_golden.py``
+imports ``slimsolve`` from ``/root/reference/pkg/src`` in the build
+container and commits the outputs as ``tests/golden/*.npz``).
+"""
+
+from __future__ import annotations
+
+import time
+from collections import deque
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.linalg
+
+# solvers.py:47 / innersolve.py:356
+DIVERGENCE_FACTOR = 1e12
+DUAL_MAX_ALPHA = 1e8
+SOLVE_CACHE_MAX_ENTRIES = 512  # solvers.py:187
+
+SCHEMES = ("cyclic", "random_cyclic", "uniform_iid")  # sampling.py:35
+
+
+# ---------------------------------------------------------------------------
+# Sampling (sampling.py:38-84)
+# ---------------------------------------------------------------------------
+
+
+def fisher_yates(m: int, rng: np.random.Generator) -> np.ndarray:
+    """Backward Fisher-Yates over 1..m with scalar bounded draws.
+
+    Follows sampling.py:38-44: one ``rng.integers(0, i + 1)`` call per
+    position i = m-1 .. 1, swapping perm[i] and perm[j].
+    """
+    perm = np.arange(1, m + 1, dtype=np.int64)
+    for i in range(m - 1, 0, -1):
+        j = int(rng.integers(0, i + 1))
+        perm[i], perm[j] = perm[j], perm[i]
+    return perm
+
+
+class OracleSampler:
+    """Restatement of ``Sampler`` (sampling.py:47-84)."""
+
+    def __init__(self, scheme: str, n_blocks: int, seed: int = 0):
+        if scheme not in SCHEMES:
+            raise ValueError(f"unknown scheme {scheme!r}")
+        if n_blocks < 1:
+            raise ValueError("n_blocks must be >= 1")
+        self.scheme = scheme
+        self.n_blocks = int(n_blocks)
+        # Philox 4x64 keyed directly by the seed (sampling.py:58)
+        self.rng = np.random.Generator(np.random.Philox(key=int(seed)))
+        self.position = 0
+        self._perm = None
+
+    def next_index(self) -> int:  # sampling.py:62-75
+        m = self.n_blocks
+        if self.scheme == "cyclic":
+            idx = self.position % m + 1
+        elif self.scheme == "uniform_iid":
+            idx = int(self.rng.integers(1, m + 1))
+        else:
+            off = self.position % m
+            if off == 0:
+                self._perm = fisher_yates(m, self.rng)
+            idx = int(self._perm[off])
+        self.position += 1
+        return idx
+
+    def indices(self, count: int) -> np.ndarray:  # sampling.py:77-79
+        return np.array([self.next_index() for _ in range(count)], dtype=np.int64)
+
+
+def sampler_indices(scheme: str, n_blocks: int, seed: int, count: int) -> np.ndarray:
+    return OracleSampler(scheme, n_blocks, seed).indices(count)
+
+
+# ---------------------------------------------------------------------------
+# Schedule (solvers.py:93-130)
+# ---------------------------------------------------------------------------
+
+
+def schedule_alpha(kind: str, alpha: float, k: int, ramp_length=None,
+                   decay_exponent: float = 1.0) -> float:
+    """alpha_k, k >= 1 (solvers.py:117-127)."""
+    if kind == "constant":
+        return alpha
+    if kind == "ramp":
+        length = ramp_length or 1
+        if k >= length:
+            return alpha
+        return alpha * (k / length)
+    return alpha / k**decay_exponent
+
+
+# ---------------------------------------------------------------------------
+# Inner solves (innersolve.py:209-215, 276-321, 340-381)
+# ---------------------------------------------------------------------------
+
+
+def stack_window(mats) -> np.ndarray:
+    """``_stack`` (innersolve.py:209-215): vstack copy, oldest first."""
+    mats = [np.atleast_2d(np.asarray(m, dtype=float)) for m in mats]
+    return np.vstack(mats) if len(mats) > 1 else mats[0]
+
+
+def dual_system(mat: np.ndarray, alpha: float) -> np.ndarray:
+    """``_dual_system`` (innersolve.py:298-302): G = alpha (M M^T) + I."""
+    g = mat @ mat.T
+    g *= alpha
+    g[np.diag_indices_from(g)] += 1.0
+    return g
+
+
+def dual_step(mats, residual: np.ndarray, alpha: float) -> np.ndarray:
+    """``dual_step`` (innersolve.py:305-321): s = alpha M^T G^{-1} [0..0; r]."""
+    mat = stack_window(mats)
+    rows = mat.shape[0]
+    residual = np.asarray(residual, dtype=float).reshape(-1)
+    y = np.zeros(rows)
+    y[rows - residual.shape[0]:] = residual
+    w = scipy.linalg.solve(dual_system(mat, alpha), y, assume_a="pos")
+    return alpha * (mat.T @ w)
+
+
+def direct_step(mats, residual: np.ndarray, alpha: float) -> np.ndarray:
+    """``direct_step``/``solve_normal`` (innersolve.py:276-295, 340-350)."""
+    newest = np.atleast_2d(np.asarray(mats[-1], dtype=float))
+    gradient = newest.T @ np.asarray(residual, dtype=float).reshape(-1)
+    mat = stack_window(mats)
+    n = mat.shape[1]
+    system = mat.T @ mat + np.eye(n) / alpha
+    return scipy.linalg.solve(system, gradient, assume_a="pos")
+
+
+def solve_step_auto(mats, residual: np.ndarray, alpha: float) -> np.ndarray:
+    """``solve_step(method="auto")`` for identity C (innersolve.py:359-381)."""
+    rows = sum(np.atleast_2d(np.asarray(m)).shape[0] for m in mats)
+    n = np.atleast_2d(np.asarray(mats[0])).shape[1]
+    if rows <= n and alpha <= DUAL_MAX_ALPHA:
+        return dual_step(mats, residual, alpha)
+    return direct_step(mats, residual, alpha)
+
+
+# ---------------------------------------------------------------------------
+# Driver (solvers.py:161-242, 438-588)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class OracleTrajectory:
+    """Field-for-field restatement of ``Trajectory`` (solvers.py:438-455)."""
+
+    ks: np.ndarray
+    epoch_fraction: np.ndarray
+    alphas: np.ndarray
+    residual_norms: np.ndarray
+    rel_errors: dict
+    wall_times: np.ndarray
+    row_status: list
+    x_final: np.ndarray
+    status: str = "ok"
+    diverged_at: int | None = None
+    iterates: list | None = None
+
+
+@dataclass
+class _State:
+    x: np.ndarray
+    window: deque
+    div_limit_sq: float
+    last_residual_norm: float = float("nan")
+    inv_cache: dict = field(default_factory=dict)
+
+
+def _dual_single_block(st: _State, index: int, a: np.ndarray, residual, alpha):
+    """``_dual_single_block`` (solvers.py:190-210), cache per (index, alpha)."""
+    key = (index, alpha)
+    inv = st.inv_cache.get(key)
+    if inv is None:
+        system = alpha * (a @ a.T)
+        system[np.diag_indices_from(system)] += 1.0
+        inv = np.linalg.inv(system)
+        if len(st.inv_cache) < SOLVE_CACHE_MAX_ENTRIES:
+            st.inv_cache[key] = inv
+    return alpha * (a.T @ (inv @ residual))
+
+
+def slimls_step(st: _State, index: int, a: np.ndarray, b: np.ndarray, alpha: float):
+    """``slimls_step`` (solvers.py:213-242) with identity C and inner="auto".
+
+    Returns False when the new iterate trips the divergence check of
+    ``_finish`` (solvers.py:169-177); the iterate is stored either way.
+    """
+    st.window.append((index, a))  # push before the solve (solvers.py:227)
+    residual = a @ st.x - b  # _sampled_residual, solvers.py:180-183
+    st.last_residual_norm = float(np.sqrt(residual @ residual))
+    if len(st.window) == 1 and a.shape[0] <= a.shape[1] and alpha <= DUAL_MAX_ALPHA:
+        s = _dual_single_block(st, index, a, residual, alpha)
+    else:
+        s = solve_step_auto([m for _, m in st.window], residual, alpha)
+    st.x = st.x - s
+    norm_sq = float(st.x @ st.x)
+    return norm_sq <= st.div_limit_sq
+
+
+def run_slimls(fetch, n_blocks: int, n_cols: int, indices, alphas, *, r: int = 0,
+               x0=None, references=None, record_every: int = 1,
+               store_iterates: bool = False) -> OracleTrajectory:
+    """Restatement of ``run`` (solvers.py:480-588) for the slimLS path.
+
+    ``fetch(i)`` returns the dense block (a_block (ell, n), b_block (ell,))
+    for 1-based index i, like ``RowBlockOperator.fetch_block``
+    (linops.py:192-206 / 270-279).  ``indices``/``alphas`` are the
+    precomputed sampler trace and alpha_k sequence, so the step count is
+    ``len(indices)``.
+    """
+    indices = np.asarray(indices, dtype=np.int64)
+    alphas = np.asarray(alphas, dtype=float)
+    steps = int(indices.shape[0])
+    x0 = np.zeros(n_cols) if x0 is None else np.asarray(x0, dtype=float).reshape(-1)
+    x0_norm = float(np.linalg.norm(x0))
+    limit = DIVERGENCE_FACTOR * (1.0 + x0_norm)  # solvers.py:144-146
+    st = _State(x=x0.copy(), window=deque(maxlen=r + 1), div_limit_sq=limit * limit)
+
+    references = references or {}
+    ref_items = [(name, np.asarray(v, dtype=float), float(np.linalg.norm(v)))
+                 for name, v in references.items()]
+    ks, efrac, al, resid, wall, statuses = [], [], [], [], [], []
+    rel = {name: [] for name, _, _ in ref_items}
+    iterates = [] if store_iterates else None
+
+    def record(k, alpha, status, dt):  # solvers.py:543-554
+        ks.append(k)
+        efrac.append(k / n_blocks)
+        al.append(alpha)
+        resid.append(st.last_residual_norm if k else np.nan)
+        wall.append(dt)
+        statuses.append(status)
+        for name, vec, nrm in ref_items:
+            diff = float(np.linalg.norm(st.x - vec))
+            rel[name].append(diff / nrm if nrm > 0 else diff)
+        if iterates is not None:
+            iterates.append(st.x.copy())
+
+    status, diverged_at = "ok", None
+    record(0, np.nan, "ok", 0.0)
+    t_prev = time.perf_counter()
+    for k in range(1, steps + 1):
+        idx = int(indices[k - 1])
+        a, b = fetch(idx)
+        alpha = float(alphas[k - 1])
+        if not alpha > 0:
+            raise ValueError(f"schedule produced alpha_{k} = {alpha} <= 0")
+        ok = slimls_step(st, idx, a, b, alpha)
+        if not ok:  # solvers.py:563-570
+            status, diverged_at = "diverged", k
+            now = time.perf_counter()
+            record(k, alpha, "diverged", now - t_prev)
+            break
+        if k % record_every == 0 or k == steps:
+            now = time.perf_counter()
+            record(k, alpha, "ok", now - t_prev)
+            t_prev = now
+
+    return OracleTrajectory(
+        ks=np.asarray(ks, dtype=np.int64), epoch_fraction=np.asarray(efrac),
+        alphas=np.asarray(al), residual_norms=np.asarray(resid),
+        rel_errors={n: np.asarray(v) for n, v in rel.items()},
+        wall_times=np.asarray(wall), row_status=statuses, x_final=st.x.copy(),
+        status=status, diverged_at=diverged_at, iterates=iterates)
+
+
+# ---------------------------------------------------------------------------
+# Block fetch helpers (linops.py:84-88, 192-206, 270-279)
+# ---------------------------------------------------------------------------
+
+
+def dense_fetch(a: np.ndarray, b: np.ndarray, ell: int):
+    """Block i = rows [(i-1) ell, i ell) of a dense matrix (linops.py:84-88)."""
+    a = np.ascontiguousarray(a, dtype=float)
+    b = np.asarray(b, dtype=float)
+
+    def fetch(i):
+        s = (i - 1) * ell
+        return a[s:s + ell], b[s:s + ell]
+    return fetch
+
+
+def csr_fetch(blocks, b: np.ndarray):
+    """Per-block CSR densified on every fetch, like linops.py:270-279.
+
+    ``blocks`` is a list of (indptr, indices, data, (ell, n)) tuples;
+    values of any float dtype are widened to fp64 (the reference stores
+    fp64, linops.py:236) and densified with scipy's ``toarray`` exactly
+    as the reference does.
+    """
+    import scipy.sparse as sp
+
+    b = np.asarray(b, dtype=float)
+    mats = [sp.csr_matrix((np.asarray(d, dtype=float), ix, ip), shape=shape)
+            for ip, ix, d, shape in blocks]
+    ell = mats[0].shape[0]
+
+    def fetch(i):
+        return mats[i - 1].toarray(), b[(i - 1) * ell:i * ell]
+    return fetch

@@ -1,0 +1,261 @@
+"""Generate golden vectors from the reference implementation itself.
+
+Run in the build container (the reference is importable only here):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+It imports the unmodified reference package ``slimsolve`` and records
+its outputs for the slimLS path: sampler traces, full ``run`` trajectories
+on small dense / sparse-tomography problems (including divergence, ramp
+and decay schedules, r = 0, fractional epochs and single-pass streams),
+``innersolve.dual_step`` outputs (the secondary seam) and the reference
+Siddon projector blocks.  The outputs are committed as ``*.npz`` next to
+this script; ``tests/test_oracle_golden.py`` pins the oracle against them
+and the GPU parity tests compare the CUDA path against them directly.
+Nothing at run time on the GPU box reads ``/root/reference``.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+REF_SRC = "/root/reference/pkg/src"
+if REF_SRC not in sys.path:
+    sys.path.insert(0, REF_SRC)
+
+from slimsolve import innersolve, tomo  # noqa: E402
+from slimsolve.linops import DenseBlockOperator, SinglePassAdapter  # noqa: E402
+from slimsolve.sampling import Sampler  # noqa: E402
+from slimsolve.solvers import Schedule, run  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def sampler_golden():
+    out = {}
+    for scheme in ("cyclic", "random_cyclic", "uniform_iid"):
+        for m in (1, 2, 7, 180, 200):
+            for seed in (0, 5, 7962):
+                count = 3 * m + 5
+                out[f"{scheme}/{m}/{seed}"] = Sampler(scheme, m, seed=seed).indices(count)
+    np.savez_compressed(os.path.join(HERE, "sampler.npz"), **out)
+
+
+def _traj_dict(prefix, traj):
+    d = {
+        f"{prefix}/ks": traj.ks,
+        f"{prefix}/epoch_fraction": traj.epoch_fraction,
+        f"{prefix}/alphas": traj.alphas,
+        f"{prefix}/residual_norms": traj.residual_norms,
+        f"{prefix}/x_final": traj.x_final,
+        f"{prefix}/status": np.array(traj.status),
+        f"{prefix}/diverged_at": np.array(-1 if traj.diverged_at is None else traj.diverged_at),
+        f"{prefix}/row_status": np.array(traj.row_status),
+    }
+    for name, vals in traj.rel_errors.items():
+        d[f"{prefix}/rel/{name}"] = vals
+    if traj.iterates is not None:
+        d[f"{prefix}/iterates"] = np.asarray(traj.iterates)
+    return d
+
+
+def _case(prefix, a, b, ell, *, scheme, seed, sched, epochs, r, x0=None,
+          refs=None, record_every=1, store_iterates=False, single_pass=False):
+    op = DenseBlockOperator(a, ell, b)
+    if single_pass:
+        op = SinglePassAdapter(op)
+    sampler = Sampler(scheme, op.n_blocks, seed=seed)
+    traj = run("slimls", op, sampler, sched, epochs=epochs, r=r, x0=x0,
+               references=refs, record_every=record_every,
+               store_iterates=store_iterates)
+    # the index trace that produced it (fresh sampler, same seed)
+    k = int(round(epochs * op.n_blocks))
+    idx = Sampler(scheme, op.n_blocks, seed=seed).indices(k)
+    d = {f"{prefix}/A": np.asarray(a, float), f"{prefix}/b": np.asarray(b, float),
+         f"{prefix}/ell": np.array(ell), f"{prefix}/r": np.array(r),
+         f"{prefix}/indices": idx, f"{prefix}/record_every": np.array(record_every),
+         f"{prefix}/scheme": np.array(scheme), f"{prefix}/seed": np.array(seed),
+         f"{prefix}/sched_kind": np.array(sched.kind),
+         f"{prefix}/sched_alpha": np.array(sched.alpha),
+         f"{prefix}/sched_ramp": np.array(-1 if sched.ramp_length is None else sched.ramp_length),
+         f"{prefix}/sched_decay": np.array(sched.decay_exponent),
+         f"{prefix}/epochs": np.array(epochs)}
+    if x0 is not None:
+        d[f"{prefix}/x0"] = np.asarray(x0, float)
+    for name, vec in (refs or {}).items():
+        d[f"{prefix}/ref/{name}"] = np.asarray(vec, float)
+    d.update(_traj_dict(prefix, traj))
+    return d
+
+
+def dense_runs():
+    out = {}
+    # solvers test scalar case (test_solvers.py:43-47): x1 = 1.6
+    out.update(_case("scalar", np.array([[2.0]]), np.array([4.0]), 1,
+                     scheme="cyclic", seed=0, sched=Schedule("constant", 1.0),
+                     epochs=1, r=0))
+    rng = np.random.default_rng(101)
+    # rows > n: the reference takes the direct (n x n) route for windows >= 3
+    a = rng.standard_normal((24, 6)); b = rng.standard_normal(24)
+    out.update(_case("direct_route", a, b, 3, scheme="uniform_iid", seed=3,
+                     sched=Schedule("constant", 0.5), epochs=3, r=2,
+                     x0=rng.standard_normal(6), refs={"x_true": np.ones(6)},
+                     record_every=2, store_iterates=True))
+    # dual route, random_cyclic, two epochs
+    a = rng.standard_normal((600, 120)) / np.sqrt(120)
+    xt = rng.standard_normal(120); b = a @ xt + 0.01 * rng.standard_normal(600)
+    out.update(_case("dense_dual", a, b, 20, scheme="random_cyclic", seed=11,
+                     sched=Schedule("constant", 100.0), epochs=2, r=4,
+                     refs={"x_true": xt, "zero": np.zeros(120)}, store_iterates=True))
+    # config-1 shape at reduced size (same generator recipe as configs[0])
+    g = np.random.Generator(np.random.Philox(key=1912))
+    a = g.standard_normal((4000, 400)) / np.sqrt(1000.0)
+    xt = g.standard_normal(400)
+    clean = a @ xt
+    eps = g.standard_normal(4000); eps *= 0.01 * np.linalg.norm(clean) / np.linalg.norm(eps)
+    cfg1 = _case("cfg1_reduced", a, clean + eps, 40, scheme="random_cyclic",
+                 seed=7962, sched=Schedule("constant", 100.0), epochs=2, r=5,
+                 refs={"x_true": xt}, record_every=5)
+    # A is regenerated from the recipe (Philox key 1912) by the tests; keep
+    # only a checksum of it here so the fixture stays small
+    cfg1["cfg1_reduced/A_sum"] = np.array([a.sum(), np.abs(a).sum(), a[17, 33]])
+    del cfg1["cfg1_reduced/A"]
+    out.update(cfg1)
+    # ramp schedule (ramp length defaults to r+1 in run, solvers.py:523-524)
+    a = rng.standard_normal((90, 40)); b = rng.standard_normal(90)
+    out.update(_case("ramp", a, b, 6, scheme="random_cyclic", seed=7,
+                     sched=Schedule("ramp", 1.0), epochs=2, r=2,
+                     refs={"x_true": np.ones(40)}))
+    out.update(_case("decay", a, b, 6, scheme="uniform_iid", seed=8,
+                     sched=Schedule("decay", 5.0, decay_exponent=0.75), epochs=2, r=3,
+                     refs={"x_true": np.ones(40)}, record_every=3))
+    # r = 0: the memoryless damped block Kaczmarz specialization
+    out.update(_case("r0", a, b, 6, scheme="cyclic", seed=0,
+                     sched=Schedule("constant", 2.0), epochs=3, r=0,
+                     refs={"x_true": np.ones(40)}, record_every=4))
+    # fractional epochs: steps = round(1.5 M)
+    out.update(_case("frac_epochs", a, b, 6, scheme="random_cyclic", seed=9,
+                     sched=Schedule("constant", 3.0), epochs=1.5, r=1,
+                     refs={"x_true": np.ones(40)}, record_every=4))
+    out.update(_case("epochs_zero", a, b, 6, scheme="random_cyclic", seed=9,
+                     sched=Schedule("constant", 3.0), epochs=0, r=1,
+                     x0=np.full(40, 0.5), refs={"x_true": np.ones(40)}))
+    # single-pass stream: cyclic, one epoch
+    out.update(_case("single_pass", a, b, 6, scheme="cyclic", seed=0,
+                     sched=Schedule("constant", 3.0), epochs=1, r=2,
+                     refs={"x_true": np.ones(40)}, single_pass=True))
+    # divergence: tiny rows, huge data and damping -> ||x|| > 1e12 at k = 1
+    a = 1e-3 * rng.standard_normal((40, 30)); b = 1e16 * np.ones(40)
+    out.update(_case("diverge", a, b, 4, scheme="cyclic", seed=0,
+                     sched=Schedule("constant", 1e6), epochs=2, r=1,
+                     refs={"x_true": np.ones(30)}, record_every=3))
+    # divergence later in the run (the first records are ok)
+    a = rng.standard_normal((40, 30)); b = rng.standard_normal(40)
+    b[20:] = 1e18
+    out.update(_case("diverge_late", a, b, 4, scheme="cyclic", seed=0,
+                     sched=Schedule("constant", 1.0), epochs=2, r=1,
+                     refs={"x_true": np.ones(30)}, record_every=2))
+    np.savez_compressed(os.path.join(HERE, "dense_runs.npz"), **out)
+
+
+def _angles_0_pi(count):
+    """Equispaced angles over [0, 180) deg mapped into (-90, 90]."""
+    deg = np.arange(count) * (180.0 / count)
+    return np.where(deg > 90.0, deg - 180.0, deg)
+
+
+def _csr_dict(prefix, blocks):
+    d = {f"{prefix}/n_blocks": np.array(len(blocks))}
+    for i, blk in enumerate(blocks):
+        blk = blk.tocsr()
+        d[f"{prefix}/{i}/indptr"] = blk.indptr.astype(np.int64)
+        d[f"{prefix}/{i}/indices"] = blk.indices.astype(np.int64)
+        d[f"{prefix}/{i}/data"] = blk.data
+        d[f"{prefix}/{i}/shape"] = np.array(blk.shape)
+    return d
+
+
+def tomo_runs():
+    out = {}
+    # 2D: grid 24, 18 views over [0, pi), 34 rays
+    grid, rays = 24, 34
+    geom = tomo.parallel_2d_geometry(_angles_0_pi(18), rays)
+    proj = tomo.build_projector(geom, grid)
+    phantom = tomo.shepp_logan(grid, dims=2)
+    b = tomo.simulate_data(proj, phantom, 0.01, seed=2)
+    op = proj.with_rhs(b)
+    sampler = Sampler("random_cyclic", op.n_blocks, seed=7)
+    traj = run("slimls", op, sampler, Schedule("constant", 1000.0), epochs=2, r=3,
+               references={"x_true": phantom.flat})
+    idx = Sampler("random_cyclic", op.n_blocks, seed=7).indices(2 * op.n_blocks)
+    out.update(_csr_dict("tomo2d/blocks", proj._blocks))
+    out.update({"tomo2d/b": b, "tomo2d/x_true": phantom.flat, "tomo2d/indices": idx,
+                "tomo2d/r": np.array(3), "tomo2d/alpha": np.array(1000.0),
+                "tomo2d/angles": _angles_0_pi(18), "tomo2d/grid": np.array(grid),
+                "tomo2d/rays": np.array(rays)})
+    out.update(_traj_dict("tomo2d", traj))
+    # 3D desk scale: grid 8, 6 random directions, 8x8 detector
+    dirs = tomo.random_directions(6, seed=4)
+    geom = tomo.parallel_3d_geometry(dirs, 8)
+    proj = tomo.build_projector(geom, 8)
+    phantom = tomo.shepp_logan(8, dims=3)
+    b = tomo.simulate_data(proj, phantom, 0.01, seed=4)
+    op = proj.with_rhs(b)
+    traj = run("slimls", op, Sampler("uniform_iid", 6, seed=3),
+               Schedule("constant", 1000.0), epochs=3, r=2,
+               references={"x_true": phantom.flat})
+    idx = Sampler("uniform_iid", 6, seed=3).indices(18)
+    out.update(_csr_dict("tomo3d/blocks", proj._blocks))
+    out.update({"tomo3d/b": b, "tomo3d/x_true": phantom.flat, "tomo3d/indices": idx,
+                "tomo3d/r": np.array(2), "tomo3d/alpha": np.array(1000.0),
+                "tomo3d/dirs": dirs})
+    out.update(_traj_dict("tomo3d", traj))
+    np.savez_compressed(os.path.join(HERE, "tomo_runs.npz"), **out)
+
+
+def projector_golden():
+    """Reference Siddon blocks for the problem generators' pin."""
+    out = {}
+    angles = [0.0, 90.0, 45.0, -30.0, 1.0, 89.0, -89.5, 60.25, 17.0]
+    for i, ang in enumerate(angles):
+        blk = tomo._view_block_2d(ang, 16, 23, 1.0)
+        out.update(_csr_dict(f"p2d/{i}", [blk]))
+        out[f"p2d/{i}/angle"] = np.array(ang)
+    dirs = np.vstack([tomo.random_directions(4, seed=11),
+                      [[1.0, 0.0, 0.0], [0.0, 0.0, 1.0],
+                       [np.cos(0.3), np.sin(0.3), 0.0]]])
+    for i, d in enumerate(dirs):
+        blk = tomo._view_block_3d(d, 6, 6, 1.0)
+        out.update(_csr_dict(f"p3d/{i}", [blk]))
+        out[f"p3d/{i}/dir"] = d
+    np.savez_compressed(os.path.join(HERE, "projector.npz"), **out)
+
+
+def dual_step_golden():
+    """innersolve.dual_step (innersolve.py:305-321) on random stacks."""
+    rng = np.random.default_rng(202)
+    out = {}
+    for c, (nblk, ell, n, alpha) in enumerate([(1, 5, 12, 1.0), (3, 4, 20, 0.01),
+                                                (4, 7, 64, 100.0), (2, 16, 40, 1e3)]):
+        blocks = [rng.standard_normal((ell, n)) for _ in range(nblk)]
+        res = rng.standard_normal(ell)
+        out[f"{c}/M"] = np.vstack(blocks)
+        out[f"{c}/ell"] = np.array(ell)
+        out[f"{c}/residual"] = res
+        out[f"{c}/alpha"] = np.array(alpha)
+        out[f"{c}/s"] = innersolve.dual_step(blocks, res, alpha)
+    np.savez_compressed(os.path.join(HERE, "dual_step.npz"), **out)
+
+
+if __name__ == "__main__":
+    sampler_golden()
+    dense_runs()
+    tomo_runs()
+    projector_golden()
+    dual_step_golden()
+    for f in sorted(os.listdir(HERE)):
+        if f.endswith(".npz"):
+            print(f, os.path.getsize(os.path.join(HERE, f)))

@@ -1,0 +1,74 @@
+"""Pin the CPU oracle against vectors produced by the reference itself."""
+
+import numpy as np
+import pytest
+
+from oracle import slimls_oracle as orc
+from tests import golden_cases as gc
+
+
+def test_sampler_traces_bit_exact():
+    d = gc.load("sampler.npz")
+    assert len(d.files) == 45
+    for key in d.files:
+        scheme, m, seed = key.split("/")
+        got = orc.sampler_indices(scheme, int(m), int(seed), len(d[key]))
+        assert np.array_equal(got, d[key]), key
+
+
+@pytest.mark.parametrize("name", gc.DENSE_CASES)
+def test_dense_runs_match_reference(name):
+    c = gc.dense_case(name)
+    ell = int(c["ell"])
+    m, n = c["A"].shape
+    fetch = orc.dense_fetch(c["A"], c["b"], ell)
+    traj = orc.run_slimls(fetch, m // ell, n, c["indices"], gc.case_alphas(c),
+                          r=int(c["r"]), x0=c.get("x0"), references=c["refs"],
+                          record_every=int(c["record_every"]),
+                          store_iterates="iterates" in c)
+    assert np.array_equal(traj.ks, c["ks"])
+    assert traj.status == str(c["status"])
+    assert (traj.diverged_at or -1) == int(c["diverged_at"])
+    assert traj.row_status == list(c["row_status"])
+    np.testing.assert_array_equal(traj.alphas, c["alphas"])
+    np.testing.assert_array_equal(traj.epoch_fraction, c["epoch_fraction"])
+    scale = max(1.0, float(np.abs(c["x_final"]).max()))
+    np.testing.assert_allclose(traj.x_final, c["x_final"], rtol=1e-10, atol=1e-12 * scale)
+    np.testing.assert_allclose(traj.residual_norms, c["residual_norms"], rtol=1e-10, equal_nan=True)
+    for name_, vals in c["rel"].items():
+        np.testing.assert_allclose(traj.rel_errors[name_], vals, rtol=1e-10)
+    if "iterates" in c:
+        np.testing.assert_allclose(np.asarray(traj.iterates), c["iterates"], rtol=1e-10, atol=1e-12)
+
+
+def test_scalar_known_answer():
+    """A=[2], b=[4], alpha=1, r=0: x1 = 1.6 (reference test_solvers.py:43-47)."""
+    c = gc.dense_case("scalar")
+    assert abs(c["x_final"][0] - 1.6) < 1e-15
+    traj = orc.run_slimls(orc.dense_fetch(c["A"], c["b"], 1), 1, 1, [1], [1.0])
+    assert abs(traj.x_final[0] - 1.6) < 1e-15
+
+
+@pytest.mark.parametrize("name", ["tomo2d", "tomo3d"])
+def test_tomo_runs_match_reference(name):
+    c = gc.tomo_case(name)
+    n = c["blocks"][0][3][1]
+    fetch = orc.csr_fetch(c["blocks"], c["b"])
+    k = len(c["indices"])
+    traj = orc.run_slimls(fetch, len(c["blocks"]), n, c["indices"],
+                          np.full(k, float(c["alpha"])), r=int(c["r"]),
+                          references={"x_true": c["x_true"]})
+    np.testing.assert_allclose(traj.x_final, c["x_final"], rtol=1e-10,
+                               atol=1e-10 * np.abs(c["x_final"]).max())
+    np.testing.assert_allclose(traj.rel_errors["x_true"], c["rel"]["x_true"], rtol=1e-10)
+    np.testing.assert_allclose(traj.residual_norms, c["residual_norms"], rtol=1e-10, equal_nan=True)
+
+
+def test_dual_step_matches_reference():
+    d = gc.load("dual_step.npz")
+    for c in range(4):
+        m = d[f"{c}/M"]
+        ell = int(d[f"{c}/ell"])
+        blocks = [m[i:i + ell] for i in range(0, m.shape[0], ell)]
+        s = orc.dual_step(blocks, d[f"{c}/residual"], float(d[f"{c}/alpha"]))
+        np.testing.assert_allclose(s, d[f"{c}/s"], rtol=1e-12, atol=1e-14)
