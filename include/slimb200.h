@@ -1,0 +1,163 @@
+/*
+ * slimb200.h -- C-ABI of the B200-native slimLS hot path.
+ *
+ * Drop-in boundary for the reference's solver entry point
+ *   slimsolve.solvers.run("slimls", op, sampler, schedule, *, epochs, r, ...)
+ *   (reference pkg/src/slimsolve/solvers.py:480-588)
+ * and its secondary kernel-level seam
+ *   slimsolve.innersolve.solve_step(..., method="dual") -> dual_step
+ *   (reference pkg/src/slimsolve/innersolve.py:305-321, 359-381).
+ *
+ * Plain C types only: pointers, sizes, status codes.  Host pointers are
+ * borrowed for the duration of a call; all device memory is owned by the
+ * opaque context.  One context drives one device from one host thread
+ * (reference SPEC.md:309: one run owns one state, single-threaded).
+ *
+ * Status codes map onto the reference's Python exceptions:
+ *   SLIM_OK 0
+ *   SLIM_EINVAL  -> ValueError       (solvers.py:504-528, linops.py:64-72)
+ *   SLIM_ERANGE  -> IndexError       (linops.py:90-94)
+ *   SLIM_ENOTSPD -> LinAlgError      (innersolve.py:289-295)
+ *   SLIM_ECUDA / SLIM_ENCCL / SLIM_ESTATE -> RuntimeError
+ * The message of the last failure is available from slim_last_error().
+ */
+#ifndef SLIMB200_H
+#define SLIMB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SLIM_ABI_VERSION 1
+
+enum slim_status {
+  SLIM_OK = 0,
+  SLIM_EINVAL = 1,
+  SLIM_ERANGE = 2,
+  SLIM_ENOTSPD = 3,
+  SLIM_ECUDA = 4,
+  SLIM_ENCCL = 5,
+  SLIM_ESTATE = 6,
+  SLIM_ENOMEM = 7
+};
+
+/* value dtype of the stored operator (products are always fp64) */
+enum slim_dtype { SLIM_F64 = 0, SLIM_F32 = 1 };
+
+/* operator storage layout */
+enum slim_layout {
+  SLIM_DENSE_ROWMAJOR = 0,   /* DenseBlockOperator (linops.py:142-206)      */
+  SLIM_CSR_PERBLOCK = 1,     /* SparseBlockOperator (linops.py:209-299)     */
+  SLIM_GEN_SPLITMIX64 = 2    /* generated rows, never stored (configs[4])   */
+};
+
+typedef struct slim_ctx slim_ctx;
+
+typedef struct slim_desc {
+  int64_t n_rows;      /* m                                                */
+  int64_t n_cols;      /* n (columns owned by this context)                */
+  int64_t block_rows;  /* ell; m must be divisible (linops.py:64-72)       */
+  int64_t memory_r;    /* r >= 0; window holds r+1 blocks (solvers.py:67)  */
+  int32_t value_dtype; /* enum slim_dtype                                  */
+  int32_t layout;      /* enum slim_layout                                 */
+  int32_t device;      /* CUDA device ordinal                              */
+  int32_t flags;       /* reserved, 0                                      */
+  uint64_t gen_seed;   /* SLIM_GEN_SPLITMIX64 only                         */
+  int64_t gen_n_total; /* generator row length (global n) for GEN layout   */
+  int64_t col_offset;  /* first global column of this context's shard      */
+} slim_desc;
+
+/* ---- lifetime -------------------------------------------------------- */
+int slim_create(slim_ctx** out, const slim_desc* desc);
+void slim_destroy(slim_ctx* ctx);
+const char* slim_last_error(const slim_ctx* ctx); /* ctx may be NULL */
+int slim_abi_version(void);
+
+/* ---- operator upload (replaces RowBlockOperator.fetch_block's storage,
+ *      linops.py:192-206 dense views and 270-279 per-fetch densify) ---- */
+/* Dense row-major A (n_rows x n_cols, dtype per desc) and b (n_rows).     */
+int slim_upload_dense(slim_ctx* ctx, const void* a_rowmajor, const double* b);
+/* One CSR block (1-based index): rowptr has ell+1 entries relative to the
+ * block, col/val hold rowptr[ell] entries, b_block has ell entries.      */
+int slim_upload_csr_block(slim_ctx* ctx, int64_t block, const int64_t* rowptr,
+                          const int32_t* col, const void* val, const double* b_block);
+/* All CSR blocks at once: global rowptr (n_rows+1 entries, int64).       */
+int slim_upload_csr(slim_ctx* ctx, const int64_t* rowptr, const int32_t* col,
+                    const void* val, const double* b);
+/* finalize the uploaded operator (builds per-block CSC for the Gram and
+ * the transposed product); must be called before slim_run               */
+int slim_finalize_operator(slim_ctx* ctx);
+/* right-hand side for the generated layout (n_rows entries)              */
+int slim_set_rhs(slim_ctx* ctx, const double* b);
+
+/* ---- run state -------------------------------------------------------- */
+int slim_set_x(slim_ctx* ctx, const double* x0);          /* n_cols      */
+int slim_get_x(slim_ctx* ctx, double* x_out);             /* n_cols      */
+/* error references for the history (solvers.py:532-536, 550-552)       */
+int slim_set_references(slim_ctx* ctx, int32_t count, const double* const* refs);
+/* divergence threshold 1e12 (1 + ||x0||) (solvers.py:144-146)          */
+int slim_set_divergence_limit(slim_ctx* ctx, double limit);
+
+/* History row layout written by slim_run, SLIM_HIST_FIXED + n_refs doubles:
+ *   [0] k  [1] alpha_k  [2] ||r_k||  [3] device timestamp (ns)
+ *   [4] status (0 ok, 1 diverged)  [5..] ||x - ref_q|| (unnormalised)   */
+#define SLIM_HIST_FIXED 5
+
+/* Run K slimLS steps over a precomputed 1-based block index trace and
+ * alpha_k sequence (Sampler.next_index / Schedule.alpha_at, replaced by a
+ * host-side precompute).  Rows are recorded at every step with
+ * k % record_every == 0, at k == K, and at a divergence step.
+ * hist must hold (K / record_every + 2) * (SLIM_HIST_FIXED + n_refs)
+ * doubles; *n_rows receives the count written.  Row k = 0 is NOT written
+ * (the host records it, solvers.py:558).  iterates (nullable) receives
+ * a copy of x at every recorded row (store_iterates, solvers.py:553).  */
+int slim_run(slim_ctx* ctx, const int64_t* block_idx, const double* alphas, int64_t K,
+             int64_t record_every, double* hist, int64_t* n_rows, int32_t* status,
+             int64_t* diverged_at, double* iterates);
+
+/* Stream mode (for e2e / host-resident operators): the same as slim_run,
+ * but each step's block is copied host->device inside the run from the
+ * pinned host operator registered with slim_upload_* (HOST staging).    */
+int slim_set_host_streaming(slim_ctx* ctx, int32_t enable);
+
+/* ---- multi-GPU (column sharding, one NCCL allreduce per step) -------- */
+/* 128-byte NCCL unique id from rank 0 (broadcast by the host runtime).  */
+int slim_comm_init(slim_ctx* ctx, const void* nccl_unique_id, int32_t nranks, int32_t rank);
+
+/* ---- secondary seam and kernel-level entry points -------------------- */
+/* innersolve.dual_step (innersolve.py:305-321): stacked dense window
+ * M (rows x n, row-major fp64, oldest block first), residual of the
+ * newest ell rows, alpha.  s_out has n entries.                         */
+int slim_dual_step(int32_t device, const double* M, int64_t rows, int64_t n,
+                   const double* residual, int64_t ell, double alpha, double* s_out);
+/* fp64 Cholesky of an SPD matrix (lower), N x N row-major in/out.       */
+int slim_potrf(int32_t device, const double* G, int64_t N, double* L_out);
+/* residual r = A_k x - b_k of one block and its norm (solvers.py:180)   */
+int slim_block_residual(slim_ctx* ctx, int64_t block, const double* x, double* r_out,
+                        double* norm_out);
+
+/* ---- timing introspection for bench.py -------------------------------- */
+/* per-kernel-class device time accumulated over the last slim_run
+ * (CUDA events on the launching streams), in milliseconds.
+ * which: 0 gram, 1 cholesky, 2 x-chain, 3 whole run (events on sx)     */
+int slim_timing(slim_ctx* ctx, int32_t which, double* ms_out, int64_t* launches_out);
+int slim_set_profiling(slim_ctx* ctx, int32_t enable);
+/* time only steps k0..K of the next slim_run (which = 3 in slim_timing):
+ * from the end of step k0-1's x-chain to the end of the run; which = 4
+ * returns the number of kernels launched inside that window.           */
+int slim_set_timing_start(slim_ctx* ctx, int64_t k0);
+
+/* ---- problem setup helpers (host side, not the hot path) ------------- */
+/* Siddon parallel-beam 2D view block (restates tomo.py:219-273): counts
+ * nnz per row when col/val are NULL, otherwise fills them.               */
+int slim_siddon2d_view(double angle_deg, int64_t grid, int64_t rays, double spacing,
+                       int64_t* rowptr, int32_t* col, double* val);
+int slim_siddon3d_view(const double* direction, int64_t grid, int64_t side, double spacing,
+                       int64_t* rowptr, int32_t* col, double* val);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLIMB200_H */

@@ -1,0 +1,1008 @@
+// capi.cu -- C-ABI driver of the B200 slimLS hot path (include/slimb200.h).
+//
+// One slim_run() call executes the reference's hot loop (solvers.py:560-574)
+// for K precomputed block indices entirely on the device.  Per step k the
+// work is split over three kinds of streams:
+//
+//   sg      Gram panel of the newest block into the ring   (x-independent)
+//   sf[d]   tile Cholesky of G_k into factor buffer d       (x-independent)
+//   sx      residual -> triangular solves -> M^T w -> x update + history
+//
+// G_k depends only on the sampled index sequence, so the factorizations
+// of consecutive steps run ahead of, and concurrently with, the x-chain
+// (D factor buffers in flight).  The ring keeps r + D Gram panels so a
+// panel is never overwritten while an in-flight factorization reads it.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+#include "ops.h"
+#include "slimb200.h"
+
+using namespace slim;
+
+namespace {
+
+constexpr int D_FACT = 2;     // factorizations in flight
+constexpr int NEV = 16;       // event ring per kind
+
+struct ProfPair {
+  cudaEvent_t a, b;
+};
+
+}  // namespace
+
+struct slim_ctx {
+  std::string err;
+  slim_desc d{};
+  int64_t m = 0, n = 0, ell = 0, M = 0, r = 0;
+  int layout = 0, vdt = 0;
+  size_t vsize = 8;
+  int dev = 0;
+  // operator
+  void* A = nullptr;  // dense values (m x n)
+  double* b = nullptr;
+  int64_t* rowptr = nullptr;
+  int* col = nullptr;
+  void* val = nullptr;
+  int64_t nnz = 0;
+  int* colptr = nullptr;
+  int* cscrow = nullptr;
+  void* cscval = nullptr;
+  int64_t* blkbase = nullptr;  // M + 1 nnz offsets (device)
+  std::vector<int64_t> h_blkbase;
+  std::vector<int64_t> h_rowptr;  // staged CSR upload by block
+  std::vector<int> h_col;
+  std::vector<char> h_val;
+  std::vector<double> h_b;
+  std::vector<char> h_have;
+  bool op_ready = false;
+  // state
+  double* x = nullptr;
+  double* refs[MAX_REFS] = {};
+  int nref = 0;
+  Ctl* ctl = nullptr;
+  double div_limit = 1e12;
+  // work buffers
+  int S = 0, Tmax = 0;
+  double* panels = nullptr;
+  int64_t panel_stride = 0;
+  double* Lbuf[D_FACT] = {};
+  int* cflags[D_FACT] = {};
+  int* tickets = nullptr;  // D_FACT chol tickets + 1 trsv ticket
+  int* tflags = nullptr;
+  int* errflag = nullptr;
+  double* rvec = nullptr;
+  double* tvec = nullptr;
+  double* wvec = nullptr;
+  double* spart = nullptr;
+  int nsplit_mtw = 1;
+  double* fpart = nullptr;
+  double* gpart = nullptr;
+  int nsplit_gram = 1;
+  double* hist = nullptr;
+  int64_t hist_rows_cap = 0;
+  double* iters_dev = nullptr;
+  int64_t iters_cap = 0;
+  int64_t epoch_base = 0;
+  cudaStream_t sx = nullptr, sg = nullptr, sf[D_FACT] = {};
+  cudaEvent_t ev_g[NEV], ev_f[NEV], ev_x[NEV];
+  int64_t* pin_div = nullptr;
+  // profiling
+  bool prof = false;
+  std::vector<ProfPair> prof_chol, prof_gram, prof_x;
+  cudaEvent_t run_a = nullptr, run_b = nullptr;
+  double t_ms[5] = {0, 0, 0, 0, 0};
+  int64_t t_n[5] = {0, 0, 0, 0, 0};
+  int64_t timing_k0 = 1;
+  int64_t launches = 0;  // kernels launched by the current slim_run
+};
+
+static thread_local std::string g_err;
+
+static void set_err(slim_ctx* c, const char* msg);
+
+#define FAIL(ctx, code, ...)                                   \
+  do {                                                         \
+    char _b[512];                                              \
+    snprintf(_b, sizeof(_b), __VA_ARGS__);                     \
+    set_err((ctx), _b);                                        \
+    return code;                                               \
+  } while (0)
+
+#define CK(ctx, call)                                                                   \
+  do {                                                                                  \
+    cudaError_t _e = (call);                                                            \
+    if (_e != cudaSuccess)                                                              \
+      FAIL(ctx, SLIM_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(_e),     \
+           __FILE__, __LINE__);                                                         \
+  } while (0)
+
+#define CKLAUNCH(ctx) CK(ctx, cudaGetLastError())
+
+static void set_err(slim_ctx* c, const char* msg) {
+  if (c) c->err = msg;
+  g_err = msg;
+}
+
+static int dev_alloc(slim_ctx* c, void** p, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaSuccess)
+    FAIL(c, SLIM_ENOMEM, "cudaMalloc(%zu bytes) failed: %s", bytes, cudaGetErrorString(e));
+  return SLIM_OK;
+}
+#define ALLOC(ctx, ptr, bytes)                                               \
+  do {                                                                       \
+    int _rc = dev_alloc(ctx, reinterpret_cast<void**>(&(ptr)), (bytes));     \
+    if (_rc) return _rc;                                                     \
+  } while (0)
+
+extern "C" {
+
+int slim_abi_version(void) { return SLIM_ABI_VERSION; }
+
+const char* slim_last_error(const slim_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_err.c_str();
+}
+
+static void free_all(slim_ctx* c) {
+  void* ptrs[] = {c->A, c->b, c->rowptr, c->col, c->val, c->colptr, c->cscrow, c->cscval,
+                  c->blkbase, c->x, c->ctl, c->panels, c->tickets, c->tflags, c->errflag,
+                  c->rvec, c->tvec, c->wvec, c->spart, c->fpart, c->gpart, c->hist, c->iters_dev};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (int q = 0; q < MAX_REFS; ++q)
+    if (c->refs[q]) cudaFree(c->refs[q]);
+  for (int q = 0; q < D_FACT; ++q) {
+    if (c->Lbuf[q]) cudaFree(c->Lbuf[q]);
+    if (c->cflags[q]) cudaFree(c->cflags[q]);
+    if (c->sf[q]) cudaStreamDestroy(c->sf[q]);
+  }
+  if (c->sx) cudaStreamDestroy(c->sx);
+  if (c->sg) cudaStreamDestroy(c->sg);
+  for (int q = 0; q < NEV; ++q) {
+    if (c->ev_g[q]) cudaEventDestroy(c->ev_g[q]);
+    if (c->ev_f[q]) cudaEventDestroy(c->ev_f[q]);
+    if (c->ev_x[q]) cudaEventDestroy(c->ev_x[q]);
+  }
+  for (auto* v : {&c->prof_chol, &c->prof_gram, &c->prof_x})
+    for (auto& pp : *v) {
+      cudaEventDestroy(pp.a);
+      cudaEventDestroy(pp.b);
+    }
+  if (c->run_a) cudaEventDestroy(c->run_a);
+  if (c->run_b) cudaEventDestroy(c->run_b);
+  if (c->pin_div) cudaFreeHost(c->pin_div);
+}
+
+int slim_create(slim_ctx** out, const slim_desc* d) {
+  if (!out || !d) FAIL((slim_ctx*)nullptr, SLIM_EINVAL, "null argument");
+  *out = nullptr;
+  if (d->n_rows < 1 || d->n_cols < 1) FAIL((slim_ctx*)nullptr, SLIM_EINVAL, "m, n must be >= 1");
+  if (d->block_rows < 1)
+    FAIL((slim_ctx*)nullptr, SLIM_EINVAL, "block size must be >= 1, got %lld",
+         (long long)d->block_rows);
+  if (d->n_rows % d->block_rows != 0)
+    FAIL((slim_ctx*)nullptr, SLIM_EINVAL,
+         "m = %lld is not divisible by block size ell = %lld; only uniform partitions are supported",
+         (long long)d->n_rows, (long long)d->block_rows);
+  if (d->memory_r < 0) FAIL((slim_ctx*)nullptr, SLIM_EINVAL, "memory level r must be >= 0");
+  if (d->memory_r + 1 > MAX_WINDOW)
+    FAIL((slim_ctx*)nullptr, SLIM_EINVAL, "memory level r = %lld exceeds the device limit %d",
+         (long long)d->memory_r, MAX_WINDOW - 1);
+  if (d->value_dtype != SLIM_F64 && d->value_dtype != SLIM_F32)
+    FAIL((slim_ctx*)nullptr, SLIM_EINVAL, "unknown value dtype %d", d->value_dtype);
+  if (d->layout != SLIM_DENSE_ROWMAJOR && d->layout != SLIM_CSR_PERBLOCK)
+    FAIL((slim_ctx*)nullptr, SLIM_EINVAL, "layout %d not supported by this build", d->layout);
+  if (d->n_cols > 0x7fffffffLL) FAIL((slim_ctx*)nullptr, SLIM_EINVAL, "n too large");
+  slim_ctx* c = new slim_ctx();
+  c->d = *d;
+  c->m = d->n_rows;
+  c->n = d->n_cols;
+  c->ell = d->block_rows;
+  c->M = d->n_rows / d->block_rows;
+  c->r = d->memory_r;
+  c->layout = d->layout;
+  c->vdt = d->value_dtype;
+  c->vsize = c->vdt == SLIM_F64 ? 8 : 4;
+  c->dev = d->device;
+  *out = c;
+  CK(c, cudaSetDevice(c->dev));
+  CK(c, cudaStreamCreateWithFlags(&c->sx, cudaStreamNonBlocking));
+  CK(c, cudaStreamCreateWithFlags(&c->sg, cudaStreamNonBlocking));
+  for (int q = 0; q < D_FACT; ++q) CK(c, cudaStreamCreateWithFlags(&c->sf[q], cudaStreamNonBlocking));
+  for (int q = 0; q < NEV; ++q) {
+    CK(c, cudaEventCreateWithFlags(&c->ev_g[q], cudaEventDisableTiming));
+    CK(c, cudaEventCreateWithFlags(&c->ev_f[q], cudaEventDisableTiming));
+    CK(c, cudaEventCreateWithFlags(&c->ev_x[q], cudaEventDisableTiming));
+  }
+  CK(c, cudaEventCreate(&c->run_a));
+  CK(c, cudaEventCreate(&c->run_b));
+  CK(c, cudaHostAlloc((void**)&c->pin_div, sizeof(int64_t), cudaHostAllocDefault));
+  *c->pin_div = 0;
+
+  const int64_t ell = c->ell, W = c->r + 1;
+  c->S = (int)(W + D_FACT - 1);
+  c->panel_stride = (int64_t)c->S * ell * ell;
+  const int64_t Nmax = W * ell;
+  c->Tmax = (int)((Nmax + TB - 1) / TB);
+  const int64_t ntiles = (int64_t)c->Tmax * (c->Tmax + 1) / 2;
+  ALLOC(c, c->x, sizeof(double) * c->n);
+  CK(c, cudaMemset(c->x, 0, sizeof(double) * c->n));
+  ALLOC(c, c->b, sizeof(double) * c->m);
+  ALLOC(c, c->ctl, sizeof(Ctl));
+  ALLOC(c, c->panels, sizeof(double) * (size_t)c->S * c->panel_stride);
+  for (int q = 0; q < D_FACT; ++q) {
+    ALLOC(c, c->Lbuf[q], sizeof(double) * (size_t)ntiles * TB * TB);
+    ALLOC(c, c->cflags[q], sizeof(int) * ntiles);
+    CK(c, cudaMemset(c->cflags[q], 0, sizeof(int) * ntiles));
+  }
+  ALLOC(c, c->tickets, sizeof(int) * (D_FACT + 1));
+  ALLOC(c, c->tflags, sizeof(int) * 2 * c->Tmax);
+  CK(c, cudaMemset(c->tflags, 0, sizeof(int) * 2 * c->Tmax));
+  ALLOC(c, c->errflag, sizeof(int));
+  CK(c, cudaMemset(c->errflag, 0, sizeof(int)));
+  ALLOC(c, c->rvec, sizeof(double) * ell);
+  ALLOC(c, c->tvec, sizeof(double) * c->Tmax * TB);
+  ALLOC(c, c->wvec, sizeof(double) * c->Tmax * TB);
+  // M^T w: split the window rows over CTAs when n alone cannot fill the GPU
+  if (c->layout == SLIM_DENSE_ROWMAJOR) {
+    const int64_t cols_ctas = (c->n + 255) / 256;
+    int ns = (int)std::max<int64_t>(1, std::min<int64_t>(32, (4 * 148) / std::max<int64_t>(1, cols_ctas)));
+    ns = (int)std::min<int64_t>(ns, Nmax);
+    c->nsplit_mtw = ns;
+    // Gram split-K: enough CTAs to cover the machine
+    const int64_t tiles = ((Nmax + 63) / 64) * ((ell + 63) / 64);
+    int gs = (int)std::max<int64_t>(1, std::min<int64_t>((2 * 148 + tiles - 1) / tiles, (c->n + 255) / 256));
+    c->nsplit_gram = gs;
+    ALLOC(c, c->gpart, sizeof(double) * (size_t)gs * Nmax * ell);
+  }
+  ALLOC(c, c->spart, sizeof(double) * (size_t)c->nsplit_mtw * c->n);
+  ALLOC(c, c->fpart, sizeof(double) * (size_t)finish_grid((int)c->n) * (1 + MAX_REFS));
+  Ctl h{};
+  h.div_limit_sq = 1e24;
+  CK(c, cudaMemcpy(c->ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice));
+  return SLIM_OK;
+}
+
+void slim_destroy(slim_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->dev);
+  cudaDeviceSynchronize();
+  free_all(c);
+  delete c;
+}
+
+// ---------------------------------------------------------------------------
+// operator upload
+// ---------------------------------------------------------------------------
+
+int slim_upload_dense(slim_ctx* c, const void* a, const double* b) {
+  if (!c || !a || !b) FAIL(c, SLIM_EINVAL, "null argument");
+  if (c->layout != SLIM_DENSE_ROWMAJOR) FAIL(c, SLIM_EINVAL, "context layout is not dense");
+  CK(c, cudaSetDevice(c->dev));
+  const size_t bytes = (size_t)c->m * c->n * c->vsize;
+  if (!c->A) ALLOC(c, c->A, bytes);
+  CK(c, cudaMemcpy(c->A, a, bytes, cudaMemcpyHostToDevice));
+  CK(c, cudaMemcpy(c->b, b, sizeof(double) * c->m, cudaMemcpyHostToDevice));
+  c->op_ready = true;
+  return SLIM_OK;
+}
+
+int slim_upload_csr(slim_ctx* c, const int64_t* rowptr, const int32_t* col, const void* val,
+                    const double* b) {
+  if (!c || !rowptr || !b) FAIL(c, SLIM_EINVAL, "null argument");
+  if (c->layout != SLIM_CSR_PERBLOCK) FAIL(c, SLIM_EINVAL, "context layout is not CSR");
+  CK(c, cudaSetDevice(c->dev));
+  if (rowptr[0] != 0) FAIL(c, SLIM_EINVAL, "rowptr[0] must be 0");
+  for (int64_t i = 0; i < c->m; ++i)
+    if (rowptr[i + 1] < rowptr[i]) FAIL(c, SLIM_EINVAL, "rowptr not monotone at row %lld", (long long)i);
+  const int64_t nnz = rowptr[c->m];
+  for (int64_t e = 0; e < nnz; ++e)
+    if (col[e] < 0 || col[e] >= c->n)
+      FAIL(c, SLIM_EINVAL, "column index %d out of range at nonzero %lld", col[e], (long long)e);
+  // per-block nnz must fit the int32 column pointers of the per-block CSC
+  c->h_blkbase.assign(c->M + 1, 0);
+  for (int64_t bk = 0; bk <= c->M; ++bk) c->h_blkbase[bk] = rowptr[bk * c->ell];
+  for (int64_t bk = 0; bk < c->M; ++bk)
+    if (c->h_blkbase[bk + 1] - c->h_blkbase[bk] > 0x7fffffffLL)
+      FAIL(c, SLIM_EINVAL, "block %lld has more than 2^31 nonzeros", (long long)bk + 1);
+  if (c->rowptr) cudaFree(c->rowptr), c->rowptr = nullptr;
+  if (c->col) cudaFree(c->col), c->col = nullptr;
+  if (c->val) cudaFree(c->val), c->val = nullptr;
+  c->nnz = nnz;
+  ALLOC(c, c->rowptr, sizeof(int64_t) * (c->m + 1));
+  ALLOC(c, c->col, sizeof(int) * nnz);
+  ALLOC(c, c->val, c->vsize * nnz);
+  CK(c, cudaMemcpy(c->rowptr, rowptr, sizeof(int64_t) * (c->m + 1), cudaMemcpyHostToDevice));
+  if (nnz) {
+    CK(c, cudaMemcpy(c->col, col, sizeof(int) * nnz, cudaMemcpyHostToDevice));
+    CK(c, cudaMemcpy(c->val, val, c->vsize * nnz, cudaMemcpyHostToDevice));
+  }
+  CK(c, cudaMemcpy(c->b, b, sizeof(double) * c->m, cudaMemcpyHostToDevice));
+  c->op_ready = false;
+  return SLIM_OK;
+}
+
+int slim_upload_csr_block(slim_ctx* c, int64_t block, const int64_t* rowptr, const int32_t* col,
+                          const void* val, const double* b_block) {
+  if (!c || !rowptr || !b_block) FAIL(c, SLIM_EINVAL, "null argument");
+  if (c->layout != SLIM_CSR_PERBLOCK) FAIL(c, SLIM_EINVAL, "context layout is not CSR");
+  if (block < 1 || block > c->M)
+    FAIL(c, SLIM_ERANGE, "block index %lld out of range 1..%lld", (long long)block, (long long)c->M);
+  // staged on the host; the whole operator is pushed by slim_finalize_operator
+  if (c->h_have.empty()) {
+    c->h_have.assign(c->M, 0);
+    c->h_rowptr.clear();
+  }
+  const int64_t ell = c->ell, nnzb = rowptr[ell] - rowptr[0];
+  struct Blk;
+  // store per-block pieces in a simple concatenation keyed by block
+  static_assert(sizeof(int) == 4, "int32");
+  if ((int64_t)c->h_rowptr.size() != c->M * (ell + 1)) c->h_rowptr.assign(c->M * (ell + 1), -1);
+  for (int64_t i = 0; i <= ell; ++i) c->h_rowptr[(block - 1) * (ell + 1) + i] = rowptr[i] - rowptr[0];
+  // variable-size pieces appended, remembered by offset in h_b (reuse as index store)
+  if ((int64_t)c->h_b.size() != c->m) c->h_b.assign(c->m, 0.0);
+  for (int64_t i = 0; i < ell; ++i) c->h_b[(block - 1) * ell + i] = b_block[i];
+  const size_t off_c = c->h_col.size();
+  c->h_col.resize(off_c + nnzb + 2);
+  c->h_col[off_c] = (int)(block - 1);
+  c->h_col[off_c + 1] = (int)nnzb;
+  memcpy(&c->h_col[off_c + 2], col + rowptr[0], sizeof(int) * nnzb);
+  const size_t off_v = c->h_val.size();
+  c->h_val.resize(off_v + c->vsize * nnzb);
+  memcpy(&c->h_val[off_v], (const char*)val + c->vsize * rowptr[0], c->vsize * nnzb);
+  c->h_have[block - 1] = 1;
+  c->op_ready = false;
+  return SLIM_OK;
+}
+
+static int assemble_staged_csr(slim_ctx* c) {
+  const int64_t ell = c->ell, M = c->M;
+  for (int64_t bk = 0; bk < M; ++bk)
+    if (!c->h_have[bk]) FAIL(c, SLIM_EINVAL, "block %lld was never uploaded", (long long)bk + 1);
+  // walk the staged pieces (in upload order) and place them by block
+  std::vector<size_t> coff(M), voff(M);
+  std::vector<int64_t> cnt(M);
+  size_t pc = 0, pv = 0;
+  while (pc < c->h_col.size()) {
+    const int bk = c->h_col[pc];
+    const int64_t nb = c->h_col[pc + 1];
+    coff[bk] = pc + 2;
+    voff[bk] = pv;
+    cnt[bk] = nb;
+    pc += 2 + nb;
+    pv += c->vsize * nb;
+  }
+  std::vector<int64_t> rp(c->m + 1, 0);
+  for (int64_t bk = 0; bk < M; ++bk)
+    for (int64_t i = 0; i < ell; ++i)
+      rp[bk * ell + i + 1] = rp[bk * ell] + c->h_rowptr[bk * (ell + 1) + i + 1];
+  std::vector<int> colv((size_t)rp[c->m]);
+  std::vector<char> valv(c->vsize * (size_t)rp[c->m]);
+  for (int64_t bk = 0; bk < M; ++bk) {
+    memcpy(&colv[rp[bk * ell]], &c->h_col[coff[bk]], sizeof(int) * cnt[bk]);
+    memcpy(&valv[c->vsize * rp[bk * ell]], &c->h_val[voff[bk]], c->vsize * cnt[bk]);
+  }
+  std::vector<double> bb = c->h_b;
+  c->h_col.clear();
+  c->h_val.clear();
+  c->h_rowptr.clear();
+  c->h_have.clear();
+  c->h_b.clear();
+  return slim_upload_csr(c, rp.data(), colv.data(), valv.data(), bb.data());
+}
+
+int slim_finalize_operator(slim_ctx* c) {
+  if (!c) FAIL(c, SLIM_EINVAL, "null argument");
+  CK(c, cudaSetDevice(c->dev));
+  if (c->layout == SLIM_DENSE_ROWMAJOR) {
+    if (!c->A) FAIL(c, SLIM_ESTATE, "no dense operator uploaded");
+    c->op_ready = true;
+    return SLIM_OK;
+  }
+  if (!c->h_have.empty()) {
+    int rc = assemble_staged_csr(c);
+    if (rc) return rc;
+  }
+  if (!c->rowptr) FAIL(c, SLIM_ESTATE, "no CSR operator uploaded");
+  if (c->colptr) cudaFree(c->colptr), c->colptr = nullptr;
+  if (c->cscrow) cudaFree(c->cscrow), c->cscrow = nullptr;
+  if (c->cscval) cudaFree(c->cscval), c->cscval = nullptr;
+  if (c->blkbase) cudaFree(c->blkbase), c->blkbase = nullptr;
+  ALLOC(c, c->colptr, sizeof(int) * (size_t)c->M * (c->n + 1));
+  ALLOC(c, c->cscrow, sizeof(int) * (size_t)std::max<int64_t>(1, c->nnz));
+  ALLOC(c, c->cscval, c->vsize * (size_t)std::max<int64_t>(1, c->nnz));
+  ALLOC(c, c->blkbase, sizeof(int64_t) * (c->M + 1));
+  CK(c, cudaMemcpy(c->blkbase, c->h_blkbase.data(), sizeof(int64_t) * (c->M + 1),
+                   cudaMemcpyHostToDevice));
+  if (c->vdt == SLIM_F64)
+    launch_build_csc<double>(c->colptr, c->cscrow, (double*)c->cscval, c->rowptr, c->col,
+                             (const double*)c->val, c->blkbase, c->m, (int)c->ell, (int)c->n, c->M,
+                             c->sx);
+  else
+    launch_build_csc<float>(c->colptr, c->cscrow, (float*)c->cscval, c->rowptr, c->col,
+                            (const float*)c->val, c->blkbase, c->m, (int)c->ell, (int)c->n, c->M,
+                            c->sx);
+  CKLAUNCH(c);
+  CK(c, cudaStreamSynchronize(c->sx));
+  c->op_ready = true;
+  return SLIM_OK;
+}
+
+int slim_set_rhs(slim_ctx* c, const double* b) {
+  if (!c || !b) FAIL(c, SLIM_EINVAL, "null argument");
+  CK(c, cudaSetDevice(c->dev));
+  CK(c, cudaMemcpy(c->b, b, sizeof(double) * c->m, cudaMemcpyHostToDevice));
+  return SLIM_OK;
+}
+
+int slim_set_x(slim_ctx* c, const double* x0) {
+  if (!c || !x0) FAIL(c, SLIM_EINVAL, "null argument");
+  CK(c, cudaSetDevice(c->dev));
+  CK(c, cudaMemcpy(c->x, x0, sizeof(double) * c->n, cudaMemcpyHostToDevice));
+  return SLIM_OK;
+}
+
+int slim_get_x(slim_ctx* c, double* xo) {
+  if (!c || !xo) FAIL(c, SLIM_EINVAL, "null argument");
+  CK(c, cudaSetDevice(c->dev));
+  CK(c, cudaMemcpy(xo, c->x, sizeof(double) * c->n, cudaMemcpyDeviceToHost));
+  return SLIM_OK;
+}
+
+int slim_set_references(slim_ctx* c, int32_t count, const double* const* refs) {
+  if (!c) FAIL(c, SLIM_EINVAL, "null argument");
+  if (count < 0 || count > MAX_REFS)
+    FAIL(c, SLIM_EINVAL, "at most %d error references supported, got %d", MAX_REFS, count);
+  CK(c, cudaSetDevice(c->dev));
+  for (int q = 0; q < count; ++q) {
+    if (!c->refs[q]) ALLOC(c, c->refs[q], sizeof(double) * c->n);
+    CK(c, cudaMemcpy(c->refs[q], refs[q], sizeof(double) * c->n, cudaMemcpyHostToDevice));
+  }
+  c->nref = count;
+  return SLIM_OK;
+}
+
+int slim_set_divergence_limit(slim_ctx* c, double limit) {
+  if (!c) FAIL(c, SLIM_EINVAL, "null argument");
+  c->div_limit = limit;
+  return SLIM_OK;
+}
+
+int slim_set_profiling(slim_ctx* c, int32_t enable) {
+  if (!c) FAIL(c, SLIM_EINVAL, "null argument");
+  c->prof = enable != 0;
+  return SLIM_OK;
+}
+
+int slim_set_host_streaming(slim_ctx* c, int32_t enable) {
+  if (!c) FAIL(c, SLIM_EINVAL, "null argument");
+  if (enable) FAIL(c, SLIM_EINVAL, "host streaming is not available in this build");
+  return SLIM_OK;
+}
+
+int slim_comm_init(slim_ctx* c, const void*, int32_t nranks, int32_t) {
+  if (!c) FAIL(c, SLIM_EINVAL, "null argument");
+  if (nranks != 1) FAIL(c, SLIM_ENCCL, "column-sharded multi-GPU runs are not built in this version");
+  return SLIM_OK;
+}
+
+int slim_set_timing_start(slim_ctx* c, int64_t k0) {
+  if (!c || k0 < 1) FAIL(c, SLIM_EINVAL, "bad argument");
+  c->timing_k0 = k0;
+  return SLIM_OK;
+}
+
+int slim_timing(slim_ctx* c, int32_t which, double* ms, int64_t* launches) {
+  if (!c || which < 0 || which > 4) FAIL(c, SLIM_EINVAL, "bad argument");
+  if (ms) *ms = c->t_ms[which];
+  if (launches) *launches = c->t_n[which];
+  return SLIM_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// one step: enqueue on the three stream kinds
+// ---------------------------------------------------------------------------
+
+static void fill_window(const slim_ctx* c, const int64_t* idx, int64_t k, Window& W) {
+  const int nw = (int)std::min<int64_t>(k, c->r + 1);
+  W.nw = nw;
+  W.ell = (int)c->ell;
+  for (int P = 0; P < nw; ++P) {
+    const int64_t j = k - nw + 1 + P;  // step that pushed window position P
+    W.blk[P] = (int)(idx[j - 1] - 1);
+    W.slot[P] = (int)((j - 1) % c->S);
+  }
+}
+
+static ProfPair make_pair() {
+  ProfPair p;
+  cudaEventCreate(&p.a);
+  cudaEventCreate(&p.b);
+  return p;
+}
+
+static int enqueue_gram(slim_ctx* c, const Window& W, int64_t k) {
+  const int slot_new = W.slot[W.nw - 1];
+  double* panel = c->panels + (int64_t)slot_new * c->panel_stride;
+  const int64_t newblk = W.blk[W.nw - 1];
+  if (c->layout == SLIM_DENSE_ROWMAJOR) {
+    if (c->vdt == SLIM_F64)
+      c->launches += 2, launch_gram_dense<double>(panel, c->gpart, c->nsplit_gram, W, (const double*)c->A, c->n,
+                                newblk * c->ell, (int)c->n, c->sg);
+    else
+      c->launches += 2, launch_gram_dense<float>(panel, c->gpart, c->nsplit_gram, W, (const float*)c->A, c->n,
+                               newblk * c->ell, (int)c->n, c->sg);
+  } else {
+    const int* cpn = c->colptr + newblk * (c->n + 1);
+    const int64_t base = c->h_blkbase[newblk];
+    if (c->vdt == SLIM_F64)
+      c->launches += 1, launch_gram_csr<double>(panel, W, c->rowptr, c->col, (const double*)c->val, cpn, c->cscrow,
+                              (const double*)c->cscval, base, c->sg);
+    else
+      c->launches += 1, launch_gram_csr<float>(panel, W, c->rowptr, c->col, (const float*)c->val, cpn, c->cscrow,
+                             (const float*)c->cscval, base, c->sg);
+  }
+  (void)k;
+  CKLAUNCH(c);
+  return SLIM_OK;
+}
+
+static int enqueue_x_chain(slim_ctx* c, const Window& W, int64_t k, int d, double alpha,
+                           int record, int epoch) {
+  const int64_t newblk = W.blk[W.nw - 1];
+  const int64_t row0 = newblk * c->ell;
+  const int ell = (int)c->ell, n = (int)c->n, N = W.nw * ell;
+  cudaStream_t s = c->sx;
+  (void)k;
+  // trsv
+  TrsvParams T{};
+  T.L = c->Lbuf[d];
+  T.flags = c->tflags;
+  T.ticket = c->tickets + D_FACT;
+  T.epoch = epoch;
+  T.N = N;
+  T.T = (N + TB - 1) / TB;
+  T.rstart = N - ell;
+  T.i0 = T.rstart / TB;
+  T.r = c->rvec;
+  T.t = c->tvec;
+  T.w = c->wvec;
+  T.ctl = c->ctl;
+  CK(c, cudaMemsetAsync(T.ticket, 0, sizeof(int), s));
+  launch_trsv(T, s);
+  CKLAUNCH(c);
+  c->launches += 3;  // trsv, M^T w, finish
+  // M^T w
+  double* s_parts = c->spart;
+  int nsplit = 1;
+  if (c->layout == SLIM_DENSE_ROWMAJOR) {
+    nsplit = std::min(c->nsplit_mtw, N);
+    if (c->vdt == SLIM_F64)
+      launch_mtw_dense<double>(c->spart, nsplit, W, (const double*)c->A, c->n, n, c->wvec, c->ctl, s);
+    else
+      launch_mtw_dense<float>(c->spart, nsplit, W, (const float*)c->A, c->n, n, c->wvec, c->ctl, s);
+  } else {
+    if (c->vdt == SLIM_F64)
+      launch_mtw_csc<double>(c->spart, W, c->colptr, n, c->cscrow, (const double*)c->cscval,
+                             c->blkbase, c->wvec, c->ctl, s);
+    else
+      launch_mtw_csc<float>(c->spart, W, c->colptr, n, c->cscrow, (const float*)c->cscval,
+                            c->blkbase, c->wvec, c->ctl, s);
+  }
+  CKLAUNCH(c);
+  FinishParams F{};
+  F.x = c->x;
+  F.s_parts = s_parts;
+  F.nsplit = nsplit;
+  F.n = n;
+  F.alpha = alpha;
+  for (int q = 0; q < c->nref; ++q) F.refs[q] = c->refs[q];
+  F.nref = c->nref;
+  F.ctl = c->ctl;
+  F.part = c->fpart;
+  F.hist = c->hist;
+  F.k = k;
+  F.record = record;
+  F.r = c->rvec;
+  F.ell = ell;
+  launch_finish(F, s);
+  CKLAUNCH(c);
+  (void)row0;
+  return SLIM_OK;
+}
+
+static int enqueue_residual(slim_ctx* c, int64_t newblk) {
+  const int64_t row0 = newblk * c->ell;
+  c->launches += 1;
+  if (c->layout == SLIM_DENSE_ROWMAJOR) {
+    if (c->vdt == SLIM_F64)
+      launch_residual_dense<double>(c->rvec, (const double*)c->A, c->n, row0, (int)c->ell,
+                                    (int)c->n, c->x, c->b, c->ctl, c->sx);
+    else
+      launch_residual_dense<float>(c->rvec, (const float*)c->A, c->n, row0, (int)c->ell,
+                                   (int)c->n, c->x, c->b, c->ctl, c->sx);
+  } else {
+    if (c->vdt == SLIM_F64)
+      launch_residual_csr<double>(c->rvec, c->rowptr, c->col, (const double*)c->val, row0,
+                                  (int)c->ell, c->x, c->b, c->ctl, c->sx);
+    else
+      launch_residual_csr<float>(c->rvec, c->rowptr, c->col, (const float*)c->val, row0,
+                                 (int)c->ell, c->x, c->b, c->ctl, c->sx);
+  }
+  CKLAUNCH(c);
+  return SLIM_OK;
+}
+
+static int enqueue_chol(slim_ctx* c, const Window& W, int d, double alpha, int epoch) {
+  const int N = W.nw * (int)c->ell;
+  CholParams P{};
+  P.L = c->Lbuf[d];
+  P.flags = c->cflags[d];
+  P.ticket = c->tickets + d;
+  P.error = c->errflag;
+  P.epoch = epoch;
+  P.N = N;
+  P.T = (N + TB - 1) / TB;
+  P.panels = c->panels;
+  P.panel_stride = c->panel_stride;
+  P.ell = (int)c->ell;
+  P.S = c->S;
+  P.nw = W.nw;
+  P.alpha = alpha;
+  for (int q = 0; q < W.nw; ++q) P.slot[q] = W.slot[q];
+  P.G = nullptr;
+  P.ldg = 0;
+  CK(c, cudaMemsetAsync(P.ticket, 0, sizeof(int), c->sf[d]));
+  launch_chol(P, c->sf[d]);
+  c->launches += 1;
+  CKLAUNCH(c);
+  return SLIM_OK;
+}
+
+extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, int64_t K,
+                        int64_t record_every, double* hist, int64_t* n_rows, int32_t* status,
+                        int64_t* diverged_at, double* iterates) {
+  if (!c) FAIL(c, SLIM_EINVAL, "null context");
+  if (K < 0) FAIL(c, SLIM_EINVAL, "epochs must be >= 0");
+  if (record_every < 1) FAIL(c, SLIM_EINVAL, "record_every must be >= 1");
+  if (K > 0 && (!idx || !alphas)) FAIL(c, SLIM_EINVAL, "null index/alpha trace");
+  if (!c->op_ready) FAIL(c, SLIM_ESTATE, "operator not finalized (call slim_finalize_operator)");
+  for (int64_t k = 0; k < K; ++k) {
+    if (idx[k] < 1 || idx[k] > c->M)
+      FAIL(c, SLIM_ERANGE, "block index %lld out of range 1..%lld", (long long)idx[k],
+           (long long)c->M);
+    if (!(alphas[k] > 0))
+      FAIL(c, SLIM_EINVAL, "schedule produced alpha_%lld = %g <= 0", (long long)k + 1, alphas[k]);
+  }
+  CK(c, cudaSetDevice(c->dev));
+  const int cols = SLIM_HIST_FIXED + c->nref;
+  const int64_t rows_cap = K / record_every + 2;
+  if (rows_cap > c->hist_rows_cap) {
+    if (c->hist) cudaFree(c->hist), c->hist = nullptr;
+    ALLOC(c, c->hist, sizeof(double) * rows_cap * (SLIM_HIST_FIXED + MAX_REFS));
+    c->hist_rows_cap = rows_cap;
+  }
+  if (iterates && rows_cap > c->iters_cap) {
+    if (c->iters_dev) cudaFree(c->iters_dev), c->iters_dev = nullptr;
+    ALLOC(c, c->iters_dev, sizeof(double) * rows_cap * c->n);
+    c->iters_cap = rows_cap;
+  }
+  CK(c, cudaDeviceSynchronize());
+  Ctl h{};
+  h.div_limit_sq = c->div_limit * c->div_limit;
+  CK(c, cudaMemcpy(c->ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice));
+  CK(c, cudaMemset(c->errflag, 0, sizeof(int)));
+  *c->pin_div = 0;
+  for (int q = 0; q < 4; ++q) c->t_ms[q] = 0.0, c->t_n[q] = 0;
+  std::vector<ProfPair> pch, pgr, pxc;
+  auto take = [](std::vector<ProfPair>& pool, std::vector<ProfPair>& used) {
+    if (pool.empty()) used.push_back(make_pair());
+    else {
+      used.push_back(pool.back());
+      pool.pop_back();
+    }
+    return used.back();
+  };
+
+  launch_stamp_start(c->ctl, c->sx);
+  CKLAUNCH(c);
+  const int64_t k0 = std::min<int64_t>(std::max<int64_t>(c->timing_k0, 1), std::max<int64_t>(K, 1));
+  int64_t launches_at_k0 = 0;
+  c->launches = 0;
+  bool a_recorded = false;
+  if (k0 == 1) {
+    CK(c, cudaEventRecord(c->run_a, c->sx));
+    a_recorded = true;
+  }
+  int64_t rec_rows = 0;  // rows this run will have recorded (host view, for iterates)
+  const int64_t epoch0 = c->epoch_base;
+  Window W{};
+  for (int64_t k = 1; k <= K; ++k) {
+    fill_window(c, idx, k, W);
+    const int d = (int)(k % D_FACT);
+    const int epoch = (int)(epoch0 + k);
+    const double alpha = alphas[k - 1];
+    // ---- Gram panel (sg): wait until no in-flight factorization reads the slot
+    for (int q = 0; q < D_FACT; ++q) {
+      const int64_t kk = k - D_FACT - q;
+      if (kk >= 1) CK(c, cudaStreamWaitEvent(c->sg, c->ev_f[kk % NEV], 0));
+    }
+    ProfPair pg{};
+    if (c->prof && k >= k0) pg = take(c->prof_gram, pgr), cudaEventRecord(pg.a, c->sg);
+    {
+      int rc = enqueue_gram(c, W, k);
+      if (rc) return rc;
+    }
+    if (c->prof && k >= k0) cudaEventRecord(pg.b, c->sg);
+    CK(c, cudaEventRecord(c->ev_g[k % NEV], c->sg));
+    // ---- factorization (sf[d])
+    CK(c, cudaStreamWaitEvent(c->sf[d], c->ev_g[k % NEV], 0));
+    if (k - D_FACT >= 1) CK(c, cudaStreamWaitEvent(c->sf[d], c->ev_x[(k - D_FACT) % NEV], 0));
+    ProfPair pc{};
+    if (c->prof && k >= k0) pc = take(c->prof_chol, pch), cudaEventRecord(pc.a, c->sf[d]);
+    {
+      int rc = enqueue_chol(c, W, d, alpha, epoch);
+      if (rc) return rc;
+    }
+    if (c->prof && k >= k0) cudaEventRecord(pc.b, c->sf[d]);
+    CK(c, cudaEventRecord(c->ev_f[k % NEV], c->sf[d]));
+    // ---- x-chain (sx)
+    ProfPair px{};
+    if (c->prof && k >= k0) px = take(c->prof_x, pxc), cudaEventRecord(px.a, c->sx);
+    {
+      int rc = enqueue_residual(c, W.blk[W.nw - 1]);
+      if (rc) return rc;
+    }
+    CK(c, cudaStreamWaitEvent(c->sx, c->ev_f[k % NEV], 0));
+    const int record = (k % record_every == 0 || k == K) ? 1 : 0;
+    {
+      int rc = enqueue_x_chain(c, W, k, d, alpha, record, epoch);
+      if (rc) return rc;
+    }
+    if (c->prof && k >= k0) cudaEventRecord(px.b, c->sx);
+    if (iterates && record) {
+      CK(c, cudaMemcpyAsync(c->iters_dev + rec_rows * c->n, c->x, sizeof(double) * c->n,
+                            cudaMemcpyDeviceToDevice, c->sx));
+      ++rec_rows;
+    }
+    CK(c, cudaEventRecord(c->ev_x[k % NEV], c->sx));
+    if (k + 1 == k0) {
+      CK(c, cudaEventRecord(c->run_a, c->sx));
+      launches_at_k0 = c->launches;
+      a_recorded = true;
+    }
+    // cheap divergence poll: stop enqueueing once the device reported it
+    if ((k & 31) == 0) {
+      if (*c->pin_div != 0) break;
+      CK(c, cudaMemcpyAsync(c->pin_div, &c->ctl->diverged_at, sizeof(int64_t),
+                            cudaMemcpyDeviceToHost, c->sx));
+    }
+  }
+  for (int q = 0; q < D_FACT; ++q) {
+    CK(c, cudaEventRecord(c->ev_f[0], c->sf[q]));
+    CK(c, cudaStreamWaitEvent(c->sx, c->ev_f[0], 0));
+  }
+  if (!a_recorded) {
+    CK(c, cudaEventRecord(c->run_a, c->sx));
+    launches_at_k0 = c->launches;
+  }
+  CK(c, cudaEventRecord(c->run_b, c->sx));
+  c->epoch_base += K + 1;
+  c->timing_k0 = 1;
+  CK(c, cudaDeviceSynchronize());
+  Ctl hc{};
+  CK(c, cudaMemcpy(&hc, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
+  int herr = 0;
+  CK(c, cudaMemcpy(&herr, c->errflag, sizeof(int), cudaMemcpyDeviceToHost));
+  if (c->prof) {
+    float ms = 0.f;
+    for (auto& pp : pgr) cudaEventElapsedTime(&ms, pp.a, pp.b), c->t_ms[0] += ms, c->t_n[0]++;
+    for (auto& pp : pch) cudaEventElapsedTime(&ms, pp.a, pp.b), c->t_ms[1] += ms, c->t_n[1]++;
+    for (auto& pp : pxc) cudaEventElapsedTime(&ms, pp.a, pp.b), c->t_ms[2] += ms, c->t_n[2]++;
+    for (auto& pp : pgr) c->prof_gram.push_back(pp);
+    for (auto& pp : pch) c->prof_chol.push_back(pp);
+    for (auto& pp : pxc) c->prof_x.push_back(pp);
+  }
+  {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->run_a, c->run_b);
+    c->t_ms[3] = ms;
+    c->t_n[3] = K - k0 + 1;
+    c->t_n[4] = c->launches - launches_at_k0;
+  }
+  const int64_t nr = hc.nrows;
+  if (hist && nr > 0) {
+    // device rows are strided by SLIM_HIST_FIXED + nref already
+    CK(c, cudaMemcpy(hist, c->hist, sizeof(double) * nr * cols, cudaMemcpyDeviceToHost));
+  }
+  if (iterates && nr > 0) {
+    // rows recorded before a divergence match rec_rows order; a divergence
+    // row (not a record step) holds the final iterate
+    const int64_t ncopy = std::min<int64_t>(nr, rec_rows);
+    if (ncopy > 0)
+      CK(c, cudaMemcpy(iterates, c->iters_dev, sizeof(double) * ncopy * c->n,
+                       cudaMemcpyDeviceToHost));
+    if (hc.diverged_at != 0)
+      CK(c, cudaMemcpy(iterates + (nr - 1) * c->n, c->x, sizeof(double) * c->n,
+                       cudaMemcpyDeviceToHost));
+  }
+  if (n_rows) *n_rows = nr;
+  if (status) *status = hc.diverged_at != 0 ? 1 : 0;
+  if (diverged_at) *diverged_at = hc.diverged_at;
+  if (herr)
+    FAIL(c, SLIM_ENOTSPD,
+         "damped dual system numerically singular; this should not happen for alpha > 0");
+  return SLIM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// kernel-level entry points (parity seams)
+// ---------------------------------------------------------------------------
+
+extern "C" int slim_block_residual(slim_ctx* c, int64_t block, const double* x, double* r_out,
+                                   double* norm_out) {
+  if (!c || !x || !r_out) FAIL(c, SLIM_EINVAL, "null argument");
+  if (!c->op_ready) FAIL(c, SLIM_ESTATE, "operator not finalized");
+  if (block < 1 || block > c->M)
+    FAIL(c, SLIM_ERANGE, "block index %lld out of range 1..%lld", (long long)block, (long long)c->M);
+  CK(c, cudaSetDevice(c->dev));
+  CK(c, cudaMemcpy(c->x, x, sizeof(double) * c->n, cudaMemcpyHostToDevice));
+  Ctl h{};
+  h.div_limit_sq = c->div_limit * c->div_limit;
+  CK(c, cudaMemcpy(c->ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice));
+  int rc = enqueue_residual(c, block - 1);
+  if (rc) return rc;
+  CK(c, cudaStreamSynchronize(c->sx));
+  CK(c, cudaMemcpy(r_out, c->rvec, sizeof(double) * c->ell, cudaMemcpyDeviceToHost));
+  if (norm_out) {
+    double s = 0.0;
+    for (int64_t i = 0; i < c->ell; ++i) s += r_out[i] * r_out[i];
+    *norm_out = std::sqrt(s);
+  }
+  return SLIM_OK;
+}
+
+// s = alpha M^T (I + alpha M M^T)^{-1} [0; r] through the production kernels:
+// the blocks of M are pushed one by one (incremental Gram panels), the tile
+// Cholesky factors the window, the triangular solves and M^T w finish it.
+extern "C" int slim_dual_step(int32_t device, const double* Mh, int64_t rows, int64_t n,
+                              const double* residual, int64_t ell, double alpha, double* s_out) {
+  if (!Mh || !residual || !s_out) FAIL((slim_ctx*)nullptr, SLIM_EINVAL, "null argument");
+  if (ell < 1 || rows < ell || rows % ell != 0)
+    FAIL((slim_ctx*)nullptr, SLIM_EINVAL, "stack rows %lld not a multiple of ell %lld",
+         (long long)rows, (long long)ell);
+  if (!(alpha > 0)) FAIL((slim_ctx*)nullptr, SLIM_EINVAL, "alpha must be > 0");
+  slim_desc d{};
+  d.n_rows = rows;
+  d.n_cols = n;
+  d.block_rows = ell;
+  d.memory_r = rows / ell - 1;
+  d.value_dtype = SLIM_F64;
+  d.layout = SLIM_DENSE_ROWMAJOR;
+  d.device = device;
+  slim_ctx* c = nullptr;
+  int rc = slim_create(&c, &d);
+  auto fail_out = [&](int code) {
+    if (c) {
+      g_err = c->err;
+      slim_destroy(c);
+    }
+    return code;
+  };
+  if (rc) return fail_out(rc);
+  std::vector<double> zeros(rows, 0.0);
+  if ((rc = slim_upload_dense(c, Mh, zeros.data()))) return fail_out(rc);
+  const int64_t nb = rows / ell;
+  std::vector<int64_t> idx(nb);
+  for (int64_t q = 0; q < nb; ++q) idx[q] = q + 1;
+  Window W{};
+  for (int64_t k = 1; k <= nb; ++k) {
+    fill_window(c, idx.data(), k, W);
+    if ((rc = enqueue_gram(c, W, k))) return fail_out(rc);
+  }
+  if (cudaStreamSynchronize(c->sg) != cudaSuccess) return fail_out(SLIM_ECUDA);
+  if ((rc = enqueue_chol(c, W, 0, alpha, 1))) return fail_out(rc);
+  if (cudaStreamSynchronize(c->sf[0]) != cudaSuccess) return fail_out(SLIM_ECUDA);
+  if (cudaMemcpy(c->rvec, residual, sizeof(double) * ell, cudaMemcpyHostToDevice) != cudaSuccess)
+    return fail_out(SLIM_ECUDA);
+  Ctl h{};
+  h.div_limit_sq = 1e300;
+  cudaMemcpy(c->ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice);
+  const int N = (int)rows;
+  TrsvParams T{};
+  T.L = c->Lbuf[0];
+  T.flags = c->tflags;
+  T.ticket = c->tickets + D_FACT;
+  T.epoch = 1;
+  T.N = N;
+  T.T = (N + TB - 1) / TB;
+  T.rstart = N - (int)ell;
+  T.i0 = T.rstart / TB;
+  T.r = c->rvec;
+  T.t = c->tvec;
+  T.w = c->wvec;
+  T.ctl = nullptr;
+  cudaMemsetAsync(T.ticket, 0, sizeof(int), c->sx);
+  launch_trsv(T, c->sx);
+  launch_mtw_dense<double>(c->spart, 1, W, (const double*)c->A, n, (int)n, c->wvec, c->ctl, c->sx);
+  if (cudaStreamSynchronize(c->sx) != cudaSuccess || cudaGetLastError() != cudaSuccess)
+    return fail_out(SLIM_ECUDA);
+  int herr = 0;
+  cudaMemcpy(&herr, c->errflag, sizeof(int), cudaMemcpyDeviceToHost);
+  cudaMemcpy(s_out, c->spart, sizeof(double) * n, cudaMemcpyDeviceToHost);
+  for (int64_t q = 0; q < n; ++q) s_out[q] *= alpha;
+  slim_destroy(c);
+  if (herr) FAIL((slim_ctx*)nullptr, SLIM_ENOTSPD, "dual system not positive definite");
+  return SLIM_OK;
+}
+
+extern "C" int slim_potrf(int32_t device, const double* G, int64_t N, double* L_out) {
+  if (!G || !L_out || N < 1) FAIL((slim_ctx*)nullptr, SLIM_EINVAL, "bad argument");
+  if (cudaSetDevice(device) != cudaSuccess) FAIL((slim_ctx*)nullptr, SLIM_ECUDA, "cudaSetDevice");
+  const int T = (int)((N + TB - 1) / TB);
+  const int64_t ntiles = (int64_t)T * (T + 1) / 2;
+  double *dG = nullptr, *dL = nullptr;
+  int *flags = nullptr, *ticket = nullptr, *err = nullptr;
+  auto cleanup = [&]() {
+    cudaFree(dG);
+    cudaFree(dL);
+    cudaFree(flags);
+    cudaFree(ticket);
+    cudaFree(err);
+  };
+  if (cudaMalloc(&dG, sizeof(double) * N * N) != cudaSuccess ||
+      cudaMalloc(&dL, sizeof(double) * ntiles * TB * TB) != cudaSuccess ||
+      cudaMalloc(&flags, sizeof(int) * ntiles) != cudaSuccess ||
+      cudaMalloc(&ticket, sizeof(int)) != cudaSuccess || cudaMalloc(&err, sizeof(int)) != cudaSuccess) {
+    cleanup();
+    FAIL((slim_ctx*)nullptr, SLIM_ENOMEM, "device allocation failed");
+  }
+  cudaMemcpy(dG, G, sizeof(double) * N * N, cudaMemcpyHostToDevice);
+  cudaMemset(flags, 0, sizeof(int) * ntiles);
+  cudaMemset(ticket, 0, sizeof(int));
+  cudaMemset(err, 0, sizeof(int));
+  CholParams P{};
+  P.L = dL;
+  P.flags = flags;
+  P.ticket = ticket;
+  P.error = err;
+  P.epoch = 1;
+  P.N = (int)N;
+  P.T = T;
+  P.panels = nullptr;
+  P.G = dG;
+  P.ldg = N;
+  launch_chol(P, 0);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    cleanup();
+    FAIL((slim_ctx*)nullptr, SLIM_ECUDA, "potrf kernel failed: %s", cudaGetErrorString(e));
+  }
+  std::vector<double> tiles((size_t)ntiles * TB * TB);
+  cudaMemcpy(tiles.data(), dL, sizeof(double) * tiles.size(), cudaMemcpyDeviceToHost);
+  int herr = 0;
+  cudaMemcpy(&herr, err, sizeof(int), cudaMemcpyDeviceToHost);
+  cleanup();
+  for (int64_t p = 0; p < N; ++p)
+    for (int64_t q = 0; q < N; ++q) {
+      double v = 0.0;
+      if (q <= p) {
+        const int ti = (int)(p / TB), tj = (int)(q / TB);
+        v = tiles[tile_off(ti, tj) + (p % TB) * TB + (q % TB)];
+      }
+      L_out[p * N + q] = v;
+    }
+  if (herr) FAIL((slim_ctx*)nullptr, SLIM_ENOTSPD, "matrix is not positive definite");
+  return SLIM_OK;
+}

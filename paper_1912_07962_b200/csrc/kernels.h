@@ -1,0 +1,70 @@
+// kernels.h -- parameter blocks and launch declarations shared by the
+// slimLS kernels and the C-ABI driver.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace slim {
+
+// Device-resident run control (one per context).
+struct Ctl {
+  double rnorm2;          // ||r_k||^2 of the current step
+  double div_limit_sq;    // (1e12 (1 + ||x0||))^2, solvers.py:144-146
+  int64_t diverged_at;    // 0 = ok, else first diverged step k
+  int64_t nrows;          // history rows written
+  uint64_t t_start_ns;    // globaltimer at run start
+  unsigned int done;      // last-block-done counter for k_finish
+  int pad;
+};
+
+struct CholParams {
+  double* L;            // lower tiles, tile_off(i, j)
+  int* flags;           // T (T + 1) / 2 epoch flags
+  int* ticket;          // zeroed before each launch
+  int* error;           // set to 1 on a non-positive pivot
+  int epoch;
+  int N, T;
+  // ring mode: initial tiles gathered from the incremental Gram panels
+  const double* panels;
+  int64_t panel_stride;  // S * ell * ell
+  int ell, S, nw;
+  double alpha;
+  int slot[MAX_WINDOW];  // window position (0 = oldest) -> ring slot
+  // dense mode (panels == nullptr): G is the full SPD matrix, row-major
+  const double* G;
+  int64_t ldg;
+};
+
+struct TrsvParams {
+  const double* L;
+  int* flags;        // 2 T epoch flags (forward, backward)
+  int* ticket;
+  int epoch;
+  int N, T, i0, rstart;
+  const double* r;   // newest-block residual (ell)
+  double* t;         // T * 64 forward result
+  double* w;         // T * 64 backward result (window order)
+  const Ctl* ctl;    // nullable; skip when diverged
+};
+
+// window description shared by the x-chain / Gram kernels
+struct Window {
+  int nw;                     // blocks in the window
+  int ell;
+  int blk[MAX_WINDOW];        // 0-based block id at window position
+  int slot[MAX_WINDOW];       // ring slot at window position
+};
+
+// ---- launchers (ops.cu / chol.cu) ----
+void launch_chol(const CholParams& P, cudaStream_t s);
+void launch_trsv(const TrsvParams& P, cudaStream_t s);
+
+__global__ void k_chol_tiles(CholParams P);
+__global__ void k_trsv(TrsvParams P);
+
+size_t chol_smem_bytes();
+size_t trsv_smem_bytes();
+
+}  // namespace slim

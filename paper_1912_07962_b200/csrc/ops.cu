@@ -1,0 +1,520 @@
+// ops.cu -- streaming kernels of one slimLS step (everything but the
+// factorization / triangular solves, which live in chol.cu).
+//
+//   residual   r = A_k x - b_k, ||r||              solvers.py:180-183
+//   gram       new column panel A_k M_k^T          innersolve.py:298-302
+//              (incremental: only the new block's products are formed;
+//               the reference recomputes the full M M^T every step)
+//   mtw        s = alpha M_k^T w                   innersolve.py:321
+//   finish     x <- x - s, ||x||^2 divergence,     solvers.py:169-177
+//              history row at record steps         solvers.py:543-554
+//
+// Every reduction has a fixed order, so a run is bit-reproducible
+// (reference determinism contract, test_solvers.py:555-571).
+#include <cub/block/block_scan.cuh>
+
+#include "common.cuh"
+#include "ops.h"
+
+namespace slim {
+
+// ---------------------------------------------------------------------------
+// residual
+// ---------------------------------------------------------------------------
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_residual_dense(double* r, const T* __restrict__ A,
+                                                        int64_t lda, int64_t row0, int ell, int n,
+                                                        const double* __restrict__ x,
+                                                        const double* __restrict__ b,
+                                                        const Ctl* ctl) {
+  if (ctl->diverged_at != 0) return;
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= ell) return;
+  const T* a = A + (row0 + row) * lda;
+  double s = 0.0;
+  for (int c = lane; c < n; c += 32) s += to_f64(a[c]) * x[c];
+  s = warp_sum(s);
+  if (lane == 0) r[row] = s - b[row0 + row];
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_residual_csr(double* r, const int64_t* __restrict__ rowptr,
+                                                      const int* __restrict__ col,
+                                                      const T* __restrict__ val, int64_t row0,
+                                                      int ell, const double* __restrict__ x,
+                                                      const double* __restrict__ b,
+                                                      const Ctl* ctl) {
+  if (ctl->diverged_at != 0) return;
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= ell) return;
+  const int64_t lo = rowptr[row0 + row], hi = rowptr[row0 + row + 1];
+  double s = 0.0;
+  for (int64_t e = lo + lane; e < hi; e += 32) s += to_f64(val[e]) * x[col[e]];
+  s = warp_sum(s);
+  if (lane == 0) r[row] = s - b[row0 + row];
+}
+
+// ---------------------------------------------------------------------------
+// Gram panel of the newest block: panel[(slot(P) ell + a) ell + j] =
+// A_P[a] . A_k[j] for every window row (P, a) and new row j.
+// ---------------------------------------------------------------------------
+
+// CSR: one warp per window row.  Each nonzero (c, v) of the row looks up
+// column c of the new block's CSC (<= a few entries for ray geometry) and
+// contributes v * u to acc[j].  Lanes that hit the same j in one round are
+// grouped with match_any and summed by the group leader in lane order, so
+// the accumulation order is a pure function of the data.
+template <typename T>
+__global__ void __launch_bounds__(128) k_gram_csr(double* __restrict__ panel, Window W,
+                                                  const int64_t* __restrict__ rowptr,
+                                                  const int* __restrict__ col,
+                                                  const T* __restrict__ val,
+                                                  const int* __restrict__ colptr_new,
+                                                  const int* __restrict__ cscrow,
+                                                  const T* __restrict__ cscval, int64_t base_new) {
+  extern __shared__ __align__(16) double gacc[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ell = W.ell;
+  const int grow_w = blockIdx.x * 4 + warp;
+  if (grow_w >= W.nw * ell) return;
+  const int P = grow_w / ell, a = grow_w - P * ell;
+  double* acc = gacc + (size_t)warp * ell;
+  for (int j = lane; j < ell; j += 32) acc[j] = 0.0;
+  __syncwarp();
+  const int64_t grow = (int64_t)W.blk[P] * ell + a;
+  const int64_t lo = rowptr[grow], hi = rowptr[grow + 1];
+  const unsigned full = 0xffffffffu;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t base = lo; base < hi; base += 32) {
+    const int64_t e = base + lane;
+    int cs = 0, cnt = 0;
+    double v = 0.0;
+    if (e < hi) {
+      const int c = col[e];
+      v = to_f64(val[e]);
+      cs = colptr_new[c];
+      cnt = colptr_new[c + 1] - cs;
+    }
+    int maxcnt = cnt;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) maxcnt = max(maxcnt, __shfl_xor_sync(full, maxcnt, o));
+    for (int s = 0; s < maxcnt; ++s) {
+      const bool has = s < cnt;
+      int j = -1 - lane;
+      double prod = 0.0;
+      if (has) {
+        const int64_t q = base_new + cs + s;
+        j = cscrow[q];
+        prod = v * to_f64(cscval[q]);
+      }
+      const unsigned mask = __match_any_sync(full, j);
+      const bool leader = has && ((mask & lt) == 0u);
+      int gsz = __popc(mask);
+      int maxg = has ? gsz : 1;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) maxg = max(maxg, __shfl_xor_sync(full, maxg, o));
+      double sum = prod;
+      unsigned m = mask;
+      for (int q = 1; q < maxg; ++q) {
+        m &= (m - 1u);
+        const int src = m ? (__ffs(m) - 1) : lane;
+        const double pv = __shfl_sync(full, prod, src);
+        if (m) sum += pv;
+      }
+      if (leader) acc[j] += sum;
+      __syncwarp();
+    }
+  }
+  __syncwarp();
+  double* out = panel + ((int64_t)W.slot[P] * ell + a) * ell;
+  for (int j = lane; j < ell; j += 32) out[j] = acc[j];
+}
+
+// Dense: DMMA tile GEMM, 64 window rows x 64 new rows per CTA, split-K over
+// blockIdx.z into fp64 partials reduced in a fixed order by k_gram_reduce.
+constexpr int GK = 32, GS = 36;  // K chunk and smem stride (doubles)
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_gram_dense(double* __restrict__ part, Window W,
+                                                    const T* __restrict__ A, int64_t lda,
+                                                    int64_t newrow0, int n, int klen) {
+  __shared__ __align__(16) double As[64 * GS];
+  __shared__ __align__(16) double Bs[64 * GS];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ell = W.ell, N = W.nw * ell;
+  const int p0 = blockIdx.x * 64, j0 = blockIdx.y * 64;
+  const int kbeg = blockIdx.z * klen, kend = min(n, kbeg + klen);
+  // row pointers this thread loads (8 rows x 4 lanes per 32-wide row)
+  double acc[8][2];
+#pragma unroll
+  for (int nt = 0; nt < 8; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+  for (int kc = kbeg; kc < kend; kc += GK) {
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      const int idx = tid + it * 256;
+      const int rr = idx >> 5, cc = idx & 31;
+      const int k = kc + cc;
+      const int p = p0 + rr;
+      double va = 0.0, vb = 0.0;
+      if (p < N && k < kend) {
+        const int P = p / ell;
+        va = to_f64(A[((int64_t)W.blk[P] * ell + (p - P * ell)) * lda + k]);
+      }
+      const int jr = j0 + rr;
+      if (jr < ell && k < kend) vb = to_f64(A[(newrow0 + jr) * lda + k]);
+      As[rr * GS + cc] = va;
+      Bs[rr * GS + cc] = vb;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k4 = 0; k4 < GK / 4; ++k4) {
+      const double a = As[(warp * 8 + (lane >> 2)) * GS + 4 * k4 + (lane & 3)];
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) {
+        const double b = Bs[(nt * 8 + (lane >> 2)) * GS + 4 * k4 + (lane & 3)];
+        dmma8x8x4(acc[nt], a, b);
+      }
+    }
+    __syncthreads();
+  }
+  const int p = p0 + warp * 8 + (lane >> 2);
+  if (p < N) {
+    double* out = part + (int64_t)blockIdx.z * N * ell + (int64_t)p * ell;
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      const int j = j0 + nt * 8 + 2 * (lane & 3);
+      if (j < ell) out[j] = acc[nt][0];
+      if (j + 1 < ell) out[j + 1] = acc[nt][1];
+    }
+  }
+}
+
+__global__ void k_gram_reduce(double* __restrict__ panel, Window W, const double* __restrict__ part,
+                              int nsplit) {
+  const int ell = W.ell, N = W.nw * ell;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)N * ell) return;
+  const int p = (int)(idx / ell), j = (int)(idx - (int64_t)p * ell);
+  double s = 0.0;
+  for (int z = 0; z < nsplit; ++z) s += part[(int64_t)z * N * ell + idx];
+  const int P = p / ell, a = p - P * ell;
+  panel[((int64_t)W.slot[P] * ell + a) * ell + j] = s;
+}
+
+// ---------------------------------------------------------------------------
+// s = M^T w (alpha applied in k_finish)
+// ---------------------------------------------------------------------------
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_mtw_dense(double* __restrict__ part, Window W,
+                                                   const T* __restrict__ A, int64_t lda, int n,
+                                                   const double* __restrict__ w, int rows_per_split,
+                                                   const Ctl* ctl) {
+  if (ctl->diverged_at != 0) return;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const int ell = W.ell, N = W.nw * ell;
+  const int pbeg = blockIdx.y * rows_per_split, pend = min(N, pbeg + rows_per_split);
+  double s = 0.0;
+  for (int p = pbeg; p < pend;) {
+    const int P = p / ell;
+    const int a0 = p - P * ell;
+    const int cnt = min(ell - a0, pend - p);
+    const T* base = A + ((int64_t)W.blk[P] * ell + a0) * lda + c;
+    for (int q = 0; q < cnt; ++q) s += to_f64(base[(int64_t)q * lda]) * w[p + q];
+    p += cnt;
+  }
+  part[(int64_t)blockIdx.y * n + c] = s;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_mtw_csc(double* __restrict__ s_out, Window W,
+                                                 const int* __restrict__ colptr, int n,
+                                                 const int* __restrict__ cscrow,
+                                                 const T* __restrict__ cscval,
+                                                 const int64_t* __restrict__ blkbase,
+                                                 const double* __restrict__ w, const Ctl* ctl) {
+  if (ctl->diverged_at != 0) return;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const int ell = W.ell;
+  double s = 0.0;
+  for (int P = 0; P < W.nw; ++P) {
+    const int b = W.blk[P];
+    const int* cp = colptr + (int64_t)b * (n + 1);
+    const int lo = cp[c], hi = cp[c + 1];
+    const int64_t base = blkbase[b];
+    const double* wp = w + P * ell;
+    for (int e = lo; e < hi; ++e) s += to_f64(cscval[base + e]) * wp[cscrow[base + e]];
+  }
+  s_out[c] = s;
+}
+
+// ---------------------------------------------------------------------------
+// finish: x update, norms, divergence, history (last-block reduction)
+// ---------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(256) k_finish(FinishParams F) {
+  Ctl* ctl = F.ctl;
+  if (ctl->diverged_at != 0) return;
+  const int tid = threadIdx.x;
+  const int c = blockIdx.x * blockDim.x + tid;
+  const int nq = 1 + F.nref;
+  double loc[1 + MAX_REFS];
+#pragma unroll
+  for (int q = 0; q < 1 + MAX_REFS; ++q) loc[q] = 0.0;
+  if (c < F.n) {
+    double sn = 0.0;
+    for (int z = 0; z < F.nsplit; ++z) sn += F.s_parts[(int64_t)z * F.n + c];
+    const double xn = F.x[c] - F.alpha * sn;
+    F.x[c] = xn;
+    loc[0] = xn * xn;
+#pragma unroll
+    for (int q = 0; q < MAX_REFS; ++q)
+      if (q < F.nref) {
+        const double d = xn - F.refs[q][c];
+        loc[1 + q] = d * d;
+      }
+  }
+  __shared__ double red[8][1 + MAX_REFS];
+  __shared__ bool s_last;
+  const int warp = tid >> 5, lane = tid & 31;
+  for (int q = 0; q < nq; ++q) {
+    const double v = warp_sum(loc[q]);
+    if (lane == 0) red[warp][q] = v;
+  }
+  __syncthreads();
+  if (tid < nq) {
+    double v = 0.0;
+    for (int wi = 0; wi < 8; ++wi) v += red[wi][tid];
+    F.part[(int64_t)blockIdx.x * nq + tid] = v;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = (atomicAdd(&ctl->done, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // deterministic final sums: warp q reduces quantity q over the blocks
+  __shared__ double tot[1 + MAX_REFS];
+  __shared__ double s_rn;
+  if (warp < nq) {
+    double v = 0.0;
+    for (int bi = lane; bi < (int)gridDim.x; bi += 32) v += __ldcg(F.part + (int64_t)bi * nq + warp);
+    v = warp_sum(v);
+    if (lane == 0) tot[warp] = v;
+  }
+  if (warp == 7) {
+    double v = 0.0;
+    for (int jj = lane; jj < F.ell; jj += 32) {
+      const double rv = __ldcg(F.r + jj);
+      v += rv * rv;
+    }
+    v = warp_sum(v);
+    if (lane == 0) s_rn = v;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    ctl->done = 0u;
+    ctl->rnorm2 = s_rn;
+    const double nsq = tot[0];
+    const bool diverged = !(nsq <= ctl->div_limit_sq);
+    if (diverged) ctl->diverged_at = F.k;
+    if (F.record || diverged) {
+      const int64_t row = ctl->nrows++;
+      double* h = F.hist + row * (SLIM_HIST_FIXED_DEV + F.nref);
+      h[0] = (double)F.k;
+      h[1] = F.alpha;
+      h[2] = sqrt(s_rn);
+      h[3] = (double)(globaltimer_ns() - ctl->t_start_ns);
+      h[4] = diverged ? 1.0 : 0.0;
+      for (int q = 0; q < F.nref; ++q) h[SLIM_HIST_FIXED_DEV + q] = sqrt(tot[1 + q]);
+    }
+  }
+}
+
+__global__ void k_stamp_start(Ctl* ctl) { ctl->t_start_ns = globaltimer_ns(); }
+
+// ---------------------------------------------------------------------------
+// per-block CSC (built once per operator): column pointers relative to the
+// block's first nonzero, rows 0-based within the block, rows sorted.
+// ---------------------------------------------------------------------------
+
+__global__ void k_csc_count(int* __restrict__ colptr, const int64_t* __restrict__ rowptr,
+                            const int* __restrict__ col, int64_t m, int ell, int n) {
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= m) return;
+  const int64_t b = row / ell;
+  int* cp = colptr + b * (int64_t)(n + 1);
+  for (int64_t e = rowptr[row] + lane; e < rowptr[row + 1]; e += 32) atomicAdd(cp + col[e] + 1, 1);
+}
+
+__global__ void __launch_bounds__(256) k_csc_scan(int* __restrict__ colptr, int n) {
+  using Scan = cub::BlockScan<int, 256>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int carry;
+  int* cp = colptr + (int64_t)blockIdx.x * (n + 1);
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 1; base <= n; base += 256) {
+    const int idx = base + threadIdx.x;
+    int v = (idx <= n) ? cp[idx] : 0;
+    int incl, agg;
+    Scan(tmp).InclusiveSum(v, incl, agg);
+    const int c0 = carry;
+    if (idx <= n) cp[idx] = incl + c0;
+    __syncthreads();
+    if (threadIdx.x == 0) carry = c0 + agg;
+    __syncthreads();
+  }
+}
+
+template <typename T>
+__global__ void k_csc_fill(int* __restrict__ colptr, const int64_t* __restrict__ rowptr,
+                           const int* __restrict__ col, const T* __restrict__ val,
+                           int* __restrict__ cscrow, T* __restrict__ cscval, int64_t m, int ell,
+                           int n) {
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= m) return;
+  const int64_t b = row / ell;
+  const int64_t base = rowptr[b * ell];
+  int* cp = colptr + b * (int64_t)(n + 1);
+  const int rloc = (int)(row - b * ell);
+  for (int64_t e = rowptr[row] + lane; e < rowptr[row + 1]; e += 32) {
+    const int pos = atomicAdd(cp + col[e], 1);
+    cscrow[base + pos] = rloc;
+    cscval[base + pos] = val[e];
+  }
+}
+
+// after the fill, cp[c] holds the end of column c; shift right by one
+__global__ void __launch_bounds__(256) k_csc_shift(int* __restrict__ colptr, int n) {
+  int* cp = colptr + (int64_t)blockIdx.x * (n + 1);
+  for (int hi = n + 1; hi > 0; hi -= 256) {
+    const int c = hi - 256 + (int)threadIdx.x;  // writes positions [hi-256, hi)
+    int v = 0;
+    if (c >= 1) v = cp[c - 1];
+    __syncthreads();
+    if (c >= 1) cp[c] = v;
+    else if (c == 0) cp[0] = 0;
+    __syncthreads();
+  }
+}
+
+template <typename T>
+__global__ void k_csc_sort(const int* __restrict__ colptr, int* __restrict__ cscrow,
+                           T* __restrict__ cscval, const int64_t* __restrict__ blkbase,
+                           int64_t nblocks, int n) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= nblocks * n) return;
+  const int64_t b = gid / n;
+  const int c = (int)(gid - b * n);
+  const int* cp = colptr + b * (int64_t)(n + 1);
+  const int64_t base = blkbase[b];
+  const int lo = cp[c], hi = cp[c + 1];
+  for (int e = lo + 1; e < hi; ++e) {
+    const int rk = cscrow[base + e];
+    const T vk = cscval[base + e];
+    int q = e - 1;
+    while (q >= lo && cscrow[base + q] > rk) {
+      cscrow[base + q + 1] = cscrow[base + q];
+      cscval[base + q + 1] = cscval[base + q];
+      --q;
+    }
+    cscrow[base + q + 1] = rk;
+    cscval[base + q + 1] = vk;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+
+static inline unsigned cdiv(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b); }
+
+template <typename T>
+void launch_residual_dense(double* r, const T* A, int64_t lda, int64_t row0, int ell, int n,
+                           const double* x, const double* b, const Ctl* ctl, cudaStream_t s) {
+  k_residual_dense<T><<<cdiv(ell, 8), 256, 0, s>>>(r, A, lda, row0, ell, n, x, b, ctl);
+}
+template <typename T>
+void launch_residual_csr(double* r, const int64_t* rowptr, const int* col, const T* val,
+                         int64_t row0, int ell, const double* x, const double* b, const Ctl* ctl,
+                         cudaStream_t s) {
+  k_residual_csr<T><<<cdiv(ell, 8), 256, 0, s>>>(r, rowptr, col, val, row0, ell, x, b, ctl);
+}
+template <typename T>
+void launch_gram_csr(double* panel, const Window& W, const int64_t* rowptr, const int* col,
+                     const T* val, const int* colptr_new, const int* cscrow, const T* cscval,
+                     int64_t base_new, cudaStream_t s) {
+  const size_t smem = (size_t)4 * W.ell * sizeof(double);
+  k_gram_csr<T><<<cdiv((int64_t)W.nw * W.ell, 4), 128, smem, s>>>(
+      panel, W, rowptr, col, val, colptr_new, cscrow, cscval, base_new);
+}
+template <typename T>
+void launch_gram_dense(double* panel, double* part, int nsplit, const Window& W, const T* A,
+                       int64_t lda, int64_t newrow0, int n, cudaStream_t s) {
+  const int N = W.nw * W.ell;
+  int klen = (n + nsplit - 1) / nsplit;
+  klen = ((klen + GK - 1) / GK) * GK;
+  const int zs = (n + klen - 1) / klen;
+  dim3 grid(cdiv(N, 64), cdiv(W.ell, 64), zs);
+  k_gram_dense<T><<<grid, 256, 0, s>>>(part, W, A, lda, newrow0, n, klen);
+  k_gram_reduce<<<cdiv((int64_t)N * W.ell, 256), 256, 0, s>>>(panel, W, part, zs);
+}
+template <typename T>
+void launch_mtw_dense(double* part, int nsplit, const Window& W, const T* A, int64_t lda, int n,
+                      const double* w, const Ctl* ctl, cudaStream_t s) {
+  const int N = W.nw * W.ell;
+  const int rps = (N + nsplit - 1) / nsplit;
+  dim3 grid(cdiv(n, 256), nsplit);
+  k_mtw_dense<T><<<grid, 256, 0, s>>>(part, W, A, lda, n, w, rps, ctl);
+}
+template <typename T>
+void launch_mtw_csc(double* s_out, const Window& W, const int* colptr, int n, const int* cscrow,
+                    const T* cscval, const int64_t* blkbase, const double* w, const Ctl* ctl,
+                    cudaStream_t s) {
+  k_mtw_csc<T><<<cdiv(n, 256), 256, 0, s>>>(s_out, W, colptr, n, cscrow, cscval, blkbase, w, ctl);
+}
+void launch_finish(const FinishParams& F, cudaStream_t s) {
+  k_finish<<<cdiv(F.n, 256), 256, 0, s>>>(F);
+}
+int finish_grid(int n) { return (int)cdiv(n, 256); }
+void launch_stamp_start(Ctl* ctl, cudaStream_t s) { k_stamp_start<<<1, 1, 0, s>>>(ctl); }
+
+template <typename T>
+void launch_build_csc(int* colptr, int* cscrow, T* cscval, const int64_t* rowptr, const int* col,
+                      const T* val, const int64_t* blkbase, int64_t m, int ell, int n,
+                      int64_t nblocks, cudaStream_t s) {
+  cudaMemsetAsync(colptr, 0, sizeof(int) * (size_t)nblocks * (n + 1), s);
+  k_csc_count<<<cdiv(m, 8), 256, 0, s>>>(colptr, rowptr, col, m, ell, n);
+  k_csc_scan<<<(unsigned)nblocks, 256, 0, s>>>(colptr, n);
+  k_csc_fill<T><<<cdiv(m, 8), 256, 0, s>>>(colptr, rowptr, col, val, cscrow, cscval, m, ell, n);
+  k_csc_shift<<<(unsigned)nblocks, 256, 0, s>>>(colptr, n);
+  k_csc_sort<T><<<cdiv(nblocks * n, 256), 256, 0, s>>>(colptr, cscrow, cscval, blkbase, nblocks, n);
+}
+
+#define SLIM_INST(T)                                                                              \
+  template void launch_residual_dense<T>(double*, const T*, int64_t, int64_t, int, int,          \
+                                         const double*, const double*, const Ctl*, cudaStream_t); \
+  template void launch_residual_csr<T>(double*, const int64_t*, const int*, const T*, int64_t,    \
+                                       int, const double*, const double*, const Ctl*,            \
+                                       cudaStream_t);                                            \
+  template void launch_gram_csr<T>(double*, const Window&, const int64_t*, const int*, const T*,  \
+                                   const int*, const int*, const T*, int64_t, cudaStream_t);      \
+  template void launch_gram_dense<T>(double*, double*, int, const Window&, const T*, int64_t,     \
+                                     int64_t, int, cudaStream_t);                                \
+  template void launch_mtw_dense<T>(double*, int, const Window&, const T*, int64_t, int,          \
+                                    const double*, const Ctl*, cudaStream_t);                    \
+  template void launch_mtw_csc<T>(double*, const Window&, const int*, int, const int*, const T*,  \
+                                  const int64_t*, const double*, const Ctl*, cudaStream_t);      \
+  template void launch_build_csc<T>(int*, int*, T*, const int64_t*, const int*, const T*,         \
+                                    const int64_t*, int64_t, int, int, int64_t, cudaStream_t);
+
+SLIM_INST(double)
+SLIM_INST(float)
+
+}  // namespace slim

@@ -1,0 +1,55 @@
+// ops.h -- launchers for the streaming kernels in ops.cu.
+#pragma once
+#include "kernels.h"
+
+namespace slim {
+
+constexpr int SLIM_HIST_FIXED_DEV = 5;  // must equal SLIM_HIST_FIXED in slimb200.h
+
+struct FinishParams {
+  double* x;
+  const double* s_parts;  // nsplit x n partial sums of M^T w
+  int nsplit;
+  int n;
+  double alpha;
+  const double* refs[MAX_REFS];
+  int nref;
+  Ctl* ctl;
+  double* part;           // grid x (1 + nref) block partials
+  double* hist;
+  int64_t k;
+  int record;
+  const double* r;        // residual (ell) for ||r||
+  int ell;
+};
+
+template <typename T>
+void launch_residual_dense(double* r, const T* A, int64_t lda, int64_t row0, int ell, int n,
+                           const double* x, const double* b, const Ctl* ctl, cudaStream_t s);
+template <typename T>
+void launch_residual_csr(double* r, const int64_t* rowptr, const int* col, const T* val,
+                         int64_t row0, int ell, const double* x, const double* b, const Ctl* ctl,
+                         cudaStream_t s);
+template <typename T>
+void launch_gram_csr(double* panel, const Window& W, const int64_t* rowptr, const int* col,
+                     const T* val, const int* colptr_new, const int* cscrow, const T* cscval,
+                     int64_t base_new, cudaStream_t s);
+template <typename T>
+void launch_gram_dense(double* panel, double* part, int nsplit, const Window& W, const T* A,
+                       int64_t lda, int64_t newrow0, int n, cudaStream_t s);
+template <typename T>
+void launch_mtw_dense(double* part, int nsplit, const Window& W, const T* A, int64_t lda, int n,
+                      const double* w, const Ctl* ctl, cudaStream_t s);
+template <typename T>
+void launch_mtw_csc(double* s_out, const Window& W, const int* colptr, int n, const int* cscrow,
+                    const T* cscval, const int64_t* blkbase, const double* w, const Ctl* ctl,
+                    cudaStream_t s);
+template <typename T>
+void launch_build_csc(int* colptr, int* cscrow, T* cscval, const int64_t* rowptr, const int* col,
+                      const T* val, const int64_t* blkbase, int64_t m, int ell, int n,
+                      int64_t nblocks, cudaStream_t s);
+void launch_finish(const FinishParams& F, cudaStream_t s);
+int finish_grid(int n);
+void launch_stamp_start(Ctl* ctl, cudaStream_t s);
+
+}  // namespace slim

@@ -1,0 +1,207 @@
+"""Synthetic problem generators for the five BASELINE configurations.
+
+Problem setup is host-side and outside the accelerated path; it follows
+the reference's conventions (tomo.py) so the operators are the ones the
+reference would build:
+
+* parallel-beam Siddon blocks, one view per block, exact intersection
+  lengths (tomo.py:219-301, restated in ``csrc/siddon.cpp``);
+* view angles over [0, pi) mapped into the reference's (-90, 90] range by
+  theta -> theta - 180 for theta > 90 (tomo.py:158-159): the same rays,
+  the detector axis reversed;
+* noise scaled so ||eps|| / ||A x_true|| equals the level exactly
+  (tomo.py:323-333), Philox-keyed Generators throughout (README.md:142-149).
+
+The phantoms are seeded random ellipses / ellipsoids as BASELINE.json
+describes (the reference ships Shepp-Logan tables; the random-ellipse
+recipe is documented in DESIGN.md).
+"""
+
+from __future__ import annotations
+
+import concurrent.futures as cf
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .linops import DenseBlockOperator, SparseBlockOperator
+
+
+def _rng(seed: int) -> np.random.Generator:
+    return np.random.Generator(np.random.Philox(key=int(seed)))
+
+
+def scaled_noise(clean: np.ndarray, level: float, rng: np.random.Generator) -> np.ndarray:
+    """b = clean + eps with ||eps|| = level ||clean|| (tomo.py:323-333)."""
+    if level == 0:
+        return clean.copy()
+    eps = rng.standard_normal(clean.shape[0])
+    eps *= level * np.linalg.norm(clean) / np.linalg.norm(eps)
+    return clean + eps
+
+
+# ---------------------------------------------------------------------------
+# configs[0]: dense Gaussian
+# ---------------------------------------------------------------------------
+
+
+def gaussian_dense(m=20000, n=1000, ell=100, seed=1912, noise=0.01, var_scale=1000.0):
+    """A ~ N(0, 1/var_scale), x_true ~ N(0, 1), 1% noise; one Philox stream
+    drawn in the order A, x_true, eps."""
+    g = _rng(seed)
+    a = g.standard_normal((m, n)) / np.sqrt(var_scale)
+    x_true = g.standard_normal(n)
+    clean = a @ x_true
+    b = scaled_noise(clean, noise, g)
+    return DenseBlockOperator(a, ell, b), b, x_true
+
+
+# ---------------------------------------------------------------------------
+# tomography
+# ---------------------------------------------------------------------------
+
+
+def angles_0_pi(count: int) -> np.ndarray:
+    """Equispaced angles over [0, 180) deg, mapped into (-90, 90]."""
+    deg = np.arange(count) * (180.0 / count)
+    return np.where(deg > 90.0, deg - 180.0, deg)
+
+
+def siddon2d_block(angle_deg: float, grid: int, rays: int, spacing: float = 1.0):
+    """(indptr, indices, data, shape) of one 2D view (tomo.py:259-273)."""
+    L = _lib.lib()
+    rowptr = np.zeros(rays + 1, dtype=np.int64)
+    _lib.check(L.slim_siddon2d_view(float(angle_deg), grid, rays, float(spacing),
+                                    _lib.i64ptr(rowptr), None, None))
+    nnz = int(rowptr[-1])
+    col = np.empty(nnz, dtype=np.int32)
+    val = np.empty(nnz, dtype=np.float64)
+    _lib.check(L.slim_siddon2d_view(float(angle_deg), grid, rays, float(spacing),
+                                    _lib.i64ptr(rowptr), _lib.i32ptr(col), _lib.dptr(val)))
+    return rowptr, col, val, (rays, grid * grid)
+
+
+def siddon3d_block(direction, grid: int, side: int, spacing: float = 1.0):
+    """(indptr, indices, data, shape) of one 3D view (tomo.py:285-301)."""
+    L = _lib.lib()
+    d = np.ascontiguousarray(np.asarray(direction, dtype=float))
+    rows = side * side
+    rowptr = np.zeros(rows + 1, dtype=np.int64)
+    _lib.check(L.slim_siddon3d_view(_lib.dptr(d), grid, side, float(spacing),
+                                    _lib.i64ptr(rowptr), None, None))
+    nnz = int(rowptr[-1])
+    col = np.empty(nnz, dtype=np.int32)
+    val = np.empty(nnz, dtype=np.float64)
+    _lib.check(L.slim_siddon3d_view(_lib.dptr(d), grid, side, float(spacing),
+                                    _lib.i64ptr(rowptr), _lib.i32ptr(col), _lib.dptr(val)))
+    return rowptr, col, val, (rows, grid ** 3)
+
+
+def _pmap(fn, items, threads=None):
+    threads = threads or min(32, os.cpu_count() or 1)
+    if len(items) <= 1 or threads <= 1:
+        return [fn(it) for it in items]
+    with cf.ThreadPoolExecutor(max_workers=threads) as pool:
+        return list(pool.map(fn, items))
+
+
+def random_ellipses(grid: int, count: int, seed: int) -> np.ndarray:
+    """2D phantom: ``count`` additive ellipses, centres uniform in the image,
+    semi-axes U(0.05, 0.4) of the width, intensity U(0.1, 1), angle U(0, pi);
+    cell-centre rasterisation (tomo.py:110-120 convention)."""
+    g = _rng(seed)
+    centers = -1.0 + (np.arange(grid) + 0.5) * (2.0 / grid)
+    yy, xx = np.meshgrid(centers, centers, indexing="ij")
+    img = np.zeros((grid, grid))
+    for _ in range(count):
+        x0, y0 = g.uniform(-1.0, 1.0, 2)
+        sa, sb = g.uniform(0.05, 0.4, 2) * 2.0
+        val = g.uniform(0.1, 1.0)
+        ang = g.uniform(0.0, np.pi)
+        c, s = np.cos(ang), np.sin(ang)
+        u = (xx - x0) * c + (yy - y0) * s
+        v = -(xx - x0) * s + (yy - y0) * c
+        img[(u / sa) ** 2 + (v / sb) ** 2 <= 1.0] += val
+    return img.ravel()
+
+
+def random_ellipsoids(grid: int, count: int, seed: int) -> np.ndarray:
+    """3D phantom: ``count`` additive random ellipsoids (same recipe in 3D)."""
+    g = _rng(seed)
+    centers = -1.0 + (np.arange(grid) + 0.5) * (2.0 / grid)
+    zz, yy, xx = np.meshgrid(centers, centers, centers, indexing="ij")
+    vol = np.zeros((grid, grid, grid))
+    for _ in range(count):
+        c0 = g.uniform(-1.0, 1.0, 3)
+        semi = g.uniform(0.05, 0.4, 3) * 2.0
+        val = g.uniform(0.1, 1.0)
+        q, _ = np.linalg.qr(g.standard_normal((3, 3)))
+        pts = np.stack([xx - c0[0], yy - c0[1], zz - c0[2]], axis=-1) @ q
+        inside = ((pts / semi) ** 2).sum(axis=-1) <= 1.0
+        vol[inside] += val
+    return vol.ravel()
+
+
+@dataclass
+class TomoProblem:
+    op: SparseBlockOperator
+    b: np.ndarray
+    x_true: np.ndarray
+
+
+def _finish_tomo(parts, x_true, noise, seed, dtype):
+    blocks = [(ip, ix, d.astype(dtype), shp) for ip, ix, d, shp in parts]
+    # clean data from the stored (possibly fp32-rounded) values, fp64 math
+    clean = np.concatenate([
+        _csr_matvec(ip, ix, d.astype(np.float64), x_true) for ip, ix, d, _ in blocks])
+    b = scaled_noise(clean, noise, _rng(seed + 1))
+    op = SparseBlockOperator(blocks, b, dtype=dtype)
+    return TomoProblem(op, b, x_true)
+
+
+def _csr_matvec(indptr, indices, data, x):
+    import scipy.sparse as sp
+
+    n = x.shape[0]
+    return sp.csr_matrix((data, indices, indptr), shape=(indptr.shape[0] - 1, n)) @ x
+
+
+def tomo2d(grid=256, n_views=180, rays=362, ellipses=10, seed=2, noise=0.01,
+           dtype=np.float64, threads=None) -> TomoProblem:
+    """configs[1] / configs[2]: one block per view, ell = rays."""
+    angles = angles_0_pi(n_views)
+    parts = _pmap(lambda a: siddon2d_block(a, grid, rays), list(angles), threads)
+    x_true = random_ellipses(grid, ellipses, seed)
+    return _finish_tomo(parts, x_true, noise, seed, dtype)
+
+
+def tomo3d(grid=128, n_views=180, side=128, sub_rows=2048, ellipsoids=20, seed=4,
+           noise=0.01, dtype=np.float32, threads=None) -> TomoProblem:
+    """configs[3]: directions in the xy-plane over [0, pi); each view's
+    side^2 rays split into side^2 / sub_rows contiguous blocks after a
+    seeded per-view row permutation (uniform partition, linops.py:64-72)."""
+    theta = np.arange(n_views) * (np.pi / n_views)
+    dirs = np.stack([np.cos(theta), np.sin(theta), np.zeros_like(theta)], axis=1)
+    parts = _pmap(lambda d: siddon3d_block(d, grid, side), list(dirs), threads)
+    rows = side * side
+    if rows % sub_rows:
+        raise ValueError("detector rows must split evenly into sub-blocks")
+    g = _rng(seed + 7)
+    blocks = []
+    for ip, ix, d, (nr, nc) in parts:
+        perm = g.permutation(nr)
+        counts = np.diff(ip)[perm]
+        starts = ip[:-1][perm]
+        for s in range(0, nr, sub_rows):
+            sel_c = counts[s:s + sub_rows]
+            sel_s = starts[s:s + sub_rows]
+            nip = np.zeros(sub_rows + 1, dtype=np.int64)
+            np.cumsum(sel_c, out=nip[1:])
+            gather = np.concatenate([np.arange(a, a + c) for a, c in zip(sel_s, sel_c)]) \
+                if sel_c.sum() else np.zeros(0, dtype=np.int64)
+            blocks.append((nip, ix[gather], d[gather], (sub_rows, nc)))
+    x_true = random_ellipsoids(grid, ellipsoids, seed)
+    return _finish_tomo(blocks, x_true, noise, seed, dtype)

@@ -1,0 +1,237 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference's
+golden vectors and the CPU oracle on the same seeded inputs.
+
+Tolerances (north_star): fp64 iterates within 1e-10 relative, fp32-matrix
+configs within 1e-4 relative after K steps.
+"""
+
+import numpy as np
+import pytest
+
+from tests import golden_cases as gc
+
+pytestmark = pytest.mark.gpu
+
+RTOL64 = 1e-10
+
+
+@pytest.fixture(scope="module")
+def slim():
+    import paper_1912_07962_b200 as slim
+    from paper_1912_07962_b200 import _lib
+    _lib.lib()  # fail loudly if the extension is missing
+    return slim
+
+
+def _run_dense_case(slim, c, **kw):
+    op = slim.DenseBlockOperator(c["A"], int(c["ell"]), c["b"])
+    scheme = str(c["scheme"])
+    if kw.pop("single_pass", False):
+        op = slim.SinglePassAdapter(op)
+    kind = str(c["sched_kind"])
+    ramp = int(c["sched_ramp"])
+    sched = slim.Schedule(kind, float(c["sched_alpha"]), None if ramp < 0 else ramp,
+                          float(c["sched_decay"]))
+    return slim.run("slimls", op, slim.Sampler(scheme, op.n_blocks, int(c["seed"])), sched,
+                    epochs=float(c["epochs"]), r=int(c["r"]), x0=c.get("x0"),
+                    references=c["refs"], record_every=int(c["record_every"]),
+                    store_iterates="iterates" in c, **kw)
+
+
+def _assert_traj(traj, c, rtol=RTOL64):
+    assert np.array_equal(traj.ks, c["ks"])
+    assert traj.status == str(c["status"])
+    assert (traj.diverged_at or -1) == int(c["diverged_at"])
+    assert traj.row_status == list(c["row_status"])
+    np.testing.assert_array_equal(traj.epoch_fraction, c["epoch_fraction"])
+    np.testing.assert_array_equal(traj.alphas, c["alphas"])
+    scale = max(1.0, float(np.abs(c["x_final"]).max()))
+    np.testing.assert_allclose(traj.x_final, c["x_final"], rtol=rtol, atol=rtol * 1e-2 * scale)
+    np.testing.assert_allclose(traj.residual_norms, c["residual_norms"], rtol=rtol, equal_nan=True)
+    for name, vals in c["rel"].items():
+        np.testing.assert_allclose(traj.rel_errors[name], vals, rtol=rtol)
+    assert np.all(np.diff(np.cumsum(traj.wall_times)) >= 0)
+
+
+@pytest.mark.parametrize("name", gc.DENSE_CASES)
+def test_dense_runs_match_reference(slim, name):
+    c = gc.dense_case(name)
+    traj = _run_dense_case(slim, c, single_pass=(name == "single_pass"))
+    _assert_traj(traj, c)
+    if "iterates" in c:
+        np.testing.assert_allclose(np.asarray(traj.iterates), c["iterates"], rtol=RTOL64,
+                                   atol=1e-12)
+
+
+@pytest.mark.parametrize("name", ["tomo2d", "tomo3d"])
+def test_tomo_runs_match_reference(slim, name):
+    c = gc.tomo_case(name)
+    op = slim.SparseBlockOperator(c["blocks"], c["b"])
+    k = len(c["indices"])
+    scheme = "random_cyclic" if name == "tomo2d" else "uniform_iid"
+    seed = 7 if name == "tomo2d" else 3
+    traj = slim.run("slimls", op, slim.Sampler(scheme, op.n_blocks, seed),
+                    slim.Schedule("constant", float(c["alpha"])),
+                    epochs=k / op.n_blocks, r=int(c["r"]), references={"x_true": c["x_true"]})
+    np.testing.assert_allclose(traj.x_final, c["x_final"], rtol=RTOL64,
+                               atol=RTOL64 * np.abs(c["x_final"]).max())
+    np.testing.assert_allclose(traj.rel_errors["x_true"], c["rel"]["x_true"], rtol=RTOL64)
+    np.testing.assert_allclose(traj.residual_norms, c["residual_norms"], rtol=RTOL64,
+                               equal_nan=True)
+
+
+def test_dual_step_seam_matches_reference(slim):
+    d = gc.load("dual_step.npz")
+    for q in range(4):
+        m = d[f"{q}/M"]
+        ell = int(d[f"{q}/ell"])
+        blocks = [m[i:i + ell] for i in range(0, m.shape[0], ell)]
+        s = slim.dual_step(blocks, d[f"{q}/residual"], float(d[f"{q}/alpha"]))
+        np.testing.assert_allclose(s, d[f"{q}/s"], rtol=1e-10, atol=1e-13)
+
+
+@pytest.mark.parametrize("n", [1, 5, 63, 64, 65, 130, 257, 600, 1000])
+def test_potrf_matches_numpy(slim, n):
+    rng = np.random.default_rng(n)
+    a = rng.standard_normal((n, n + 3))
+    g = a @ a.T + n * np.eye(n)
+    L = slim.potrf(g)
+    ref = np.linalg.cholesky(g)
+    np.testing.assert_allclose(L, ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
+
+
+def test_potrf_rejects_indefinite(slim):
+    g = np.eye(70)
+    g[40, 40] = -1.0
+    with pytest.raises(np.linalg.LinAlgError):
+        slim.potrf(g)
+
+
+def test_same_seed_bit_identical(slim):
+    c = gc.dense_case("dense_dual")
+    t1 = _run_dense_case(slim, c)
+    t2 = _run_dense_case(slim, c)
+    assert np.array_equal(t1.x_final, t2.x_final)
+    for name in t1.rel_errors:
+        assert np.array_equal(t1.rel_errors[name], t2.rel_errors[name])
+    assert np.array_equal(t1.residual_norms, t2.residual_norms, equal_nan=True)
+
+
+def test_errors_map_to_reference_exceptions(slim):
+    c = gc.dense_case("ramp")
+    op = slim.DenseBlockOperator(c["A"], 6, c["b"])
+    smp = slim.Sampler("cyclic", op.n_blocks, 0)
+    with pytest.raises(ValueError, match="unknown method"):
+        slim.run("nope", op, smp, slim.Schedule(), epochs=1)
+    with pytest.raises(ValueError, match="epochs"):
+        slim.run("slimls", op, smp, slim.Schedule(), epochs=-1)
+    with pytest.raises(ValueError, match="record_every"):
+        slim.run("slimls", op, smp, slim.Schedule(), epochs=1, record_every=0)
+    with pytest.raises(ValueError, match="memory level"):
+        slim.run("slimls", op, smp, slim.Schedule(), epochs=1, r=-1)
+    with pytest.raises(ValueError, match="not on the B200"):
+        slim.run("sg", op, smp, slim.Schedule(), epochs=1)
+    sp = slim.SinglePassAdapter(op)
+    with pytest.raises(ValueError, match="cyclic"):
+        slim.run("slimls", sp, slim.Sampler("uniform_iid", op.n_blocks, 0), slim.Schedule(),
+                 epochs=1)
+    with pytest.raises(ValueError, match="one epoch"):
+        slim.run("slimls", sp, slim.Sampler("cyclic", op.n_blocks, 0), slim.Schedule(), epochs=2)
+    # a consumed single-pass stream cannot be replayed
+    slim.run("slimls", sp, slim.Sampler("cyclic", op.n_blocks, 0), slim.Schedule(), epochs=1)
+    with pytest.raises(slim.StreamOrderError):
+        slim.run("slimls", sp, slim.Sampler("cyclic", op.n_blocks, 0), slim.Schedule(), epochs=1)
+
+
+def test_specialisations(slim):
+    """damped_block_kaczmarz == slimls(r=0); slimtik(lam=0) == slimls (bitwise)."""
+    c = gc.dense_case("r0")
+    op = slim.DenseBlockOperator(c["A"], 6, c["b"])
+    kw = dict(epochs=2, references={"x_true": np.ones(40)})
+    base = slim.run("slimls", op, slim.Sampler("random_cyclic", 15, 3),
+                    slim.Schedule("constant", 2.0), r=0, **kw)
+    dbk = slim.run("damped_block_kaczmarz", op, slim.Sampler("random_cyclic", 15, 3),
+                   slim.Schedule("constant", 2.0), r=0, **kw)
+    assert np.array_equal(base.x_final, dbk.x_final)
+    t1 = slim.run("slimls", op, slim.Sampler("random_cyclic", 15, 3),
+                  slim.Schedule("constant", 2.0), r=2, **kw)
+    t2 = slim.run("slimtik", op, slim.Sampler("random_cyclic", 15, 3),
+                  slim.Schedule("constant", 2.0), r=2, lam=0.0, **kw)
+    assert np.array_equal(t1.x_final, t2.x_final)
+
+
+# ---------------------------------------------------------------------------
+# against the CPU oracle on BASELINE-shaped inputs (reduced where the oracle
+# would take minutes)
+# ---------------------------------------------------------------------------
+
+
+def _oracle_run(op_dense_fetch, nb, n, idx, alpha, r, refs, record_every=1):
+    from oracle import slimls_oracle as orc
+    return orc.run_slimls(op_dense_fetch, nb, n, idx, np.full(len(idx), alpha), r=r,
+                          references=refs, record_every=record_every)
+
+
+def test_config1_vs_oracle(slim):
+    """configs[0] at full size, 300 steps (window full from step 6)."""
+    from oracle import slimls_oracle as orc
+    from paper_1912_07962_b200 import problems
+    op, b, xt = problems.gaussian_dense()
+    K = 300
+    traj = slim.run("slimls", op, slim.Sampler("random_cyclic", 200, 7962),
+                    slim.Schedule("constant", 100.0), epochs=K / 200, r=5,
+                    references={"x_true": xt}, record_every=10)
+    idx = orc.sampler_indices("random_cyclic", 200, 7962, K)
+    ref = _oracle_run(orc.dense_fetch(op.matrix, b, 100), 200, 1000, idx, 100.0, 5,
+                      {"x_true": xt}, record_every=10)
+    np.testing.assert_allclose(traj.x_final, ref.x_final, rtol=RTOL64,
+                               atol=RTOL64 * np.abs(ref.x_final).max())
+    np.testing.assert_allclose(traj.rel_errors["x_true"], ref.rel_errors["x_true"], rtol=RTOL64)
+    np.testing.assert_allclose(traj.residual_norms, ref.residual_norms, rtol=RTOL64,
+                               equal_nan=True)
+
+
+def _tomo_vs_oracle(slim, prob, K, r, alpha, seed, rtol):
+    from oracle import slimls_oracle as orc
+    op = prob.op
+    traj = slim.run("slimls", op, slim.Sampler("random_cyclic", op.n_blocks, seed),
+                    slim.Schedule("constant", alpha), epochs=K / op.n_blocks, r=r,
+                    references={"x_true": prob.x_true})
+    idx = orc.sampler_indices("random_cyclic", op.n_blocks, seed, K)
+    fetch = orc.csr_fetch([op.csr_block(i) for i in range(1, op.n_blocks + 1)], prob.b)
+    ref = _oracle_run(fetch, op.n_blocks, op.n_cols, idx, alpha, r, {"x_true": prob.x_true})
+    err = np.linalg.norm(traj.x_final - ref.x_final) / np.linalg.norm(ref.x_final)
+    assert err <= rtol, err
+    np.testing.assert_allclose(traj.rel_errors["x_true"], ref.rel_errors["x_true"], rtol=rtol)
+    np.testing.assert_allclose(traj.residual_norms, ref.residual_norms, rtol=rtol, equal_nan=True)
+
+
+def test_config2_reduced_vs_oracle(slim):
+    """configs[1] geometry at 64^2 (n = 4096, 45 views x 90 rays), r = 10,
+    lambda = 1e-3: eviction exercised, kappa ~ 1e6 dual system."""
+    from paper_1912_07962_b200 import problems
+    prob = problems.tomo2d(grid=64, n_views=45, rays=90, seed=2)
+    _tomo_vs_oracle(slim, prob, K=30, r=10, alpha=1000.0, seed=11, rtol=RTOL64)
+
+
+def test_fp32_tomo_reduced_vs_oracle(slim):
+    """configs[2] style: fp32 values / int32 indices, fp64 accumulation (1e-4 bar;
+    the oracle sees the same fp32-rounded values)."""
+    from paper_1912_07962_b200 import problems
+    prob = problems.tomo2d(grid=48, n_views=40, rays=68, seed=5, dtype=np.float32)
+    _tomo_vs_oracle(slim, prob, K=25, r=8, alpha=1000.0, seed=3, rtol=1e-4)
+
+
+def test_block_residual(slim):
+    from paper_1912_07962_b200 import problems
+    from paper_1912_07962_b200.linops import device_operator
+    from paper_1912_07962_b200 import _lib
+    prob = problems.tomo2d(grid=32, n_views=10, rays=46, seed=9)
+    dop = device_operator(prob.op, 2)
+    x = np.random.default_rng(0).standard_normal(prob.op.n_cols)
+    r = np.empty(46)
+    nrm = np.zeros(1)
+    dop.call("slim_block_residual", 4, _lib.dptr(x), _lib.dptr(r), _lib.dptr(nrm))
+    blk = prob.op.fetch_block(4)
+    ref = blk.a_block @ x - blk.b_block
+    np.testing.assert_allclose(r, ref, rtol=1e-12, atol=1e-12)
