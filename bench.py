@@ -225,7 +225,7 @@ def run_ours(args, world, rank, local, dist):
                 "avg_launch_ms": chol_ms, "launches": timing["cholesky_count"]}
     # ---- e2e through the public API, host-resident fresh operator ----
     e2e = None
-    if rank == 0 or world > 1:
+    if not args.quick:
         op2 = slim.SparseBlockOperator([op.csr_block(i) for i in range(1, M + 1)], b)
         h2d = sum(p[0].nbytes + p[1].nbytes + p[2].nbytes for p in op2._parts) + b.nbytes \
             + 2 * xt.nbytes + total * 16
@@ -244,7 +244,7 @@ def run_ours(args, world, rank, local, dist):
         assert tr2.status == "ok"
     if rank != 0:
         return
-    cb = cpu_sample(prob, r, alpha, CFG["sampler_seed"]) if world == 1 else None
+    cb = cpu_sample(prob, r, alpha, CFG["sampler_seed"]) if world == 1 and not args.quick else None
     line = {"metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_win / args.steps,
             "higher_is_better": True, "scaling": "weak" if world > 1 else "weak",
@@ -266,6 +266,8 @@ def main():
     ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--quick", action="store_true",
+                    help="skip the CPU baseline and the e2e leg (profiling runs)")
     args = ap.parse_args()
     world, rank, local, dist = _dist()
     if args.impl == "reference":
