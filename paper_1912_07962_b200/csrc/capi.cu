@@ -29,7 +29,7 @@ using namespace slim;
 
 namespace {
 
-constexpr int D_FACT = 2;     // factorizations in flight
+constexpr int D_FACT = 3;     // factorizations in flight
 constexpr int NEV = 16;       // event ring per kind
 
 struct ProfPair {
@@ -74,6 +74,7 @@ struct slim_ctx {
   double* panels = nullptr;
   int64_t panel_stride = 0;
   double* Lbuf[D_FACT] = {};
+  double* Dinv[D_FACT] = {};
   int* cflags[D_FACT] = {};
   int* tickets = nullptr;  // D_FACT chol tickets + 1 trsv ticket
   int* tflags = nullptr;
@@ -162,6 +163,7 @@ static void free_all(slim_ctx* c) {
     if (c->refs[q]) cudaFree(c->refs[q]);
   for (int q = 0; q < D_FACT; ++q) {
     if (c->Lbuf[q]) cudaFree(c->Lbuf[q]);
+    if (c->Dinv[q]) cudaFree(c->Dinv[q]);
     if (c->cflags[q]) cudaFree(c->cflags[q]);
     if (c->sf[q]) cudaStreamDestroy(c->sf[q]);
   }
@@ -241,6 +243,7 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
   ALLOC(c, c->panels, sizeof(double) * (size_t)c->S * c->panel_stride);
   for (int q = 0; q < D_FACT; ++q) {
     ALLOC(c, c->Lbuf[q], sizeof(double) * (size_t)ntiles * TB * TB);
+    ALLOC(c, c->Dinv[q], sizeof(double) * (size_t)c->Tmax * 512);
     ALLOC(c, c->cflags[q], sizeof(int) * ntiles);
     CK(c, cudaMemset(c->cflags[q], 0, sizeof(int) * ntiles));
   }
@@ -568,6 +571,7 @@ static int enqueue_x_chain(slim_ctx* c, const Window& W, int64_t k, int d, doubl
   // trsv
   TrsvParams T{};
   T.L = c->Lbuf[d];
+  T.Dinv = c->Dinv[d];
   T.flags = c->tflags;
   T.ticket = c->tickets + D_FACT;
   T.epoch = epoch;
@@ -648,6 +652,7 @@ static int enqueue_chol(slim_ctx* c, const Window& W, int d, double alpha, int e
   const int N = W.nw * (int)c->ell;
   CholParams P{};
   P.L = c->Lbuf[d];
+  P.Dinv = c->Dinv[d];
   P.flags = c->cflags[d];
   P.ticket = c->tickets + d;
   P.error = c->errflag;
@@ -922,6 +927,7 @@ extern "C" int slim_dual_step(int32_t device, const double* Mh, int64_t rows, in
   const int N = (int)rows;
   TrsvParams T{};
   T.L = c->Lbuf[0];
+  T.Dinv = c->Dinv[0];
   T.flags = c->tflags;
   T.ticket = c->tickets + D_FACT;
   T.epoch = 1;
@@ -952,17 +958,19 @@ extern "C" int slim_potrf(int32_t device, const double* G, int64_t N, double* L_
   if (cudaSetDevice(device) != cudaSuccess) FAIL((slim_ctx*)nullptr, SLIM_ECUDA, "cudaSetDevice");
   const int T = (int)((N + TB - 1) / TB);
   const int64_t ntiles = (int64_t)T * (T + 1) / 2;
-  double *dG = nullptr, *dL = nullptr;
+  double *dG = nullptr, *dL = nullptr, *dD = nullptr;
   int *flags = nullptr, *ticket = nullptr, *err = nullptr;
   auto cleanup = [&]() {
     cudaFree(dG);
     cudaFree(dL);
+    cudaFree(dD);
     cudaFree(flags);
     cudaFree(ticket);
     cudaFree(err);
   };
   if (cudaMalloc(&dG, sizeof(double) * N * N) != cudaSuccess ||
       cudaMalloc(&dL, sizeof(double) * ntiles * TB * TB) != cudaSuccess ||
+      cudaMalloc(&dD, sizeof(double) * T * 512) != cudaSuccess ||
       cudaMalloc(&flags, sizeof(int) * ntiles) != cudaSuccess ||
       cudaMalloc(&ticket, sizeof(int)) != cudaSuccess || cudaMalloc(&err, sizeof(int)) != cudaSuccess) {
     cleanup();
@@ -974,6 +982,7 @@ extern "C" int slim_potrf(int32_t device, const double* G, int64_t N, double* L_
   cudaMemset(err, 0, sizeof(int));
   CholParams P{};
   P.L = dL;
+  P.Dinv = dD;
   P.flags = flags;
   P.ticket = ticket;
   P.error = err;

@@ -31,13 +31,11 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
-// spin until *p >= want (epoch-valued flags; one thread spins, CTA then syncs)
+// spin until *p >= want (epoch-valued flags; one thread spins, CTA then
+// syncs).  Tight spin: the producer is resident and the flag sits in L2,
+// so any sleep only adds latency to the factorization's critical path.
 __device__ __forceinline__ void wait_flag(const int* p, int want) {
-  if (ld_acquire(p) >= want) return;
-  unsigned ns = 32;
   while (ld_acquire(p) < want) {
-    __nanosleep(ns);
-    if (ns < 512) ns <<= 1;
   }
 }
 

@@ -21,6 +21,7 @@ struct Ctl {
 
 struct CholParams {
   double* L;            // lower tiles, tile_off(i, j)
+  double* Dinv;         // T x 512: inverses of the 8x8 diagonal blocks of L_jj
   int* flags;           // T (T + 1) / 2 epoch flags
   int* ticket;          // zeroed before each launch
   int* error;           // set to 1 on a non-positive pivot
@@ -39,6 +40,7 @@ struct CholParams {
 
 struct TrsvParams {
   const double* L;
+  const double* Dinv;
   int* flags;        // 2 T epoch flags (forward, backward)
   int* ticket;
   int epoch;
