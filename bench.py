@@ -100,6 +100,7 @@ class ClockSampler:
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.QUERY}",
                  "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.5)  # let nvidia-smi attach before the timed region starts
         except OSError:
             self.proc = None
         return self
@@ -193,7 +194,8 @@ def run_ours(args, world, rank, local, dist):
     op, b, xt = prob.op, prob.b, prob.x_true
     r, alpha = CFG["r"], CFG["alpha"]
     seed = CFG["sampler_seed"] + rank
-    wprime = max(args.warmup, r + 1)
+    D = int(os.environ.get("SLIM_BATCH", "4"))
+    wprime = -(-max(args.warmup, r + 1) // D) * D  # whole factorization batches
     total = wprime + args.steps
     M = op.n_blocks
     # upload + kernel warm-up (untimed)
@@ -211,14 +213,16 @@ def run_ours(args, world, rank, local, dist):
     value = world * args.steps / t_win
     # ---- roofline of the dominant kernel (tile Cholesky), per launch ----
     N = (r + 1) * CFG["rays"]
-    flops_chol = N ** 3 / 3.0
+    per_launch = args.steps / max(1, timing["cholesky_count"])  # systems per batched launch
+    flops_chol = per_launch * N ** 3 / 3.0
     chol_ms = timing["cholesky_ms"] / max(1, timing["cholesky_count"])
     achieved = flops_chol / (chol_ms * 1e-3) / 1e12
-    agg = flops_chol * args.steps / (timing["window_ms"] * 1e-3) / 1e12
+    agg = (N ** 3 / 3.0) * args.steps / (timing["window_ms"] * 1e-3) / 1e12
     roofline = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
                 "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
-                "kernel": "k_chol_tiles (fp64 DMMA tile-DAG Cholesky, N=3982)",
-                "algorithmic_per_launch": f"N^3/3 = {flops_chol:.4g} flop",
+                "kernel": f"k_chol_tiles (fp64 DMMA tile-DAG Cholesky, {per_launch:g} systems "
+                          f"of N=3982 interleaved per launch)",
+                "algorithmic_per_launch": f"{per_launch:g} x N^3/3 = {flops_chol:.4g} flop",
                 "peak_source": "FP64 DMMA peak measured on this pool (tools/microbench/fp64_rates.cu)",
                 "aggregate_tflops_over_window": agg,
                 "aggregate_frac": agg / FP64_PEAK_TFLOPS,

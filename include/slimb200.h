@@ -134,6 +134,10 @@ int slim_dual_step(int32_t device, const double* M, int64_t rows, int64_t n,
                    const double* residual, int64_t ell, double alpha, double* s_out);
 /* fp64 Cholesky of an SPD matrix (lower), N x N row-major in/out.       */
 int slim_potrf(int32_t device, const double* G, int64_t N, double* L_out);
+/* debug variant: per-tile globaltimer trace (4 stamps per ticket: start,
+ * accumulation done, dependency ready, published) and the event time     */
+int slim_potrf_traced(int32_t device, const double* G, int64_t N, double* L_out,
+                      unsigned long long* trace_out, double* ms_out);
 /* residual r = A_k x - b_k of one block and its norm (solvers.py:180)   */
 int slim_block_residual(slim_ctx* ctx, int64_t block, const double* x, double* r_out,
                         double* norm_out);

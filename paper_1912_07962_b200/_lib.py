@@ -27,7 +27,7 @@ EXPORTS = (
     "slim_upload_dense", "slim_upload_csr_block", "slim_upload_csr", "slim_finalize_operator",
     "slim_set_rhs", "slim_set_x", "slim_get_x", "slim_set_references",
     "slim_set_divergence_limit", "slim_run", "slim_set_host_streaming", "slim_comm_init",
-    "slim_dual_step", "slim_potrf", "slim_block_residual", "slim_timing", "slim_set_profiling", "slim_set_timing_start",
+    "slim_dual_step", "slim_potrf", "slim_potrf_traced", "slim_block_residual", "slim_timing", "slim_set_profiling", "slim_set_timing_start",
     "slim_siddon2d_view", "slim_siddon3d_view",
 )
 
@@ -68,6 +68,7 @@ _SIGS = {
     "slim_comm_init": (C.c_int, [_P, _P, _I32, _I32]),
     "slim_dual_step": (C.c_int, [_I32, _DP, _I64, _I64, _DP, _I64, _D, _DP]),
     "slim_potrf": (C.c_int, [_I32, _DP, _I64, _DP]),
+    "slim_potrf_traced": (C.c_int, [_I32, _DP, _I64, _DP, C.POINTER(C.c_uint64), _DP]),
     "slim_block_residual": (C.c_int, [_P, _I64, _DP, _DP, _DP]),
     "slim_timing": (C.c_int, [_P, _I32, _DP, _I64P]),
     "slim_set_profiling": (C.c_int, [_P, _I32]),

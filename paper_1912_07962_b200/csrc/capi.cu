@@ -1,23 +1,27 @@
 // capi.cu -- C-ABI driver of the B200 slimLS hot path (include/slimb200.h).
 //
 // One slim_run() call executes the reference's hot loop (solvers.py:560-574)
-// for K precomputed block indices entirely on the device.  Per step k the
-// work is split over three kinds of streams:
+// for K precomputed block indices entirely on the device.  The work is split
+// over three streams:
 //
-//   sg      Gram panel of the newest block into the ring   (x-independent)
-//   sf[d]   tile Cholesky of G_k into factor buffer d       (x-independent)
-//   sx      residual -> triangular solves -> M^T w -> x update + history
+//   sg   Gram panel of each step's newest block into the ring (x-independent)
+//   sf   one batched tile-DAG Cholesky per D consecutive steps (x-independent)
+//   sx   per step: residual -> triangular solves -> M^T w -> x update + history
 //
-// G_k depends only on the sampled index sequence, so the factorizations
-// of consecutive steps run ahead of, and concurrently with, the x-chain
-// (D factor buffers in flight).  The ring keeps r + D Gram panels so a
-// panel is never overwritten while an in-flight factorization reads it.
+// G_k depends only on the sampled index sequence, so the factorizations of
+// D consecutive steps are interleaved in ONE launch (their critical paths
+// overlap instead of running back to back) and run ahead of the x-chain.
+// Factor buffers come in two sets of D (batch B+1 factors while the x-chain
+// consumes batch B); the ring keeps r + 2D Gram panels so no panel is
+// overwritten while a factorization that reads it may still be running.
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -29,8 +33,8 @@ using namespace slim;
 
 namespace {
 
-constexpr int D_FACT = 3;     // factorizations in flight
 constexpr int NEV = 16;       // event ring per kind
+constexpr int D_DEFAULT = 4;  // systems per batched factorization
 
 struct ProfPair {
   cudaEvent_t a, b;
@@ -73,10 +77,11 @@ struct slim_ctx {
   int S = 0, Tmax = 0;
   double* panels = nullptr;
   int64_t panel_stride = 0;
-  double* Lbuf[D_FACT] = {};
-  double* Dinv[D_FACT] = {};
-  int* cflags[D_FACT] = {};
-  int* tickets = nullptr;  // D_FACT chol tickets + 1 trsv ticket
+  int D = D_DEFAULT;                 // batch size
+  std::vector<double*> Lbuf, Dinv;   // 2 D factor buffers
+  std::vector<int*> cflags;
+  int* tickets = nullptr;  // [0] chol ticket, [1] trsv ticket
+  std::map<std::vector<int>, int2*> maps;  // cached task maps by batch shape
   int* tflags = nullptr;
   int* errflag = nullptr;
   double* rvec = nullptr;
@@ -92,7 +97,7 @@ struct slim_ctx {
   double* iters_dev = nullptr;
   int64_t iters_cap = 0;
   int64_t epoch_base = 0;
-  cudaStream_t sx = nullptr, sg = nullptr, sf[D_FACT] = {};
+  cudaStream_t sx = nullptr, sg = nullptr, sf = nullptr;
   cudaEvent_t ev_g[NEV], ev_f[NEV], ev_x[NEV];
   int64_t* pin_div = nullptr;
   // profiling
@@ -161,12 +166,11 @@ static void free_all(slim_ctx* c) {
     if (p) cudaFree(p);
   for (int q = 0; q < MAX_REFS; ++q)
     if (c->refs[q]) cudaFree(c->refs[q]);
-  for (int q = 0; q < D_FACT; ++q) {
-    if (c->Lbuf[q]) cudaFree(c->Lbuf[q]);
-    if (c->Dinv[q]) cudaFree(c->Dinv[q]);
-    if (c->cflags[q]) cudaFree(c->cflags[q]);
-    if (c->sf[q]) cudaStreamDestroy(c->sf[q]);
-  }
+  for (double* p : c->Lbuf) cudaFree(p);
+  for (double* p : c->Dinv) cudaFree(p);
+  for (int* p : c->cflags) cudaFree(p);
+  for (auto& kv : c->maps) cudaFree(kv.second);
+  if (c->sf) cudaStreamDestroy(c->sf);
   if (c->sx) cudaStreamDestroy(c->sx);
   if (c->sg) cudaStreamDestroy(c->sg);
   for (int q = 0; q < NEV; ++q) {
@@ -219,7 +223,8 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
   CK(c, cudaSetDevice(c->dev));
   CK(c, cudaStreamCreateWithFlags(&c->sx, cudaStreamNonBlocking));
   CK(c, cudaStreamCreateWithFlags(&c->sg, cudaStreamNonBlocking));
-  for (int q = 0; q < D_FACT; ++q) CK(c, cudaStreamCreateWithFlags(&c->sf[q], cudaStreamNonBlocking));
+  CK(c, cudaStreamCreateWithFlags(&c->sf, cudaStreamNonBlocking));
+  if (const char* env = getenv("SLIM_BATCH")) c->D = std::max(1, std::min(MAX_BATCH, atoi(env)));
   for (int q = 0; q < NEV; ++q) {
     CK(c, cudaEventCreateWithFlags(&c->ev_g[q], cudaEventDisableTiming));
     CK(c, cudaEventCreateWithFlags(&c->ev_f[q], cudaEventDisableTiming));
@@ -231,7 +236,7 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
   *c->pin_div = 0;
 
   const int64_t ell = c->ell, W = c->r + 1;
-  c->S = (int)(W + D_FACT - 1);
+  c->S = (int)(c->r + 2 * c->D);
   c->panel_stride = (int64_t)c->S * ell * ell;
   const int64_t Nmax = W * ell;
   c->Tmax = (int)((Nmax + TB - 1) / TB);
@@ -241,13 +246,16 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
   ALLOC(c, c->b, sizeof(double) * c->m);
   ALLOC(c, c->ctl, sizeof(Ctl));
   ALLOC(c, c->panels, sizeof(double) * (size_t)c->S * c->panel_stride);
-  for (int q = 0; q < D_FACT; ++q) {
+  c->Lbuf.assign(2 * c->D, nullptr);
+  c->Dinv.assign(2 * c->D, nullptr);
+  c->cflags.assign(2 * c->D, nullptr);
+  for (int q = 0; q < 2 * c->D; ++q) {
     ALLOC(c, c->Lbuf[q], sizeof(double) * (size_t)ntiles * TB * TB);
     ALLOC(c, c->Dinv[q], sizeof(double) * (size_t)c->Tmax * 512);
     ALLOC(c, c->cflags[q], sizeof(int) * ntiles);
     CK(c, cudaMemset(c->cflags[q], 0, sizeof(int) * ntiles));
   }
-  ALLOC(c, c->tickets, sizeof(int) * (D_FACT + 1));
+  ALLOC(c, c->tickets, sizeof(int) * 2);
   ALLOC(c, c->tflags, sizeof(int) * 2 * c->Tmax);
   CK(c, cudaMemset(c->tflags, 0, sizeof(int) * 2 * c->Tmax));
   ALLOC(c, c->errflag, sizeof(int));
@@ -573,7 +581,7 @@ static int enqueue_x_chain(slim_ctx* c, const Window& W, int64_t k, int d, doubl
   T.L = c->Lbuf[d];
   T.Dinv = c->Dinv[d];
   T.flags = c->tflags;
-  T.ticket = c->tickets + D_FACT;
+  T.ticket = c->tickets + 1;
   T.epoch = epoch;
   T.N = N;
   T.T = (N + TB - 1) / TB;
@@ -648,28 +656,51 @@ static int enqueue_residual(slim_ctx* c, int64_t newblk) {
   return SLIM_OK;
 }
 
-static int enqueue_chol(slim_ctx* c, const Window& W, int d, double alpha, int epoch) {
-  const int N = W.nw * (int)c->ell;
+// device task map for a batch shape (cached)
+static int2* task_map(slim_ctx* c, const std::vector<int>& Ts, int* ntasks) {
+  auto it = c->maps.find(Ts);
+  std::vector<int2> h = chol_task_map(Ts.data(), (int)Ts.size());
+  *ntasks = (int)h.size();
+  if (it != c->maps.end()) return it->second;
+  int2* d = nullptr;
+  if (cudaMalloc(&d, sizeof(int2) * h.size()) != cudaSuccess) return nullptr;
+  cudaMemcpy(d, h.data(), sizeof(int2) * h.size(), cudaMemcpyHostToDevice);
+  c->maps[Ts] = d;
+  return d;
+}
+
+// one launch factors the systems of steps k0 .. k0 + nb - 1 into factor
+// buffer set `set` (buffers set * D + b)
+static int enqueue_chol_batch(slim_ctx* c, const Window* Ws, int nb, int set, const double* alphas,
+                              int64_t k0, int64_t epoch0) {
   CholParams P{};
-  P.L = c->Lbuf[d];
-  P.Dinv = c->Dinv[d];
-  P.flags = c->cflags[d];
-  P.ticket = c->tickets + d;
+  std::vector<int> Ts(nb);
+  for (int b = 0; b < nb; ++b) {
+    const int N = Ws[b].nw * (int)c->ell;
+    CholMat& M = P.m[b];
+    const int buf = set * c->D + b;
+    M.L = c->Lbuf[buf];
+    M.Dinv = c->Dinv[buf];
+    M.flags = c->cflags[buf];
+    M.N = N;
+    M.T = (N + TB - 1) / TB;
+    M.nw = Ws[b].nw;
+    M.epoch = (int)(epoch0 + k0 + b);
+    M.alpha = alphas[k0 + b - 1];
+    for (int q = 0; q < Ws[b].nw; ++q) M.slot[q] = Ws[b].slot[q];
+    Ts[b] = M.T;
+  }
+  P.nb = nb;
+  P.map = task_map(c, Ts, &P.ntasks);
+  if (!P.map) FAIL(c, SLIM_ENOMEM, "task map allocation failed");
+  P.ticket = c->tickets;
   P.error = c->errflag;
-  P.epoch = epoch;
-  P.N = N;
-  P.T = (N + TB - 1) / TB;
   P.panels = c->panels;
   P.panel_stride = c->panel_stride;
   P.ell = (int)c->ell;
   P.S = c->S;
-  P.nw = W.nw;
-  P.alpha = alpha;
-  for (int q = 0; q < W.nw; ++q) P.slot[q] = W.slot[q];
-  P.G = nullptr;
-  P.ldg = 0;
-  CK(c, cudaMemsetAsync(P.ticket, 0, sizeof(int), c->sf[d]));
-  launch_chol(P, c->sf[d]);
+  CK(c, cudaMemsetAsync(P.ticket, 0, sizeof(int), c->sf));
+  launch_chol(P, c->sf);
   c->launches += 1;
   CKLAUNCH(c);
   return SLIM_OK;
@@ -732,72 +763,77 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
   }
   int64_t rec_rows = 0;  // rows this run will have recorded (host view, for iterates)
   const int64_t epoch0 = c->epoch_base;
-  Window W{};
-  for (int64_t k = 1; k <= K; ++k) {
-    fill_window(c, idx, k, W);
-    const int d = (int)(k % D_FACT);
-    const int epoch = (int)(epoch0 + k);
-    const double alpha = alphas[k - 1];
-    // ---- Gram panel (sg): wait until no in-flight factorization reads the slot
-    for (int q = 0; q < D_FACT; ++q) {
-      const int64_t kk = k - D_FACT - q;
-      if (kk >= 1) CK(c, cudaStreamWaitEvent(c->sg, c->ev_f[kk % NEV], 0));
-    }
+  const int D = c->D;
+  std::vector<Window> Ws(D);
+  const int64_t nbatch = (K + D - 1) / D;
+  bool stop = false;
+  for (int64_t B = 0; B < nbatch && !stop; ++B) {
+    const int64_t kb0 = B * D + 1;
+    const int nb = (int)std::min<int64_t>(D, K - kb0 + 1);
+    const int set = (int)(B & 1);
+    for (int b = 0; b < nb; ++b) fill_window(c, idx, kb0 + b, Ws[b]);
+    // ---- Gram panels (sg): the ring slots they overwrite were last read by
+    // the factorization of batch B - 2
+    if (B >= 2) CK(c, cudaStreamWaitEvent(c->sg, c->ev_f[(B - 2) % NEV], 0));
     ProfPair pg{};
-    if (c->prof && k >= k0) pg = take(c->prof_gram, pgr), cudaEventRecord(pg.a, c->sg);
-    {
-      int rc = enqueue_gram(c, W, k);
+    const bool prof_b = c->prof && kb0 >= k0;
+    if (prof_b) pg = take(c->prof_gram, pgr), cudaEventRecord(pg.a, c->sg);
+    for (int b = 0; b < nb; ++b) {
+      int rc = enqueue_gram(c, Ws[b], kb0 + b);
       if (rc) return rc;
     }
-    if (c->prof && k >= k0) cudaEventRecord(pg.b, c->sg);
-    CK(c, cudaEventRecord(c->ev_g[k % NEV], c->sg));
-    // ---- factorization (sf[d])
-    CK(c, cudaStreamWaitEvent(c->sf[d], c->ev_g[k % NEV], 0));
-    if (k - D_FACT >= 1) CK(c, cudaStreamWaitEvent(c->sf[d], c->ev_x[(k - D_FACT) % NEV], 0));
+    if (prof_b) cudaEventRecord(pg.b, c->sg);
+    CK(c, cudaEventRecord(c->ev_g[B % NEV], c->sg));
+    // ---- batched factorization (sf): buffer set reused from batch B - 2
+    CK(c, cudaStreamWaitEvent(c->sf, c->ev_g[B % NEV], 0));
+    if (B >= 2) CK(c, cudaStreamWaitEvent(c->sf, c->ev_x[(B - 2) % NEV], 0));
     ProfPair pc{};
-    if (c->prof && k >= k0) pc = take(c->prof_chol, pch), cudaEventRecord(pc.a, c->sf[d]);
+    if (prof_b) pc = take(c->prof_chol, pch), cudaEventRecord(pc.a, c->sf);
     {
-      int rc = enqueue_chol(c, W, d, alpha, epoch);
+      int rc = enqueue_chol_batch(c, Ws.data(), nb, set, alphas, kb0, epoch0);
       if (rc) return rc;
     }
-    if (c->prof && k >= k0) cudaEventRecord(pc.b, c->sf[d]);
-    CK(c, cudaEventRecord(c->ev_f[k % NEV], c->sf[d]));
-    // ---- x-chain (sx)
-    ProfPair px{};
-    if (c->prof && k >= k0) px = take(c->prof_x, pxc), cudaEventRecord(px.a, c->sx);
-    {
-      int rc = enqueue_residual(c, W.blk[W.nw - 1]);
-      if (rc) return rc;
+    if (prof_b) cudaEventRecord(pc.b, c->sf);
+    CK(c, cudaEventRecord(c->ev_f[B % NEV], c->sf));
+    // ---- x-chain (sx), one step at a time
+    for (int b = 0; b < nb; ++b) {
+      const int64_t k = kb0 + b;
+      const Window& W = Ws[b];
+      const double alpha = alphas[k - 1];
+      ProfPair px{};
+      if (c->prof && k >= k0) px = take(c->prof_x, pxc), cudaEventRecord(px.a, c->sx);
+      {
+        int rc = enqueue_residual(c, W.blk[W.nw - 1]);
+        if (rc) return rc;
+      }
+      if (b == 0) CK(c, cudaStreamWaitEvent(c->sx, c->ev_f[B % NEV], 0));
+      const int record = (k % record_every == 0 || k == K) ? 1 : 0;
+      {
+        int rc = enqueue_x_chain(c, W, k, set * D + b, alpha, record, (int)(epoch0 + k));
+        if (rc) return rc;
+      }
+      if (c->prof && k >= k0) cudaEventRecord(px.b, c->sx);
+      if (iterates && record) {
+        CK(c, cudaMemcpyAsync(c->iters_dev + rec_rows * c->n, c->x, sizeof(double) * c->n,
+                              cudaMemcpyDeviceToDevice, c->sx));
+        ++rec_rows;
+      }
+      if (k + 1 == k0) {
+        CK(c, cudaEventRecord(c->run_a, c->sx));
+        launches_at_k0 = c->launches;
+        a_recorded = true;
+      }
     }
-    CK(c, cudaStreamWaitEvent(c->sx, c->ev_f[k % NEV], 0));
-    const int record = (k % record_every == 0 || k == K) ? 1 : 0;
-    {
-      int rc = enqueue_x_chain(c, W, k, d, alpha, record, epoch);
-      if (rc) return rc;
-    }
-    if (c->prof && k >= k0) cudaEventRecord(px.b, c->sx);
-    if (iterates && record) {
-      CK(c, cudaMemcpyAsync(c->iters_dev + rec_rows * c->n, c->x, sizeof(double) * c->n,
-                            cudaMemcpyDeviceToDevice, c->sx));
-      ++rec_rows;
-    }
-    CK(c, cudaEventRecord(c->ev_x[k % NEV], c->sx));
-    if (k + 1 == k0) {
-      CK(c, cudaEventRecord(c->run_a, c->sx));
-      launches_at_k0 = c->launches;
-      a_recorded = true;
-    }
+    CK(c, cudaEventRecord(c->ev_x[B % NEV], c->sx));
     // cheap divergence poll: stop enqueueing once the device reported it
-    if ((k & 31) == 0) {
-      if (*c->pin_div != 0) break;
+    if ((B & 7) == 7) {
+      if (*c->pin_div != 0) stop = true;
       CK(c, cudaMemcpyAsync(c->pin_div, &c->ctl->diverged_at, sizeof(int64_t),
                             cudaMemcpyDeviceToHost, c->sx));
     }
   }
-  for (int q = 0; q < D_FACT; ++q) {
-    CK(c, cudaEventRecord(c->ev_f[0], c->sf[q]));
-    CK(c, cudaStreamWaitEvent(c->sx, c->ev_f[0], 0));
-  }
+  CK(c, cudaEventRecord(c->ev_f[0], c->sf));
+  CK(c, cudaStreamWaitEvent(c->sx, c->ev_f[0], 0));
   if (!a_recorded) {
     CK(c, cudaEventRecord(c->run_a, c->sx));
     launches_at_k0 = c->launches;
@@ -917,8 +953,12 @@ extern "C" int slim_dual_step(int32_t device, const double* Mh, int64_t rows, in
     if ((rc = enqueue_gram(c, W, k))) return fail_out(rc);
   }
   if (cudaStreamSynchronize(c->sg) != cudaSuccess) return fail_out(SLIM_ECUDA);
-  if ((rc = enqueue_chol(c, W, 0, alpha, 1))) return fail_out(rc);
-  if (cudaStreamSynchronize(c->sf[0]) != cudaSuccess) return fail_out(SLIM_ECUDA);
+  {
+    std::vector<double> al(nb, alpha);
+    if ((rc = enqueue_chol_batch(c, &W, 1, 0, al.data(), nb, 1 - nb)))
+      return fail_out(rc);
+  }
+  if (cudaStreamSynchronize(c->sf) != cudaSuccess) return fail_out(SLIM_ECUDA);
   if (cudaMemcpy(c->rvec, residual, sizeof(double) * ell, cudaMemcpyHostToDevice) != cudaSuccess)
     return fail_out(SLIM_ECUDA);
   Ctl h{};
@@ -929,7 +969,7 @@ extern "C" int slim_dual_step(int32_t device, const double* Mh, int64_t rows, in
   T.L = c->Lbuf[0];
   T.Dinv = c->Dinv[0];
   T.flags = c->tflags;
-  T.ticket = c->tickets + D_FACT;
+  T.ticket = c->tickets + 1;
   T.epoch = 1;
   T.N = N;
   T.T = (N + TB - 1) / TB;
@@ -953,7 +993,20 @@ extern "C" int slim_dual_step(int32_t device, const double* Mh, int64_t rows, in
   return SLIM_OK;
 }
 
+static int potrf_impl(int32_t device, const double* G, int64_t N, double* L_out,
+                      unsigned long long* trace_out, double* ms_out);
+
 extern "C" int slim_potrf(int32_t device, const double* G, int64_t N, double* L_out) {
+  return potrf_impl(device, G, N, L_out, nullptr, nullptr);
+}
+
+extern "C" int slim_potrf_traced(int32_t device, const double* G, int64_t N, double* L_out,
+                                 unsigned long long* trace_out, double* ms_out) {
+  return potrf_impl(device, G, N, L_out, trace_out, ms_out);
+}
+
+static int potrf_impl(int32_t device, const double* G, int64_t N, double* L_out,
+                      unsigned long long* trace_out, double* ms_out) {
   if (!G || !L_out || N < 1) FAIL((slim_ctx*)nullptr, SLIM_EINVAL, "bad argument");
   if (cudaSetDevice(device) != cudaSuccess) FAIL((slim_ctx*)nullptr, SLIM_ECUDA, "cudaSetDevice");
   const int T = (int)((N + TB - 1) / TB);
@@ -981,19 +1034,55 @@ extern "C" int slim_potrf(int32_t device, const double* G, int64_t N, double* L_
   cudaMemset(ticket, 0, sizeof(int));
   cudaMemset(err, 0, sizeof(int));
   CholParams P{};
-  P.L = dL;
-  P.Dinv = dD;
-  P.flags = flags;
+  P.m[0].L = dL;
+  P.m[0].Dinv = dD;
+  P.m[0].flags = flags;
+  P.m[0].epoch = 1;
+  P.m[0].N = (int)N;
+  P.m[0].T = T;
+  P.m[0].alpha = 1.0;
+  P.nb = 1;
+  std::vector<int2> hmap = chol_task_map(&T, 1);
+  P.ntasks = (int)hmap.size();
+  int2* dmap = nullptr;
+  cudaMalloc(&dmap, sizeof(int2) * hmap.size());
+  cudaMemcpy(dmap, hmap.data(), sizeof(int2) * hmap.size(), cudaMemcpyHostToDevice);
+  P.map = dmap;
   P.ticket = ticket;
   P.error = err;
-  P.epoch = 1;
-  P.N = (int)N;
-  P.T = T;
   P.panels = nullptr;
   P.G = dG;
   P.ldg = N;
+  unsigned long long* dtr = nullptr;
+  if (trace_out) {
+    cudaMalloc(&dtr, sizeof(unsigned long long) * 4 * ntiles);
+    cudaMemset(dtr, 0, sizeof(unsigned long long) * 4 * ntiles);
+    // warm-up launch so the traced one does not include module load
+    launch_chol(P, 0);
+    cudaDeviceSynchronize();
+    cudaMemset(ticket, 0, sizeof(int));
+    P.m[0].epoch = 2;
+  }
+  P.trace = dtr;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, 0);
   launch_chol(P, 0);
+  cudaEventRecord(e1, 0);
   cudaError_t e = cudaDeviceSynchronize();
+  if (ms_out) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    *ms_out = ms;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (dtr) {
+    cudaMemcpy(trace_out, dtr, sizeof(unsigned long long) * 4 * ntiles, cudaMemcpyDeviceToHost);
+    cudaFree(dtr);
+  }
+  cudaFree(dmap);
   if (e != cudaSuccess) {
     cleanup();
     FAIL((slim_ctx*)nullptr, SLIM_ECUDA, "potrf kernel failed: %s", cudaGetErrorString(e));

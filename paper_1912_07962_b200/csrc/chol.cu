@@ -28,6 +28,8 @@
 // triangular solves of the x-chain reuse the same small inverses.  Only
 // 8x8 blocks are inverted, so the backward error stays that of a
 // substitution (the 8x8 blocks of a Cholesky factor are well conditioned).
+#include <vector>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -35,16 +37,16 @@ namespace slim {
 
 constexpr unsigned FULL = 0xffffffffu;
 
-__device__ __forceinline__ double chol_g_elem(const CholParams& P, int p, int q) {
+__device__ __forceinline__ double chol_g_elem(const CholParams& P, const CholMat& M, int p, int q) {
   // requires q <= p < N
   if (P.panels != nullptr) {
     const int pb = p / P.ell, a = p - pb * P.ell;
     const int qb = q / P.ell, c = q - qb * P.ell;
     // product A_P[a] . A_Q[c] was stored when block P (the newer) was pushed:
     // panel[slot(P)] row (slot(Q) * ell + c), column a
-    const double* pan = P.panels + (int64_t)P.slot[pb] * P.panel_stride;
-    const double v = pan[((int64_t)P.slot[qb] * P.ell + c) * P.ell + a];
-    return P.alpha * v + (p == q ? 1.0 : 0.0);
+    const double* pan = P.panels + (int64_t)M.slot[pb] * P.panel_stride;
+    const double v = pan[((int64_t)M.slot[qb] * P.ell + c) * P.ell + a];
+    return M.alpha * v + (p == q ? 1.0 : 0.0);
   }
   return P.G[(int64_t)p * P.ldg + q];
 }
@@ -72,16 +74,31 @@ __device__ __forceinline__ void store_tile(double* g, const double* s, int tid) 
   }
 }
 
+// fp64 1/sqrt(x): MUFU.RSQ64H seed + two Newton steps (~1 ulp), so the
+// pivot chain pays ~50 cycles per column instead of a sqrt and a divide
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = 0.5 * x;
+  double e = fma(-h * y, y, 0.5);
+  y = fma(y, e, y);
+  e = fma(-h * y, y, 0.5);
+  return fma(y, e, y);
+}
+
 // ---------------------------------------------------------------------------
 // POTRF of the 64x64 tile in S (lower part valid), plus the inverses of its
 // eight 8x8 diagonal blocks into Dv[q * 64 + i * 8 + k] (lower, row-major).
+// Panels of 8 columns: warp 0 factors the panel in registers; the lane that
+// owns the next pivot row computes that pivot's reciprocal square root
+// before the rest of the rank-1 update, so the serial chain per column is
+// one shuffle, one multiply, one FMA and one rsqrt.
 // ---------------------------------------------------------------------------
-__device__ void potrf_tile_blocked(double* S, double* Dv, int tid, int* error) {
+__device__ void potrf_tile_blocked(double* S, double* Dv, double* rdiag, int tid, int* error) {
   const int warp = tid >> 5, lane = tid & 31;
   for (int p = 0; p < 8; ++p) {
     const int c0 = 8 * p;
     if (warp == 0) {
-      // panel rows c0 .. 63: lane owns rows r0 = c0 + lane, r1 = r0 + 32
       const int r0 = c0 + lane, r1 = r0 + 32;
       double v0[8], v1[8];
 #pragma unroll
@@ -89,22 +106,31 @@ __device__ void potrf_tile_blocked(double* S, double* Dv, int tid, int* error) {
         v0[c] = (r0 < TB) ? S[r0 * TS + c0 + c] : 0.0;
         v1[c] = (r1 < TB) ? S[r1 * TS + c0 + c] : 0.0;
       }
-      bool bad = false;
+      bool bad = (lane == 0) && !(v0[0] > 0.0);
+      double myinv = rsqrt_nr(v0[0]);  // meaningful on lane 0 only
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
-        const double d = __shfl_sync(FULL, v0[c], c);
-        bad |= !(d > 0.0);
-        const double inv = rsqrt(d);
-        v0[c] = (lane > c) ? v0[c] * inv : ((lane == c) ? d * inv : 0.0);
-        v1[c] = v1[c] * inv;
+        const double inv = __shfl_sync(FULL, myinv, c);
+        const double l0 = v0[c] * inv, l1 = v1[c] * inv;
+        if (c < 7) {
+          // next pivot, on the lane that owns row c0 + c + 1
+          const double dn = fma(-l0, l0, v0[c + 1]);
+          if (lane == c + 1) {
+            bad |= !(dn > 0.0);
+            myinv = rsqrt_nr(dn);
+          }
+        }
 #pragma unroll
         for (int j = c + 1; j < 8; ++j) {
-          const double ljc = __shfl_sync(FULL, v0[c], j);
-          v0[j] -= v0[c] * ljc;
-          v1[j] -= v1[c] * ljc;
+          const double ljc = __shfl_sync(FULL, l0, j);
+          v0[j] = fma(-l0, ljc, v0[j]);
+          v1[j] = fma(-l1, ljc, v1[j]);
         }
+        v0[c] = l0;
+        v1[c] = l1;
+        if (lane == c) rdiag[c0 + c] = inv;
       }
-      if (lane == 0 && bad) atomicExch(error, 1);
+      if (__any_sync(FULL, bad) && lane == 0) atomicExch(error, 1);
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         if (r0 < TB) S[r0 * TS + c0 + c] = (lane >= c) ? v0[c] : 0.0;
@@ -135,10 +161,10 @@ __device__ void potrf_tile_blocked(double* S, double* Dv, int tid, int* error) {
     }
     __syncthreads();
   }
-  // zero the strict upper triangle outside the (already clean) panel writes
+  // zero the strict upper triangle of the off-diagonal 8x8 blocks
   for (int e = tid; e < TB * TB; e += 256) {
     const int r = e >> 6, c = e & 63;
-    if (c > r) S[r * TS + c] = 0.0;
+    if ((c >> 3) > (r >> 3)) S[r * TS + c] = 0.0;
   }
   // inverses of the diagonal 8x8 blocks: warp q, lane c < 8 solves column c
   if (lane < 8) {
@@ -150,7 +176,7 @@ __device__ void potrf_tile_blocked(double* S, double* Dv, int tid, int* error) {
       double s = (i == c) ? 1.0 : 0.0;
 #pragma unroll
       for (int k = 0; k < i; ++k) s -= L[i * TS + k] * x[k];
-      x[i] = s / L[i * TS + i];
+      x[i] = s * rdiag[8 * q + i];
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) Dv[q * 64 + i * 8 + c] = x[i];
@@ -159,9 +185,9 @@ __device__ void potrf_tile_blocked(double* S, double* Dv, int tid, int* error) {
 }
 
 // ---------------------------------------------------------------------------
-// X L^T = C (X, C: 64x64 in As; L = L_jj in Bs; Dv = inverses of its 8x8
-// diagonal blocks).  Warp w owns rows 8w..8w+7 and never waits on another
-// warp: column block q is  X_q = (C_q - sum_{p<q} X_p L_qp^T) Dinv_q^T.
+// X L^T = C (X, C: 64x64 in X (stride TS); L = L_jj in Lj; Dv = inverses of
+// its 8x8 diagonal blocks).  Warp w owns rows 8w..8w+7 and never waits on
+// another warp: column block q is X_q = (C_q - sum_{p<q} X_p L_qp^T) Dinv_q^T.
 // ---------------------------------------------------------------------------
 __device__ void trsm_tile_warp(double* As, const double* Bs, const double* Dv, int warp,
                                int lane) {
@@ -197,27 +223,22 @@ __device__ void trsm_tile_warp(double* As, const double* Bs, const double* Dv, i
   }
 }
 
-__global__ void __launch_bounds__(256, 3) k_chol_tiles(CholParams P) {
-  extern __shared__ __align__(16) double smem[];
-  double* As = smem;
-  double* Bs = smem + TB * TS;
-  double* Dv = Bs + TB * TS;  // 512 doubles
-  __shared__ int s_task;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) s_task = atomicAdd(P.ticket, 1);
-  __syncthreads();
-  int rem = s_task;
-  const int T = P.T;
-  if (rem >= T * (T + 1) / 2) return;
-  int j = 0;
-  while (rem >= T - j) {
-    rem -= T - j;
-    ++j;
-  }
-  const int i = j + rem;
+// ---------------------------------------------------------------------------
+// tile Cholesky kernel
+// ---------------------------------------------------------------------------
+constexpr int KC = 32;          // K chunk of one pipeline stage
+constexpr int KS = 36;          // stage row stride (doubles): same 2-wavefront pattern as TS
+constexpr int STAGE = 2 * TB * KS;  // A half + B half
 
-  // ---- fused assembly: C = alpha * Gram + I (lower), identity padding ----
-  double acc[8][2];
+// shared layout (doubles): Sg[TB*TS] | stage[2][STAGE] | Dv[512] | rdiag[64]
+constexpr int SM_SG = 0;
+constexpr int SM_ST = TB * TS;
+constexpr int SM_DV = SM_ST + 2 * STAGE;
+constexpr int SM_RD = SM_DV + 512;
+constexpr int SM_TOTAL = SM_RD + 64;
+
+__device__ __forceinline__ void init_acc(const CholParams& P, const CholMat& M, int i, int j,
+                                         int warp, int lane, double (&acc)[8][2]) {
   const int p = i * TB + warp * 8 + (lane >> 2);
 #pragma unroll
   for (int nt = 0; nt < 8; ++nt) {
@@ -225,67 +246,167 @@ __global__ void __launch_bounds__(256, 3) k_chol_tiles(CholParams P) {
     for (int e = 0; e < 2; ++e) {
       const int q = j * TB + nt * 8 + 2 * (lane & 3) + e;
       double v;
-      if (p >= P.N || q >= P.N) v = (p == q) ? 1.0 : 0.0;
+      if (p >= M.N || q >= M.N) v = (p == q) ? 1.0 : 0.0;
       else if (q > p) v = 0.0;
-      else v = chol_g_elem(P, p, q);
+      else v = chol_g_elem(P, M, p, q);
       acc[nt][e] = v;
     }
   }
+}
 
-  // ---- left-looking update over the finished tiles of columns k < j ----
-  const int arow = (warp * 8 + (lane >> 2)) * TS + (lane & 3);
-  for (int k = 0; k < j; ++k) {
-    if (tid == 0) {
-      wait_flag(P.flags + (i * (i + 1) / 2 + k), P.epoch);
-      wait_flag(P.flags + (j * (j + 1) / 2 + k), P.epoch);
+// C_(ra, j) -= sum_{k in [kb, ke)} L_(ra,k) L_(j,k)^T   into accA, and when
+// PAIR also C_(j,j) -= L_(j,k) L_(j,k)^T into accB.  Tiles stream through a
+// two-stage cp.async pipeline in K chunks of 32; thread 0 waits on the
+// producers' flags just before a tile's first chunk is issued.
+template <bool PAIR>
+__device__ void accumulate(const CholMat& P, int ra, int j, int kb, int ke, double* stage,
+                           double (&accA)[8][2], double (&accB)[8][2], int tid) {
+  const int warp = tid >> 5, lane = tid & 31;
+  const int nchunk = 2 * (ke - kb);
+  if (nchunk <= 0) return;
+  auto issue = [&](int u) {
+    const int k = kb + (u >> 1), h = u & 1;
+    if (h == 0) {
+      if (tid == 0) {
+        wait_flag(P.flags + (ra * (ra + 1) / 2 + k), P.epoch);
+        wait_flag(P.flags + (j * (j + 1) / 2 + k), P.epoch);
+      }
+      __syncthreads();
+    }
+    double* st = stage + (u & 1) * STAGE;
+    const double* ga = P.L + tile_off(ra, k) + h * KC;
+    const double* gb = P.L + tile_off(j, k) + h * KC;
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int c = tid + it * 256;  // 1024 16-byte chunks per operand half
+      const int row = c >> 4, cc = (c & 15) * 2;
+      cp_async16(st + row * KS + cc, ga + row * TB + cc);
+      cp_async16(st + TB * KS + row * KS + cc, gb + row * TB + cc);
+    }
+    cp_async_commit();
+  };
+  issue(0);
+  const int arow = (warp * 8 + (lane >> 2)) * KS + (lane & 3);
+  const int brow = (lane >> 2) * KS + (lane & 3);
+  for (int u = 0; u < nchunk; ++u) {
+    if (u + 1 < nchunk) {
+      issue(u + 1);
+      cp_async_wait_1();
+    } else {
+      cp_async_wait_all();
     }
     __syncthreads();
-    load_tile_async(As, P.L + tile_off(i, k), tid);
-    load_tile_async(Bs, P.L + tile_off(j, k), tid);
-    cp_async_commit();
-    cp_async_wait_all();
-    __syncthreads();
-#pragma unroll 4
-    for (int k4 = 0; k4 < TB / 4; ++k4) {
-      const double a = -As[arow + 4 * k4];
+    const double* sa = stage + (u & 1) * STAGE;
+    const double* sb = sa + TB * KS;
+#pragma unroll
+    for (int k4 = 0; k4 < KC / 4; ++k4) {
+      const double a = -sa[arow + 4 * k4];
+      double ad = 0.0;
+      if (PAIR) ad = -sb[arow + 4 * k4];
 #pragma unroll
       for (int nt = 0; nt < 8; ++nt) {
-        const double b = Bs[(nt * 8 + (lane >> 2)) * TS + 4 * k4 + (lane & 3)];
-        dmma8x8x4(acc[nt], a, b);
+        const double b = sb[nt * 8 * KS + brow + 4 * k4];
+        dmma8x8x4(accA[nt], a, b);
+        if (PAIR) dmma8x8x4(accB[nt], ad, b);
       }
     }
     __syncthreads();
   }
+}
 
-  // ---- finalize: POTRF on the diagonal, TRSM against L_jj below it ----
+__device__ __forceinline__ void acc_to_smem(double* X, const double (&acc)[8][2], int warp, int lane) {
 #pragma unroll
   for (int nt = 0; nt < 8; ++nt) {
-    As[(warp * 8 + (lane >> 2)) * TS + nt * 8 + 2 * (lane & 3)] = acc[nt][0];
-    As[(warp * 8 + (lane >> 2)) * TS + nt * 8 + 2 * (lane & 3) + 1] = acc[nt][1];
+    X[(warp * 8 + (lane >> 2)) * TS + nt * 8 + 2 * (lane & 3)] = acc[nt][0];
+    X[(warp * 8 + (lane >> 2)) * TS + nt * 8 + 2 * (lane & 3) + 1] = acc[nt][1];
   }
+}
+
+__device__ __forceinline__ void publish(const CholMat& P, int i, int j, int tid) {
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    st_release(P.flags + (i * (i + 1) / 2 + j), P.epoch);
+  }
+}
+
+// Task order (host-built map, see chol_task_order): per system, column by
+// column, the PAIR task (diagonal (j, j) plus the first sub-diagonal
+// (j + 1, j), so the critical TRSM reuses L_jj straight from shared
+// memory) is placed right after the first off-diagonal tile of column j - 1
+// it depends on -- one column ahead of the bulk tiles -- and the systems of
+// a batch are merged in proportion.  Every task's dependencies carry smaller
+// tickets, so spinning on them cannot deadlock.
+__global__ void __launch_bounds__(256, 2) k_chol_tiles(CholParams P) {
+  extern __shared__ __align__(16) double smem[];
+  double* Sg = smem + SM_SG;
+  double* stage = smem + SM_ST;
+  double* Dv = smem + SM_DV;
+  double* rdiag = smem + SM_RD;
+  double* X = stage;  // 64 x TS work tile overlays the (then idle) stages
+  __shared__ int s_task;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) s_task = atomicAdd(P.ticket, 1);
+  __syncthreads();
+  if (s_task >= P.ntasks) return;
+  const int2 e = P.map[s_task];
+  const CholMat& M = P.m[e.x];
+  const int i = e.y >> 16, j = e.y & 0xffff;
+  const int T = M.T;
+  unsigned long long* tr = (P.trace != nullptr && tid == 0) ? P.trace + 4 * (int64_t)s_task : nullptr;
+  if (tr) tr[0] = globaltimer_ns();
+  double accA[8][2], accB[8][2];
+
   if (i == j) {
+    // ---------------- pair task: (j, j) and (j + 1, j) ----------------
+    const bool has_sub = j + 1 < T;
+    init_acc(P, M, j, j, warp, lane, accB);
+    if (has_sub) {
+      init_acc(P, M, j + 1, j, warp, lane, accA);
+      accumulate<true>(M, j + 1, j, 0, j - 1 > 0 ? j - 1 : 0, stage, accA, accB, tid);
+    }
+    // last update of the diagonal alone, then factor it right away
+    if (j >= 1) accumulate<false>(M, j, j, has_sub ? j - 1 : 0, j, stage, accB, accB, tid);
+    if (tr) tr[1] = globaltimer_ns();
+    acc_to_smem(Sg, accB, warp, lane);
     __syncthreads();
-    potrf_tile_blocked(As, Dv, tid, P.error);
-    // publish the small inverses with the tile
-    if (tid < 256) {
+    potrf_tile_blocked(Sg, Dv, rdiag, tid, P.error);
+    if (tr) tr[2] = globaltimer_ns();
+    store_tile(M.L + tile_off(j, j), Sg, tid);
+    {
       double2 v = *reinterpret_cast<const double2*>(Dv + 2 * tid);
-      *reinterpret_cast<double2*>(P.Dinv + (int64_t)j * 512 + 2 * tid) = v;
+      *reinterpret_cast<double2*>(M.Dinv + (int64_t)j * 512 + 2 * tid) = v;
+    }
+    publish(M, j, j, tid);
+    if (has_sub) {
+      if (j >= 1) accumulate<false>(M, j + 1, j, j - 1, j, stage, accA, accA, tid);
+      acc_to_smem(X, accA, warp, lane);
+      __syncwarp();
+      trsm_tile_warp(X, Sg, Dv, warp, lane);
+      __syncthreads();
+      store_tile(M.L + tile_off(j + 1, j), X, tid);
+      publish(M, j + 1, j, tid);
     }
   } else {
-    if (tid == 0) wait_flag(P.flags + (j * (j + 1) / 2 + j), P.epoch);
+    // ---------------- off-diagonal tile (i, j), i >= j + 2 ----------------
+    init_acc(P, M, i, j, warp, lane, accA);
+    accumulate<false>(M, i, j, 0, j, stage, accA, accA, tid);
+    if (tr) tr[1] = globaltimer_ns();
+    if (tid == 0) wait_flag(M.flags + (j * (j + 1) / 2 + j), M.epoch);
+    if (tr) tr[2] = globaltimer_ns();
     __syncthreads();
-    load_tile_async(Bs, P.L + tile_off(j, j), tid);
-    load_dinv_async(Dv, P.Dinv + (int64_t)j * 512, tid);
+    load_tile_async(Sg, M.L + tile_off(j, j), tid);
+    load_dinv_async(Dv, M.Dinv + (int64_t)j * 512, tid);
     cp_async_commit();
+    acc_to_smem(X, accA, warp, lane);
     cp_async_wait_all();
     __syncthreads();
-    trsm_tile_warp(As, Bs, Dv, warp, lane);
+    trsm_tile_warp(X, Sg, Dv, warp, lane);
     __syncthreads();
+    store_tile(M.L + tile_off(i, j), X, tid);
+    publish(M, i, j, tid);
   }
-  store_tile(P.L + tile_off(i, j), As, tid);
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) st_release(P.flags + (i * (i + 1) / 2 + j), P.epoch);
+  if (tr) tr[3] = globaltimer_ns();
 }
 
 // ---------------------------------------------------------------------------
@@ -433,12 +554,58 @@ __global__ void __launch_bounds__(256, 2) k_trsv(TrsvParams P) {
   if (fwd) diag_solve_fwd(vec, Ld, Dv, u, tid);
   else diag_solve_bwd(vec, Ld, Dv, u, tid);
   if (tid < TB) (fwd ? P.t : P.w)[(int64_t)i * TB + tid] = vec[tid];
-  __threadfence();
   __syncthreads();
-  if (tid == 0) st_release((fwd ? fflag : bflag) + i, P.epoch);
+  if (tid == 0) {
+    __threadfence();
+    st_release((fwd ? fflag : bflag) + i, P.epoch);
+  }
 }
 
-size_t chol_smem_bytes() { return (size_t)(2 * TB * TS + 512) * sizeof(double); }
+size_t chol_smem_bytes() { return (size_t)SM_TOTAL * sizeof(double); }
+int chol_num_tasks(int T) { return T * (T - 1) / 2 + 1; }
+
+// per-system task order: pair(0), then for each column j its first
+// off-diagonal tile (j + 2, j), the pair of column j + 1, and the rest of
+// column j.  Encoded as (i << 16) | j with i == j for pair tasks.
+static std::vector<int> task_order_one(int T) {
+  std::vector<int> seq;
+  seq.reserve(chol_num_tasks(T));
+  seq.push_back(0);  // pair(0)
+  for (int j = 0; j < T; ++j) {
+    if (j + 2 < T) seq.push_back(((j + 2) << 16) | j);
+    if (j + 1 < T) seq.push_back(((j + 1) << 16) | (j + 1));
+    for (int i = j + 3; i < T; ++i) seq.push_back((i << 16) | j);
+  }
+  return seq;
+}
+
+// merged ticket map of a batch: systems interleaved in proportion to their
+// task counts (round robin for equal sizes), each system's order preserved
+std::vector<int2> chol_task_map(const int* Ts, int nb) {
+  std::vector<std::vector<int>> per(nb);
+  size_t total = 0;
+  for (int b = 0; b < nb; ++b) {
+    per[b] = task_order_one(Ts[b]);
+    total += per[b].size();
+  }
+  std::vector<int2> out;
+  out.reserve(total);
+  std::vector<size_t> pos(nb, 0);
+  while (out.size() < total) {
+    int best = -1;
+    double bestkey = 1e300;
+    for (int b = 0; b < nb; ++b) {
+      if (pos[b] >= per[b].size()) continue;
+      const double key = (pos[b] + 0.5) / (double)per[b].size();
+      if (key < bestkey) {
+        bestkey = key;
+        best = b;
+      }
+    }
+    out.push_back(make_int2(best, per[best][pos[best]++]));
+  }
+  return out;
+}
 size_t trsv_smem_bytes() { return (size_t)(3 * TB * TS + 512 + 2 * TB + 4 * TB + 8) * sizeof(double); }
 
 void launch_chol(const CholParams& P, cudaStream_t s) {
@@ -450,8 +617,7 @@ void launch_chol(const CholParams& P, cudaStream_t s) {
                          (int)trsv_smem_bytes());
     configured = true;
   }
-  const int ntiles = P.T * (P.T + 1) / 2;
-  k_chol_tiles<<<ntiles, 256, chol_smem_bytes(), s>>>(P);
+  k_chol_tiles<<<P.ntasks, 256, chol_smem_bytes(), s>>>(P);
 }
 
 void launch_trsv(const TrsvParams& P, cudaStream_t s) {

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace slim {
@@ -19,23 +21,32 @@ struct Ctl {
   int pad;
 };
 
-struct CholParams {
+// one system of a batched factorization
+struct CholMat {
   double* L;            // lower tiles, tile_off(i, j)
   double* Dinv;         // T x 512: inverses of the 8x8 diagonal blocks of L_jj
   int* flags;           // T (T + 1) / 2 epoch flags
+  int N, T, nw, epoch;
+  double alpha;
+  int slot[MAX_WINDOW];  // window position (0 = oldest) -> ring slot
+};
+
+struct CholParams {
+  CholMat m[MAX_BATCH];
+  int nb;               // systems in this launch
+  int ntasks;
+  const int2* map;      // ticket -> (system, (i << 16) | j); i == j marks a pair task
   int* ticket;          // zeroed before each launch
   int* error;           // set to 1 on a non-positive pivot
-  int epoch;
-  int N, T;
   // ring mode: initial tiles gathered from the incremental Gram panels
   const double* panels;
   int64_t panel_stride;  // S * ell * ell
-  int ell, S, nw;
-  double alpha;
-  int slot[MAX_WINDOW];  // window position (0 = oldest) -> ring slot
-  // dense mode (panels == nullptr): G is the full SPD matrix, row-major
+  int ell, S;
+  // dense mode (panels == nullptr, nb == 1): G is the full SPD matrix, row-major
   const double* G;
   int64_t ldg;
+  // optional timeline (debug): 4 globaltimer stamps per ticket
+  unsigned long long* trace;
 };
 
 struct TrsvParams {
@@ -61,12 +72,14 @@ struct Window {
 
 // ---- launchers (ops.cu / chol.cu) ----
 void launch_chol(const CholParams& P, cudaStream_t s);
+std::vector<int2> chol_task_map(const int* Ts, int nb);
 void launch_trsv(const TrsvParams& P, cudaStream_t s);
 
 __global__ void k_chol_tiles(CholParams P);
 __global__ void k_trsv(TrsvParams P);
 
 size_t chol_smem_bytes();
+int chol_num_tasks(int T);
 size_t trsv_smem_bytes();
 
 }  // namespace slim
