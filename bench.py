@@ -194,7 +194,7 @@ def run_ours(args, world, rank, local, dist):
     op, b, xt = prob.op, prob.b, prob.x_true
     r, alpha = CFG["r"], CFG["alpha"]
     seed = CFG["sampler_seed"] + rank
-    D = int(os.environ.get("SLIM_BATCH", "4"))
+    D = int(os.environ.get("SLIM_BATCH", "8"))
     wprime = -(-max(args.warmup, r + 1) // D) * D  # whole factorization batches
     total = wprime + args.steps
     M = op.n_blocks

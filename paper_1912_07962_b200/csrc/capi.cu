@@ -34,7 +34,7 @@ using namespace slim;
 namespace {
 
 constexpr int NEV = 16;       // event ring per kind
-constexpr int D_DEFAULT = 4;  // systems per batched factorization
+constexpr int D_DEFAULT = 8;  // systems per batched factorization
 
 struct ProfPair {
   cudaEvent_t a, b;
@@ -221,9 +221,14 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
   c->dev = d->device;
   *out = c;
   CK(c, cudaSetDevice(c->dev));
-  CK(c, cudaStreamCreateWithFlags(&c->sx, cudaStreamNonBlocking));
-  CK(c, cudaStreamCreateWithFlags(&c->sg, cudaStreamNonBlocking));
-  CK(c, cudaStreamCreateWithFlags(&c->sf, cudaStreamNonBlocking));
+  // the small latency-critical kernels (x-chain, Gram panels) get the
+  // higher priority so their CTAs are dispatched ahead of pending tiles of a
+  // running batched factorization instead of waiting for its tail
+  int prio_lo = 0, prio_hi = 0;
+  CK(c, cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  CK(c, cudaStreamCreateWithPriority(&c->sx, cudaStreamNonBlocking, prio_hi));
+  CK(c, cudaStreamCreateWithPriority(&c->sg, cudaStreamNonBlocking, prio_hi));
+  CK(c, cudaStreamCreateWithPriority(&c->sf, cudaStreamNonBlocking, prio_lo));
   if (const char* env = getenv("SLIM_BATCH")) c->D = std::max(1, std::min(MAX_BATCH, atoi(env)));
   for (int q = 0; q < NEV; ++q) {
     CK(c, cudaEventCreateWithFlags(&c->ev_g[q], cudaEventDisableTiming));

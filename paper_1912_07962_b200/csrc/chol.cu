@@ -37,7 +37,19 @@ namespace slim {
 
 constexpr unsigned FULL = 0xffffffffu;
 
-__device__ __forceinline__ double chol_g_elem(const CholParams& P, const CholMat& M, int p, int q) {
+// per-CTA view of its system: scalars in registers, window slots in shared
+// memory (indexing the kernel-parameter array with the runtime system id
+// would turn every field access into a dynamically indexed constant load)
+struct MatRT {
+  double* L;
+  double* Dinv;
+  int* flags;
+  int N, T, epoch;
+  double alpha;
+  const int* slot;  // shared memory
+};
+
+__device__ __forceinline__ double chol_g_elem(const CholParams& P, const MatRT& M, int p, int q) {
   // requires q <= p < N
   if (P.panels != nullptr) {
     const int pb = p / P.ell, a = p - pb * P.ell;
@@ -237,7 +249,7 @@ constexpr int SM_DV = SM_ST + 2 * STAGE;
 constexpr int SM_RD = SM_DV + 512;
 constexpr int SM_TOTAL = SM_RD + 64;
 
-__device__ __forceinline__ void init_acc(const CholParams& P, const CholMat& M, int i, int j,
+__device__ __forceinline__ void init_acc(const CholParams& P, const MatRT& M, int i, int j,
                                          int warp, int lane, double (&acc)[8][2]) {
   const int p = i * TB + warp * 8 + (lane >> 2);
 #pragma unroll
@@ -259,7 +271,7 @@ __device__ __forceinline__ void init_acc(const CholParams& P, const CholMat& M, 
 // two-stage cp.async pipeline in K chunks of 32; thread 0 waits on the
 // producers' flags just before a tile's first chunk is issued.
 template <bool PAIR>
-__device__ void accumulate(const CholMat& P, int ra, int j, int kb, int ke, double* stage,
+__device__ void accumulate(const MatRT& P, int ra, int j, int kb, int ke, double* stage,
                            double (&accA)[8][2], double (&accB)[8][2], int tid) {
   const int warp = tid >> 5, lane = tid & 31;
   const int nchunk = 2 * (ke - kb);
@@ -322,7 +334,7 @@ __device__ __forceinline__ void acc_to_smem(double* X, const double (&acc)[8][2]
   }
 }
 
-__device__ __forceinline__ void publish(const CholMat& P, int i, int j, int tid) {
+__device__ __forceinline__ void publish(const MatRT& P, int i, int j, int tid) {
   __syncthreads();
   if (tid == 0) {
     __threadfence();
@@ -345,12 +357,24 @@ __global__ void __launch_bounds__(256, 2) k_chol_tiles(CholParams P) {
   double* rdiag = smem + SM_RD;
   double* X = stage;  // 64 x TS work tile overlays the (then idle) stages
   __shared__ int s_task;
+  __shared__ int s_slot[MAX_WINDOW];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) s_task = atomicAdd(P.ticket, 1);
   __syncthreads();
   if (s_task >= P.ntasks) return;
   const int2 e = P.map[s_task];
-  const CholMat& M = P.m[e.x];
+  const CholMat& Mp = P.m[e.x];
+  MatRT M;
+  M.L = Mp.L;
+  M.Dinv = Mp.Dinv;
+  M.flags = Mp.flags;
+  M.N = Mp.N;
+  M.T = Mp.T;
+  M.epoch = Mp.epoch;
+  M.alpha = Mp.alpha;
+  if (tid < MAX_WINDOW) s_slot[tid] = Mp.slot[tid];
+  M.slot = s_slot;
+  __syncthreads();
   const int i = e.y >> 16, j = e.y & 0xffff;
   const int T = M.T;
   unsigned long long* tr = (P.trace != nullptr && tid == 0) ? P.trace + 4 * (int64_t)s_task : nullptr;

@@ -6,8 +6,6 @@ CMD="python bench.py --steps 4 --warmup 3 --quick"
 timeout 600 $CMD > gpurun_out/plain.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_list.log 2>&1
 echo "list rc=$?"
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_chol_tiles -s 23 -c 1 -o gpurun_out/chol_full $CMD > gpurun_out/ncu_full.log 2>&1
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_chol_tiles -s 4 -c 1 -o gpurun_out/chol_full $CMD > gpurun_out/ncu_full.log 2>&1
 echo "full rc=$?"
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_trsv -s 23 -c 1 -o gpurun_out/trsv_full $CMD > gpurun_out/ncu_gram.log 2>&1
-echo "gram rc=$?"
 tail -3 gpurun_out/ncu_full.log
