@@ -777,6 +777,20 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
     const int nb = (int)std::min<int64_t>(D, K - kb0 + 1);
     const int set = (int)(B & 1);
     for (int b = 0; b < nb; ++b) fill_window(c, idx, kb0 + b, Ws[b]);
+    if (kb0 <= k0 && k0 < kb0 + nb && k0 > 1 && !a_recorded) {
+      // timing window starts here: join every stream first, so no work of
+      // the timed steps (factorizations run ahead of the x-chain) starts
+      // before the window opens -- a conservative steady-state measurement
+      CK(c, cudaEventRecord(c->ev_g[(B + NEV - 1) % NEV], c->sg));
+      CK(c, cudaStreamWaitEvent(c->sx, c->ev_g[(B + NEV - 1) % NEV], 0));
+      CK(c, cudaEventRecord(c->ev_f[(B + NEV - 1) % NEV], c->sf));
+      CK(c, cudaStreamWaitEvent(c->sx, c->ev_f[(B + NEV - 1) % NEV], 0));
+      CK(c, cudaEventRecord(c->run_a, c->sx));
+      CK(c, cudaStreamWaitEvent(c->sg, c->run_a, 0));
+      CK(c, cudaStreamWaitEvent(c->sf, c->run_a, 0));
+      launches_at_k0 = c->launches;
+      a_recorded = true;
+    }
     // ---- Gram panels (sg): the ring slots they overwrite were last read by
     // the factorization of batch B - 2
     if (B >= 2) CK(c, cudaStreamWaitEvent(c->sg, c->ev_f[(B - 2) % NEV], 0));
@@ -823,11 +837,7 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
                               cudaMemcpyDeviceToDevice, c->sx));
         ++rec_rows;
       }
-      if (k + 1 == k0) {
-        CK(c, cudaEventRecord(c->run_a, c->sx));
-        launches_at_k0 = c->launches;
-        a_recorded = true;
-      }
+
     }
     CK(c, cudaEventRecord(c->ev_x[B % NEV], c->sx));
     // cheap divergence poll: stop enqueueing once the device reported it

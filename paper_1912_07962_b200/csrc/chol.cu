@@ -153,23 +153,44 @@ __device__ void potrf_tile_blocked(double* S, double* Dv, double* rdiag, int tid
     // trailing update of 8x8 blocks (bi, bj), p < bj <= bi <= 7, via DMMA
     const int nb = 7 - p;
     const int nblk = nb * (nb + 1) / 2;
-    for (int e = warp; e < nblk; e += 8) {
-      int bi = p + 1, rem = e;
-      while (rem > bi - (p + 1)) {
-        rem -= bi - p;
-        ++bi;
-      }
-      const int bj = p + 1 + rem;
-      double* cp = S + (8 * bi + (lane >> 2)) * TS + 8 * bj + 2 * (lane & 3);
-      double acc[2] = {cp[0], cp[1]};
+    // up to 4 blocks per warp, two independent chains at a time
+#pragma unroll 1
+    for (int u0 = 0; u0 < 4; u0 += 2) {
+      double acc[2][2], a[2][2], b[2][2];
+      int off[2];
+      bool on[2];
 #pragma unroll
-      for (int ks = 0; ks < 2; ++ks) {
-        const double a = -S[(8 * bi + (lane >> 2)) * TS + c0 + 4 * ks + (lane & 3)];
-        const double b = S[(8 * bj + (lane >> 2)) * TS + c0 + 4 * ks + (lane & 3)];
-        dmma8x8x4(acc, a, b);
+      for (int u = 0; u < 2; ++u) {
+        const int e = warp + 8 * (u0 + u);
+        on[u] = e < nblk;
+        int bi = p + 1, rem = on[u] ? e : 0;
+        while (rem > bi - (p + 1)) {
+          rem -= bi - p;
+          ++bi;
+        }
+        const int bj = p + 1 + rem;
+        off[u] = (8 * bi + (lane >> 2)) * TS + 8 * bj + 2 * (lane & 3);
+        if (on[u]) {
+          acc[u][0] = S[off[u]];
+          acc[u][1] = S[off[u] + 1];
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks) {
+            a[u][ks] = -S[(8 * bi + (lane >> 2)) * TS + c0 + 4 * ks + (lane & 3)];
+            b[u][ks] = S[(8 * bj + (lane >> 2)) * TS + c0 + 4 * ks + (lane & 3)];
+          }
+        }
       }
-      cp[0] = acc[0];
-      cp[1] = acc[1];
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+          if (on[u]) dmma8x8x4(acc[u], a[u][ks], b[u][ks]);
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        if (on[u]) {
+          S[off[u]] = acc[u][0];
+          S[off[u] + 1] = acc[u][1];
+        }
     }
     __syncthreads();
   }
@@ -251,17 +272,19 @@ constexpr int SM_TOTAL = SM_RD + 64;
 
 __device__ __forceinline__ void init_acc(const CholParams& P, const MatRT& M, int i, int j,
                                          int warp, int lane, double (&acc)[8][2]) {
-  const int p = i * TB + warp * 8 + (lane >> 2);
+  // warp tile: rows 16 (warp >> 1) .. +15, columns 32 (warp & 1) .. +31;
+  // accumulator f = rb * 4 + cb holds the 8x8 block (rb, cb) of it
 #pragma unroll
-  for (int nt = 0; nt < 8; ++nt) {
+  for (int f = 0; f < 8; ++f) {
+    const int p = i * TB + 16 * (warp >> 1) + 8 * (f >> 2) + (lane >> 2);
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
-      const int q = j * TB + nt * 8 + 2 * (lane & 3) + e;
+      const int q = j * TB + 32 * (warp & 1) + 8 * (f & 3) + 2 * (lane & 3) + e;
       double v;
       if (p >= M.N || q >= M.N) v = (p == q) ? 1.0 : 0.0;
       else if (q > p) v = 0.0;
       else v = chol_g_elem(P, M, p, q);
-      acc[nt][e] = v;
+      acc[f][e] = v;
     }
   }
 }
@@ -298,8 +321,8 @@ __device__ void accumulate(const MatRT& P, int ra, int j, int kb, int ke, double
     cp_async_commit();
   };
   issue(0);
-  const int arow = (warp * 8 + (lane >> 2)) * KS + (lane & 3);
-  const int brow = (lane >> 2) * KS + (lane & 3);
+  const int arow = (16 * (warp >> 1) + (lane >> 2)) * KS + (lane & 3);
+  const int brow = (32 * (warp & 1) + (lane >> 2)) * KS + (lane & 3);
   for (int u = 0; u < nchunk; ++u) {
     if (u + 1 < nchunk) {
       issue(u + 1);
@@ -312,14 +335,18 @@ __device__ void accumulate(const MatRT& P, int ra, int j, int kb, int ke, double
     const double* sb = sa + TB * KS;
 #pragma unroll
     for (int k4 = 0; k4 < KC / 4; ++k4) {
-      const double a = -sa[arow + 4 * k4];
-      double ad = 0.0;
-      if (PAIR) ad = -sb[arow + 4 * k4];
+      double a[2], ad[2], b[4];
 #pragma unroll
-      for (int nt = 0; nt < 8; ++nt) {
-        const double b = sb[nt * 8 * KS + brow + 4 * k4];
-        dmma8x8x4(accA[nt], a, b);
-        if (PAIR) dmma8x8x4(accB[nt], ad, b);
+      for (int rb = 0; rb < 2; ++rb) {
+        a[rb] = -sa[arow + rb * 8 * KS + 4 * k4];
+        if (PAIR) ad[rb] = -sb[arow + rb * 8 * KS + 4 * k4];
+      }
+#pragma unroll
+      for (int cb = 0; cb < 4; ++cb) b[cb] = sb[brow + cb * 8 * KS + 4 * k4];
+#pragma unroll
+      for (int f = 0; f < 8; ++f) {
+        dmma8x8x4(accA[f], a[f >> 2], b[f & 3]);
+        if (PAIR) dmma8x8x4(accB[f], ad[f >> 2], b[f & 3]);
       }
     }
     __syncthreads();
@@ -328,9 +355,11 @@ __device__ void accumulate(const MatRT& P, int ra, int j, int kb, int ke, double
 
 __device__ __forceinline__ void acc_to_smem(double* X, const double (&acc)[8][2], int warp, int lane) {
 #pragma unroll
-  for (int nt = 0; nt < 8; ++nt) {
-    X[(warp * 8 + (lane >> 2)) * TS + nt * 8 + 2 * (lane & 3)] = acc[nt][0];
-    X[(warp * 8 + (lane >> 2)) * TS + nt * 8 + 2 * (lane & 3) + 1] = acc[nt][1];
+  for (int f = 0; f < 8; ++f) {
+    double* dst = X + (16 * (warp >> 1) + 8 * (f >> 2) + (lane >> 2)) * TS + 32 * (warp & 1) +
+                  8 * (f & 3) + 2 * (lane & 3);
+    dst[0] = acc[f][0];
+    dst[1] = acc[f][1];
   }
 }
 
@@ -405,7 +434,7 @@ __global__ void __launch_bounds__(256, 2) k_chol_tiles(CholParams P) {
     if (has_sub) {
       if (j >= 1) accumulate<false>(M, j + 1, j, j - 1, j, stage, accA, accA, tid);
       acc_to_smem(X, accA, warp, lane);
-      __syncwarp();
+      __syncthreads();
       trsm_tile_warp(X, Sg, Dv, warp, lane);
       __syncthreads();
       store_tile(M.L + tile_off(j + 1, j), X, tid);
