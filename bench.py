@@ -218,8 +218,16 @@ def run_ours(args, world, rank, local, dist):
     chol_ms = timing["cholesky_ms"] / max(1, timing["cholesky_count"])
     achieved = flops_chol / (chol_ms * 1e-3) / 1e12
     agg = (N ** 3 / 3.0) * args.steps / (timing["window_ms"] * 1e-3) / 1e12
+    traffic = None
+    try:  # dram bytes per launch from the committed ncu --set full capture
+        with open(os.path.join(ROOT, "profiles", "ncu_chol_r01.json")) as fh:
+            prof = json.load(fh)
+        if int(prof.get("systems_per_launch", 0)) == int(round(per_launch)):
+            traffic = prof["dram_bytes_per_launch"]
+    except (OSError, ValueError, KeyError):
+        pass
     roofline = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
-                "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
                 "kernel": f"k_chol_tiles (fp64 DMMA tile-DAG Cholesky, {per_launch:g} systems "
                           f"of N=3982 interleaved per launch)",
                 "algorithmic_per_launch": f"{per_launch:g} x N^3/3 = {flops_chol:.4g} flop",
