@@ -91,6 +91,9 @@ int slim_upload_csr(slim_ctx* ctx, const int64_t* rowptr, const int32_t* col,
 int slim_finalize_operator(slim_ctx* ctx);
 /* right-hand side for the generated layout (n_rows entries)              */
 int slim_set_rhs(slim_ctx* ctx, const double* b);
+/* generated layout, problem setup: out = A x over all n_rows rows, fp64
+ * accumulation of the generated fp32 entries (x has n_cols entries)      */
+int slim_gen_apply(slim_ctx* ctx, const double* x, double* out);
 
 /* ---- run state -------------------------------------------------------- */
 int slim_set_x(slim_ctx* ctx, const double* x0);          /* n_cols      */

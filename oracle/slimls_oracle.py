@@ -325,3 +325,51 @@ def csr_fetch(blocks, b: np.ndarray):
     def fetch(i):
         return mats[i - 1].toarray(), b[(i - 1) * ell:i * ell]
     return fetch
+
+
+# ---------------------------------------------------------------------------
+# configs[4] generator (BASELINE.json configs[4])
+# A[i, j] = fp32((2u - 1) / sqrt(n)), u = (splitmix64(seed ^ (i n + j)) >> 11) 2^-53
+# The reference has no generator operator; this is the RowBlockOperator
+# subclass the survey prescribes, restated independently of the product.
+# ---------------------------------------------------------------------------
+
+_M64 = (1 << 64) - 1
+
+
+def splitmix64_scalar(z: int) -> int:
+    """Published splitmix64 finaliser on a Python int (reference for tests)."""
+    z = (z + 0x9E3779B97F4A7C15) & _M64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return z ^ (z >> 31)
+
+
+def gen_entry_scalar(seed: int, i: int, j: int, n: int) -> float:
+    z = splitmix64_scalar(seed ^ ((i * n + j) & _M64))
+    u = (z >> 11) * 2.0**-53
+    return float(np.float32((2.0 * u - 1.0) / np.sqrt(float(n))))
+
+
+def gen_rows(seed: int, row0: int, rows: int, n: int) -> np.ndarray:
+    """Vectorised generator rows [row0, row0 + rows) as fp64 of the fp32 values."""
+    i = (np.uint64(row0) + np.arange(rows, dtype=np.uint64))[:, None]
+    j = np.arange(n, dtype=np.uint64)[None, :]
+    with np.errstate(over="ignore"):
+        z = np.uint64(seed) ^ (i * np.uint64(n) + j)
+        z = z + np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    u = (z >> np.uint64(11)).astype(np.float64) * 2.0**-53
+    return ((2.0 * u - 1.0) / np.sqrt(float(n))).astype(np.float32).astype(np.float64)
+
+
+def gen_fetch(seed: int, n: int, ell: int, b: np.ndarray):
+    """fetch(i) of the generated operator, like linops.py:192-206."""
+    b = np.asarray(b, dtype=float)
+
+    def fetch(i):
+        s = (i - 1) * ell
+        return gen_rows(seed, s, ell, n), b[s:s + ell]
+    return fetch

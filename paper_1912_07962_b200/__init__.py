@@ -8,6 +8,7 @@ work runs as hand-written sm_100a CUDA kernels behind the C-ABI in
 
 from .linops import (
     DenseBlockOperator,
+    GeneratedBlockOperator,
     RowBlockOperator,
     SampleBlock,
     SinglePassAdapter,

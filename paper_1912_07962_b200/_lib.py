@@ -25,7 +25,7 @@ SLIM_HIST_FIXED = 5
 EXPORTS = (
     "slim_create", "slim_destroy", "slim_last_error", "slim_abi_version",
     "slim_upload_dense", "slim_upload_csr_block", "slim_upload_csr", "slim_finalize_operator",
-    "slim_set_rhs", "slim_set_x", "slim_get_x", "slim_set_references",
+    "slim_set_rhs", "slim_gen_apply", "slim_set_x", "slim_get_x", "slim_set_references",
     "slim_set_divergence_limit", "slim_run", "slim_set_host_streaming", "slim_comm_init",
     "slim_dual_step", "slim_potrf", "slim_potrf_traced", "slim_block_residual", "slim_timing", "slim_set_profiling", "slim_set_timing_start",
     "slim_siddon2d_view", "slim_siddon3d_view",
@@ -59,6 +59,7 @@ _SIGS = {
     "slim_upload_csr": (C.c_int, [_P, _I64P, _I32P, _P, _DP]),
     "slim_finalize_operator": (C.c_int, [_P]),
     "slim_set_rhs": (C.c_int, [_P, _DP]),
+    "slim_gen_apply": (C.c_int, [_P, _DP, _DP]),
     "slim_set_x": (C.c_int, [_P, _DP]),
     "slim_get_x": (C.c_int, [_P, _DP]),
     "slim_set_references": (C.c_int, [_P, _I32, C.POINTER(_DP)]),

@@ -67,6 +67,11 @@ struct slim_ctx {
   std::vector<double> h_b;
   std::vector<char> h_have;
   bool op_ready = false;
+  bool rhs_set = false;
+  // generated layout (configs[4]): ring of generated window blocks, S x ell x n fp32
+  float* gring = nullptr;
+  uint64_t gen_seed = 0;
+  int64_t gen_n_total = 0, col_offset = 0;
   // state
   double* x = nullptr;
   double* refs[MAX_REFS] = {};
@@ -159,7 +164,7 @@ const char* slim_last_error(const slim_ctx* ctx) {
 }
 
 static void free_all(slim_ctx* c) {
-  void* ptrs[] = {c->A, c->b, c->rowptr, c->col, c->val, c->colptr, c->cscrow, c->cscval,
+  void* ptrs[] = {c->gring, c->A, c->b, c->rowptr, c->col, c->val, c->colptr, c->cscrow, c->cscval,
                   c->blkbase, c->x, c->ctl, c->panels, c->tickets, c->tflags, c->errflag,
                   c->rvec, c->tvec, c->wvec, c->spart, c->fpart, c->gpart, c->hist, c->iters_dev};
   for (void* p : ptrs)
@@ -205,8 +210,15 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
          (long long)d->memory_r, MAX_WINDOW - 1);
   if (d->value_dtype != SLIM_F64 && d->value_dtype != SLIM_F32)
     FAIL((slim_ctx*)nullptr, SLIM_EINVAL, "unknown value dtype %d", d->value_dtype);
-  if (d->layout != SLIM_DENSE_ROWMAJOR && d->layout != SLIM_CSR_PERBLOCK)
+  if (d->layout != SLIM_DENSE_ROWMAJOR && d->layout != SLIM_CSR_PERBLOCK &&
+      d->layout != SLIM_GEN_SPLITMIX64)
     FAIL((slim_ctx*)nullptr, SLIM_EINVAL, "layout %d not supported by this build", d->layout);
+  if (d->layout == SLIM_GEN_SPLITMIX64 && d->value_dtype != SLIM_F32)
+    FAIL((slim_ctx*)nullptr, SLIM_EINVAL, "the generated layout produces fp32 values");
+  if (d->layout == SLIM_GEN_SPLITMIX64 &&
+      (d->gen_n_total < d->n_cols || d->col_offset < 0 || d->col_offset + d->n_cols > d->gen_n_total))
+    FAIL((slim_ctx*)nullptr, SLIM_EINVAL, "generated layout: bad column shard [%lld, %lld) of n=%lld",
+         (long long)d->col_offset, (long long)(d->col_offset + d->n_cols), (long long)d->gen_n_total);
   if (d->n_cols > 0x7fffffffLL) FAIL((slim_ctx*)nullptr, SLIM_EINVAL, "n too large");
   slim_ctx* c = new slim_ctx();
   c->d = *d;
@@ -219,6 +231,9 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
   c->vdt = d->value_dtype;
   c->vsize = c->vdt == SLIM_F64 ? 8 : 4;
   c->dev = d->device;
+  c->gen_seed = d->gen_seed;
+  c->gen_n_total = d->gen_n_total;
+  c->col_offset = d->col_offset;
   *out = c;
   CK(c, cudaSetDevice(c->dev));
   // the small latency-critical kernels (x-chain, Gram panels) get the
@@ -269,7 +284,9 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
   ALLOC(c, c->tvec, sizeof(double) * c->Tmax * TB);
   ALLOC(c, c->wvec, sizeof(double) * c->Tmax * TB);
   // M^T w: split the window rows over CTAs when n alone cannot fill the GPU
-  if (c->layout == SLIM_DENSE_ROWMAJOR) {
+  if (c->layout == SLIM_GEN_SPLITMIX64)
+    ALLOC(c, c->gring, sizeof(float) * (size_t)c->S * ell * c->n);
+  if (c->layout != SLIM_CSR_PERBLOCK) {
     const int64_t cols_ctas = (c->n + 255) / 256;
     int ns = (int)std::max<int64_t>(1, std::min<int64_t>(32, (4 * 148) / std::max<int64_t>(1, cols_ctas)));
     ns = (int)std::min<int64_t>(ns, Nmax);
@@ -424,6 +441,11 @@ int slim_finalize_operator(slim_ctx* c) {
     c->op_ready = true;
     return SLIM_OK;
   }
+  if (c->layout == SLIM_GEN_SPLITMIX64) {
+    if (!c->rhs_set) FAIL(c, SLIM_ESTATE, "generated operator needs its right-hand side (slim_set_rhs)");
+    c->op_ready = true;
+    return SLIM_OK;
+  }
   if (!c->h_have.empty()) {
     int rc = assemble_staged_csr(c);
     if (rc) return rc;
@@ -457,6 +479,27 @@ int slim_set_rhs(slim_ctx* c, const double* b) {
   if (!c || !b) FAIL(c, SLIM_EINVAL, "null argument");
   CK(c, cudaSetDevice(c->dev));
   CK(c, cudaMemcpy(c->b, b, sizeof(double) * c->m, cudaMemcpyHostToDevice));
+  c->rhs_set = true;
+  return SLIM_OK;
+}
+
+int slim_gen_apply(slim_ctx* c, const double* x, double* out) {
+  if (!c || !x || !out) FAIL(c, SLIM_EINVAL, "null argument");
+  if (c->layout != SLIM_GEN_SPLITMIX64) FAIL(c, SLIM_EINVAL, "context layout is not generated");
+  CK(c, cudaSetDevice(c->dev));
+  double *dx = nullptr, *dout = nullptr;
+  ALLOC(c, dx, sizeof(double) * c->n);
+  if (dev_alloc(c, reinterpret_cast<void**>(&dout), sizeof(double) * c->m)) {
+    cudaFree(dx);
+    return SLIM_ENOMEM;
+  }
+  cudaMemcpy(dx, x, sizeof(double) * c->n, cudaMemcpyHostToDevice);
+  launch_gen_apply(dout, c->gen_seed, c->m, (int)c->n, c->gen_n_total, c->col_offset, dx, c->sx);
+  cudaError_t e = cudaStreamSynchronize(c->sx);
+  if (e == cudaSuccess) e = cudaMemcpy(out, dout, sizeof(double) * c->m, cudaMemcpyDeviceToHost);
+  cudaFree(dx);
+  cudaFree(dout);
+  if (e != cudaSuccess) FAIL(c, SLIM_ECUDA, "gen_apply failed: %s", cudaGetErrorString(e));
   return SLIM_OK;
 }
 
@@ -536,8 +579,10 @@ static void fill_window(const slim_ctx* c, const int64_t* idx, int64_t k, Window
   W.ell = (int)c->ell;
   for (int P = 0; P < nw; ++P) {
     const int64_t j = k - nw + 1 + P;  // step that pushed window position P
-    W.blk[P] = (int)(idx[j - 1] - 1);
     W.slot[P] = (int)((j - 1) % c->S);
+    // storage block: the row block of A, or (generated) the ring slot the
+    // block was generated into when it was sampled
+    W.blk[P] = c->layout == SLIM_GEN_SPLITMIX64 ? W.slot[P] : (int)(idx[j - 1] - 1);
   }
 }
 
@@ -548,11 +593,18 @@ static ProfPair make_pair() {
   return p;
 }
 
-static int enqueue_gram(slim_ctx* c, const Window& W, int64_t k) {
+static int enqueue_gram(slim_ctx* c, const Window& W, int64_t k, int64_t real_blk) {
   const int slot_new = W.slot[W.nw - 1];
   double* panel = c->panels + (int64_t)slot_new * c->panel_stride;
   const int64_t newblk = W.blk[W.nw - 1];
-  if (c->layout == SLIM_DENSE_ROWMAJOR) {
+  if (c->layout == SLIM_GEN_SPLITMIX64) {
+    launch_gen_block(c->gring + (int64_t)slot_new * c->ell * c->n, c->gen_seed, real_blk * c->ell,
+                     (int)c->ell, (int)c->n, c->gen_n_total, c->col_offset, c->sg);
+    CKLAUNCH(c);
+    c->launches += 3;
+    launch_gram_dense<float>(panel, c->gpart, c->nsplit_gram, W, c->gring, c->n,
+                             newblk * c->ell, (int)c->n, c->sg);
+  } else if (c->layout == SLIM_DENSE_ROWMAJOR) {
     if (c->vdt == SLIM_F64)
       c->launches += 2, launch_gram_dense<double>(panel, c->gpart, c->nsplit_gram, W, (const double*)c->A, c->n,
                                 newblk * c->ell, (int)c->n, c->sg);
@@ -603,7 +655,10 @@ static int enqueue_x_chain(slim_ctx* c, const Window& W, int64_t k, int d, doubl
   // M^T w
   double* s_parts = c->spart;
   int nsplit = 1;
-  if (c->layout == SLIM_DENSE_ROWMAJOR) {
+  if (c->layout == SLIM_GEN_SPLITMIX64) {
+    nsplit = std::min(c->nsplit_mtw, N);
+    launch_mtw_dense<float>(c->spart, nsplit, W, c->gring, c->n, n, c->wvec, c->ctl, s);
+  } else if (c->layout == SLIM_DENSE_ROWMAJOR) {
     nsplit = std::min(c->nsplit_mtw, N);
     if (c->vdt == SLIM_F64)
       launch_mtw_dense<double>(c->spart, nsplit, W, (const double*)c->A, c->n, n, c->wvec, c->ctl, s);
@@ -639,15 +694,20 @@ static int enqueue_x_chain(slim_ctx* c, const Window& W, int64_t k, int d, doubl
   return SLIM_OK;
 }
 
-static int enqueue_residual(slim_ctx* c, int64_t newblk) {
+// newblk: storage block (row block of A, or generated ring slot); real_blk:
+// the sampled block index (rows of b)
+static int enqueue_residual(slim_ctx* c, int64_t newblk, int64_t real_blk) {
   const int64_t row0 = newblk * c->ell;
   c->launches += 1;
-  if (c->layout == SLIM_DENSE_ROWMAJOR) {
+  if (c->layout == SLIM_GEN_SPLITMIX64) {
+    launch_residual_dense<float>(c->rvec, c->gring, c->n, row0, real_blk * c->ell, (int)c->ell,
+                                 (int)c->n, c->x, c->b, c->ctl, c->sx);
+  } else if (c->layout == SLIM_DENSE_ROWMAJOR) {
     if (c->vdt == SLIM_F64)
-      launch_residual_dense<double>(c->rvec, (const double*)c->A, c->n, row0, (int)c->ell,
+      launch_residual_dense<double>(c->rvec, (const double*)c->A, c->n, row0, row0, (int)c->ell,
                                     (int)c->n, c->x, c->b, c->ctl, c->sx);
     else
-      launch_residual_dense<float>(c->rvec, (const float*)c->A, c->n, row0, (int)c->ell,
+      launch_residual_dense<float>(c->rvec, (const float*)c->A, c->n, row0, row0, (int)c->ell,
                                    (int)c->n, c->x, c->b, c->ctl, c->sx);
   } else {
     if (c->vdt == SLIM_F64)
@@ -792,13 +852,15 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
       a_recorded = true;
     }
     // ---- Gram panels (sg): the ring slots they overwrite were last read by
-    // the factorization of batch B - 2
+    // the factorization (and, for generated blocks, the x-chain) of batch B - 2
     if (B >= 2) CK(c, cudaStreamWaitEvent(c->sg, c->ev_f[(B - 2) % NEV], 0));
+    if (B >= 2 && c->layout == SLIM_GEN_SPLITMIX64)
+      CK(c, cudaStreamWaitEvent(c->sg, c->ev_x[(B - 2) % NEV], 0));
     ProfPair pg{};
     const bool prof_b = c->prof && kb0 >= k0;
     if (prof_b) pg = take(c->prof_gram, pgr), cudaEventRecord(pg.a, c->sg);
     for (int b = 0; b < nb; ++b) {
-      int rc = enqueue_gram(c, Ws[b], kb0 + b);
+      int rc = enqueue_gram(c, Ws[b], kb0 + b, idx[kb0 + b - 1] - 1);
       if (rc) return rc;
     }
     if (prof_b) cudaEventRecord(pg.b, c->sg);
@@ -821,8 +883,10 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
       const double alpha = alphas[k - 1];
       ProfPair px{};
       if (c->prof && k >= k0) px = take(c->prof_x, pxc), cudaEventRecord(px.a, c->sx);
+      if (b == 0 && c->layout == SLIM_GEN_SPLITMIX64)
+        CK(c, cudaStreamWaitEvent(c->sx, c->ev_g[B % NEV], 0));  // generated block ready
       {
-        int rc = enqueue_residual(c, W.blk[W.nw - 1]);
+        int rc = enqueue_residual(c, W.blk[W.nw - 1], idx[k - 1] - 1);
         if (rc) return rc;
       }
       if (b == 0) CK(c, cudaStreamWaitEvent(c->sx, c->ev_f[B % NEV], 0));
@@ -917,7 +981,11 @@ extern "C" int slim_block_residual(slim_ctx* c, int64_t block, const double* x, 
   Ctl h{};
   h.div_limit_sq = c->div_limit * c->div_limit;
   CK(c, cudaMemcpy(c->ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice));
-  int rc = enqueue_residual(c, block - 1);
+  if (c->layout == SLIM_GEN_SPLITMIX64) {
+    launch_gen_block(c->gring, c->gen_seed, (block - 1) * c->ell, (int)c->ell, (int)c->n,
+                     c->gen_n_total, c->col_offset, c->sx);
+  }
+  int rc = enqueue_residual(c, c->layout == SLIM_GEN_SPLITMIX64 ? 0 : block - 1, block - 1);
   if (rc) return rc;
   CK(c, cudaStreamSynchronize(c->sx));
   CK(c, cudaMemcpy(r_out, c->rvec, sizeof(double) * c->ell, cudaMemcpyDeviceToHost));
@@ -965,7 +1033,7 @@ extern "C" int slim_dual_step(int32_t device, const double* Mh, int64_t rows, in
   Window W{};
   for (int64_t k = 1; k <= nb; ++k) {
     fill_window(c, idx.data(), k, W);
-    if ((rc = enqueue_gram(c, W, k))) return fail_out(rc);
+    if ((rc = enqueue_gram(c, W, k, k - 1))) return fail_out(rc);
   }
   if (cudaStreamSynchronize(c->sg) != cudaSuccess) return fail_out(SLIM_ECUDA);
   {

@@ -66,7 +66,8 @@ struct TrsvParams {
 struct Window {
   int nw;                     // blocks in the window
   int ell;
-  int blk[MAX_WINDOW];        // 0-based block id at window position
+  int blk[MAX_WINDOW];        // storage block of window position (row block of A,
+                              // or the generated-block ring slot)
   int slot[MAX_WINDOW];       // ring slot at window position
 };
 

@@ -11,6 +11,8 @@
 //
 // Every reduction has a fixed order, so a run is bit-reproducible
 // (reference determinism contract, test_solvers.py:555-571).
+#include <algorithm>
+
 #include <cub/block/block_scan.cuh>
 
 #include "common.cuh"
@@ -24,7 +26,8 @@ namespace slim {
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_residual_dense(double* r, const T* __restrict__ A,
-                                                        int64_t lda, int64_t row0, int ell, int n,
+                                                        int64_t lda, int64_t row0, int64_t brow0,
+                                                        int ell, int n,
                                                         const double* __restrict__ x,
                                                         const double* __restrict__ b,
                                                         const Ctl* ctl) {
@@ -35,7 +38,47 @@ __global__ void __launch_bounds__(256) k_residual_dense(double* r, const T* __re
   double s = 0.0;
   for (int c = lane; c < n; c += 32) s += to_f64(a[c]) * x[c];
   s = warp_sum(s);
-  if (lane == 0) r[row] = s - b[row0 + row];
+  if (lane == 0) r[row] = s - b[brow0 + row];
+}
+
+// ---------------------------------------------------------------------------
+// configs[4] generator: A[i, j] = fp32((2u - 1) / sqrt(n)),
+// u = (splitmix64(seed ^ (i n + j)) >> 11) 2^-53, evaluated in fp64.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ float gen_elem(uint64_t seed, uint64_t i, uint64_t j, uint64_t n_total,
+                                         double sqrt_n) {
+  const uint64_t z = splitmix64(seed ^ (i * n_total + j));
+  const double u = (double)(z >> 11) * 0x1.0p-53;
+  return (float)((2.0 * u - 1.0) / sqrt_n);
+}
+
+// one sampled block (ell rows from global row row0) into dst (ell x n_local)
+__global__ void __launch_bounds__(256) k_gen_block(float* __restrict__ dst, uint64_t seed,
+                                                   int64_t row0, int ell, int n_local,
+                                                   int64_t n_total, int64_t col0) {
+  const double sq = sqrt((double)n_total);
+  const int64_t total = (int64_t)ell * n_local;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = e / n_local, c = e - a * n_local;
+    dst[e] = gen_elem(seed, (uint64_t)(row0 + a), (uint64_t)(col0 + c), (uint64_t)n_total, sq);
+  }
+}
+
+// out[i] = sum_j A[i, j] x[j] over all m rows (problem setup: clean data)
+__global__ void __launch_bounds__(256) k_gen_apply(double* __restrict__ out, uint64_t seed,
+                                                   int64_t m, int n_local, int64_t n_total,
+                                                   int64_t col0, const double* __restrict__ x) {
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= m) return;
+  const double sq = sqrt((double)n_total);
+  double s = 0.0;
+  for (int c = lane; c < n_local; c += 32)
+    s += (double)gen_elem(seed, (uint64_t)row, (uint64_t)(col0 + c), (uint64_t)n_total, sq) * x[c];
+  s = warp_sum(s);
+  if (lane == 0) out[row] = s;
 }
 
 template <typename T>
@@ -436,9 +479,20 @@ __global__ void k_csc_sort(const int* __restrict__ colptr, int* __restrict__ csc
 static inline unsigned cdiv(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b); }
 
 template <typename T>
-void launch_residual_dense(double* r, const T* A, int64_t lda, int64_t row0, int ell, int n,
-                           const double* x, const double* b, const Ctl* ctl, cudaStream_t s) {
-  k_residual_dense<T><<<cdiv(ell, 8), 256, 0, s>>>(r, A, lda, row0, ell, n, x, b, ctl);
+void launch_residual_dense(double* r, const T* A, int64_t lda, int64_t row0, int64_t brow0,
+                           int ell, int n, const double* x, const double* b, const Ctl* ctl,
+                           cudaStream_t s) {
+  k_residual_dense<T><<<cdiv(ell, 8), 256, 0, s>>>(r, A, lda, row0, brow0, ell, n, x, b, ctl);
+}
+void launch_gen_block(float* dst, uint64_t seed, int64_t row0, int ell, int n_local,
+                      int64_t n_total, int64_t col0, cudaStream_t s) {
+  const int64_t total = (int64_t)ell * n_local;
+  const unsigned grid = (unsigned)std::min<int64_t>(cdiv(total, 256), 148 * 16);
+  k_gen_block<<<grid, 256, 0, s>>>(dst, seed, row0, ell, n_local, n_total, col0);
+}
+void launch_gen_apply(double* out, uint64_t seed, int64_t m, int n_local, int64_t n_total,
+                      int64_t col0, const double* x, cudaStream_t s) {
+  k_gen_apply<<<cdiv(m, 8), 256, 0, s>>>(out, seed, m, n_local, n_total, col0, x);
 }
 template <typename T>
 void launch_residual_csr(double* r, const int64_t* rowptr, const int* col, const T* val,
@@ -498,7 +552,7 @@ void launch_build_csc(int* colptr, int* cscrow, T* cscval, const int64_t* rowptr
 }
 
 #define SLIM_INST(T)                                                                              \
-  template void launch_residual_dense<T>(double*, const T*, int64_t, int64_t, int, int,          \
+  template void launch_residual_dense<T>(double*, const T*, int64_t, int64_t, int64_t, int, int, \
                                          const double*, const double*, const Ctl*, cudaStream_t); \
   template void launch_residual_csr<T>(double*, const int64_t*, const int*, const T*, int64_t,    \
                                        int, const double*, const double*, const Ctl*,            \

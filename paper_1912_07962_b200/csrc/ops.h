@@ -24,8 +24,13 @@ struct FinishParams {
 };
 
 template <typename T>
-void launch_residual_dense(double* r, const T* A, int64_t lda, int64_t row0, int ell, int n,
-                           const double* x, const double* b, const Ctl* ctl, cudaStream_t s);
+void launch_residual_dense(double* r, const T* A, int64_t lda, int64_t row0, int64_t brow0,
+                           int ell, int n, const double* x, const double* b, const Ctl* ctl,
+                           cudaStream_t s);
+void launch_gen_block(float* dst, uint64_t seed, int64_t row0, int ell, int n_local,
+                      int64_t n_total, int64_t col0, cudaStream_t s);
+void launch_gen_apply(double* out, uint64_t seed, int64_t m, int n_local, int64_t n_total,
+                      int64_t col0, const double* x, cudaStream_t s);
 template <typename T>
 void launch_residual_csr(double* r, const int64_t* rowptr, const int* col, const T* val,
                          int64_t row0, int ell, const double* x, const double* b, const Ctl* ctl,

@@ -281,6 +281,85 @@ class SinglePassAdapter(RowBlockOperator):
         return self._op
 
 
+def splitmix64(z: np.ndarray) -> np.ndarray:
+    """splitmix64 finaliser on uint64 arrays (wrapping arithmetic)."""
+    z = z + np.uint64(0x9E3779B97F4A7C15)
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+def generated_rows(seed: int, row0: int, rows: int, n: int, col0: int = 0,
+                   cols: int | None = None) -> np.ndarray:
+    """A[i, j] = fp32((2u - 1) / sqrt(n)), u = (splitmix64(seed ^ (i n + j)) >> 11) 2^-53.
+
+    Host evaluation of the configs[4] generator; bit-identical to the device
+    kernel (every operation is exactly rounded IEEE fp64, then one fp32 cast).
+    """
+    cols = n - col0 if cols is None else cols
+    i = (np.uint64(row0) + np.arange(rows, dtype=np.uint64))[:, None]
+    j = (np.uint64(col0) + np.arange(cols, dtype=np.uint64))[None, :]
+    with np.errstate(over="ignore"):
+        z = splitmix64(np.uint64(seed) ^ (i * np.uint64(n) + j))
+    u = (z >> np.uint64(11)).astype(np.float64) * 2.0**-53
+    return ((2.0 * u - 1.0) / np.sqrt(float(n))).astype(np.float32)
+
+
+class GeneratedBlockOperator(RowBlockOperator):
+    """configs[4] streaming operator: rows generated from (seed, i, j), never stored.
+
+    ``fetch_block`` evaluates the generator on the host (for inspection and
+    the oracle); the device path generates each sampled block in-kernel
+    into a ring of window blocks.
+    """
+
+    access_mode = "random_access"
+
+    def __init__(self, n_rows: int, n_cols: int, ell: int, seed: int, b=None):
+        self.n_rows, self.n_cols = int(n_rows), int(n_cols)
+        self.block_rows = int(ell)
+        self.n_blocks = _check_partition(self.n_rows, self.block_rows)
+        self.seed = int(seed)
+        self._b = None
+        if b is not None:
+            self._bind_rhs(b)
+
+    _bind_rhs = DenseBlockOperator._bind_rhs
+
+    def with_rhs(self, b) -> "GeneratedBlockOperator":
+        return GeneratedBlockOperator(self.n_rows, self.n_cols, self.block_rows, self.seed, b)
+
+    def has_rhs(self) -> bool:
+        return self._b is not None
+
+    @property
+    def rhs(self) -> np.ndarray:
+        if self._b is None:
+            raise ValueError("operator has no right-hand side bound")
+        return self._b
+
+    def block_values(self, i: int) -> np.ndarray:
+        s, _ = self.row_range(i)
+        return generated_rows(self.seed, s, self.block_rows, self.n_cols)
+
+    def fetch_block(self, i: int) -> SampleBlock:
+        self._check_index(i)
+        if self._b is None:
+            raise ValueError("operator has no right-hand side bound; use with_rhs(b)")
+        s, e = self.row_range(i)
+        return SampleBlock(i, self.block_values(i).astype(np.float64), self._b[s:e])
+
+    def apply_device(self, x: np.ndarray, device: int = 0) -> np.ndarray:
+        """A x over all rows by the device generator (fp64 accumulation)."""
+        dop = DeviceOperator(n_rows=self.n_rows, n_cols=self.n_cols, ell=self.block_rows, r=0,
+                             layout=_lib.SLIM_GEN_SPLITMIX64, dtype=np.float32, device=device,
+                             gen_seed=self.seed, gen_n_total=self.n_cols)
+        x = np.ascontiguousarray(np.asarray(x, dtype=float))
+        out = np.empty(self.n_rows)
+        dop.call("slim_gen_apply", _lib.dptr(x), _lib.dptr(out))
+        return out
+
+
 # ---------------------------------------------------------------------------
 # device binding
 # ---------------------------------------------------------------------------
@@ -289,13 +368,17 @@ class SinglePassAdapter(RowBlockOperator):
 class DeviceOperator:
     """Owns one C-ABI context holding the operator in HBM."""
 
-    def __init__(self, *, n_rows, n_cols, ell, r, layout, dtype, device=0):
+    def __init__(self, *, n_rows, n_cols, ell, r, layout, dtype, device=0, gen_seed=0,
+                 gen_n_total=0, col_offset=0):
         L = _lib.lib()
         d = _lib.SlimDesc()
         d.n_rows, d.n_cols, d.block_rows, d.memory_r = n_rows, n_cols, ell, r
         d.value_dtype = _lib.SLIM_F32 if np.dtype(dtype) == np.float32 else _lib.SLIM_F64
         d.layout = layout
         d.device = int(device)
+        d.gen_seed = int(gen_seed)
+        d.gen_n_total = int(gen_n_total)
+        d.col_offset = int(col_offset)
         ctx = C.c_void_p()
         rc = L.slim_create(C.byref(ctx), C.byref(d))
         if rc != _lib.SLIM_OK:
@@ -339,6 +422,13 @@ def device_operator(op, r: int, device: int = 0) -> DeviceOperator:
         return dop
     b = np.ascontiguousarray(np.asarray(src.rhs if hasattr(src, "rhs") else None, dtype=float))
     m, n, ell = src.n_rows, src.n_cols, src.block_rows
+    if isinstance(src, GeneratedBlockOperator):
+        dop = DeviceOperator(n_rows=m, n_cols=n, ell=ell, r=r, layout=_lib.SLIM_GEN_SPLITMIX64,
+                             dtype=np.float32, device=device, gen_seed=src.seed, gen_n_total=n)
+        dop.call("slim_set_rhs", _lib.dptr(b))
+        dop.call("slim_finalize_operator")
+        cache[key] = dop
+        return dop
     a = _dense_source(src)
     if a is not None:
         dtype = np.float32 if a.dtype == np.float32 else np.float64

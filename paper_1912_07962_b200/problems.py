@@ -27,7 +27,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .linops import DenseBlockOperator, SparseBlockOperator
+from .linops import DenseBlockOperator, GeneratedBlockOperator, SparseBlockOperator
 
 
 def _rng(seed: int) -> np.random.Generator:
@@ -205,3 +205,20 @@ def tomo3d(grid=128, n_views=180, side=128, sub_rows=2048, ellipsoids=20, seed=4
             blocks.append((nip, ix[gather], d[gather], (sub_rows, nc)))
     x_true = random_ellipsoids(grid, ellipsoids, seed)
     return _finish_tomo(blocks, x_true, noise, seed, dtype)
+
+
+# ---------------------------------------------------------------------------
+# configs[4]: streaming dense LS, A generated by splitmix64, never stored
+# ---------------------------------------------------------------------------
+
+
+def generated_dense(n=65536, m=4194304, ell=256, seed=1912, noise=0.005, device=0):
+    """A[i, j] = fp32((2u - 1) / sqrt(n)) from splitmix64(seed ^ (i n + j));
+    x_true ~ N(0, 1) (Philox key seed); b = A x_true by the device generator
+    (fp64 accumulation) plus Gaussian noise scaled to ``noise`` of ||A x_true||
+    (Philox key seed + 1)."""
+    op = GeneratedBlockOperator(m, n, ell, seed)
+    x_true = _rng(seed).standard_normal(n)
+    clean = op.apply_device(x_true, device=device)
+    b = scaled_noise(clean, noise, _rng(seed + 1))
+    return op.with_rhs(b), b, x_true

@@ -235,3 +235,48 @@ def test_block_residual(slim):
     blk = prob.op.fetch_block(4)
     ref = blk.a_block @ x - blk.b_block
     np.testing.assert_allclose(r, ref, rtol=1e-12, atol=1e-12)
+
+
+# ---------------------------------------------------------------------------
+# configs[4]: generated operator (splitmix64 rows, never stored)
+# ---------------------------------------------------------------------------
+
+
+def test_generated_device_rows_bit_exact(slim):
+    """Device generator == host generator: A x computed both ways agrees to
+    fp64 summation-order level, and one generated block's residual matches."""
+    from paper_1912_07962_b200.linops import GeneratedBlockOperator, device_operator
+    from paper_1912_07962_b200 import _lib
+    from oracle import slimls_oracle as orc
+    n, ell, m = 3000, 40, 400
+    op = GeneratedBlockOperator(m, n, ell, seed=5)
+    x = np.random.default_rng(1).standard_normal(n)
+    dev = op.apply_device(x)
+    host = orc.gen_rows(5, 0, m, n) @ x
+    np.testing.assert_allclose(dev, host, rtol=1e-12, atol=1e-13)
+    op = op.with_rhs(host)
+    dop = device_operator(op, 2)
+    r = np.empty(ell)
+    nrm = np.zeros(1)
+    dop.call("slim_block_residual", 7, _lib.dptr(x), _lib.dptr(r), _lib.dptr(nrm))
+    ref = orc.gen_rows(5, 6 * ell, ell, n) @ x - host[6 * ell:7 * ell]
+    np.testing.assert_allclose(r, ref, atol=1e-12)
+
+
+def test_generated_run_vs_oracle(slim):
+    """configs[4] shape at reduced size: n = 2048, ell = 64, r = 20, lambda = 1e-2,
+    cyclic single pass; window fills at step 21, 30 steps checked."""
+    from oracle import slimls_oracle as orc
+    from paper_1912_07962_b200 import problems
+    n, ell, m, K, r = 2048, 64, 64 * 48, 30, 20
+    op, b, xt = problems.generated_dense(n=n, m=m, ell=ell, seed=1912)
+    traj = slim.run("slimls", slim.SinglePassAdapter(op), slim.Sampler("cyclic", op.n_blocks, 0),
+                    slim.Schedule("constant", 100.0), epochs=K / op.n_blocks, r=r,
+                    references={"x_true": xt})
+    idx = orc.sampler_indices("cyclic", op.n_blocks, 0, K)
+    ref = orc.run_slimls(orc.gen_fetch(1912, n, ell, b), op.n_blocks, n, idx, np.full(K, 100.0),
+                         r=r, references={"x_true": xt})
+    err = np.linalg.norm(traj.x_final - ref.x_final) / np.linalg.norm(ref.x_final)
+    assert err <= 1e-10, err
+    np.testing.assert_allclose(traj.rel_errors["x_true"], ref.rel_errors["x_true"], rtol=1e-10)
+    np.testing.assert_allclose(traj.residual_norms, ref.residual_norms, rtol=1e-10, equal_nan=True)

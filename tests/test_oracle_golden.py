@@ -72,3 +72,20 @@ def test_dual_step_matches_reference():
         blocks = [m[i:i + ell] for i in range(0, m.shape[0], ell)]
         s = orc.dual_step(blocks, d[f"{c}/residual"], float(d[f"{c}/alpha"]))
         np.testing.assert_allclose(s, d[f"{c}/s"], rtol=1e-12, atol=1e-14)
+
+
+def test_generator_vectorised_matches_scalar():
+    """The oracle's vectorised splitmix64 generator equals the scalar restatement."""
+    rows = orc.gen_rows(1912, 5, 3, 1000)
+    for a in range(3):
+        for j in (0, 1, 17, 999):
+            assert rows[a, j] == orc.gen_entry_scalar(1912, 5 + a, j, 1000)
+    # known splitmix64 outputs (published reference values for seed 0 stream)
+    assert orc.splitmix64_scalar(0) == 0xE220A8397B1DCDAF
+
+
+def test_product_generator_matches_oracle():
+    from paper_1912_07962_b200.linops import generated_rows
+    a = generated_rows(77, 1000, 8, 4096).astype(np.float64)
+    b = orc.gen_rows(77, 1000, 8, 4096)
+    assert np.array_equal(a, b)
