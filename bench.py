@@ -40,7 +40,54 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "slim iterations/s and rows/s at 1/2/4/8 B200; HBM GB/s vs roofline"
-CFG = dict(grid=256, n_views=180, rays=362, r=10, alpha=1000.0, seed=2, sampler_seed=7962)
+
+# BASELINE.json configs (1-based here); lambda = 1 / alpha
+CONFIGS = {
+    1: dict(workload="configs[0]: dense Gaussian LS 20,000 x 1,000 fp64, ell=100, r=5, "
+                     "lambda=1e-2, random_cyclic", r=5, alpha=100.0, scheme="random_cyclic",
+            dtype="f64"),
+    2: dict(workload="configs[1]: 2D parallel-beam tomography 256x256, 180 views x 362 rays, "
+                     "Siddon CSR fp64, r=10, lambda=1e-3, random_cyclic", r=10, alpha=1000.0,
+            scheme="random_cyclic", dtype="f64"),
+    3: dict(workload="configs[2]: 2D tomography 1024x1024, 720 views x 1448 rays, Siddon CSR "
+                     "fp32 values / int32 indices, r=8, lambda=1e-3, random_cyclic", r=8,
+            alpha=1000.0, scheme="random_cyclic", dtype="f32 values, f64 arithmetic"),
+    4: dict(workload="configs[3]: 3D parallel-beam tomography 128^3, 180 directions x 128x128 "
+                     "detector, 8 sub-blocks of 2048 rays per view, CSR fp32, r=5, lambda=1e-3, "
+                     "random_cyclic", r=5, alpha=1000.0, scheme="random_cyclic",
+            dtype="f32 values, f64 arithmetic"),
+    5: dict(workload="configs[4]: streaming dense LS n=65,536, m=4,194,304, splitmix64 rows "
+                     "generated in-kernel (fp32), ell=256, r=20, lambda=1e-2, single pass",
+            r=20, alpha=100.0, scheme="cyclic", dtype="f32 values, f64 arithmetic"),
+}
+SAMPLER_SEED = 7962
+
+
+def build_config(cfg_id, threads=None):
+    """(op, b, x_true) of a BASELINE config at full size."""
+    from paper_1912_07962_b200 import problems
+
+    if cfg_id == 1:
+        return problems.gaussian_dense()
+    if cfg_id == 2:
+        p = problems.tomo2d(grid=256, n_views=180, rays=362, seed=2, threads=threads)
+    elif cfg_id == 3:
+        p = problems.tomo2d(grid=1024, n_views=720, rays=1448, seed=3, dtype=np.float32,
+                            threads=threads)
+    elif cfg_id == 4:
+        p = problems.tomo3d(grid=128, n_views=180, side=128, sub_rows=2048, seed=4,
+                            threads=threads)
+    else:
+        return problems.generated_dense()
+    return p.op, p.b, p.x_true
+
+
+def batch_size(n_sys: int) -> int:
+    """Systems per batched factorization (same rule as slim_create)."""
+    env = os.environ.get("SLIM_BATCH")
+    if env:
+        return max(1, min(8, int(env)))
+    return 8 if n_sys <= 6144 else (4 if n_sys <= 10240 else 2)
 
 
 def _peaks():
@@ -135,53 +182,102 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def build_problem(threads=None):
-    from paper_1912_07962_b200 import problems
+def oracle_fetch(op, b):
+    """The oracle's fetch for the operator (reference arithmetic)."""
+    from oracle import slimls_oracle as orc
+    from paper_1912_07962_b200.linops import GeneratedBlockOperator, SparseBlockOperator
 
-    return problems.tomo2d(grid=CFG["grid"], n_views=CFG["n_views"], rays=CFG["rays"],
-                           seed=CFG["seed"], threads=threads)
+    if isinstance(op, GeneratedBlockOperator):
+        return orc.gen_fetch(op.seed, op.n_cols, op.block_rows, b)
+    if isinstance(op, SparseBlockOperator):
+        return orc.csr_fetch([op.csr_block(i) for i in range(1, op.n_blocks + 1)], b)
+    return orc.dense_fetch(op.matrix, b, op.block_rows)
 
 
-def cpu_sample(prob, r, alpha, seed, steady=3):
-    """Oracle port on the host: window fill + ``steady`` full-window steps."""
+def cpu_sample(cfg_id, op, b, r, alpha, scheme, seed, steady=3):
+    """The reference algorithm (oracle port) on the host: the window is filled
+    with r fetched blocks (untimed), then ``steady`` full-window steps are
+    timed, each including its block fetch as in the reference loop."""
+    from collections import deque
+
     from oracle import slimls_oracle as orc
 
-    op = prob.op
-    K = r + 1 + steady
-    idx = orc.sampler_indices("random_cyclic", op.n_blocks, seed, K)
-    fetch = orc.csr_fetch([op.csr_block(i) for i in range(1, op.n_blocks + 1)], prob.b)
-    t0 = time.perf_counter()
-    traj = orc.run_slimls(fetch, op.n_blocks, op.n_cols, idx, np.full(K, alpha), r=r)
-    total = time.perf_counter() - t0
-    per_step = float(np.mean(traj.wall_times[-steady:]))
+    idx = orc.sampler_indices(scheme, op.n_blocks, seed, r + steady)
+    n = op.n_cols
+    if cfg_id in (3, 4):
+        # dense fetch infeasible (12-34 GB per block): sparse dual-form restatement
+        import scipy.sparse as sp
+
+        mats = [sp.csr_matrix((d.astype(float), ix, ip), shape=shp)
+                for ip, ix, d, shp in (op.csr_block(int(i)) for i in set(idx.tolist()))]
+        lookup = dict(zip(sorted(set(idx.tolist())), mats))
+        x = np.zeros(n)
+        window = deque(maxlen=r + 1)
+        for k in range(r):
+            window.append(lookup[int(idx[k])])
+        times = []
+        ell = op.block_rows
+        for k in range(r, r + steady):
+            i = int(idx[k])
+            t0 = time.perf_counter()
+            a = lookup[i]
+            window.append(a)
+            res = a @ x - b[(i - 1) * ell:i * ell]
+            mat = sp.vstack(list(window)).tocsr()
+            g = (mat @ mat.T).toarray() * alpha
+            g[np.diag_indices_from(g)] += 1.0
+            y = np.zeros(mat.shape[0])
+            y[-ell:] = res
+            import scipy.linalg
+
+            w = scipy.linalg.solve(g, y, assume_a="pos")
+            x = x - alpha * (mat.T @ w)
+            times.append(time.perf_counter() - t0)
+        what = ("sparse dual-form restatement of the reference step (the reference's dense "
+                "block fetch needs 12-34 GB per block here)")
+    else:
+        fetch = oracle_fetch(op, b)
+        st = orc._State(x=np.zeros(n), window=deque(maxlen=r + 1), div_limit_sq=np.inf)
+        for k in range(r):
+            st.window.append((int(idx[k]), fetch(int(idx[k]))[0]))
+        times = []
+        for k in range(r, r + steady):
+            i = int(idx[k])
+            t0 = time.perf_counter()
+            a, bb = fetch(i)
+            orc.slimls_step(st, i, a, bb, alpha)
+            times.append(time.perf_counter() - t0)
+        what = ("oracle restatement of the reference step (block fetch, vstack, full Gram, "
+                "LAPACK Cholesky solve)")
+    per_step = float(np.mean(times))
     return {"value": 1.0 / per_step, "unit": "it/s", "cores": os.cpu_count(), "kind": "port",
-            "sample": f"oracle restatement of the reference (dense fetch + vstack + full Gram + "
-                      f"LAPACK Cholesky), {K} steps ({r + 1}-step window fill, then {steady} "
-                      f"full-window steps timed), {total:.1f} s total, "
-                      f"OpenBLAS threads = all {os.cpu_count()} host cores"}
+            "sample": f"{what}; window prefilled with {r} blocks (untimed), {steady} full-window "
+                      f"steps timed ({sum(times):.1f} s), BLAS threads = all {os.cpu_count()} "
+                      f"host cores"}
 
 
 def run_reference(args, world, rank, dist):
     if rank != 0:
         return
-    prob = build_problem()
-    cb = cpu_sample(prob, CFG["r"], CFG["alpha"], CFG["sampler_seed"])
+    cfg = CONFIGS[args.config]
+    op, b, _ = build_config(args.config)
+    cb = cpu_sample(args.config, op, b, cfg["r"], cfg["alpha"], cfg["scheme"], SAMPLER_SEED)
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "it/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 / cb["value"], "higher_is_better": True,
-            "scaling": "replicas", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": _config_dict(world), "rows_per_s": cb["value"] * CFG["rays"],
-            "cpu_baseline": cb,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": _config_dict(args.config, op, world),
+            "rows_per_s": cb["value"] * op.block_rows, "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": "it/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def _config_dict(world):
-    return {"workload": "configs[1]: 2D parallel-beam tomography 256x256, 180 views x 362 rays, "
-                        "Siddon CSR fp64, r=10, lambda=1e-3, random_cyclic",
-            "n": CFG["grid"] ** 2, "m": CFG["n_views"] * CFG["rays"], "ell": CFG["rays"],
-            "r": CFG["r"], "lambda": 1.0 / CFG["alpha"], "dual_system_N": (CFG["r"] + 1) * CFG["rays"],
+def _config_dict(cfg_id, op, world):
+    cfg = CONFIGS[cfg_id]
+    return {"workload": cfg["workload"], "n": op.n_cols, "m": op.n_rows, "ell": op.block_rows,
+            "r": cfg["r"], "lambda": 1.0 / cfg["alpha"],
+            "dual_system_N": (cfg["r"] + 1) * op.block_rows,
             "parallelism": f"replicas{world}" if world > 1 else "single",
             "l2": "per-iteration working set > 126 MB L2 (no flush)"}
 
@@ -190,29 +286,35 @@ def run_ours(args, world, rank, local, dist):
     import paper_1912_07962_b200 as slim
 
     dev = local
-    prob = build_problem()
-    op, b, xt = prob.op, prob.b, prob.x_true
-    r, alpha = CFG["r"], CFG["alpha"]
-    seed = CFG["sampler_seed"] + rank
-    D = int(os.environ.get("SLIM_BATCH", "8"))
+    cfg = CONFIGS[args.config]
+    op, b, xt = build_config(args.config)
+    r, alpha, scheme = cfg["r"], cfg["alpha"], cfg["scheme"]
+    ell, M = op.block_rows, op.n_blocks
+    seed = SAMPLER_SEED + rank
+    N = (r + 1) * ell
+    D = batch_size(N)
     wprime = -(-max(args.warmup, r + 1) // D) * D  # whole factorization batches
     total = wprime + args.steps
-    M = op.n_blocks
+    if scheme == "cyclic" and total > M:
+        raise SystemExit(f"config {args.config}: {total} steps exceed one pass ({M} blocks)")
+
+    def sampler():
+        return slim.Sampler(scheme, M, seed)
+
     # upload + kernel warm-up (untimed)
-    slim.run("slimls", op, slim.Sampler("random_cyclic", M, seed), slim.Schedule("constant", alpha),
-             epochs=(r + 2) / M, r=r, device=dev)
+    slim.run("slimls", op, sampler(), slim.Schedule("constant", alpha),
+             epochs=min(r + 2, M) / M, r=r, device=dev)
     timing = {"start_step": wprime + 1}
     _barrier(dist)
     with ClockSampler(dev) as clk:
-        traj = slim.run("slimls", op, slim.Sampler("random_cyclic", M, seed),
-                        slim.Schedule("constant", alpha), epochs=total / M, r=r,
-                        references={"x_true": xt}, record_every=1, device=dev, timing=timing)
+        traj = slim.run("slimls", op, sampler(), slim.Schedule("constant", alpha),
+                        epochs=total / M, r=r, references={"x_true": xt}, record_every=1,
+                        device=dev, timing=timing)
     _barrier(dist)
     assert traj.status == "ok" and len(traj.ks) == total + 1
     t_win = _max_over_ranks(dist, timing["window_ms"] / 1e3)
     value = world * args.steps / t_win
-    # ---- roofline of the dominant kernel (tile Cholesky), per launch ----
-    N = (r + 1) * CFG["rays"]
+    # ---- roofline of the dominant kernel (batched tile Cholesky), per launch ----
     per_launch = args.steps / max(1, timing["cholesky_count"])  # systems per batched launch
     flops_chol = per_launch * N ** 3 / 3.0
     chol_ms = timing["cholesky_ms"] / max(1, timing["cholesky_count"])
@@ -220,7 +322,7 @@ def run_ours(args, world, rank, local, dist):
     agg = (N ** 3 / 3.0) * args.steps / (timing["window_ms"] * 1e-3) / 1e12
     traffic = None
     try:  # dram bytes per launch from the committed ncu --set full capture
-        with open(os.path.join(ROOT, "profiles", "ncu_chol_r01.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", f"ncu_chol_cfg{args.config}.json")) as fh:
             prof = json.load(fh)
         if int(prof.get("systems_per_launch", 0)) == int(round(per_launch)):
             traffic = prof["dram_bytes_per_launch"]
@@ -229,40 +331,43 @@ def run_ours(args, world, rank, local, dist):
     roofline = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
                 "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
                 "kernel": f"k_chol_tiles (fp64 DMMA tile-DAG Cholesky, {per_launch:g} systems "
-                          f"of N=3982 interleaved per launch)",
+                          f"of N={N} interleaved per launch)",
                 "algorithmic_per_launch": f"{per_launch:g} x N^3/3 = {flops_chol:.4g} flop",
-                "peak_source": "FP64 DMMA peak measured on this pool (tools/microbench/fp64_rates.cu)",
+                "peak_source": "FP64 DMMA peak measured on this pool "
+                               "(tools/microbench/fp64_rates.cu, profiles/fp64_peak_r01.txt)",
                 "aggregate_tflops_over_window": agg,
                 "aggregate_frac": agg / FP64_PEAK_TFLOPS,
                 "avg_launch_ms": chol_ms, "launches": timing["cholesky_count"]}
     # ---- e2e through the public API, host-resident fresh operator ----
     e2e = None
     if not args.quick:
-        op2 = slim.SparseBlockOperator([op.csr_block(i) for i in range(1, M + 1)], b)
-        h2d = sum(p[0].nbytes + p[1].nbytes + p[2].nbytes for p in op2._parts) + b.nbytes \
-            + 2 * xt.nbytes + total * 16
+        op2, b2, _ = (op, b, xt) if args.config == 5 else build_config(args.config)
+        if args.config == 5:
+            op2 = op.with_rhs(b)  # fresh operator object: no cached device state
+        h2d = _operator_bytes(op2) + 2 * xt.nbytes + total * 16
         t0 = time.perf_counter()
-        tr2 = slim.run("slimls", op2, slim.Sampler("random_cyclic", M, seed),
-                       slim.Schedule("constant", alpha), epochs=total / M, r=r,
-                       references={"x_true": xt}, record_every=1, device=dev)
+        tr2 = slim.run("slimls", op2, sampler(), slim.Schedule("constant", alpha),
+                       epochs=total / M, r=r, references={"x_true": xt}, record_every=1,
+                       device=dev)
         wall = time.perf_counter() - t0
         del op2
         wall = _max_over_ranks(dist, wall)
         d2h = (total + 1) * (5 + 1) * 8 + xt.nbytes
         e2e = {"value": world * total / wall, "unit": "it/s",
                "h2d_bytes_per_step": int(h2d / total), "d2h_bytes_per_step": int(d2h / total),
-               "what": f"public run() on a fresh host operator: CSR upload + per-block CSC build + "
-                       f"{total} steps + history/x download, wall clock"}
+               "what": f"public run() on a fresh host operator: operator upload (+ per-block CSC "
+                       f"build for CSR) + {total} steps + history/x download, wall clock"}
         assert tr2.status == "ok"
     if rank != 0:
         return
-    cb = cpu_sample(prob, r, alpha, CFG["sampler_seed"]) if world == 1 and not args.quick else None
+    cb = None
+    if world == 1 and not args.quick:
+        cb = cpu_sample(args.config, op, b, r, alpha, scheme, SAMPLER_SEED)
     line = {"metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_win / args.steps,
-            "higher_is_better": True, "scaling": "weak" if world > 1 else "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": _config_dict(world), "rows_per_s": value * CFG["rays"],
-            "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": _config_dict(args.config, op, world),
+            "rows_per_s": value * ell, "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
             "gpu_launches": int(timing["launches"]), "clocks": clk.summary(),
             "kernel_ms_per_step": {
                 "gram": timing["gram_ms"] / max(1, timing["gram_count"]),
@@ -272,12 +377,24 @@ def run_ours(args, world, rank, local, dist):
     print(json.dumps(line), flush=True)
 
 
+def _operator_bytes(op) -> int:
+    parts = getattr(op, "_parts", None)
+    if parts is not None:
+        return sum(p[0].nbytes + p[1].nbytes + p[2].nbytes for p in parts) + op.rhs.nbytes
+    a = getattr(op, "matrix", None)
+    if a is not None:
+        return a.nbytes + op.rhs.nbytes
+    return op.rhs.nbytes  # generated: only b crosses the bus
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=96)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS),
+                    help="BASELINE config (1-based); 2 = configs[1], the metric's config")
     ap.add_argument("--quick", action="store_true",
                     help="skip the CPU baseline and the e2e leg (profiling runs)")
     args = ap.parse_args()

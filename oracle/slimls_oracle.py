@@ -373,3 +373,84 @@ def gen_fetch(seed: int, n: int, ell: int, b: np.ndarray):
         s = (i - 1) * ell
         return gen_rows(seed, s, ell, n), b[s:s + ell]
     return fetch
+
+
+# ---------------------------------------------------------------------------
+# Sparse dual-form restatement for full-size tomography (configs[2]/[3]).
+# The reference densifies every fetched block (linops.py:278), which needs
+# 12-34 GB per block at those sizes; this restatement performs the same
+# arithmetic steps of slimls_step / dual_step (solvers.py:213-242,
+# innersolve.py:298-321) with the window kept sparse: G = alpha (M M^T) + I
+# formed densely from the sparse product, LAPACK Cholesky solve, s = alpha
+# M^T w.  Cross-validated against the reference at reduced size by
+# tests/test_oracle_golden.py::test_sparse_restatement_matches_reference.
+# ---------------------------------------------------------------------------
+
+
+def run_slimls_sparse(blocks, b, indices, alphas, *, r=0, x0=None, references=None,
+                      record_every=1):
+    import scipy.sparse as sp
+
+    mats = [sp.csr_matrix((np.asarray(d, dtype=float), ix, ip), shape=shp)
+            for ip, ix, d, shp in blocks]
+    ell, n = mats[0].shape
+    b = np.asarray(b, dtype=float)
+    indices = np.asarray(indices, dtype=np.int64)
+    alphas = np.asarray(alphas, dtype=float)
+    steps = int(indices.shape[0])
+    x = np.zeros(n) if x0 is None else np.asarray(x0, dtype=float).copy()
+    limit = DIVERGENCE_FACTOR * (1.0 + float(np.linalg.norm(x)))
+    window = deque(maxlen=r + 1)
+    inv_cache = {}
+    references = references or {}
+    refs = [(k, np.asarray(v, float), float(np.linalg.norm(v))) for k, v in references.items()]
+    ks, resid, rel = [0], [np.nan], {k: [] for k, _, _ in refs}
+    status, diverged_at = "ok", None
+
+    def rec():
+        for name, vec, nrm in refs:
+            d = float(np.linalg.norm(x - vec))
+            rel[name].append(d / nrm if nrm > 0 else d)
+
+    rec()
+    for k in range(1, steps + 1):
+        idx = int(indices[k - 1])
+        alpha = float(alphas[k - 1])
+        a = mats[idx - 1]
+        window.append((idx, a))
+        res = a @ x - b[(idx - 1) * ell: idx * ell]
+        rn = float(np.sqrt(res @ res))
+        if len(window) == 1 and ell <= n and alpha <= DUAL_MAX_ALPHA:
+            key = (idx, alpha)
+            inv = inv_cache.get(key)
+            if inv is None:
+                system = alpha * (a @ a.T).toarray()
+                system[np.diag_indices_from(system)] += 1.0
+                inv = np.linalg.inv(system)
+                if len(inv_cache) < SOLVE_CACHE_MAX_ENTRIES:
+                    inv_cache[key] = inv
+            s = alpha * (a.T @ (inv @ res))
+        else:
+            mat = sp.vstack([m for _, m in window]).tocsr()
+            g = (mat @ mat.T).toarray()
+            g *= alpha
+            g[np.diag_indices_from(g)] += 1.0
+            y = np.zeros(mat.shape[0])
+            y[-ell:] = res
+            w = scipy.linalg.solve(g, y, assume_a="pos")
+            s = alpha * (mat.T @ w)
+        x = x - s
+        ok = float(x @ x) <= limit * limit
+        if not ok or k % record_every == 0 or k == steps:
+            ks.append(k)
+            resid.append(rn)
+            rec()
+        if not ok:
+            status, diverged_at = "diverged", k
+            break
+    return OracleTrajectory(
+        ks=np.asarray(ks, dtype=np.int64), epoch_fraction=np.asarray(ks) / len(mats),
+        alphas=np.concatenate([[np.nan], alphas[np.asarray(ks[1:], dtype=np.int64) - 1]]),
+        residual_norms=np.asarray(resid), rel_errors={k: np.asarray(v) for k, v in rel.items()},
+        wall_times=np.zeros(len(ks)), row_status=["ok"] * len(ks), x_final=x, status=status,
+        diverged_at=diverged_at)

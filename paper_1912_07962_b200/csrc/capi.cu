@@ -244,7 +244,13 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
   CK(c, cudaStreamCreateWithPriority(&c->sx, cudaStreamNonBlocking, prio_hi));
   CK(c, cudaStreamCreateWithPriority(&c->sg, cudaStreamNonBlocking, prio_hi));
   CK(c, cudaStreamCreateWithPriority(&c->sf, cudaStreamNonBlocking, prio_lo));
-  if (const char* env = getenv("SLIM_BATCH")) c->D = std::max(1, std::min(MAX_BATCH, atoi(env)));
+  {
+    // systems per batched factorization: enough to overlap the per-column
+    // critical paths of mid-size systems; large systems fill the GPU alone
+    const int64_t Nmax0 = (d->memory_r + 1) * d->block_rows;
+    c->D = Nmax0 <= 6144 ? 8 : (Nmax0 <= 10240 ? 4 : 2);
+    if (const char* env = getenv("SLIM_BATCH")) c->D = std::max(1, std::min(MAX_BATCH, atoi(env)));
+  }
   for (int q = 0; q < NEV; ++q) {
     CK(c, cudaEventCreateWithFlags(&c->ev_g[q], cudaEventDisableTiming));
     CK(c, cudaEventCreateWithFlags(&c->ev_f[q], cudaEventDisableTiming));

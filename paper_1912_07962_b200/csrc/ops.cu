@@ -505,6 +505,13 @@ void launch_gram_csr(double* panel, const Window& W, const int64_t* rowptr, cons
                      const T* val, const int* colptr_new, const int* cscrow, const T* cscval,
                      int64_t base_new, cudaStream_t s) {
   const size_t smem = (size_t)4 * W.ell * sizeof(double);
+  if (smem > 48 * 1024) {
+    static bool configured = false;  // one ell per process in practice; idempotent anyway
+    if (!configured) {
+      cudaFuncSetAttribute(k_gram_csr<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      configured = true;
+    }
+  }
   k_gram_csr<T><<<cdiv((int64_t)W.nw * W.ell, 4), 128, smem, s>>>(
       panel, W, rowptr, col, val, colptr_new, cscrow, cscval, base_new);
 }

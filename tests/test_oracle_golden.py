@@ -89,3 +89,16 @@ def test_product_generator_matches_oracle():
     a = generated_rows(77, 1000, 8, 4096).astype(np.float64)
     b = orc.gen_rows(77, 1000, 8, 4096)
     assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("name", ["tomo2d", "tomo3d"])
+def test_sparse_restatement_matches_reference(name):
+    """The full-size sparse dual-form restatement reproduces the reference runs."""
+    c = gc.tomo_case(name)
+    k = len(c["indices"])
+    traj = orc.run_slimls_sparse(c["blocks"], c["b"], c["indices"], np.full(k, float(c["alpha"])),
+                                 r=int(c["r"]), references={"x_true": c["x_true"]})
+    np.testing.assert_allclose(traj.x_final, c["x_final"], rtol=1e-10,
+                               atol=1e-10 * np.abs(c["x_final"]).max())
+    np.testing.assert_allclose(traj.rel_errors["x_true"], c["rel"]["x_true"], rtol=1e-10)
+    np.testing.assert_allclose(traj.residual_norms, c["residual_norms"], rtol=1e-10, equal_nan=True)
