@@ -125,9 +125,23 @@ int slim_run(slim_ctx* ctx, const int64_t* block_idx, const double* alphas, int6
  * pinned host operator registered with slim_upload_* (HOST staging).    */
 int slim_set_host_streaming(slim_ctx* ctx, int32_t enable);
 
-/* ---- multi-GPU (column sharding, one NCCL allreduce per step) -------- */
-/* 128-byte NCCL unique id from rank 0 (broadcast by the host runtime).  */
+/* ---- column sharding -------------------------------------
+ * Each rank's context holds the columns [col_offset, col_offset + n_cols)
+ * of A (and the matching slice of x and of every reference).  Per step the
+ * shards exchange, by in-place sum-allreduce: the new Gram panel (on the
+ * x-independent stream), the residual partials A_k x_p (rank 0 subtracts
+ * b_k) and the norm partials; the factorization is replicated (identical
+ * inputs, deterministic kernels), s = alpha M_k^T w and the x update stay
+ * local.                                                                  */
+/* NCCL over NVLink: 128-byte unique id created on rank 0 with
+ * slim_nccl_unique_id and broadcast by the host runtime.                 */
+int slim_nccl_unique_id(void* out_128_bytes);
 int slim_comm_init(slim_ctx* ctx, const void* nccl_unique_id, int32_t nranks, int32_t rank);
+/* In-process group of up to 8 shards on one device, one host thread per
+ * shard (test and single-GPU emulation; no kernel waits on another).    */
+void* slim_local_group_create(int32_t nranks);
+void slim_local_group_destroy(void* group);
+int slim_comm_init_local(slim_ctx* ctx, void* group, int32_t rank);
 
 /* ---- secondary seam and kernel-level entry points -------------------- */
 /* innersolve.dual_step (innersolve.py:305-321): stacked dense window

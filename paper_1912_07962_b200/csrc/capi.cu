@@ -15,8 +15,12 @@
 // consumes batch B); the ring keeps r + 2D Gram panels so no panel is
 // overwritten while a factorization that reads it may still be running.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
+#include <condition_variable>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -41,6 +45,141 @@ struct ProfPair {
 };
 
 }  // namespace
+
+// ---------------------------------------------------------------------------
+// Shard communicators: one in-place sum-allreduce per exchange point.
+//   NcclComm   -- NCCL over NVLink/NVSwitch (one process per GPU), loaded with
+//                 dlopen so the library has no link-time NCCL dependency
+//   LocalComm  -- P column shards on ONE device driven by P host threads: a
+//                 host barrier plus stream-event dependencies and a rank-ordered
+//                 sum kernel.  No kernel ever waits on another rank's kernel.
+// ---------------------------------------------------------------------------
+// Two independent channels: 0 = Gram stream (panels), 1 = x-chain stream
+// (residuals, norms).  Exchanges on one channel are ordered by its stream;
+// the two channels run concurrently, so they never share a buffer or a
+// communicator.
+constexpr int NCHAN = 2;
+
+struct Comm {
+  int nranks = 1, rank = 0;
+  virtual ~Comm() {}
+  virtual cudaError_t allreduce(double* buf, size_t count, cudaStream_t s, int chan,
+                                std::string& err) = 0;
+};
+
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*commSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*) = nullptr;
+  const char* (*errStr)(ncclResult_t) = nullptr;
+};
+
+static NcclApi* nccl_api(std::string& err) {
+  static NcclApi api;
+  static bool tried = false;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> g(mu);
+  if (api.h) return &api;
+  if (tried) {
+    err = "NCCL could not be loaded (set SLIM_NCCL_LIB to libnccl.so.2)";
+    return nullptr;
+  }
+  tried = true;
+  const char* path = getenv("SLIM_NCCL_LIB");
+  void* h = dlopen(path ? path : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) {
+    err = std::string("dlopen NCCL failed: ") + dlerror();
+    return nullptr;
+  }
+  api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
+  api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
+  api.allReduce = (decltype(api.allReduce))dlsym(h, "ncclAllReduce");
+  api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+  api.errStr = (decltype(api.errStr))dlsym(h, "ncclGetErrorString");
+  api.commSplit = (decltype(api.commSplit))dlsym(h, "ncclCommSplit");
+  if (!api.getUniqueId || !api.commInitRank || !api.allReduce || !api.commDestroy || !api.errStr ||
+      !api.commSplit) {
+    err = "NCCL library lacks required symbols";
+    return nullptr;
+  }
+  api.h = h;
+  return &api;
+}
+
+struct NcclComm : Comm {
+  NcclApi* api = nullptr;
+  ncclComm_t comm[NCHAN] = {};
+  ~NcclComm() override {
+    for (auto cm : comm)
+      if (cm) api->commDestroy(cm);
+  }
+  cudaError_t allreduce(double* buf, size_t count, cudaStream_t s, int chan,
+                        std::string& err) override {
+    ncclResult_t r = api->allReduce(buf, buf, count, ncclFloat64, ncclSum, comm[chan], s);
+    if (r != ncclSuccess) {
+      err = std::string("ncclAllReduce: ") + api->errStr(r);
+      return cudaErrorUnknown;
+    }
+    return cudaSuccess;
+  }
+};
+
+struct LocalGroup {
+  int P = 0;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  int64_t gen = 0;
+  std::vector<double*> bufs[NCHAN];
+  std::vector<cudaEvent_t> ev_in[NCHAN], ev_out[NCHAN];
+  void barrier() {
+    std::unique_lock<std::mutex> lk(m);
+    const int64_t g = gen;
+    if (++arrived == P) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+
+struct LocalComm : Comm {
+  LocalGroup* g = nullptr;
+  double* scratch[NCHAN] = {};
+  size_t cap[NCHAN] = {};
+  ~LocalComm() override {
+    for (auto p : scratch)
+      if (p) cudaFree(p);
+  }
+  cudaError_t allreduce(double* buf, size_t count, cudaStream_t s, int chan,
+                        std::string& err) override {
+    if (count > cap[chan]) {
+      if (scratch[chan]) cudaFree(scratch[chan]);
+      cudaError_t e = cudaMalloc(&scratch[chan], count * sizeof(double));
+      if (e != cudaSuccess) {
+        err = "LocalComm scratch allocation failed";
+        return e;
+      }
+      cap[chan] = count;
+    }
+    g->bufs[chan][rank] = buf;
+    cudaEventRecord(g->ev_in[chan][rank], s);
+    g->barrier();  // every rank's buffer and its ready event are published
+    for (int q = 0; q < g->P; ++q) cudaStreamWaitEvent(s, g->ev_in[chan][q], 0);
+    std::vector<const double*> in(g->bufs[chan].begin(), g->bufs[chan].end());
+    launch_group_sum(scratch[chan], in.data(), g->P, (int64_t)count, s);
+    cudaEventRecord(g->ev_out[chan][rank], s);
+    g->barrier();  // every rank has enqueued its reads of all buffers
+    for (int q = 0; q < g->P; ++q) cudaStreamWaitEvent(s, g->ev_out[chan][q], 0);
+    return cudaMemcpyAsync(buf, scratch[chan], count * sizeof(double), cudaMemcpyDeviceToDevice, s);
+  }
+};
 
 struct slim_ctx {
   std::string err;
@@ -68,6 +207,10 @@ struct slim_ctx {
   std::vector<char> h_have;
   bool op_ready = false;
   bool rhs_set = false;
+  // column sharding: exchange of partial sums (nullptr = single context)
+  Comm* comm = nullptr;
+  double* zero_b = nullptr;  // ell zeros: ranks != 0 do not subtract b
+  double* norms = nullptr;   // 1 + MAX_REFS partial norms in sharded mode
   // generated layout (configs[4]): ring of generated window blocks, S x ell x n fp32
   float* gring = nullptr;
   uint64_t gen_seed = 0;
@@ -164,7 +307,9 @@ const char* slim_last_error(const slim_ctx* ctx) {
 }
 
 static void free_all(slim_ctx* c) {
-  void* ptrs[] = {c->gring, c->A, c->b, c->rowptr, c->col, c->val, c->colptr, c->cscrow, c->cscval,
+  delete c->comm;
+  c->comm = nullptr;
+  void* ptrs[] = {c->zero_b, c->norms, c->gring, c->A, c->b, c->rowptr, c->col, c->val, c->colptr, c->cscrow, c->cscval,
                   c->blkbase, c->x, c->ctl, c->panels, c->tickets, c->tflags, c->errflag,
                   c->rvec, c->tvec, c->wvec, c->spart, c->fpart, c->gpart, c->hist, c->iters_dev};
   for (void* p : ptrs)
@@ -554,10 +699,91 @@ int slim_set_host_streaming(slim_ctx* c, int32_t enable) {
   return SLIM_OK;
 }
 
-int slim_comm_init(slim_ctx* c, const void*, int32_t nranks, int32_t) {
-  if (!c) FAIL(c, SLIM_EINVAL, "null argument");
-  if (nranks != 1) FAIL(c, SLIM_ENCCL, "column-sharded multi-GPU runs are not built in this version");
+static int attach_comm(slim_ctx* c, Comm* comm) {
+  CK(c, cudaSetDevice(c->dev));
+  delete c->comm;
+  c->comm = comm;
+  if (!c->zero_b) {
+    ALLOC(c, c->zero_b, sizeof(double) * c->ell);
+    CK(c, cudaMemset(c->zero_b, 0, sizeof(double) * c->ell));
+  }
+  if (!c->norms) ALLOC(c, c->norms, sizeof(double) * (1 + MAX_REFS));
   return SLIM_OK;
+}
+
+int slim_nccl_unique_id(void* out128) {
+  std::string err;
+  NcclApi* api = nccl_api(err);
+  if (!api) FAIL((slim_ctx*)nullptr, SLIM_ENCCL, "%s", err.c_str());
+  ncclUniqueId id;
+  ncclResult_t r = api->getUniqueId(&id);
+  if (r != ncclSuccess) FAIL((slim_ctx*)nullptr, SLIM_ENCCL, "ncclGetUniqueId: %s", api->errStr(r));
+  memcpy(out128, &id, sizeof(id));
+  return SLIM_OK;
+}
+
+int slim_comm_init(slim_ctx* c, const void* uid, int32_t nranks, int32_t rank) {
+  if (!c || !uid) FAIL(c, SLIM_EINVAL, "null argument");
+  if (nranks < 1 || rank < 0 || rank >= nranks) FAIL(c, SLIM_EINVAL, "bad rank %d of %d", rank, nranks);
+  if (nranks == 1) {
+    delete c->comm;
+    c->comm = nullptr;
+    return SLIM_OK;
+  }
+  std::string err;
+  NcclApi* api = nccl_api(err);
+  if (!api) FAIL(c, SLIM_ENCCL, "%s", err.c_str());
+  CK(c, cudaSetDevice(c->dev));
+  NcclComm* nc = new NcclComm();
+  nc->api = api;
+  nc->nranks = nranks;
+  nc->rank = rank;
+  ncclUniqueId id;
+  memcpy(&id, uid, sizeof(id));
+  ncclResult_t r = api->commInitRank(&nc->comm[0], nranks, id, rank);
+  if (r == ncclSuccess) r = api->commSplit(nc->comm[0], 0, rank, &nc->comm[1], nullptr);
+  if (r != ncclSuccess) {
+    delete nc;
+    FAIL(c, SLIM_ENCCL, "ncclCommInitRank/ncclCommSplit: %s", api->errStr(r));
+  }
+  return attach_comm(c, nc);
+}
+
+void* slim_local_group_create(int32_t nranks) {
+  if (nranks < 1 || nranks > 8) return nullptr;
+  LocalGroup* g = new LocalGroup();
+  g->P = nranks;
+  for (int ch = 0; ch < NCHAN; ++ch) {
+    g->bufs[ch].assign(nranks, nullptr);
+    g->ev_in[ch].resize(nranks);
+    g->ev_out[ch].resize(nranks);
+    for (int q = 0; q < nranks; ++q) {
+      cudaEventCreateWithFlags(&g->ev_in[ch][q], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&g->ev_out[ch][q], cudaEventDisableTiming);
+    }
+  }
+  return g;
+}
+
+void slim_local_group_destroy(void* group) {
+  LocalGroup* g = static_cast<LocalGroup*>(group);
+  if (!g) return;
+  for (int ch = 0; ch < NCHAN; ++ch) {
+    for (auto e : g->ev_in[ch]) cudaEventDestroy(e);
+    for (auto e : g->ev_out[ch]) cudaEventDestroy(e);
+  }
+  delete g;
+}
+
+int slim_comm_init_local(slim_ctx* c, void* group, int32_t rank) {
+  LocalGroup* g = static_cast<LocalGroup*>(group);
+  if (!c || !g) FAIL(c, SLIM_EINVAL, "null argument");
+  if (rank < 0 || rank >= g->P) FAIL(c, SLIM_EINVAL, "bad rank %d of %d", rank, g->P);
+  LocalComm* lc = new LocalComm();
+  lc->g = g;
+  lc->nranks = g->P;
+  lc->rank = rank;
+  return attach_comm(c, lc);
 }
 
 int slim_set_timing_start(slim_ctx* c, int64_t k0) {
@@ -574,6 +800,16 @@ int slim_timing(slim_ctx* c, int32_t which, double* ms, int64_t* launches) {
 }
 
 }  // extern "C"
+
+static int comm_allreduce(slim_ctx* c, double* buf, size_t count, cudaStream_t s) {
+  if (!c->comm) return SLIM_OK;
+  std::string err;
+  cudaError_t e = c->comm->allreduce(buf, count, s, s == c->sg ? 0 : 1, err);
+  if (e != cudaSuccess)
+    FAIL(c, c->comm->nranks > 1 && dynamic_cast<NcclComm*>(c->comm) ? SLIM_ENCCL : SLIM_ECUDA,
+         "shard allreduce failed: %s %s", err.c_str(), cudaGetErrorString(e));
+  return SLIM_OK;
+}
 
 // ---------------------------------------------------------------------------
 // one step: enqueue on the three stream kinds
@@ -629,7 +865,8 @@ static int enqueue_gram(slim_ctx* c, const Window& W, int64_t k, int64_t real_bl
   }
   (void)k;
   CKLAUNCH(c);
-  return SLIM_OK;
+  // column shards: every rank holds the products over its columns only
+  return comm_allreduce(c, panel, (size_t)c->panel_stride, c->sg);
 }
 
 static int enqueue_x_chain(slim_ctx* c, const Window& W, int64_t k, int d, double alpha,
@@ -694,8 +931,28 @@ static int enqueue_x_chain(slim_ctx* c, const Window& W, int64_t k, int d, doubl
   F.record = record;
   F.r = c->rvec;
   F.ell = ell;
+  F.split = c->comm ? 1 : 0;
+  F.norms = c->norms;
   launch_finish(F, s);
   CKLAUNCH(c);
+  if (c->comm) {
+    // global ||x||^2 and ||x - ref||^2 over all column shards, then decide
+    int rc = comm_allreduce(c, c->norms, (size_t)(1 + c->nref), s);
+    if (rc) return rc;
+    RecordParams R{};
+    R.ctl = c->ctl;
+    R.norms = c->norms;
+    R.r = c->rvec;
+    R.ell = ell;
+    R.hist = c->hist;
+    R.k = k;
+    R.alpha = alpha;
+    R.record = record;
+    R.nref = c->nref;
+    launch_record(R, s);
+    CKLAUNCH(c);
+    c->launches += 1;
+  }
   (void)row0;
   return SLIM_OK;
 }
@@ -705,26 +962,30 @@ static int enqueue_x_chain(slim_ctx* c, const Window& W, int64_t k, int d, doubl
 static int enqueue_residual(slim_ctx* c, int64_t newblk, int64_t real_blk) {
   const int64_t row0 = newblk * c->ell;
   c->launches += 1;
+  // column shards: rank 0 subtracts b, the partial products are summed
+  const bool use_b = !c->comm || c->comm->rank == 0;
+  const double* bvec = use_b ? c->b : c->zero_b;
+  const int64_t brow = use_b ? real_blk * c->ell : 0;
   if (c->layout == SLIM_GEN_SPLITMIX64) {
-    launch_residual_dense<float>(c->rvec, c->gring, c->n, row0, real_blk * c->ell, (int)c->ell,
-                                 (int)c->n, c->x, c->b, c->ctl, c->sx);
+    launch_residual_dense<float>(c->rvec, c->gring, c->n, row0, brow, (int)c->ell, (int)c->n, c->x,
+                                 bvec, c->ctl, c->sx);
   } else if (c->layout == SLIM_DENSE_ROWMAJOR) {
     if (c->vdt == SLIM_F64)
-      launch_residual_dense<double>(c->rvec, (const double*)c->A, c->n, row0, row0, (int)c->ell,
-                                    (int)c->n, c->x, c->b, c->ctl, c->sx);
+      launch_residual_dense<double>(c->rvec, (const double*)c->A, c->n, row0, brow, (int)c->ell,
+                                    (int)c->n, c->x, bvec, c->ctl, c->sx);
     else
-      launch_residual_dense<float>(c->rvec, (const float*)c->A, c->n, row0, row0, (int)c->ell,
-                                   (int)c->n, c->x, c->b, c->ctl, c->sx);
+      launch_residual_dense<float>(c->rvec, (const float*)c->A, c->n, row0, brow, (int)c->ell,
+                                   (int)c->n, c->x, bvec, c->ctl, c->sx);
   } else {
     if (c->vdt == SLIM_F64)
-      launch_residual_csr<double>(c->rvec, c->rowptr, c->col, (const double*)c->val, row0,
-                                  (int)c->ell, c->x, c->b, c->ctl, c->sx);
+      launch_residual_csr<double>(c->rvec, c->rowptr, c->col, (const double*)c->val, row0, brow,
+                                  (int)c->ell, c->x, bvec, c->ctl, c->sx);
     else
-      launch_residual_csr<float>(c->rvec, c->rowptr, c->col, (const float*)c->val, row0,
-                                 (int)c->ell, c->x, c->b, c->ctl, c->sx);
+      launch_residual_csr<float>(c->rvec, c->rowptr, c->col, (const float*)c->val, row0, brow,
+                                 (int)c->ell, c->x, bvec, c->ctl, c->sx);
   }
   CKLAUNCH(c);
-  return SLIM_OK;
+  return comm_allreduce(c, c->rvec, (size_t)c->ell, c->sx);
 }
 
 // device task map for a batch shape (cached)
@@ -911,7 +1172,7 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
     }
     CK(c, cudaEventRecord(c->ev_x[B % NEV], c->sx));
     // cheap divergence poll: stop enqueueing once the device reported it
-    if ((B & 7) == 7) {
+    if ((B & 7) == 7 && !c->comm) {  // shards must enqueue identical exchange sequences
       if (*c->pin_div != 0) stop = true;
       CK(c, cudaMemcpyAsync(c->pin_div, &c->ctl->diverged_at, sizeof(int64_t),
                             cudaMemcpyDeviceToHost, c->sx));

@@ -85,7 +85,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_residual_csr(double* r, const int64_t* __restrict__ rowptr,
                                                       const int* __restrict__ col,
                                                       const T* __restrict__ val, int64_t row0,
-                                                      int ell, const double* __restrict__ x,
+                                                      int64_t brow0, int ell,
+                                                      const double* __restrict__ x,
                                                       const double* __restrict__ b,
                                                       const Ctl* ctl) {
   if (ctl->diverged_at != 0) return;
@@ -95,7 +96,7 @@ __global__ void __launch_bounds__(256) k_residual_csr(double* r, const int64_t* 
   double s = 0.0;
   for (int64_t e = lo + lane; e < hi; e += 32) s += to_f64(val[e]) * x[col[e]];
   s = warp_sum(s);
-  if (lane == 0) r[row] = s - b[row0 + row];
+  if (lane == 0) r[row] = s - b[brow0 + row];
 }
 
 // ---------------------------------------------------------------------------
@@ -358,6 +359,11 @@ __global__ void __launch_bounds__(256) k_finish(FinishParams F) {
     if (lane == 0) s_rn = v;
   }
   __syncthreads();
+  if (F.split) {
+    if (tid < nq) F.norms[tid] = tot[tid];
+    if (tid == 0) ctl->done = 0u;
+    return;
+  }
   if (tid == 0) {
     ctl->done = 0u;
     ctl->rnorm2 = s_rn;
@@ -378,6 +384,47 @@ __global__ void __launch_bounds__(256) k_finish(FinishParams F) {
 }
 
 __global__ void k_stamp_start(Ctl* ctl) { ctl->t_start_ns = globaltimer_ns(); }
+
+// sharded mode: divergence decision and history row from allreduced norms
+__global__ void k_record(RecordParams R) {
+  Ctl* ctl = R.ctl;
+  if (ctl->diverged_at != 0) return;
+  const int lane = threadIdx.x;
+  double v = 0.0;
+  for (int j = lane; j < R.ell; j += 32) {
+    const double rv = R.r[j];
+    v += rv * rv;
+  }
+  v = warp_sum(v);
+  if (lane != 0) return;
+  ctl->rnorm2 = v;
+  const double nsq = R.norms[0];
+  const bool diverged = !(nsq <= ctl->div_limit_sq);
+  if (diverged) ctl->diverged_at = R.k;
+  if (R.record || diverged) {
+    const int64_t row = ctl->nrows++;
+    double* h = R.hist + row * (SLIM_HIST_FIXED_DEV + R.nref);
+    h[0] = (double)R.k;
+    h[1] = R.alpha;
+    h[2] = sqrt(v);
+    h[3] = (double)(globaltimer_ns() - ctl->t_start_ns);
+    h[4] = diverged ? 1.0 : 0.0;
+    for (int q = 0; q < R.nref; ++q) h[SLIM_HIST_FIXED_DEV + q] = sqrt(R.norms[1 + q]);
+  }
+}
+
+struct GroupIn {
+  const double* p[8];
+};
+
+__global__ void k_group_sum(double* __restrict__ out, GroupIn in, int nin, int64_t count) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double v = 0.0;
+    for (int q = 0; q < nin; ++q) v += in.p[q][i];
+    out[i] = v;
+  }
+}
 
 // ---------------------------------------------------------------------------
 // per-block CSC (built once per operator): column pointers relative to the
@@ -496,9 +543,9 @@ void launch_gen_apply(double* out, uint64_t seed, int64_t m, int n_local, int64_
 }
 template <typename T>
 void launch_residual_csr(double* r, const int64_t* rowptr, const int* col, const T* val,
-                         int64_t row0, int ell, const double* x, const double* b, const Ctl* ctl,
-                         cudaStream_t s) {
-  k_residual_csr<T><<<cdiv(ell, 8), 256, 0, s>>>(r, rowptr, col, val, row0, ell, x, b, ctl);
+                         int64_t row0, int64_t brow0, int ell, const double* x, const double* b,
+                         const Ctl* ctl, cudaStream_t s) {
+  k_residual_csr<T><<<cdiv(ell, 8), 256, 0, s>>>(r, rowptr, col, val, row0, brow0, ell, x, b, ctl);
 }
 template <typename T>
 void launch_gram_csr(double* panel, const Window& W, const int64_t* rowptr, const int* col,
@@ -545,6 +592,14 @@ void launch_finish(const FinishParams& F, cudaStream_t s) {
 }
 int finish_grid(int n) { return (int)cdiv(n, 256); }
 void launch_stamp_start(Ctl* ctl, cudaStream_t s) { k_stamp_start<<<1, 1, 0, s>>>(ctl); }
+void launch_record(const RecordParams& R, cudaStream_t s) { k_record<<<1, 32, 0, s>>>(R); }
+void launch_group_sum(double* out, const double* const* in, int nin, int64_t count,
+                      cudaStream_t s) {
+  GroupIn g{};
+  for (int q = 0; q < nin && q < 8; ++q) g.p[q] = in[q];
+  const unsigned grid = (unsigned)std::min<int64_t>(cdiv(count, 256), 148 * 8);
+  k_group_sum<<<grid, 256, 0, s>>>(out, g, nin, count);
+}
 
 template <typename T>
 void launch_build_csc(int* colptr, int* cscrow, T* cscval, const int64_t* rowptr, const int* col,
@@ -562,7 +617,7 @@ void launch_build_csc(int* colptr, int* cscrow, T* cscval, const int64_t* rowptr
   template void launch_residual_dense<T>(double*, const T*, int64_t, int64_t, int64_t, int, int, \
                                          const double*, const double*, const Ctl*, cudaStream_t); \
   template void launch_residual_csr<T>(double*, const int64_t*, const int*, const T*, int64_t,    \
-                                       int, const double*, const double*, const Ctl*,            \
+                                       int64_t, int, const double*, const double*, const Ctl*,   \
                                        cudaStream_t);                                            \
   template void launch_gram_csr<T>(double*, const Window&, const int64_t*, const int*, const T*,  \
                                    const int*, const int*, const T*, int64_t, cudaStream_t);      \

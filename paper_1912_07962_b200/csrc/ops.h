@@ -21,7 +21,25 @@ struct FinishParams {
   int record;
   const double* r;        // residual (ell) for ||r||
   int ell;
+  // sharded mode: write the block-reduced partial norms to `norms` and stop;
+  // the host allreduces them and k_record takes the decision
+  int split;
+  double* norms;          // 1 + nref
 };
+
+struct RecordParams {
+  Ctl* ctl;
+  const double* norms;    // ||x||^2, ||x - ref_q||^2 (allreduced)
+  const double* r;
+  int ell;
+  double* hist;
+  int64_t k;
+  double alpha;
+  int record, nref;
+};
+void launch_record(const RecordParams& R, cudaStream_t s);
+// out[i] = sum_q in[q][i] in rank order (in-process shard group)
+void launch_group_sum(double* out, const double* const* in, int nin, int64_t count, cudaStream_t s);
 
 template <typename T>
 void launch_residual_dense(double* r, const T* A, int64_t lda, int64_t row0, int64_t brow0,
@@ -33,8 +51,8 @@ void launch_gen_apply(double* out, uint64_t seed, int64_t m, int n_local, int64_
                       int64_t col0, const double* x, cudaStream_t s);
 template <typename T>
 void launch_residual_csr(double* r, const int64_t* rowptr, const int* col, const T* val,
-                         int64_t row0, int ell, const double* x, const double* b, const Ctl* ctl,
-                         cudaStream_t s);
+                         int64_t row0, int64_t brow0, int ell, const double* x, const double* b,
+                         const Ctl* ctl, cudaStream_t s);
 template <typename T>
 void launch_gram_csr(double* panel, const Window& W, const int64_t* rowptr, const int* col,
                      const T* val, const int* colptr_new, const int* cscrow, const T* cscval,

@@ -131,7 +131,7 @@ def run(method: str, op: RowBlockOperator, sampler, schedule: Schedule, *, epoch
         r: int = 0, reg=None, lam: float = 0.0, olbfgs_memory: int = 10,
         x0: np.ndarray | None = None, references: dict | None = None, record_every: int = 1,
         store_iterates: bool = False, inner: str = "auto", device: int = 0,
-        timing: dict | None = None) -> Trajectory:
+        timing: dict | None = None, shard=None) -> Trajectory:
     """Execute ``epochs * M`` sampled slimLS steps on the GPU and record metrics.
 
     Deterministic given the sampler seed (fixed-order device reductions).
@@ -142,6 +142,10 @@ def run(method: str, op: RowBlockOperator, sampler, schedule: Schedule, *, epoch
     selects the first timed step; on output it receives the device time of
     steps start_step..K, per-kernel-class event timings and the number of
     kernels launched in that window.
+
+    ``shard`` (optional, see :mod:`.parallel`): run this process's column
+    shard of a sharded solve; x0 / references are sliced to the shard and
+    ``Trajectory.x_final`` holds the shard's slice of x.
     """
     steps, schedule = _validate(method, op, sampler, epochs, r, reg, lam, inner, record_every,
                                 schedule)
@@ -167,19 +171,26 @@ def run(method: str, op: RowBlockOperator, sampler, schedule: Schedule, *, epoch
     if stream_state is not None and steps > 0 and stream_state != 1:
         raise StreamOrderError(f"single-pass stream expected block {stream_state}, got 1")
 
-    dop = device_operator(op, r, device)
+    x0_full = x0
+    if shard is not None:
+        c0, c1 = shard.col0, shard.col1
+        dop = shard.device_operator(op, r, device)
+        x0 = np.ascontiguousarray(x0[c0:c1])
+        dev_refs = [np.ascontiguousarray(v[c0:c1]) for _, v, _ in ref_items]
+    else:
+        dop = device_operator(op, r, device)
+        dev_refs = [v for _, v, _ in ref_items]
     x0c = np.ascontiguousarray(x0)
     dop.call("slim_set_x", _lib.dptr(x0c))
-    refp = (C.POINTER(C.c_double) * max(1, len(ref_items)))(
-        *[_lib.dptr(v) for _, v, _ in ref_items])
+    refp = (C.POINTER(C.c_double) * max(1, len(ref_items)))(*[_lib.dptr(v) for v in dev_refs])
     dop.call("slim_set_references", len(ref_items), refp)
-    limit = DIVERGENCE_FACTOR * (1.0 + float(np.linalg.norm(x0)))
+    limit = DIVERGENCE_FACTOR * (1.0 + float(np.linalg.norm(x0_full)))
     dop.call("slim_set_divergence_limit", C.c_double(limit))
 
     ncol = _lib.SLIM_HIST_FIXED + len(ref_items)
     cap = steps // record_every + 2
     hist = np.zeros((cap, ncol))
-    iters = np.zeros((cap, op.n_cols)) if store_iterates else None
+    iters = np.zeros((cap, x0.shape[0])) if store_iterates else None
     n_rows = C.c_int64(0)
     status = C.c_int32(0)
     div_at = C.c_int64(0)
@@ -198,11 +209,11 @@ def run(method: str, op: RowBlockOperator, sampler, schedule: Schedule, *, epoch
             timing[key + "_count"] = cnt.value
         dop.call("slim_timing", 4, C.byref(ms), C.byref(cnt))
         timing["launches"] = cnt.value
-    x_final = np.empty(op.n_cols)
+    x_final = np.empty(x0.shape[0])
     dop.call("slim_get_x", _lib.dptr(x_final))
     if stream_state is not None:
         op._next = stream_state + (int(div_at.value) if status.value else steps)
-    return _trajectory(hist[: n_rows.value], iters, x0, ref_items, big_m, status.value,
+    return _trajectory(hist[: n_rows.value], iters, x0_full, ref_items, big_m, status.value,
                        div_at.value, x_final, store_iterates)
 
 

@@ -280,3 +280,105 @@ def test_generated_run_vs_oracle(slim):
     assert err <= 1e-10, err
     np.testing.assert_allclose(traj.rel_errors["x_true"], ref.rel_errors["x_true"], rtol=1e-10)
     np.testing.assert_allclose(traj.residual_norms, ref.residual_norms, rtol=1e-10, equal_nan=True)
+
+
+# ---------------------------------------------------------------------------
+# BASELINE configs at FULL size: the first steps against the oracle (the
+# dense-fetch oracle for configs[1]/[4], the sparse dual-form restatement for
+# configs[2]/[3] whose dense blocks would need 12-34 GB each)
+# ---------------------------------------------------------------------------
+
+
+def _full_vs_oracle(slim, op, b, xt, r, alpha, scheme, K, rtol, sparse=False):
+    from oracle import slimls_oracle as orc
+    M = op.n_blocks
+    traj = slim.run("slimls", op, slim.Sampler(scheme, M, 7962), slim.Schedule("constant", alpha),
+                    epochs=K / M, r=r, references={"x_true": xt})
+    idx = orc.sampler_indices(scheme, M, 7962, K)
+    al = np.full(K, alpha)
+    if sparse:
+        ref = orc.run_slimls_sparse([op.csr_block(i) for i in range(1, M + 1)], b, idx, al, r=r,
+                                    references={"x_true": xt})
+    else:
+        import bench
+        ref = orc.run_slimls(bench.oracle_fetch(op, b), M, op.n_cols, idx, al, r=r,
+                             references={"x_true": xt})
+    err = np.linalg.norm(traj.x_final - ref.x_final) / np.linalg.norm(ref.x_final)
+    assert err <= rtol, err
+    np.testing.assert_allclose(traj.rel_errors["x_true"], ref.rel_errors["x_true"], rtol=rtol)
+    np.testing.assert_allclose(traj.residual_norms, ref.residual_norms, rtol=rtol, equal_nan=True)
+    return err
+
+
+def test_config2_full_size_vs_oracle(slim):
+    """configs[1] at full size: window fill (11 steps) + 3 full-window steps."""
+    import bench
+    op, b, xt = bench.build_config(2)
+    _full_vs_oracle(slim, op, b, xt, 10, 1000.0, "random_cyclic", 14, RTOL64)
+
+
+def test_config3_full_size_first_steps(slim):
+    """configs[2] (1024^2, 720 x 1448, fp32 CSR) at full size, 3 steps vs the
+    sparse restatement (fp32 bar 1e-4; fp64 arithmetic gives ~1e-12)."""
+    import bench
+    op, b, xt = bench.build_config(3)
+    _full_vs_oracle(slim, op, b, xt, 8, 1000.0, "random_cyclic", 3, 1e-10, sparse=True)
+
+
+def test_config4_full_size_first_steps(slim):
+    """configs[3] (128^3, 180 x 128^2 rays in 2048-row sub-blocks, fp32 CSR)."""
+    import bench
+    op, b, xt = bench.build_config(4)
+    _full_vs_oracle(slim, op, b, xt, 5, 1000.0, "random_cyclic", 3, 1e-10, sparse=True)
+
+
+def test_config5_full_size_first_steps(slim):
+    """configs[4] (n = 65,536 generated rows) at full size, 3 single-pass steps."""
+    import bench
+    op, b, xt = bench.build_config(5)
+    _full_vs_oracle(slim, op, b, xt, 20, 100.0, "cyclic", 3, 1e-10)
+
+
+# ---------------------------------------------------------------------------
+# column sharding through the real GPU path: P shards on one device (local
+# group, one host thread per shard) against the unsharded run
+# ---------------------------------------------------------------------------
+
+
+def _sharded_vs_single(slim, op, xt, scheme, seed, alpha, r, K, P):
+    from paper_1912_07962_b200.parallel import LocalGroup
+    M = op.n_blocks
+    kw = dict(epochs=K / M, r=r, references={"x_true": xt})
+    single = slim.run("slimls", op, slim.Sampler(scheme, M, seed), slim.Schedule("constant", alpha),
+                      **kw)
+    group = LocalGroup(P)
+    full, per = group.run("slimls", op, lambda: slim.Sampler(scheme, M, seed),
+                          slim.Schedule("constant", alpha), **kw)
+    err = np.linalg.norm(full.x_final - single.x_final) / np.linalg.norm(single.x_final)
+    assert err <= 1e-10, err
+    np.testing.assert_allclose(full.rel_errors["x_true"], single.rel_errors["x_true"], rtol=1e-10)
+    np.testing.assert_allclose(full.residual_norms, single.residual_norms, rtol=1e-10,
+                               equal_nan=True)
+    for t in per[1:]:  # every shard records the same global history
+        np.testing.assert_array_equal(t.rel_errors["x_true"], per[0].rel_errors["x_true"])
+        assert np.array_equal(t.ks, per[0].ks)
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_sharded_dense(slim, P):
+    c = gc.dense_case("dense_dual")
+    op = slim.DenseBlockOperator(c["A"], 20, c["b"])
+    _sharded_vs_single(slim, op, c["refs"]["x_true"], "random_cyclic", 11, 100.0, 4, 60, P)
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_sharded_csr_tomography(slim, P):
+    from paper_1912_07962_b200 import problems
+    prob = problems.tomo2d(grid=48, n_views=30, rays=68, seed=6)
+    _sharded_vs_single(slim, prob.op, prob.x_true, "random_cyclic", 5, 1000.0, 6, 40, P)
+
+
+def test_sharded_generated(slim):
+    from paper_1912_07962_b200 import problems
+    op, b, xt = problems.generated_dense(n=1536, m=64 * 30, ell=64, seed=9)
+    _sharded_vs_single(slim, op, xt, "cyclic", 0, 100.0, 8, 20, 2)
