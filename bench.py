@@ -273,12 +273,13 @@ def run_reference(args, world, rank, dist):
     print(json.dumps(line), flush=True)
 
 
-def _config_dict(cfg_id, op, world):
+def _config_dict(cfg_id, op, world, sharded=False):
     cfg = CONFIGS[cfg_id]
     return {"workload": cfg["workload"], "n": op.n_cols, "m": op.n_rows, "ell": op.block_rows,
             "r": cfg["r"], "lambda": 1.0 / cfg["alpha"],
             "dual_system_N": (cfg["r"] + 1) * op.block_rows,
-            "parallelism": f"replicas{world}" if world > 1 else "single",
+            "parallelism": (f"columns{world}" if sharded else f"replicas{world}") if world > 1
+            else "single",
             "l2": "per-iteration working set > 126 MB L2 (no flush)"}
 
 
@@ -298,22 +299,35 @@ def run_ours(args, world, rank, local, dist):
     if scheme == "cyclic" and total > M:
         raise SystemExit(f"config {args.config}: {total} steps exceed one pass ({M} blocks)")
 
+    sharded = world > 1 and args.shard == "columns"
+    if sharded:
+        from paper_1912_07962_b200.parallel import NcclShard
+
+        import torch
+
+        torch.cuda.set_device(dev)
+        shard = NcclShard.from_torch(op.n_cols)
+        seed = SAMPLER_SEED  # one solve: every shard walks the same index trace
+    else:
+        shard = None
+
     def sampler():
         return slim.Sampler(scheme, M, seed)
 
     # upload + kernel warm-up (untimed)
     slim.run("slimls", op, sampler(), slim.Schedule("constant", alpha),
-             epochs=min(r + 2, M) / M, r=r, device=dev)
+             epochs=min(r + 2, M) / M, r=r, device=dev, shard=shard)
     timing = {"start_step": wprime + 1}
     _barrier(dist)
     with ClockSampler(dev) as clk:
         traj = slim.run("slimls", op, sampler(), slim.Schedule("constant", alpha),
                         epochs=total / M, r=r, references={"x_true": xt}, record_every=1,
-                        device=dev, timing=timing)
+                        device=dev, timing=timing, shard=shard)
     _barrier(dist)
     assert traj.status == "ok" and len(traj.ks) == total + 1
     t_win = _max_over_ranks(dist, timing["window_ms"] / 1e3)
-    value = world * args.steps / t_win
+    # replicas: every rank solves its own problem; columns: all ranks one solve
+    value = (1 if sharded else world) * args.steps / t_win
     # ---- roofline of the dominant kernel (batched tile Cholesky), per launch ----
     per_launch = args.steps / max(1, timing["cholesky_count"])  # systems per batched launch
     flops_chol = per_launch * N ** 3 / 3.0
@@ -340,7 +354,7 @@ def run_ours(args, world, rank, local, dist):
                 "avg_launch_ms": chol_ms, "launches": timing["cholesky_count"]}
     # ---- e2e through the public API, host-resident fresh operator ----
     e2e = None
-    if not args.quick:
+    if not args.quick and not sharded:
         op2, b2, _ = (op, b, xt) if args.config == 5 else build_config(args.config)
         if args.config == 5:
             op2 = op.with_rhs(b)  # fresh operator object: no cached device state
@@ -365,8 +379,9 @@ def run_ours(args, world, rank, local, dist):
         cb = cpu_sample(args.config, op, b, r, alpha, scheme, SAMPLER_SEED)
     line = {"metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_win / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": _config_dict(args.config, op, world),
+            "higher_is_better": True, "scaling": "strong" if sharded else "weak",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": _config_dict(args.config, op, world, sharded),
             "rows_per_s": value * ell, "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
             "gpu_launches": int(timing["launches"]), "clocks": clk.summary(),
             "kernel_ms_per_step": {
@@ -395,6 +410,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS),
                     help="BASELINE config (1-based); 2 = configs[1], the metric's config")
+    ap.add_argument("--shard", default="replicas", choices=["replicas", "columns"],
+                    help="N > 1: independent replicas (default) or one column-sharded solve "
+                         "(NCCL allreduce of Gram panel / residual / norm partials per step)")
     ap.add_argument("--quick", action="store_true",
                     help="skip the CPU baseline and the e2e leg (profiling runs)")
     args = ap.parse_args()

@@ -29,6 +29,7 @@
 #include <string>
 #include <vector>
 
+#include "gram_tc.h"
 #include "kernels.h"
 #include "ops.h"
 #include "slimb200.h"
@@ -213,6 +214,9 @@ struct slim_ctx {
   double* norms = nullptr;   // 1 + MAX_REFS partial norms in sharded mode
   // generated layout (configs[4]): ring of generated window blocks, S x ell x n fp32
   float* gring = nullptr;
+  float* gring_hi = nullptr;  // 3xTF32 split of the ring for the tcgen05 Gram
+  float* gring_lo = nullptr;
+  bool use_tc = false;
   uint64_t gen_seed = 0;
   int64_t gen_n_total = 0, col_offset = 0;
   // state
@@ -309,7 +313,7 @@ const char* slim_last_error(const slim_ctx* ctx) {
 static void free_all(slim_ctx* c) {
   delete c->comm;
   c->comm = nullptr;
-  void* ptrs[] = {c->zero_b, c->norms, c->gring, c->A, c->b, c->rowptr, c->col, c->val, c->colptr, c->cscrow, c->cscval,
+  void* ptrs[] = {c->gring_hi, c->gring_lo, c->zero_b, c->norms, c->gring, c->A, c->b, c->rowptr, c->col, c->val, c->colptr, c->cscrow, c->cscval,
                   c->blkbase, c->x, c->ctl, c->panels, c->tickets, c->tflags, c->errflag,
                   c->rvec, c->tvec, c->wvec, c->spart, c->fpart, c->gpart, c->hist, c->iters_dev};
   for (void* p : ptrs)
@@ -435,8 +439,15 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
   ALLOC(c, c->tvec, sizeof(double) * c->Tmax * TB);
   ALLOC(c, c->wvec, sizeof(double) * c->Tmax * TB);
   // M^T w: split the window rows over CTAs when n alone cannot fill the GPU
-  if (c->layout == SLIM_GEN_SPLITMIX64)
+  if (c->layout == SLIM_GEN_SPLITMIX64) {
     ALLOC(c, c->gring, sizeof(float) * (size_t)c->S * ell * c->n);
+    const char* env = getenv("SLIM_GRAM_TC");
+    c->use_tc = gram_tc_supported((int)ell, c->n) && !(env && env[0] == '0');
+    if (c->use_tc) {
+      ALLOC(c, c->gring_hi, sizeof(float) * (size_t)c->S * ell * c->n);
+      ALLOC(c, c->gring_lo, sizeof(float) * (size_t)c->S * ell * c->n);
+    }
+  }
   if (c->layout != SLIM_CSR_PERBLOCK) {
     const int64_t cols_ctas = (c->n + 255) / 256;
     int ns = (int)std::max<int64_t>(1, std::min<int64_t>(32, (4 * 148) / std::max<int64_t>(1, cols_ctas)));
@@ -446,7 +457,9 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
     const int64_t tiles = ((Nmax + 63) / 64) * ((ell + 63) / 64);
     int gs = (int)std::max<int64_t>(1, std::min<int64_t>((2 * 148 + tiles - 1) / tiles, (c->n + 255) / 256));
     c->nsplit_gram = gs;
-    ALLOC(c, c->gpart, sizeof(double) * (size_t)gs * Nmax * ell);
+    int parts = gs;
+    if (c->use_tc) parts = std::max<int>(parts, (int)(c->n / gram_tc_kchunk(c->n, 1)));
+    ALLOC(c, c->gpart, sizeof(double) * (size_t)parts * Nmax * ell);
   }
   ALLOC(c, c->spart, sizeof(double) * (size_t)c->nsplit_mtw * c->n);
   ALLOC(c, c->fpart, sizeof(double) * (size_t)finish_grid((int)c->n) * (1 + MAX_REFS));
@@ -840,12 +853,38 @@ static int enqueue_gram(slim_ctx* c, const Window& W, int64_t k, int64_t real_bl
   double* panel = c->panels + (int64_t)slot_new * c->panel_stride;
   const int64_t newblk = W.blk[W.nw - 1];
   if (c->layout == SLIM_GEN_SPLITMIX64) {
-    launch_gen_block(c->gring + (int64_t)slot_new * c->ell * c->n, c->gen_seed, real_blk * c->ell,
+    const int64_t off = (int64_t)slot_new * c->ell * c->n;
+    launch_gen_block(c->gring + off, c->use_tc ? c->gring_hi + off : nullptr,
+                     c->use_tc ? c->gring_lo + off : nullptr, c->gen_seed, real_blk * c->ell,
                      (int)c->ell, (int)c->n, c->gen_n_total, c->col_offset, c->sg);
     CKLAUNCH(c);
     c->launches += 3;
-    launch_gram_dense<float>(panel, c->gpart, c->nsplit_gram, W, c->gring, c->n,
-                             newblk * c->ell, (int)c->n, c->sg);
+    if (c->use_tc) {
+      // tcgen05 3xTF32: 128-row window tiles straight from the generated ring
+      GramTcParams G{};
+      const int N = W.nw * (int)c->ell;
+      const int mtiles = N / 128;
+      G.out = c->gpart;
+      G.nwin = N;
+      G.ell = (int)c->ell;
+      G.kchunk = gram_tc_kchunk(c->n, mtiles);
+      G.brow = slot_new * (int)c->ell;
+      for (int t = 0; t < mtiles; ++t) {
+        const int p = 128 * t, P = p / (int)c->ell;
+        G.arow[t] = W.slot[P] * (int)c->ell + (p - P * (int)c->ell);
+      }
+      const int kcs = (int)(c->n / G.kchunk);
+      CK(c, launch_gram_tf32x3(c->gring_hi, c->gring_lo, (int64_t)c->S * c->ell, c->n, G, mtiles,
+                               kcs, c->sg));
+      launch_gram_reduce(panel, W, c->gpart, kcs, c->sg);
+      // the self-product diagonal (row sums of squares) exactly in fp64
+      launch_gram_diag_fp64(panel + (int64_t)slot_new * c->ell * c->ell, c->ell, c->gring + off,
+                            (int)c->ell, (int)c->n, c->sg);
+      c->launches += 2;
+    } else {
+      launch_gram_dense<float>(panel, c->gpart, c->nsplit_gram, W, c->gring, c->n,
+                               newblk * c->ell, (int)c->n, c->sg);
+    }
   } else if (c->layout == SLIM_DENSE_ROWMAJOR) {
     if (c->vdt == SLIM_F64)
       c->launches += 2, launch_gram_dense<double>(panel, c->gpart, c->nsplit_gram, W, (const double*)c->A, c->n,
@@ -1249,8 +1288,8 @@ extern "C" int slim_block_residual(slim_ctx* c, int64_t block, const double* x, 
   h.div_limit_sq = c->div_limit * c->div_limit;
   CK(c, cudaMemcpy(c->ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice));
   if (c->layout == SLIM_GEN_SPLITMIX64) {
-    launch_gen_block(c->gring, c->gen_seed, (block - 1) * c->ell, (int)c->ell, (int)c->n,
-                     c->gen_n_total, c->col_offset, c->sx);
+    launch_gen_block(c->gring, nullptr, nullptr, c->gen_seed, (block - 1) * c->ell, (int)c->ell,
+                     (int)c->n, c->gen_n_total, c->col_offset, c->sx);
   }
   int rc = enqueue_residual(c, c->layout == SLIM_GEN_SPLITMIX64 ? 0 : block - 1, block - 1);
   if (rc) return rc;

@@ -67,6 +67,16 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 template <typename T>
 __device__ __forceinline__ double to_f64(T v) { return static_cast<double>(v); }
 
+// 3xTF32 operand split: x ~= hi + lo, both exact TF32 (round to nearest)
+__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
+  uint32_t h, l;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+  const float r = x - __uint_as_float(h);
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(r));
+  hi = __uint_as_float(h);
+  lo = __uint_as_float(l);
+}
+
 // splitmix64 (configs[4] generator): z += golden; z = (z ^ z>>30) * c1;
 // z = (z ^ z>>27) * c2; z ^= z>>31
 __host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t z) {

@@ -53,8 +53,10 @@ __device__ __forceinline__ float gen_elem(uint64_t seed, uint64_t i, uint64_t j,
   return (float)((2.0 * u - 1.0) / sqrt_n);
 }
 
-// one sampled block (ell rows from global row row0) into dst (ell x n_local)
-__global__ void __launch_bounds__(256) k_gen_block(float* __restrict__ dst, uint64_t seed,
+// one sampled block (ell rows from global row row0) into dst (ell x n_local);
+// with hi/lo non-null also the 3xTF32 operand split for the tensor-core Gram
+__global__ void __launch_bounds__(256) k_gen_block(float* __restrict__ dst, float* __restrict__ hi,
+                                                   float* __restrict__ lo, uint64_t seed,
                                                    int64_t row0, int ell, int n_local,
                                                    int64_t n_total, int64_t col0) {
   const double sq = sqrt((double)n_total);
@@ -62,7 +64,15 @@ __global__ void __launch_bounds__(256) k_gen_block(float* __restrict__ dst, uint
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t a = e / n_local, c = e - a * n_local;
-    dst[e] = gen_elem(seed, (uint64_t)(row0 + a), (uint64_t)(col0 + c), (uint64_t)n_total, sq);
+    const float v =
+        gen_elem(seed, (uint64_t)(row0 + a), (uint64_t)(col0 + c), (uint64_t)n_total, sq);
+    dst[e] = v;
+    if (hi != nullptr) {
+      float h, l;
+      split_tf32(v, h, l);
+      hi[e] = h;
+      lo[e] = l;
+    }
   }
 }
 
@@ -531,11 +541,11 @@ void launch_residual_dense(double* r, const T* A, int64_t lda, int64_t row0, int
                            cudaStream_t s) {
   k_residual_dense<T><<<cdiv(ell, 8), 256, 0, s>>>(r, A, lda, row0, brow0, ell, n, x, b, ctl);
 }
-void launch_gen_block(float* dst, uint64_t seed, int64_t row0, int ell, int n_local,
-                      int64_t n_total, int64_t col0, cudaStream_t s) {
+void launch_gen_block(float* dst, float* hi, float* lo, uint64_t seed, int64_t row0, int ell,
+                      int n_local, int64_t n_total, int64_t col0, cudaStream_t s) {
   const int64_t total = (int64_t)ell * n_local;
   const unsigned grid = (unsigned)std::min<int64_t>(cdiv(total, 256), 148 * 16);
-  k_gen_block<<<grid, 256, 0, s>>>(dst, seed, row0, ell, n_local, n_total, col0);
+  k_gen_block<<<grid, 256, 0, s>>>(dst, hi, lo, seed, row0, ell, n_local, n_total, col0);
 }
 void launch_gen_apply(double* out, uint64_t seed, int64_t m, int n_local, int64_t n_total,
                       int64_t col0, const double* x, cudaStream_t s) {
@@ -573,6 +583,35 @@ void launch_gram_dense(double* panel, double* part, int nsplit, const Window& W,
   k_gram_dense<T><<<grid, 256, 0, s>>>(part, W, A, lda, newrow0, n, klen);
   k_gram_reduce<<<cdiv((int64_t)N * W.ell, 256), 256, 0, s>>>(panel, W, part, zs);
 }
+// exact fp64 diagonal of A_k A_k^T (row sums of squares) into the panel: the
+// tensor core accumulates in truncating fp32, which biases these large
+// all-positive sums; every other entry has mixed signs and small partials
+__global__ void __launch_bounds__(256) k_gram_diag_fp64(double* __restrict__ panel_diag, int64_t ld,
+                                                        const float* __restrict__ A, int ell,
+                                                        int n) {
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= ell) return;
+  const float* a = A + (int64_t)row * n;
+  double s = 0.0;
+  for (int c = lane; c < n; c += 32) {
+    const double v = (double)a[c];
+    s += v * v;
+  }
+  s = warp_sum(s);
+  if (lane == 0) panel_diag[(int64_t)row * ld + row] = s;
+}
+
+void launch_gram_diag_fp64(double* panel_diag, int64_t ld, const float* A, int ell, int n,
+                           cudaStream_t s) {
+  k_gram_diag_fp64<<<cdiv(ell, 8), 256, 0, s>>>(panel_diag, ld, A, ell, n);
+}
+
+void launch_gram_reduce(double* panel, const Window& W, const double* part, int nsplit,
+                        cudaStream_t s) {
+  const int64_t cnt = (int64_t)W.nw * W.ell * W.ell;
+  k_gram_reduce<<<cdiv(cnt, 256), 256, 0, s>>>(panel, W, part, nsplit);
+}
+
 template <typename T>
 void launch_mtw_dense(double* part, int nsplit, const Window& W, const T* A, int64_t lda, int n,
                       const double* w, const Ctl* ctl, cudaStream_t s) {

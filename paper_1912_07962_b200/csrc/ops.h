@@ -45,8 +45,8 @@ template <typename T>
 void launch_residual_dense(double* r, const T* A, int64_t lda, int64_t row0, int64_t brow0,
                            int ell, int n, const double* x, const double* b, const Ctl* ctl,
                            cudaStream_t s);
-void launch_gen_block(float* dst, uint64_t seed, int64_t row0, int ell, int n_local,
-                      int64_t n_total, int64_t col0, cudaStream_t s);
+void launch_gen_block(float* dst, float* hi, float* lo, uint64_t seed, int64_t row0, int ell,
+                      int n_local, int64_t n_total, int64_t col0, cudaStream_t s);
 void launch_gen_apply(double* out, uint64_t seed, int64_t m, int n_local, int64_t n_total,
                       int64_t col0, const double* x, cudaStream_t s);
 template <typename T>
@@ -72,6 +72,10 @@ void launch_build_csc(int* colptr, int* cscrow, T* cscval, const int64_t* rowptr
                       const T* val, const int64_t* blkbase, int64_t m, int ell, int n,
                       int64_t nblocks, cudaStream_t s);
 void launch_finish(const FinishParams& F, cudaStream_t s);
+void launch_gram_reduce(double* panel, const Window& W, const double* part, int nsplit,
+                        cudaStream_t s);
+void launch_gram_diag_fp64(double* panel_diag, int64_t ld, const float* A, int ell, int n,
+                           cudaStream_t s);
 int finish_grid(int n);
 void launch_stamp_start(Ctl* ctl, cudaStream_t s);
 
