@@ -415,6 +415,13 @@ def _dense_source(op):
 def device_operator(op, r: int, device: int = 0) -> DeviceOperator:
     """Upload ``op`` (once per (device, r)) and return its device context."""
     src = op.source if isinstance(op, SinglePassAdapter) else getattr(op, "_op", op)
+    if hasattr(src, "consume_all") and src.access_mode == "single_pass":
+        # a file stream: one in-order pass into HBM, cached on the stream object
+        cache = src.__dict__.setdefault("_slim_device_cache", {})
+        key = (int(device), int(r), "stream")
+        if key not in cache:
+            cache[key] = device_operator(src.consume_all(), r, device)
+        return cache[key]
     cache = src.__dict__.setdefault("_slim_device_cache", {})
     key = (int(device), int(r), id(getattr(src, "_b", None)))
     dop = cache.get(key)

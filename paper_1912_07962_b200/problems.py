@@ -222,3 +222,64 @@ def generated_dense(n=65536, m=4194304, ell=256, seed=1912, noise=0.005, device=
     clean = op.apply_device(x_true, device=device)
     b = scaled_noise(clean, noise, _rng(seed + 1))
     return op.with_rhs(b), b, x_true
+
+
+# ---------------------------------------------------------------------------
+# Shepp-Logan head phantoms for the reference's tomo2d / tomo3d problem kinds
+# (tomo.py:100-135): the published 2D table (Shepp & Logan 1974) and the
+# contrast-enhanced 3D variant, cell-centre rasterisation on [-1, 1]^d.
+# ---------------------------------------------------------------------------
+
+# (x0, y0, semi_a, semi_b, angle_deg, additive intensity)
+_SL2D = ((0.0, 0.0, 0.69, 0.92, 0.0, 2.0), (0.0, -0.0184, 0.6624, 0.874, 0.0, -0.98),
+         (0.22, 0.0, 0.11, 0.31, -18.0, -0.02), (-0.22, 0.0, 0.16, 0.41, 18.0, -0.02),
+         (0.0, 0.35, 0.21, 0.25, 0.0, 0.01), (0.0, 0.1, 0.046, 0.046, 0.0, 0.01),
+         (0.0, -0.1, 0.046, 0.046, 0.0, 0.01), (-0.08, -0.605, 0.046, 0.023, 0.0, 0.01),
+         (0.0, -0.605, 0.023, 0.023, 0.0, 0.01), (0.06, -0.605, 0.023, 0.046, 0.0, 0.01))
+# (intensity, semi_a, semi_b, semi_c, x0, y0, z0, phi, theta, psi), z-x-z Euler degrees
+_SL3D = ((1.0, 0.69, 0.92, 0.81, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0),
+         (-0.8, 0.6624, 0.874, 0.78, 0.0, -0.0184, 0.0, 0.0, 0.0, 0.0),
+         (-0.2, 0.11, 0.31, 0.22, 0.22, 0.0, 0.0, -18.0, 0.0, 10.0),
+         (-0.2, 0.16, 0.41, 0.28, -0.22, 0.0, 0.0, 18.0, 0.0, 10.0),
+         (0.1, 0.21, 0.25, 0.41, 0.0, 0.35, -0.15, 0.0, 0.0, 0.0),
+         (0.1, 0.046, 0.046, 0.05, 0.0, 0.1, 0.25, 0.0, 0.0, 0.0),
+         (0.1, 0.046, 0.046, 0.05, 0.0, -0.1, 0.25, 0.0, 0.0, 0.0),
+         (0.1, 0.046, 0.023, 0.05, -0.08, -0.605, 0.0, 0.0, 0.0, 0.0),
+         (0.1, 0.023, 0.023, 0.02, 0.0, -0.605, 0.0, 0.0, 0.0, 0.0),
+         (0.1, 0.023, 0.046, 0.02, 0.06, -0.605, 0.0, 0.0, 0.0, 0.0))
+
+
+def shepp_logan_2d(n: int) -> np.ndarray:
+    centers = -1.0 + (np.arange(n) + 0.5) * (2.0 / n)
+    yy, xx = np.meshgrid(centers, centers, indexing="ij")
+    img = np.zeros((n, n))
+    for x0, y0, sa, sb, ang, value in _SL2D:
+        c, s = np.cos(np.radians(ang)), np.sin(np.radians(ang))
+        u = (xx - x0) * c + (yy - y0) * s
+        v = -(xx - x0) * s + (yy - y0) * c
+        img[(u / sa) ** 2 + (v / sb) ** 2 <= 1.0] += value
+    img[np.abs(img) < 1e-15] = 0.0
+    return img.ravel()
+
+
+def _euler_zxz(phi, theta, psi):
+    cphi, sphi = np.cos(np.radians(phi)), np.sin(np.radians(phi))
+    cth, sth = np.cos(np.radians(theta)), np.sin(np.radians(theta))
+    cpsi, spsi = np.cos(np.radians(psi)), np.sin(np.radians(psi))
+    return np.array([
+        [cpsi * cphi - cth * sphi * spsi, cpsi * sphi + cth * cphi * spsi, spsi * sth],
+        [-spsi * cphi - cth * sphi * cpsi, -spsi * sphi + cth * cphi * cpsi, cpsi * sth],
+        [sth * sphi, -sth * cphi, cth]])
+
+
+def shepp_logan_3d(n: int) -> np.ndarray:
+    centers = -1.0 + (np.arange(n) + 0.5) * (2.0 / n)
+    zz, yy, xx = np.meshgrid(centers, centers, centers, indexing="ij")
+    vol = np.zeros((n, n, n))
+    pts = np.stack([xx.ravel(), yy.ravel(), zz.ravel()])
+    for value, sa, sb, sc, x0, y0, z0, phi, theta, psi in _SL3D:
+        local = _euler_zxz(phi, theta, psi) @ (pts - np.array([[x0], [y0], [z0]]))
+        inside = (local[0] / sa) ** 2 + (local[1] / sb) ** 2 + (local[2] / sc) ** 2 <= 1.0
+        vol.ravel()[inside] += value
+    vol[np.abs(vol) < 1e-15] = 0.0
+    return vol.ravel()

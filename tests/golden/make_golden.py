@@ -250,7 +250,82 @@ def dual_step_golden():
     np.savez_compressed(os.path.join(HERE, "dual_step.npz"), **out)
 
 
+HARNESS_CFGS = {
+    "gauss": """
+[problem]
+kind = gaussian
+m = 240
+n = 40
+blocks = 20
+noise_level = 0.01
+seed = 3
+[method]
+name = slimls
+r = 2
+[schedule]
+kind = constant
+alpha = 2.0
+[sampler]
+scheme = random_cyclic
+[run]
+epochs = 2
+replicates = 3
+base_seed = 11
+error_references = x_true,x_ls
+record_every = 4
+""",
+    "wedge": """
+[problem]
+kind = tomo2d
+grid = 24
+views = 12
+half_angle = 60
+noise_level = 0.01
+seed = 2
+[method]
+name = slimls
+r = 2
+[schedule]
+kind = ramp
+alpha = 1.0
+[sampler]
+scheme = random_cyclic
+[run]
+epochs = 1
+replicates = 2
+base_seed = 7
+error_references = x_true
+""",
+}
+
+
+def harness_golden():
+    """Reference harness CSV outputs and parsed configs (harness.py:183-313)."""
+    import dataclasses
+    import tempfile
+
+    from slimsolve import config as refcfg, harness
+
+    out = {}
+    for name, text in HARNESS_CFGS.items():
+        with tempfile.TemporaryDirectory() as tmp:
+            cfg = refcfg.parse_config(text).with_overrides(output=os.path.join(tmp, name))
+            res = harness.run_experiment(cfg)
+            for kind, path in (("metrics", res.metrics_path), ("aggregate", res.aggregate_path),
+                               ("replicates", res.replicates_path)):
+                with open(path) as fh:
+                    out[f"{name}/{kind}"] = np.array(fh.read())
+        out[f"{name}/cfg_text"] = np.array(text)
+    cfgdir = "/root/reference/pkg/configs"
+    for f in sorted(os.listdir(cfgdir)):
+        parsed = dataclasses.asdict(refcfg.load_config(os.path.join(cfgdir, f)))
+        out[f"cfgfile/{f}/text"] = np.array(open(os.path.join(cfgdir, f)).read())
+        out[f"cfgfile/{f}/parsed"] = np.array(repr(parsed))
+    np.savez_compressed(os.path.join(HERE, "harness.npz"), **out)
+
+
 if __name__ == "__main__":
+    harness_golden()
     sampler_golden()
     dense_runs()
     tomo_runs()
