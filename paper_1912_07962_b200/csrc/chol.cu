@@ -299,9 +299,22 @@ __device__ void accumulate(const MatRT& P, int ra, int j, int kb, int ke, double
   const int warp = tid >> 5, lane = tid & 31;
   const int nchunk = 2 * (ke - kb);
   if (nchunk <= 0) return;
+  // All dependency flags of this task are probed once, in parallel: tiles of
+  // earlier columns are usually long published, so only the k-steps past the
+  // ready prefix pay a (serial) acquire wait later.
+  __shared__ int s_ready;
+  if (tid == 0) s_ready = ke;
+  __syncthreads();
+  for (int k = kb + tid; k < ke; k += blockDim.x) {
+    const bool ok = ld_acquire(P.flags + (ra * (ra + 1) / 2 + k)) >= P.epoch &&
+                    ld_acquire(P.flags + (j * (j + 1) / 2 + k)) >= P.epoch;
+    if (!ok) atomicMin(&s_ready, k);
+  }
+  __syncthreads();
+  const int kready = s_ready;
   auto issue = [&](int u) {
     const int k = kb + (u >> 1), h = u & 1;
-    if (h == 0) {
+    if (h == 0 && k >= kready) {
       if (tid == 0) {
         wait_flag(P.flags + (ra * (ra + 1) / 2 + k), P.epoch);
         wait_flag(P.flags + (j * (j + 1) / 2 + k), P.epoch);
