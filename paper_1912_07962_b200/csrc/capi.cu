@@ -1070,9 +1070,12 @@ static int enqueue_chol_batch(slim_ctx* c, const Window* Ws, int nb, int set, co
   P.panel_stride = c->panel_stride;
   P.ell = (int)c->ell;
   P.S = c->S;
+  P.tile_base[0] = 0;
+  for (int b = 0; b < nb; ++b) P.tile_base[b + 1] = P.tile_base[b] + Ts[b] * (Ts[b] + 1) / 2;
+  launch_assemble(P, c->sf);
   CK(c, cudaMemsetAsync(P.ticket, 0, sizeof(int), c->sf));
   launch_chol(P, c->sf);
-  c->launches += 1;
+  c->launches += 2;
   CKLAUNCH(c);
   return SLIM_OK;
 }
@@ -1442,11 +1445,14 @@ static int potrf_impl(int32_t device, const double* G, int64_t N, double* L_out,
   P.panels = nullptr;
   P.G = dG;
   P.ldg = N;
+  P.tile_base[0] = 0;
+  P.tile_base[1] = (int)ntiles;
   unsigned long long* dtr = nullptr;
   if (trace_out) {
     cudaMalloc(&dtr, sizeof(unsigned long long) * 4 * ntiles);
     cudaMemset(dtr, 0, sizeof(unsigned long long) * 4 * ntiles);
     // warm-up launch so the traced one does not include module load
+    launch_assemble(P, 0);
     launch_chol(P, 0);
     cudaDeviceSynchronize();
     cudaMemset(ticket, 0, sizeof(int));
@@ -1456,6 +1462,7 @@ static int potrf_impl(int32_t device, const double* G, int64_t N, double* L_out,
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
+  launch_assemble(P, 0);
   cudaEventRecord(e0, 0);
   launch_chol(P, 0);
   cudaEventRecord(e1, 0);

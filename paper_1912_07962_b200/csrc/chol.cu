@@ -49,20 +49,6 @@ struct MatRT {
   const int* slot;  // shared memory
 };
 
-__device__ __forceinline__ double chol_g_elem(const CholParams& P, const MatRT& M, int p, int q) {
-  // requires q <= p < N
-  if (P.panels != nullptr) {
-    const int pb = p / P.ell, a = p - pb * P.ell;
-    const int qb = q / P.ell, c = q - qb * P.ell;
-    // product A_P[a] . A_Q[c] was stored when block P (the newer) was pushed:
-    // panel[slot(P)] row (slot(Q) * ell + c), column a
-    const double* pan = P.panels + (int64_t)M.slot[pb] * P.panel_stride;
-    const double v = pan[((int64_t)M.slot[qb] * P.ell + c) * P.ell + a];
-    return M.alpha * v + (p == q ? 1.0 : 0.0);
-  }
-  return P.G[(int64_t)p * P.ldg + q];
-}
-
 __device__ __forceinline__ void load_tile_async(double* s, const double* g, int tid) {
 #pragma unroll
   for (int it = 0; it < 8; ++it) {
@@ -270,23 +256,64 @@ constexpr int SM_DV = SM_ST + 2 * STAGE;
 constexpr int SM_RD = SM_DV + 512;
 constexpr int SM_TOTAL = SM_RD + 64;
 
+// the tile (i, j) of G was assembled in place by k_assemble (tile-major)
 __device__ __forceinline__ void init_acc(const CholParams& P, const MatRT& M, int i, int j,
                                          int warp, int lane, double (&acc)[8][2]) {
   // warp tile: rows 16 (warp >> 1) .. +15, columns 32 (warp & 1) .. +31;
   // accumulator f = rb * 4 + cb holds the 8x8 block (rb, cb) of it
+  (void)P;
+  const double* t = M.L + tile_off(i, j);
 #pragma unroll
   for (int f = 0; f < 8; ++f) {
-    const int p = i * TB + 16 * (warp >> 1) + 8 * (f >> 2) + (lane >> 2);
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int q = j * TB + 32 * (warp & 1) + 8 * (f & 3) + 2 * (lane & 3) + e;
-      double v;
-      if (p >= M.N || q >= M.N) v = (p == q) ? 1.0 : 0.0;
-      else if (q > p) v = 0.0;
-      else v = chol_g_elem(P, M, p, q);
-      acc[f][e] = v;
-    }
+    const int r = 16 * (warp >> 1) + 8 * (f >> 2) + (lane >> 2);
+    const int c = 32 * (warp & 1) + 8 * (f & 3) + 2 * (lane & 3);
+    const double2 v = __ldcg(reinterpret_cast<const double2*>(t + r * TB + c));
+    acc[f][0] = v.x;
+    acc[f][1] = v.y;
   }
+}
+
+// G = alpha * (Gram ring) + I, identity padding, written tile-major into the
+// factor buffers (one CTA per 64x64 tile of every system of the batch).
+// The ring stores a product block with consecutive rows p contiguous, so a
+// warp reads 32 consecutive p of one column q (coalesced) and the tile is
+// transposed through shared memory into row-major order.
+__global__ void __launch_bounds__(256) k_assemble(CholParams P) {
+  __shared__ double sh[TB][TB + 1];
+  // locate (system, tile) of this CTA
+  int b = 0;
+  while (b + 1 < P.nb && (int)blockIdx.x >= P.tile_base[b + 1]) ++b;
+  const CholMat& Mp = P.m[b];
+  int t = blockIdx.x - P.tile_base[b];
+  int I = 0;
+  while (t > I) {
+    t -= I + 1;
+    ++I;
+  }
+  const int J = t;
+  const int N = Mp.N, ell = P.ell;
+  const double alpha = Mp.alpha;
+  const int tid = threadIdx.x;
+  const int pl = tid & 63;
+  const int p = I * TB + pl;
+  for (int qs = tid >> 6; qs < TB; qs += 4) {
+    const int q = J * TB + qs;
+    double v;
+    if (p >= N || q >= N) v = (p == q) ? 1.0 : 0.0;
+    else if (q > p) v = 0.0;
+    else if (P.panels != nullptr) {
+      const int pb = p / ell, a = p - pb * ell;
+      const int qb = q / ell, c = q - qb * ell;
+      const double* pan = P.panels + (int64_t)Mp.slot[pb] * P.panel_stride;
+      v = alpha * pan[((int64_t)Mp.slot[qb] * ell + c) * ell + a] + (p == q ? 1.0 : 0.0);
+    } else {
+      v = P.G[(int64_t)p * P.ldg + q];
+    }
+    sh[pl][qs] = v;
+  }
+  __syncthreads();
+  double* dst = Mp.L + tile_off(I, J);
+  for (int e = tid; e < TB * TB; e += 256) dst[e] = sh[e >> 6][e & 63];
 }
 
 // C_(ra, j) -= sum_{k in [kb, ke)} L_(ra,k) L_(j,k)^T   into accA, and when
@@ -673,6 +700,10 @@ std::vector<int2> chol_task_map(const int* Ts, int nb) {
   return out;
 }
 size_t trsv_smem_bytes() { return (size_t)(3 * TB * TS + 512 + 2 * TB + 4 * TB + 8) * sizeof(double); }
+
+void launch_assemble(const CholParams& P, cudaStream_t s) {
+  k_assemble<<<P.tile_base[P.nb], 256, 0, s>>>(P);
+}
 
 void launch_chol(const CholParams& P, cudaStream_t s) {
   static bool configured = false;

@@ -47,6 +47,8 @@ struct CholParams {
   int64_t ldg;
   // optional timeline (debug): 4 globaltimer stamps per ticket
   unsigned long long* trace;
+  // k_assemble: first CTA of each system (tile counts prefix-summed)
+  int tile_base[MAX_BATCH + 1];
 };
 
 struct TrsvParams {
@@ -73,6 +75,9 @@ struct Window {
 
 // ---- launchers (ops.cu / chol.cu) ----
 void launch_chol(const CholParams& P, cudaStream_t s);
+// G tiles of every system of the batch into its factor buffer
+// (P.tile_base[b] = first CTA of system b, P.tile_base[nb] = total)
+void launch_assemble(const CholParams& P, cudaStream_t s);
 std::vector<int2> chol_task_map(const int* Ts, int nb);
 void launch_trsv(const TrsvParams& P, cudaStream_t s);
 
