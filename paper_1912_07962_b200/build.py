@@ -26,7 +26,8 @@ LIB = os.path.join(HERE, "libslimb200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-              "-Xptxas", "-warn-spills", *GENCODE, f"-I{INCLUDE}", f"-I{CSRC}"]
+              "-Xptxas", "-warn-spills", *GENCODE, f"-I{INCLUDE}", f"-I{CSRC}",
+              *os.environ.get("SLIM_NVCC_EXTRA", "").split()]
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", f"-I{INCLUDE}"]
 
 

@@ -231,6 +231,7 @@ struct slim_ctx {
   int64_t panel_stride = 0;
   int D = D_DEFAULT;                 // batch size
   std::vector<double*> Lbuf, Dinv;   // 2 D factor buffers
+  std::vector<CUtensorMap> Lmap;     // TMA views of the factor buffers
   std::vector<int*> cflags;
   int* tickets = nullptr;  // [0] chol ticket, [1] trsv ticket
   std::map<std::vector<int>, int2*> maps;  // cached task maps by batch shape
@@ -422,10 +423,13 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
   ALLOC(c, c->ctl, sizeof(Ctl));
   ALLOC(c, c->panels, sizeof(double) * (size_t)c->S * c->panel_stride);
   c->Lbuf.assign(2 * c->D, nullptr);
+  c->Lmap.resize(2 * c->D);
   c->Dinv.assign(2 * c->D, nullptr);
   c->cflags.assign(2 * c->D, nullptr);
   for (int q = 0; q < 2 * c->D; ++q) {
     ALLOC(c, c->Lbuf[q], sizeof(double) * (size_t)ntiles * TB * TB);
+    if (!tma_map_f64_sw128(&c->Lmap[q], c->Lbuf[q], ntiles * TB, TB, 16, TB))
+      FAIL(c, SLIM_ECUDA, "TMA descriptor for the factor buffer could not be encoded");
     ALLOC(c, c->Dinv[q], sizeof(double) * (size_t)c->Tmax * 512);
     ALLOC(c, c->cflags[q], sizeof(int) * ntiles);
     CK(c, cudaMemset(c->cflags[q], 0, sizeof(int) * ntiles));
@@ -1050,6 +1054,7 @@ static int enqueue_chol_batch(slim_ctx* c, const Window* Ws, int nb, int set, co
     const int N = Ws[b].nw * (int)c->ell;
     CholMat& M = P.m[b];
     const int buf = set * c->D + b;
+    M.map = c->Lmap[buf];
     M.L = c->Lbuf[buf];
     M.Dinv = c->Dinv[buf];
     M.flags = c->cflags[buf];
@@ -1426,6 +1431,10 @@ static int potrf_impl(int32_t device, const double* G, int64_t N, double* L_out,
   cudaMemset(ticket, 0, sizeof(int));
   cudaMemset(err, 0, sizeof(int));
   CholParams P{};
+  if (!tma_map_f64_sw128(&P.m[0].map, dL, ntiles * TB, TB, 16, TB)) {
+    cleanup();
+    FAIL((slim_ctx*)nullptr, SLIM_ECUDA, "TMA descriptor could not be encoded");
+  }
   P.m[0].L = dL;
   P.m[0].Dinv = dD;
   P.m[0].flags = flags;

@@ -41,6 +41,7 @@ constexpr unsigned FULL = 0xffffffffu;
 // memory (indexing the kernel-parameter array with the runtime system id
 // would turn every field access into a dynamically indexed constant load)
 struct MatRT {
+  const CUtensorMap* map;  // kernel-parameter (grid-constant) TMA view of L
   double* L;
   double* Dinv;
   int* flags;
@@ -245,16 +246,21 @@ __device__ void trsm_tile_warp(double* As, const double* Bs, const double* Dv, i
 // ---------------------------------------------------------------------------
 // tile Cholesky kernel
 // ---------------------------------------------------------------------------
-constexpr int KC = 32;          // K chunk of one pipeline stage
-constexpr int KS = 36;          // stage row stride (doubles): same 2-wavefront pattern as TS
-constexpr int STAGE = 2 * TB * KS;  // A half + B half
+// K chunks of 16 fp64 (one 128-byte swizzle row per tile row) stream through a
+// 4-stage TMA ring: a stage holds the 64x16 slices of both operand tiles.
+constexpr int KC = 16;
+constexpr int NSTAGE = 4;
+constexpr int BOX_BYTES = TB * KC * 8;         // 8 KB
+constexpr int STAGE_BYTES = 2 * BOX_BYTES;     // 16 KB
 
-// shared layout (doubles): Sg[TB*TS] | stage[2][STAGE] | Dv[512] | rdiag[64]
-constexpr int SM_SG = 0;
-constexpr int SM_ST = TB * TS;
-constexpr int SM_DV = SM_ST + 2 * STAGE;
-constexpr int SM_RD = SM_DV + 512;
-constexpr int SM_TOTAL = SM_RD + 64;
+// dynamic shared layout (bytes, from a 1024-aligned base):
+//   stage ring [NSTAGE][STAGE_BYTES] | Sg[TB*TS] | Dv[512] | rdiag[64]
+// the 64 x TS work tile X overlays the stage ring once the operands are consumed
+constexpr int SMB_ST = 0;
+constexpr int SMB_SG = NSTAGE * STAGE_BYTES;
+constexpr int SMB_DV = SMB_SG + TB * TS * 8;
+constexpr int SMB_RD = SMB_DV + 512 * 8;
+constexpr int SMB_TOTAL = SMB_RD + 64 * 8 + 1024;  // + alignment slack
 
 // the tile (i, j) of G was assembled in place by k_assemble (tile-major)
 __device__ __forceinline__ void init_acc(const CholParams& P, const MatRT& M, int i, int j,
@@ -316,81 +322,142 @@ __global__ void __launch_bounds__(256) k_assemble(CholParams P) {
   for (int e = tid; e < TB * TB; e += 256) dst[e] = sh[e >> 6][e & 63];
 }
 
+// ---- TMA + mbarrier pipeline helpers ----
+struct Pipe {
+  uint64_t* full;    // NSTAGE, tx-count barriers (one arrival: the producer)
+  uint64_t* empty;   // NSTAGE, one arrival per consumer warp
+  uint32_t seq;      // chunks consumed so far by this CTA (uniform)
+};
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void bar_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nW_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra W_%=;\n}\n" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(su32(dst)),
+      "l"(map), "r"(su32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+// generic-proxy writes of other CTAs (acquired through a flag) made visible
+// to this thread's subsequent async-proxy (TMA) reads
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+
 // C_(ra, j) -= sum_{k in [kb, ke)} L_(ra,k) L_(j,k)^T   into accA, and when
-// PAIR also C_(j,j) -= L_(j,k) L_(j,k)^T into accB.  Tiles stream through a
-// two-stage cp.async pipeline in K chunks of 32; thread 0 waits on the
-// producers' flags just before a tile's first chunk is issued.
+// PAIR also C_(j,j) -= L_(j,k) L_(j,k)^T into accB.  Thread 0 issues one 2D
+// TMA box per operand per K chunk (64 rows x 16 fp64, SWIZZLE_128B) three
+// chunks ahead; every warp releases a stage with one mbarrier arrival, so
+// there is no CTA-wide barrier in the loop.  Dependency flags are probed
+// once in parallel; only k-steps past the ready prefix make thread 0 wait.
 template <bool PAIR>
-__device__ void accumulate(const MatRT& P, int ra, int j, int kb, int ke, double* stage,
-                           double (&accA)[8][2], double (&accB)[8][2], int tid) {
+__device__ void accumulate(const MatRT& P, int ra, int j, int kb, int ke, uint8_t* stage,
+                           Pipe& pipe, double (&accA)[8][2], double (&accB)[8][2], int tid) {
   const int warp = tid >> 5, lane = tid & 31;
-  const int nchunk = 2 * (ke - kb);
+  const int nchunk = (TB / KC) * (ke - kb);
   if (nchunk <= 0) return;
-  // All dependency flags of this task are probed once, in parallel: tiles of
-  // earlier columns are usually long published, so only the k-steps past the
-  // ready prefix pay a (serial) acquire wait later.
-  __shared__ int s_ready;
-  if (tid == 0) s_ready = ke;
-  __syncthreads();
-  for (int k = kb + tid; k < ke; k += blockDim.x) {
-    const bool ok = ld_acquire(P.flags + (ra * (ra + 1) / 2 + k)) >= P.epoch &&
-                    ld_acquire(P.flags + (j * (j + 1) / 2 + k)) >= P.epoch;
-    if (!ok) atomicMin(&s_ready, k);
-  }
-  __syncthreads();
-  const int kready = s_ready;
-  auto issue = [&](int u) {
-    const int k = kb + (u >> 1), h = u & 1;
-    if (h == 0 && k >= kready) {
-      if (tid == 0) {
-        wait_flag(P.flags + (ra * (ra + 1) / 2 + k), P.epoch);
-        wait_flag(P.flags + (j * (j + 1) / 2 + k), P.epoch);
+  // Thread 0 -- the TMA issuer -- probes every dependency flag of the task
+  // once with relaxed loads, then one acquire fence and one proxy fence make
+  // all the ready tiles visible to its async-proxy (TMA) reads.
+  int kready = ke;
+  if (tid == 0) {
+    const int* fa = P.flags + ra * (ra + 1) / 2;
+    const int* fb = P.flags + j * (j + 1) / 2;
+    for (int k = kb; k < ke; ++k) {
+      int va, vb;
+      asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(va) : "l"(fa + k) : "memory");
+      asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(vb) : "l"(fb + k) : "memory");
+      if (va < P.epoch || vb < P.epoch) {
+        kready = k;
+        break;
       }
-      __syncthreads();
     }
-    double* st = stage + (u & 1) * STAGE;
-    const double* ga = P.L + tile_off(ra, k) + h * KC;
-    const double* gb = P.L + tile_off(j, k) + h * KC;
-#pragma unroll
-    for (int it = 0; it < 4; ++it) {
-      const int c = tid + it * 256;  // 1024 16-byte chunks per operand half
-      const int row = c >> 4, cc = (c & 15) * 2;
-      cp_async16(st + row * KS + cc, ga + row * TB + cc);
-      cp_async16(st + TB * KS + row * KS + cc, gb + row * TB + cc);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    fence_proxy_async();
+  }
+  auto issue = [&](int u) {  // thread 0 only
+    const uint32_t q = pipe.seq + u;
+    const int st = q % NSTAGE;
+    bar_wait(&pipe.empty[st], ((q / NSTAGE) & 1) ^ 1);
+    const int k = kb + u / (TB / KC), c = u % (TB / KC);
+    if (c == 0 && k >= kready) {
+      wait_flag(P.flags + (ra * (ra + 1) / 2 + k), P.epoch);
+      wait_flag(P.flags + (j * (j + 1) / 2 + k), P.epoch);
+      fence_proxy_async();
     }
-    cp_async_commit();
+    uint8_t* dst = stage + st * STAGE_BYTES;
+    bar_expect(&pipe.full[st], STAGE_BYTES);
+    tma2d(dst, P.map, &pipe.full[st], KC * c, (ra * (ra + 1) / 2 + k) * TB);
+    tma2d(dst + BOX_BYTES, P.map, &pipe.full[st], KC * c, (j * (j + 1) / 2 + k) * TB);
   };
-  issue(0);
-  const int arow = (16 * (warp >> 1) + (lane >> 2)) * KS + (lane & 3);
-  const int brow = (32 * (warp & 1) + (lane >> 2)) * KS + (lane & 3);
+  if (tid == 0)
+    for (int u = 0; u < NSTAGE - 1 && u < nchunk; ++u) issue(u);
+  // swizzled fragment offsets: row r of a box is 128 B, the 16-byte chunk
+  // holding columns (2 m, 2 m + 1) sits at position m ^ (r & 7); every
+  // fragment row base is a multiple of 8, so r & 7 = lane >> 2
+  const int sw = lane >> 2;
+  uint32_t colofs[KC / 4];
+#pragma unroll
+  for (int k4 = 0; k4 < KC / 4; ++k4)
+    colofs[k4] = (uint32_t)((((2 * k4 + ((lane & 3) >> 1)) ^ sw) << 4) + ((lane & 1) << 3));
+  const uint32_t arow = (uint32_t)(16 * (warp >> 1) + (lane >> 2)) * 128u;
+  const uint32_t brow = (uint32_t)(32 * (warp & 1) + (lane >> 2)) * 128u;
   for (int u = 0; u < nchunk; ++u) {
-    if (u + 1 < nchunk) {
-      issue(u + 1);
-      cp_async_wait_1();
-    } else {
-      cp_async_wait_all();
-    }
-    __syncthreads();
-    const double* sa = stage + (u & 1) * STAGE;
-    const double* sb = sa + TB * KS;
+    if (tid == 0 && u + NSTAGE - 1 < nchunk) issue(u + NSTAGE - 1);
+    const uint32_t q = pipe.seq + u;
+    const int st = q % NSTAGE;
+    bar_wait(&pipe.full[st], (q / NSTAGE) & 1);
+    __syncwarp();
+    const uint8_t* sa = stage + st * STAGE_BYTES;
+    const uint8_t* sb = sa + BOX_BYTES;
 #pragma unroll
     for (int k4 = 0; k4 < KC / 4; ++k4) {
       double a[2], ad[2], b[4];
 #pragma unroll
       for (int rb = 0; rb < 2; ++rb) {
-        a[rb] = -sa[arow + rb * 8 * KS + 4 * k4];
-        if (PAIR) ad[rb] = -sb[arow + rb * 8 * KS + 4 * k4];
+        a[rb] = -*reinterpret_cast<const double*>(sa + arow + rb * 8 * 128 + colofs[k4]);
+        if (PAIR) ad[rb] = -*reinterpret_cast<const double*>(sb + arow + rb * 8 * 128 + colofs[k4]);
       }
 #pragma unroll
-      for (int cb = 0; cb < 4; ++cb) b[cb] = sb[brow + cb * 8 * KS + 4 * k4];
+      for (int cb = 0; cb < 4; ++cb)
+        b[cb] = *reinterpret_cast<const double*>(sb + brow + cb * 8 * 128 + colofs[k4]);
 #pragma unroll
       for (int f = 0; f < 8; ++f) {
         dmma8x8x4(accA[f], a[f >> 2], b[f & 3]);
         if (PAIR) dmma8x8x4(accB[f], ad[f >> 2], b[f & 3]);
       }
     }
-    __syncthreads();
+    // the next TMA into this stage is an async-proxy write: the warp's
+    // generic reads of the stage are ordered before it by the warp barrier
+    // plus one proxy fence ahead of the release (without the fence the TMA
+    // can overwrite a stage that is still being read -- observed on B200)
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      bar_arrive(&pipe.empty[st]);
+    }
   }
+  pipe.seq += nchunk;
 }
 
 __device__ __forceinline__ void acc_to_smem(double* X, const double (&acc)[8][2], int warp, int lane) {
@@ -403,7 +470,11 @@ __device__ __forceinline__ void acc_to_smem(double* X, const double (&acc)[8][2]
   }
 }
 
+// Every thread that stored part of the tile makes its generic-proxy writes
+// visible to the async proxy (consumers read tiles with TMA), then thread 0
+// releases the flag.
 __device__ __forceinline__ void publish(const MatRT& P, int i, int j, int tid) {
+  fence_proxy_async();
   __syncthreads();
   if (tid == 0) {
     __threadfence();
@@ -418,22 +489,32 @@ __device__ __forceinline__ void publish(const MatRT& P, int i, int j, int tid) {
 // it depends on -- one column ahead of the bulk tiles -- and the systems of
 // a batch are merged in proportion.  Every task's dependencies carry smaller
 // tickets, so spinning on them cannot deadlock.
-__global__ void __launch_bounds__(256, 2) k_chol_tiles(CholParams P) {
-  extern __shared__ __align__(16) double smem[];
-  double* Sg = smem + SM_SG;
-  double* stage = smem + SM_ST;
-  double* Dv = smem + SM_DV;
-  double* rdiag = smem + SM_RD;
-  double* X = stage;  // 64 x TS work tile overlays the (then idle) stages
+__global__ void __launch_bounds__(256, 2) k_chol_tiles(const __grid_constant__ CholParams P) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);  // SW128 tiles
+  uint8_t* stage = base + SMB_ST;
+  double* Sg = reinterpret_cast<double*>(base + SMB_SG);
+  double* Dv = reinterpret_cast<double*>(base + SMB_DV);
+  double* rdiag = reinterpret_cast<double*>(base + SMB_RD);
+  double* X = reinterpret_cast<double*>(stage);  // work tile, once the stages are drained
   __shared__ int s_task;
   __shared__ int s_slot[MAX_WINDOW];
+  __shared__ __align__(8) uint64_t s_full[NSTAGE], s_empty[NSTAGE];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) s_task = atomicAdd(P.ticket, 1);
+  if (tid == 0) {
+    s_task = atomicAdd(P.ticket, 1);
+    for (int q = 0; q < NSTAGE; ++q) {
+      bar_init(&s_full[q], 1);
+      bar_init(&s_empty[q], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __syncthreads();
   if (s_task >= P.ntasks) return;
   const int2 e = P.map[s_task];
   const CholMat& Mp = P.m[e.x];
   MatRT M;
+  M.map = &Mp.map;
   M.L = Mp.L;
   M.Dinv = Mp.Dinv;
   M.flags = Mp.flags;
@@ -443,7 +524,9 @@ __global__ void __launch_bounds__(256, 2) k_chol_tiles(CholParams P) {
   M.alpha = Mp.alpha;
   if (tid < MAX_WINDOW) s_slot[tid] = Mp.slot[tid];
   M.slot = s_slot;
+  if (tid == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(M.map) : "memory");
   __syncthreads();
+  Pipe pipe{s_full, s_empty, 0u};
   const int i = e.y >> 16, j = e.y & 0xffff;
   const int T = M.T;
   unsigned long long* tr = (P.trace != nullptr && tid == 0) ? P.trace + 4 * (int64_t)s_task : nullptr;
@@ -456,10 +539,10 @@ __global__ void __launch_bounds__(256, 2) k_chol_tiles(CholParams P) {
     init_acc(P, M, j, j, warp, lane, accB);
     if (has_sub) {
       init_acc(P, M, j + 1, j, warp, lane, accA);
-      accumulate<true>(M, j + 1, j, 0, j - 1 > 0 ? j - 1 : 0, stage, accA, accB, tid);
+      accumulate<true>(M, j + 1, j, 0, j - 1 > 0 ? j - 1 : 0, stage, pipe, accA, accB, tid);
     }
     // last update of the diagonal alone, then factor it right away
-    if (j >= 1) accumulate<false>(M, j, j, has_sub ? j - 1 : 0, j, stage, accB, accB, tid);
+    if (j >= 1) accumulate<false>(M, j, j, has_sub ? j - 1 : 0, j, stage, pipe, accB, accB, tid);
     if (tr) tr[1] = globaltimer_ns();
     acc_to_smem(Sg, accB, warp, lane);
     __syncthreads();
@@ -472,7 +555,8 @@ __global__ void __launch_bounds__(256, 2) k_chol_tiles(CholParams P) {
     }
     publish(M, j, j, tid);
     if (has_sub) {
-      if (j >= 1) accumulate<false>(M, j + 1, j, j - 1, j, stage, accA, accA, tid);
+      if (j >= 1) accumulate<false>(M, j + 1, j, j - 1, j, stage, pipe, accA, accA, tid);
+      __syncthreads();  // every warp is done reading the stages X overlays
       acc_to_smem(X, accA, warp, lane);
       __syncthreads();
       trsm_tile_warp(X, Sg, Dv, warp, lane);
@@ -483,7 +567,7 @@ __global__ void __launch_bounds__(256, 2) k_chol_tiles(CholParams P) {
   } else {
     // ---------------- off-diagonal tile (i, j), i >= j + 2 ----------------
     init_acc(P, M, i, j, warp, lane, accA);
-    accumulate<false>(M, i, j, 0, j, stage, accA, accA, tid);
+    accumulate<false>(M, i, j, 0, j, stage, pipe, accA, accA, tid);
     if (tr) tr[1] = globaltimer_ns();
     if (tid == 0) wait_flag(M.flags + (j * (j + 1) / 2 + j), M.epoch);
     if (tr) tr[2] = globaltimer_ns();
@@ -654,7 +738,7 @@ __global__ void __launch_bounds__(256, 2) k_trsv(TrsvParams P) {
   }
 }
 
-size_t chol_smem_bytes() { return (size_t)SM_TOTAL * sizeof(double); }
+size_t chol_smem_bytes() { return (size_t)SMB_TOTAL; }
 int chol_num_tasks(int T) { return T * (T - 1) / 2 + 1; }
 
 // per-system task order: pair(0), then for each column j its first

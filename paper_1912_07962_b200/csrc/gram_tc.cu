@@ -263,6 +263,20 @@ static bool make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t n,
   return r == CUDA_SUCCESS;
 }
 
+bool tma_map_f64_sw128(CUtensorMap* m, const double* base, int64_t rows, int64_t cols,
+                       int box_cols, int box_rows) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(cols * sizeof(double))};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)base, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 bool gram_tc_supported(int ell, int64_t n) {
   return ell == tc::BN && n % tc::BK == 0 && get_encode() != nullptr;
 }

@@ -1,5 +1,6 @@
 // gram_tc.h -- tcgen05 3xTF32 Gram panel (see gram_tc.cu).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -17,6 +18,9 @@ struct GramTcParams {
 };
 
 bool gram_tc_supported(int ell, int64_t n);
+// 2D fp64 TMA map (cols innermost), box (box_cols, box_rows), SWIZZLE_128B
+bool tma_map_f64_sw128(CUtensorMap* m, const double* base, int64_t rows, int64_t cols,
+                       int box_cols, int box_rows);
 size_t gram_tc_smem_bytes();
 int gram_tc_kchunk(int64_t n, int mtiles);
 cudaError_t launch_gram_tf32x3(const float* ring_hi, const float* ring_lo, int64_t ring_rows,

@@ -1,6 +1,7 @@
 // kernels.h -- parameter blocks and launch declarations shared by the
 // slimLS kernels and the C-ABI driver.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -23,6 +24,7 @@ struct Ctl {
 
 // one system of a batched factorization
 struct CholMat {
+  CUtensorMap map;      // TMA view of L: (tiles * 64) x 64 fp64, box 16 x 64, SW128
   double* L;            // lower tiles, tile_off(i, j)
   double* Dinv;         // T x 512: inverses of the 8x8 diagonal blocks of L_jj
   int* flags;           // T (T + 1) / 2 epoch flags
@@ -81,7 +83,7 @@ void launch_assemble(const CholParams& P, cudaStream_t s);
 std::vector<int2> chol_task_map(const int* Ts, int nb);
 void launch_trsv(const TrsvParams& P, cudaStream_t s);
 
-__global__ void k_chol_tiles(CholParams P);
+__global__ void k_chol_tiles(const __grid_constant__ CholParams P);
 __global__ void k_trsv(TrsvParams P);
 
 size_t chol_smem_bytes();
