@@ -234,7 +234,13 @@ struct slim_ctx {
   std::vector<CUtensorMap> Lmap;     // TMA views of the factor buffers
   std::vector<int*> cflags;
   int* tickets = nullptr;  // [0] chol ticket, [1] trsv ticket
-  std::map<std::vector<int>, int2*> maps;  // cached task maps by batch shape
+  struct TaskMap {
+    int2* dev;
+    int ntasks;
+    double flops;  // algorithmic fp64 flops of the tiles the batch factors
+  };
+  std::map<std::vector<SysShape>, TaskMap> maps;  // cached task maps by batch shape
+  double chol_flops = 0.0;  // profiled factorizations: algorithmic flops
   int* tflags = nullptr;
   int* errflag = nullptr;
   double* rvec = nullptr;
@@ -324,7 +330,7 @@ static void free_all(slim_ctx* c) {
   for (double* p : c->Lbuf) cudaFree(p);
   for (double* p : c->Dinv) cudaFree(p);
   for (int* p : c->cflags) cudaFree(p);
-  for (auto& kv : c->maps) cudaFree(kv.second);
+  for (auto& kv : c->maps) cudaFree(kv.second.dev);
   if (c->sf) cudaStreamDestroy(c->sf);
   if (c->sx) cudaStreamDestroy(c->sx);
   if (c->sg) cudaStreamDestroy(c->sg);
@@ -810,7 +816,12 @@ int slim_set_timing_start(slim_ctx* c, int64_t k0) {
 }
 
 int slim_timing(slim_ctx* c, int32_t which, double* ms, int64_t* launches) {
-  if (!c || which < 0 || which > 4) FAIL(c, SLIM_EINVAL, "bad argument");
+  if (!c || which < 0 || which > 5) FAIL(c, SLIM_EINVAL, "bad argument");
+  if (which == 5) {  // algorithmic flops of the profiled factorization launches
+    if (ms) *ms = c->chol_flops;
+    if (launches) *launches = c->t_n[1];
+    return SLIM_OK;
+  }
   if (ms) *ms = c->t_ms[which];
   if (launches) *launches = c->t_n[which];
   return SLIM_OK;
@@ -832,12 +843,22 @@ static int comm_allreduce(slim_ctx* c, double* buf, size_t count, cudaStream_t s
 // one step: enqueue on the three stream kinds
 // ---------------------------------------------------------------------------
 
+// Window of step k (1-based) in slot order: the block sampled at step j sits
+// at position (j - 1) mod (r + 1) for as long as it stays in the window, so
+// the dual systems of consecutive steps differ in one block row/column (the
+// reference stacks oldest first, innersolve.py:298-302; G is the same matrix
+// up to a symmetric permutation, w and s = alpha M^T w are unchanged).
 static void fill_window(const slim_ctx* c, const int64_t* idx, int64_t k, Window& W) {
-  const int nw = (int)std::min<int64_t>(k, c->r + 1);
+  const int64_t Wn = c->r + 1;
+  const int nw = (int)std::min<int64_t>(k, Wn);
   W.nw = nw;
   W.ell = (int)c->ell;
+  const int pk = (int)((k - 1) % Wn);
+  W.newp = pk;
   for (int P = 0; P < nw; ++P) {
-    const int64_t j = k - nw + 1 + P;  // step that pushed window position P
+    const int age = (int)((pk - P + Wn) % Wn);
+    const int64_t j = k - age;  // step that put its block at position P
+    W.age[P] = age;
     W.slot[P] = (int)((j - 1) % c->S);
     // storage block: the row block of A, or (generated) the ring slot the
     // block was generated into when it was sampled
@@ -853,9 +874,9 @@ static ProfPair make_pair() {
 }
 
 static int enqueue_gram(slim_ctx* c, const Window& W, int64_t k, int64_t real_blk) {
-  const int slot_new = W.slot[W.nw - 1];
+  const int slot_new = W.slot[W.newp];
   double* panel = c->panels + (int64_t)slot_new * c->panel_stride;
-  const int64_t newblk = W.blk[W.nw - 1];
+  const int64_t newblk = W.blk[W.newp];
   if (c->layout == SLIM_GEN_SPLITMIX64) {
     const int64_t off = (int64_t)slot_new * c->ell * c->n;
     launch_gen_block(c->gring + off, c->use_tc ? c->gring_hi + off : nullptr,
@@ -914,8 +935,6 @@ static int enqueue_gram(slim_ctx* c, const Window& W, int64_t k, int64_t real_bl
 
 static int enqueue_x_chain(slim_ctx* c, const Window& W, int64_t k, int d, double alpha,
                            int record, int epoch) {
-  const int64_t newblk = W.blk[W.nw - 1];
-  const int64_t row0 = newblk * c->ell;
   const int ell = (int)c->ell, n = (int)c->n, N = W.nw * ell;
   cudaStream_t s = c->sx;
   (void)k;
@@ -928,7 +947,8 @@ static int enqueue_x_chain(slim_ctx* c, const Window& W, int64_t k, int d, doubl
   T.epoch = epoch;
   T.N = N;
   T.T = (N + TB - 1) / TB;
-  T.rstart = N - ell;
+  T.rstart = W.newp * ell;
+  T.rend = T.rstart + ell;
   T.i0 = T.rstart / TB;
   T.r = c->rvec;
   T.t = c->tvec;
@@ -996,7 +1016,6 @@ static int enqueue_x_chain(slim_ctx* c, const Window& W, int64_t k, int d, doubl
     CKLAUNCH(c);
     c->launches += 1;
   }
-  (void)row0;
   return SLIM_OK;
 }
 
@@ -1031,26 +1050,41 @@ static int enqueue_residual(slim_ctx* c, int64_t newblk, int64_t real_blk) {
   return comm_allreduce(c, c->rvec, (size_t)c->ell, c->sx);
 }
 
-// device task map for a batch shape (cached)
-static int2* task_map(slim_ctx* c, const std::vector<int>& Ts, int* ntasks) {
-  auto it = c->maps.find(Ts);
-  std::vector<int2> h = chol_task_map(Ts.data(), (int)Ts.size());
-  *ntasks = (int)h.size();
-  if (it != c->maps.end()) return it->second;
-  int2* d = nullptr;
-  if (cudaMalloc(&d, sizeof(int2) * h.size()) != cudaSuccess) return nullptr;
-  cudaMemcpy(d, h.data(), sizeof(int2) * h.size(), cudaMemcpyHostToDevice);
-  c->maps[Ts] = d;
-  return d;
+// device task map for a batch shape (cached; shapes repeat with period r + 1)
+// Algorithmic flops per tile task (they sum to (64 T)^3 / 3 for a full
+// factorization): off-diagonal (i, j) 2 * 64^3 j (updates) + 64^3 (TRSM);
+// diagonal (j, j) 64^3 j (SYRK) + 64^3 / 3 (POTRF).
+static const slim_ctx::TaskMap* task_map(slim_ctx* c, const std::vector<SysShape>& sh) {
+  auto it = c->maps.find(sh);
+  if (it != c->maps.end()) return &it->second;
+  std::vector<int2> h = chol_task_map(sh.data(), (int)sh.size(), (int)(c->r + 1), (int)c->ell);
+  const double t3 = (double)TB * TB * TB;
+  double flops = 0.0;
+  for (const int2& e : h) {
+    const int i = e.y >> 16, j = e.y & 0xffff;
+    if (i == j) {
+      flops += t3 * j + t3 / 3.0;
+      if (j + 1 < sh[e.x].T) flops += 2.0 * t3 * j + t3;
+    } else {
+      flops += 2.0 * t3 * j + t3;
+    }
+  }
+  slim_ctx::TaskMap tm{nullptr, (int)h.size(), flops};
+  if (h.empty()) h.push_back(make_int2(0, 0));
+  if (cudaMalloc(&tm.dev, sizeof(int2) * h.size()) != cudaSuccess) return nullptr;
+  cudaMemcpy(tm.dev, h.data(), sizeof(int2) * h.size(), cudaMemcpyHostToDevice);
+  return &(c->maps[sh] = tm);
 }
 
 // one launch factors the systems of steps k0 .. k0 + nb - 1 into factor
-// buffer set `set` (buffers set * D + b)
+// buffer set `set` (buffers set * D + b); tiles shared with step k0 - 1 come
+// from buffer `prev` (the previous batch's last system, -1 for none)
 static int enqueue_chol_batch(slim_ctx* c, const Window* Ws, int nb, int set, const double* alphas,
-                              int64_t k0, int64_t epoch0) {
+                              int64_t k0, int64_t epoch0, int prev, double* flops = nullptr) {
   CholParams P{};
-  std::vector<int> Ts(nb);
+  std::vector<SysShape> sh(nb);
   for (int b = 0; b < nb; ++b) {
+    const int64_t k = k0 + b;
     const int N = Ws[b].nw * (int)c->ell;
     CholMat& M = P.m[b];
     const int buf = set * c->D + b;
@@ -1061,27 +1095,41 @@ static int enqueue_chol_batch(slim_ctx* c, const Window* Ws, int nb, int set, co
     M.N = N;
     M.T = (N + TB - 1) / TB;
     M.nw = Ws[b].nw;
-    M.epoch = (int)(epoch0 + k0 + b);
-    M.alpha = alphas[k0 + b - 1];
-    for (int q = 0; q < Ws[b].nw; ++q) M.slot[q] = Ws[b].slot[q];
-    Ts[b] = M.T;
+    M.epoch = (int)(epoch0 + k);
+    M.alpha = alphas[k - 1];
+    M.pnew = Ws[b].newp;
+    // a new damping changes every entry of G; the first step has no predecessor
+    // (and a batch without a predecessor buffer starts from scratch)
+    M.full = (k == 1 || alphas[k - 1] != alphas[k - 2] || (b == 0 && prev < 0)) ? 1 : 0;
+    for (int q = 0; q < Ws[b].nw; ++q) M.slot[q] = Ws[b].slot[q], M.age[q] = Ws[b].age[q];
+    sh[b] = SysShape{M.T, M.pnew, M.full};
   }
   P.nb = nb;
-  P.map = task_map(c, Ts, &P.ntasks);
-  if (!P.map) FAIL(c, SLIM_ENOMEM, "task map allocation failed");
+  const slim_ctx::TaskMap* tm = task_map(c, sh);
+  if (!tm) FAIL(c, SLIM_ENOMEM, "task map allocation failed");
+  P.map = tm->dev;
+  P.ntasks = tm->ntasks;
+  if (flops) *flops = tm->flops;
   P.ticket = c->tickets;
   P.error = c->errflag;
   P.panels = c->panels;
   P.panel_stride = c->panel_stride;
   P.ell = (int)c->ell;
   P.S = c->S;
+  P.W = (int)(c->r + 1);
+  P.prevL = prev >= 0 ? c->Lbuf[prev] : nullptr;
+  P.prevDinv = prev >= 0 ? c->Dinv[prev] : nullptr;
   P.tile_base[0] = 0;
-  for (int b = 0; b < nb; ++b) P.tile_base[b + 1] = P.tile_base[b] + Ts[b] * (Ts[b] + 1) / 2;
+  for (int b = 0; b < nb; ++b) P.tile_base[b + 1] = P.tile_base[b] + sh[b].T * (sh[b].T + 1) / 2;
   launch_assemble(P, c->sf);
-  CK(c, cudaMemsetAsync(P.ticket, 0, sizeof(int), c->sf));
-  launch_chol(P, c->sf);
-  c->launches += 2;
+  c->launches += 1;
   CKLAUNCH(c);
+  if (P.ntasks > 0) {
+    CK(c, cudaMemsetAsync(P.ticket, 0, sizeof(int), c->sf));
+    launch_chol(P, c->sf);
+    c->launches += 1;
+    CKLAUNCH(c);
+  }
   return SLIM_OK;
 }
 
@@ -1120,6 +1168,7 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
   CK(c, cudaMemset(c->errflag, 0, sizeof(int)));
   *c->pin_div = 0;
   for (int q = 0; q < 4; ++q) c->t_ms[q] = 0.0, c->t_n[q] = 0;
+  c->chol_flops = 0.0;
   std::vector<ProfPair> pch, pgr, pxc;
   auto take = [](std::vector<ProfPair>& pool, std::vector<ProfPair>& used) {
     if (pool.empty()) used.push_back(make_pair());
@@ -1185,8 +1234,11 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
     ProfPair pc{};
     if (prof_b) pc = take(c->prof_chol, pch), cudaEventRecord(pc.a, c->sf);
     {
-      int rc = enqueue_chol_batch(c, Ws.data(), nb, set, alphas, kb0, epoch0);
+      double fl = 0.0;
+      int rc = enqueue_chol_batch(c, Ws.data(), nb, set, alphas, kb0, epoch0,
+                                  B >= 1 ? (1 - set) * D + (D - 1) : -1, &fl);
       if (rc) return rc;
+      if (prof_b) c->chol_flops += fl;
     }
     if (prof_b) cudaEventRecord(pc.b, c->sf);
     CK(c, cudaEventRecord(c->ev_f[B % NEV], c->sf));
@@ -1200,10 +1252,14 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
       if (b == 0 && c->layout == SLIM_GEN_SPLITMIX64)
         CK(c, cudaStreamWaitEvent(c->sx, c->ev_g[B % NEV], 0));  // generated block ready
       {
-        int rc = enqueue_residual(c, W.blk[W.nw - 1], idx[k - 1] - 1);
+        int rc = enqueue_residual(c, W.blk[W.newp], idx[k - 1] - 1);
         if (rc) return rc;
       }
-      if (b == 0) CK(c, cudaStreamWaitEvent(c->sx, c->ev_f[B % NEV], 0));
+      if (b == 0) {
+        CK(c, cudaStreamWaitEvent(c->sx, c->ev_f[B % NEV], 0));
+        // the x-chain's own time: not the wait for the batch's factors
+        if (c->prof && k >= k0) cudaEventRecord(px.a, c->sx);
+      }
       const int record = (k % record_every == 0 || k == K) ? 1 : 0;
       {
         int rc = enqueue_x_chain(c, W, k, set * D + b, alpha, record, (int)(epoch0 + k));
@@ -1352,7 +1408,7 @@ extern "C" int slim_dual_step(int32_t device, const double* Mh, int64_t rows, in
   if (cudaStreamSynchronize(c->sg) != cudaSuccess) return fail_out(SLIM_ECUDA);
   {
     std::vector<double> al(nb, alpha);
-    if ((rc = enqueue_chol_batch(c, &W, 1, 0, al.data(), nb, 1 - nb)))
+    if ((rc = enqueue_chol_batch(c, &W, 1, 0, al.data(), nb, 1 - nb, -1)))
       return fail_out(rc);
   }
   if (cudaStreamSynchronize(c->sf) != cudaSuccess) return fail_out(SLIM_ECUDA);
@@ -1370,7 +1426,8 @@ extern "C" int slim_dual_step(int32_t device, const double* Mh, int64_t rows, in
   T.epoch = 1;
   T.N = N;
   T.T = (N + TB - 1) / TB;
-  T.rstart = N - (int)ell;
+  T.rstart = W.newp * (int)ell;
+  T.rend = T.rstart + (int)ell;
   T.i0 = T.rstart / TB;
   T.r = c->rvec;
   T.t = c->tvec;
@@ -1443,7 +1500,11 @@ static int potrf_impl(int32_t device, const double* G, int64_t N, double* L_out,
   P.m[0].T = T;
   P.m[0].alpha = 1.0;
   P.nb = 1;
-  std::vector<int2> hmap = chol_task_map(&T, 1);
+  P.m[0].full = 1;
+  P.W = 1;
+  P.ell = TB;
+  SysShape shape{T, 0, 1};
+  std::vector<int2> hmap = chol_task_map(&shape, 1, 1, TB);
   P.ntasks = (int)hmap.size();
   int2* dmap = nullptr;
   cudaMalloc(&dmap, sizeof(int2) * hmap.size());

@@ -28,6 +28,7 @@
 // triangular solves of the x-chain reuse the same small inverses.  Only
 // 8x8 blocks are inverted, so the backward error stays that of a
 // substitution (the 8x8 blocks of a Cholesky factor are well conditioned).
+#include <algorithm>
 #include <vector>
 
 #include "common.cuh"
@@ -37,9 +38,9 @@ namespace slim {
 
 constexpr unsigned FULL = 0xffffffffu;
 
-// per-CTA view of its system: scalars in registers, window slots in shared
-// memory (indexing the kernel-parameter array with the runtime system id
-// would turn every field access into a dynamically indexed constant load)
+// per-CTA view of its system, in registers (indexing the kernel-parameter
+// array with the runtime system id would turn every field access into a
+// dynamically indexed constant load)
 struct MatRT {
   const CUtensorMap* map;  // kernel-parameter (grid-constant) TMA view of L
   double* L;
@@ -47,7 +48,6 @@ struct MatRT {
   int* flags;
   int N, T, epoch;
   double alpha;
-  const int* slot;  // shared memory
 };
 
 __device__ __forceinline__ void load_tile_async(double* s, const double* g, int tid) {
@@ -281,9 +281,14 @@ __device__ __forceinline__ void init_acc(const CholParams& P, const MatRT& M, in
 
 // G = alpha * (Gram ring) + I, identity padding, written tile-major into the
 // factor buffers (one CTA per 64x64 tile of every system of the batch).
-// The ring stores a product block with consecutive rows p contiguous, so a
-// warp reads 32 consecutive p of one column q (coalesced) and the tile is
-// transposed through shared memory into row-major order.
+// Entry (p, q) is the product of two window blocks; the ring keeps it in the
+// panel of the newer of the two, with the newer block's rows contiguous.
+// Pass 1 reads the entries whose row block is the newer one with threads
+// along p, pass 2 the others with threads along q (both coalesced); the
+// tile is transposed through shared memory into row-major order.
+// Tiles that are not fresh for this step are either produced by an earlier
+// system of the batch (its tile task stores them here) or, when no system of
+// the batch recomputes them, copied from the previous batch's last system.
 __global__ void __launch_bounds__(256) k_assemble(CholParams P) {
   __shared__ double sh[TB][TB + 1];
   // locate (system, tile) of this CTA
@@ -298,27 +303,59 @@ __global__ void __launch_bounds__(256) k_assemble(CholParams P) {
   }
   const int J = t;
   const int N = Mp.N, ell = P.ell;
-  const double alpha = Mp.alpha;
   const int tid = threadIdx.x;
-  const int pl = tid & 63;
-  const int p = I * TB + pl;
-  for (int qs = tid >> 6; qs < TB; qs += 4) {
-    const int q = J * TB + qs;
-    double v;
-    if (p >= N || q >= N) v = (p == q) ? 1.0 : 0.0;
-    else if (q > p) v = 0.0;
-    else if (P.panels != nullptr) {
-      const int pb = p / ell, a = p - pb * ell;
-      const int qb = q / ell, c = q - qb * ell;
-      const double* pan = P.panels + (int64_t)Mp.slot[pb] * P.panel_stride;
-      v = alpha * pan[((int64_t)Mp.slot[qb] * ell + c) * ell + a] + (p == q ? 1.0 : 0.0);
-    } else {
-      v = P.G[(int64_t)p * P.ldg + q];
+  const int64_t toff = tile_off(I, J);
+  if (!tile_fresh(Mp.full, Mp.pnew, P.W, ell, I, J)) {
+    for (int bb = b - 1; bb >= 0; --bb)
+      if (tile_fresh(P.m[bb].full, P.m[bb].pnew, P.W, ell, I, J)) return;  // produced in-batch
+    const double2* src = reinterpret_cast<const double2*>(P.prevL + toff);
+    double2* dst = reinterpret_cast<double2*>(Mp.L + toff);
+    for (int e = tid; e < TB * TB / 2; e += 256) dst[e] = __ldcg(src + e);
+    if (I == J)
+      for (int e = tid; e < 512; e += 256) Mp.Dinv[(int64_t)J * 512 + e] = __ldcg(P.prevDinv + (int64_t)J * 512 + e);
+    if (tid == 0) Mp.flags[I * (I + 1) / 2 + J] = Mp.epoch;  // next kernel: stream-ordered
+    return;
+  }
+  const double alpha = Mp.alpha;
+  const int ll = tid & 63;
+  // pass 1: threads along p
+  {
+    const int p = I * TB + ll;
+    const bool prow = p < N;
+    const int pb = prow ? p / ell : 0, a = p - pb * ell;
+    for (int qs = tid >> 6; qs < TB; qs += 4) {
+      const int q = J * TB + qs;
+      double v;
+      if (!prow || q >= N) v = (p == q) ? 1.0 : 0.0;
+      else if (q > p) v = 0.0;
+      else if (P.panels != nullptr) {
+        const int qb = q / ell, c = q - qb * ell;
+        if (Mp.age[qb] < Mp.age[pb]) continue;  // column block newer: pass 2
+        const double* pan = P.panels + (int64_t)Mp.slot[pb] * P.panel_stride;
+        v = alpha * pan[((int64_t)Mp.slot[qb] * ell + c) * ell + a] + (p == q ? 1.0 : 0.0);
+      } else {
+        v = P.G[(int64_t)p * P.ldg + q];
+      }
+      sh[ll][qs] = v;
     }
-    sh[pl][qs] = v;
+  }
+  // pass 2: threads along q, entries whose column block is the newer one
+  if (P.panels != nullptr) {
+    const int q = J * TB + ll;
+    if (q < N) {
+      const int qb = q / ell, c = q - qb * ell;
+      const double* pan = P.panels + (int64_t)Mp.slot[qb] * P.panel_stride;
+      for (int ps = tid >> 6; ps < TB; ps += 4) {
+        const int p = I * TB + ps;
+        if (p >= N || q > p) continue;
+        const int pb = p / ell, a = p - pb * ell;
+        if (!(Mp.age[qb] < Mp.age[pb])) continue;
+        sh[ps][ll] = alpha * pan[((int64_t)Mp.slot[pb] * ell + a) * ell + c];
+      }
+    }
   }
   __syncthreads();
-  double* dst = Mp.L + tile_off(I, J);
+  double* dst = Mp.L + toff;
   for (int e = tid; e < TB * TB; e += 256) dst[e] = sh[e >> 6][e & 63];
 }
 
@@ -482,13 +519,35 @@ __device__ __forceinline__ void publish(const MatRT& P, int i, int j, int tid) {
   }
 }
 
-// Task order (host-built map, see chol_task_order): per system, column by
-// column, the PAIR task (diagonal (j, j) plus the first sub-diagonal
-// (j + 1, j), so the critical TRSM reuses L_jj straight from shared
-// memory) is placed right after the first off-diagonal tile of column j - 1
-// it depends on -- one column ahead of the bulk tiles -- and the systems of
-// a batch are merged in proportion.  Every task's dependencies carry smaller
-// tickets, so spinning on them cannot deadlock.
+// Later systems of the batch that do not recompute tile (i, j) hold the
+// same tile bit for bit: store this system's copy (and, for a diagonal
+// tile, its 8x8 inverses) into their buffers and publish it there.
+__device__ void forward_tile(const CholParams& P, int b, int i, int j, const double* S,
+                             const double* Dv, int tid) {
+  for (int bb = b + 1; bb < P.nb; ++bb) {
+    const CholMat& M2 = P.m[bb];
+    if (tile_fresh(M2.full, M2.pnew, P.W, P.ell, i, j)) break;  // recomputed from here on
+    store_tile(M2.L + tile_off(i, j), S, tid);
+    if (Dv != nullptr) {
+      const double2 v = *reinterpret_cast<const double2*>(Dv + 2 * tid);
+      *reinterpret_cast<double2*>(M2.Dinv + (int64_t)j * 512 + 2 * tid) = v;
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      st_release(M2.flags + (i * (i + 1) / 2 + j), M2.epoch);
+    }
+  }
+}
+
+// Task order (host-built map, see chol_task_map): per column, the PAIR task
+// (diagonal (j, j) plus the first sub-diagonal (j + 1, j), so the critical
+// TRSM reuses L_jj straight from shared memory) is placed right after the
+// first off-diagonal tile of column j - 1 it depends on -- one column ahead
+// of the bulk tiles.  Only the tiles a step recomputes are tasks; shared
+// tiles arrive through forward_tile or k_assemble.  Every task's
+// dependencies carry smaller tickets, so spinning on them cannot deadlock.
 __global__ void __launch_bounds__(256, 2) k_chol_tiles(const __grid_constant__ CholParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);  // SW128 tiles
@@ -498,7 +557,6 @@ __global__ void __launch_bounds__(256, 2) k_chol_tiles(const __grid_constant__ C
   double* rdiag = reinterpret_cast<double*>(base + SMB_RD);
   double* X = reinterpret_cast<double*>(stage);  // work tile, once the stages are drained
   __shared__ int s_task;
-  __shared__ int s_slot[MAX_WINDOW];
   __shared__ __align__(8) uint64_t s_full[NSTAGE], s_empty[NSTAGE];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
@@ -522,8 +580,6 @@ __global__ void __launch_bounds__(256, 2) k_chol_tiles(const __grid_constant__ C
   M.T = Mp.T;
   M.epoch = Mp.epoch;
   M.alpha = Mp.alpha;
-  if (tid < MAX_WINDOW) s_slot[tid] = Mp.slot[tid];
-  M.slot = s_slot;
   if (tid == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(M.map) : "memory");
   __syncthreads();
   Pipe pipe{s_full, s_empty, 0u};
@@ -563,9 +619,11 @@ __global__ void __launch_bounds__(256, 2) k_chol_tiles(const __grid_constant__ C
       __syncthreads();
       store_tile(M.L + tile_off(j + 1, j), X, tid);
       publish(M, j + 1, j, tid);
+      forward_tile(P, e.x, j + 1, j, X, nullptr, tid);
     }
+    forward_tile(P, e.x, j, j, Sg, Dv, tid);
   } else {
-    // ---------------- off-diagonal tile (i, j), i >= j + 2 ----------------
+    // ---------------- off-diagonal tile (i, j), i > j -----------------
     init_acc(P, M, i, j, warp, lane, accA);
     accumulate<false>(M, i, j, 0, j, stage, pipe, accA, accA, tid);
     if (tr) tr[1] = globaltimer_ns();
@@ -582,12 +640,14 @@ __global__ void __launch_bounds__(256, 2) k_chol_tiles(const __grid_constant__ C
     __syncthreads();
     store_tile(M.L + tile_off(i, j), X, tid);
     publish(M, i, j, tid);
+    forward_tile(P, e.x, i, j, X, nullptr, tid);
   }
   if (tr) tr[3] = globaltimer_ns();
 }
 
 // ---------------------------------------------------------------------------
-// Triangular solves  t = L^{-1} y  (y zero above row N - ell),  w = L^{-T} t.
+// Triangular solves  t = L^{-1} y  (y = r on the new block's rows, zero
+// elsewhere; t is zero above tile row i0),  w = L^{-T} t.
 // One launch; tickets 0..nf-1 run the forward tile rows i0..T-1 in order,
 // the rest run the backward tile rows T-1..0.  Every tile the task needs is
 // already final (the factorization finished before this launch), so it is
@@ -678,7 +738,7 @@ __global__ void __launch_bounds__(256, 2) k_trsv(TrsvParams P) {
   if (fwd) {
     if (tid < TB) {
       const int pr = i * TB + tid;
-      vec[tid] = (pr >= P.rstart && pr < P.N) ? P.r[pr - P.rstart] : 0.0;
+      vec[tid] = (pr >= P.rstart && pr < P.rend) ? P.r[pr - P.rstart] : 0.0;
     }
   } else {
     if (i >= i0) {
@@ -739,47 +799,40 @@ __global__ void __launch_bounds__(256, 2) k_trsv(TrsvParams P) {
 }
 
 size_t chol_smem_bytes() { return (size_t)SMB_TOTAL; }
-int chol_num_tasks(int T) { return T * (T - 1) / 2 + 1; }
 
-// per-system task order: pair(0), then for each column j its first
-// off-diagonal tile (j + 2, j), the pair of column j + 1, and the rest of
-// column j.  Encoded as (i << 16) | j with i == j for pair tasks.
-static std::vector<int> task_order_one(int T) {
-  std::vector<int> seq;
-  seq.reserve(chol_num_tasks(T));
-  seq.push_back(0);  // pair(0)
-  for (int j = 0; j < T; ++j) {
-    if (j + 2 < T) seq.push_back(((j + 2) << 16) | j);
-    if (j + 1 < T) seq.push_back(((j + 1) << 16) | (j + 1));
-    for (int i = j + 3; i < T; ++i) seq.push_back((i << 16) | j);
-  }
-  return seq;
-}
-
-// merged ticket map of a batch: systems interleaved in proportion to their
-// task counts (round robin for equal sizes), each system's order preserved
-std::vector<int2> chol_task_map(const int* Ts, int nb) {
-  std::vector<std::vector<int>> per(nb);
-  size_t total = 0;
-  for (int b = 0; b < nb; ++b) {
-    per[b] = task_order_one(Ts[b]);
-    total += per[b].size();
-  }
+// Ticket order.  A system's tasks are its fresh tiles (tile_fresh), grouped
+// by column: pair(0) opens group -1; group j holds, in this order, the
+// stand-alone (j + 1, j) (column j not fresh but that row is), the first
+// off-diagonal tile (j + 2, j), the pair of column j + 1 (one column ahead
+// of the bulk, so the critical diagonal chain is never queued behind it) and
+// the rest of column j.  Encoded as (i << 16) | j with i == j for pair tasks.
+// The batch is merged group-major, system-minor: a tile a system shares
+// with an earlier system of the batch is produced by that system's task in
+// the same or an earlier group, so every dependency holds a smaller ticket
+// and spinning on it cannot deadlock.
+std::vector<int2> chol_task_map(const SysShape* sh, int nb, int W, int ell) {
+  int Tmax = 0;
+  for (int b = 0; b < nb; ++b) Tmax = std::max(Tmax, sh[b].T);
   std::vector<int2> out;
-  out.reserve(total);
-  std::vector<size_t> pos(nb, 0);
-  while (out.size() < total) {
-    int best = -1;
-    double bestkey = 1e300;
+  auto fresh = [&](int b, int i, int j) {
+    return tile_fresh(sh[b].full, sh[b].pnew, W, ell, i, j);
+  };
+  for (int g = -1; g < Tmax; ++g) {
     for (int b = 0; b < nb; ++b) {
-      if (pos[b] >= per[b].size()) continue;
-      const double key = (pos[b] + 0.5) / (double)per[b].size();
-      if (key < bestkey) {
-        bestkey = key;
-        best = b;
+      const int T = sh[b].T;
+      if (g >= T) continue;
+      if (g < 0) {
+        if (fresh(b, 0, 0)) out.push_back(make_int2(b, 0));
+        continue;
       }
+      const int j = g;
+      const bool col_fresh = fresh(b, j, j);  // the whole column then is
+      if (!col_fresh && j + 1 < T && fresh(b, j + 1, j)) out.push_back(make_int2(b, ((j + 1) << 16) | j));
+      if (j + 2 < T && fresh(b, j + 2, j)) out.push_back(make_int2(b, ((j + 2) << 16) | j));
+      if (j + 1 < T && fresh(b, j + 1, j + 1)) out.push_back(make_int2(b, ((j + 1) << 16) | (j + 1)));
+      for (int i = j + 3; i < T; ++i)
+        if (fresh(b, i, j)) out.push_back(make_int2(b, (i << 16) | j));
     }
-    out.push_back(make_int2(best, per[best][pos[best]++]));
   }
   return out;
 }

@@ -30,7 +30,12 @@ struct CholMat {
   int* flags;           // T (T + 1) / 2 epoch flags
   int N, T, nw, epoch;
   double alpha;
-  int slot[MAX_WINDOW];  // window position (0 = oldest) -> ring slot
+  // window positions are fixed slots: the block of step k sits at position
+  // (k - 1) mod (r + 1), so consecutive systems differ in one block row
+  int pnew;              // position of this step's new block
+  int full;              // 1: every tile is recomputed (first step, alpha changed)
+  int slot[MAX_WINDOW];  // window position -> ring slot
+  int age[MAX_WINDOW];   // window position -> steps since its block arrived (0 = new)
 };
 
 struct CholParams {
@@ -44,6 +49,11 @@ struct CholParams {
   const double* panels;
   int64_t panel_stride;  // S * ell * ell
   int ell, S;
+  int W;                 // window positions (r + 1)
+  // tiles a system shares with the previous batch's last system (step
+  // k0 - 1) are copied from its factor buffer by k_assemble
+  const double* prevL;
+  const double* prevDinv;
   // dense mode (panels == nullptr, nb == 1): G is the full SPD matrix, row-major
   const double* G;
   int64_t ldg;
@@ -59,7 +69,7 @@ struct TrsvParams {
   int* flags;        // 2 T epoch flags (forward, backward)
   int* ticket;
   int epoch;
-  int N, T, i0, rstart;
+  int N, T, i0, rstart, rend;  // y = r on rows [rstart, rend), zero elsewhere
   const double* r;   // newest-block residual (ell)
   double* t;         // T * 64 forward result
   double* w;         // T * 64 backward result (window order)
@@ -73,21 +83,44 @@ struct Window {
   int blk[MAX_WINDOW];        // storage block of window position (row block of A,
                               // or the generated-block ring slot)
   int slot[MAX_WINDOW];       // ring slot at window position
+  int age[MAX_WINDOW];        // steps since the block at the position arrived
+  int newp;                   // position of the newest block
 };
+
+// batch shape of one system, for the (cached) ticket order
+struct SysShape {
+  int T, pnew, full;
+  bool operator<(const SysShape& o) const {
+    return T != o.T ? T < o.T : (pnew != o.pnew ? pnew < o.pnew : full < o.full);
+  }
+};
+
+// Does step k recompute tile (i, j)?  Only tiles whose rows or columns reach
+// the new block's position (or everything, on a full step); the others are
+// bit-identical to step k - 1's.
+__host__ __device__ inline bool tile_fresh(int full, int pnew, int W, int ell, int i, int j) {
+  if (full) return true;
+  int pj = (TB * j + TB - 1) / ell;  // last position touched by tile column j
+  if (pj > W - 1) pj = W - 1;
+  if (pnew <= pj) return true;
+  const int s0 = (TB * i) / ell;
+  int s1 = (TB * i + TB - 1) / ell;
+  if (s1 > W - 1) s1 = W - 1;
+  return pnew >= s0 && pnew <= s1;
+}
 
 // ---- launchers (ops.cu / chol.cu) ----
 void launch_chol(const CholParams& P, cudaStream_t s);
 // G tiles of every system of the batch into its factor buffer
 // (P.tile_base[b] = first CTA of system b, P.tile_base[nb] = total)
 void launch_assemble(const CholParams& P, cudaStream_t s);
-std::vector<int2> chol_task_map(const int* Ts, int nb);
+std::vector<int2> chol_task_map(const SysShape* sh, int nb, int W, int ell);
 void launch_trsv(const TrsvParams& P, cudaStream_t s);
 
 __global__ void k_chol_tiles(const __grid_constant__ CholParams P);
 __global__ void k_trsv(TrsvParams P);
 
 size_t chol_smem_bytes();
-int chol_num_tasks(int T);
 size_t trsv_smem_bytes();
 
 }  // namespace slim

@@ -209,6 +209,8 @@ def run(method: str, op: RowBlockOperator, sampler, schedule: Schedule, *, epoch
             timing[key + "_count"] = cnt.value
         dop.call("slim_timing", 4, C.byref(ms), C.byref(cnt))
         timing["launches"] = cnt.value
+        dop.call("slim_timing", 5, C.byref(ms), C.byref(cnt))
+        timing["cholesky_flops"] = ms.value
     x_final = np.empty(x0.shape[0])
     dop.call("slim_get_x", _lib.dptr(x_final))
     if stream_state is not None:
