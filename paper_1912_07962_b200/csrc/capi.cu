@@ -230,7 +230,8 @@ struct slim_ctx {
   double* panels = nullptr;
   int64_t panel_stride = 0;
   int D = D_DEFAULT;                 // batch size
-  std::vector<double*> Lbuf, Dinv;   // 2 D factor buffers
+  int trsv_C = 0;                    // triangular-solve cluster size (0 = by T)
+  std::vector<double*> Lbuf, Dinv, Linv;  // 2 D factor buffers (+ 8x8 and 64x64 diagonal inverses)
   std::vector<CUtensorMap> Lmap;     // TMA views of the factor buffers
   std::vector<int*> cflags;
   int* tickets = nullptr;  // [0] chol ticket, [1] trsv ticket
@@ -329,6 +330,7 @@ static void free_all(slim_ctx* c) {
     if (c->refs[q]) cudaFree(c->refs[q]);
   for (double* p : c->Lbuf) cudaFree(p);
   for (double* p : c->Dinv) cudaFree(p);
+  for (double* p : c->Linv) cudaFree(p);
   for (int* p : c->cflags) cudaFree(p);
   for (auto& kv : c->maps) cudaFree(kv.second.dev);
   if (c->sf) cudaStreamDestroy(c->sf);
@@ -406,6 +408,7 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
     const int64_t Nmax0 = (d->memory_r + 1) * d->block_rows;
     c->D = Nmax0 <= 6144 ? 8 : (Nmax0 <= 10240 ? 4 : 2);
     if (const char* env = getenv("SLIM_BATCH")) c->D = std::max(1, std::min(MAX_BATCH, atoi(env)));
+    if (const char* env = getenv("SLIM_TRSV_CLUSTER")) c->trsv_C = std::max(1, std::min(16, atoi(env)));
   }
   for (int q = 0; q < NEV; ++q) {
     CK(c, cudaEventCreateWithFlags(&c->ev_g[q], cudaEventDisableTiming));
@@ -431,12 +434,14 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
   c->Lbuf.assign(2 * c->D, nullptr);
   c->Lmap.resize(2 * c->D);
   c->Dinv.assign(2 * c->D, nullptr);
+  c->Linv.assign(2 * c->D, nullptr);
   c->cflags.assign(2 * c->D, nullptr);
   for (int q = 0; q < 2 * c->D; ++q) {
     ALLOC(c, c->Lbuf[q], sizeof(double) * (size_t)ntiles * TB * TB);
     if (!tma_map_f64_sw128(&c->Lmap[q], c->Lbuf[q], ntiles * TB, TB, 16, TB))
       FAIL(c, SLIM_ECUDA, "TMA descriptor for the factor buffer could not be encoded");
     ALLOC(c, c->Dinv[q], sizeof(double) * (size_t)c->Tmax * 512);
+    ALLOC(c, c->Linv[q], sizeof(double) * (size_t)c->Tmax * TB * TB);
     ALLOC(c, c->cflags[q], sizeof(int) * ntiles);
     CK(c, cudaMemset(c->cflags[q], 0, sizeof(int) * ntiles));
   }
@@ -941,21 +946,17 @@ static int enqueue_x_chain(slim_ctx* c, const Window& W, int64_t k, int d, doubl
   // trsv
   TrsvParams T{};
   T.L = c->Lbuf[d];
-  T.Dinv = c->Dinv[d];
-  T.flags = c->tflags;
-  T.ticket = c->tickets + 1;
-  T.epoch = epoch;
+  T.Linv = c->Linv[d];
   T.N = N;
   T.T = (N + TB - 1) / TB;
   T.rstart = W.newp * ell;
   T.rend = T.rstart + ell;
   T.i0 = T.rstart / TB;
   T.r = c->rvec;
-  T.t = c->tvec;
   T.w = c->wvec;
   T.ctl = c->ctl;
-  CK(c, cudaMemsetAsync(T.ticket, 0, sizeof(int), s));
-  launch_trsv(T, s);
+  T.C = c->trsv_C > 0 ? std::min(c->trsv_C, T.T) : trsv_cluster_size(T.T);
+  CK(c, launch_trsv(T, s));
   CKLAUNCH(c);
   c->launches += 3;  // trsv, M^T w, finish
   // M^T w
@@ -1091,6 +1092,7 @@ static int enqueue_chol_batch(slim_ctx* c, const Window* Ws, int nb, int set, co
     M.map = c->Lmap[buf];
     M.L = c->Lbuf[buf];
     M.Dinv = c->Dinv[buf];
+    M.Linv = c->Linv[buf];
     M.flags = c->cflags[buf];
     M.N = N;
     M.T = (N + TB - 1) / TB;
@@ -1130,6 +1132,9 @@ static int enqueue_chol_batch(slim_ctx* c, const Window* Ws, int nb, int set, co
     c->launches += 1;
     CKLAUNCH(c);
   }
+  launch_diag_inv(P, c->sf);  // the x-chain's diagonal solves are 64x64 products
+  c->launches += 1;
+  CKLAUNCH(c);
   return SLIM_OK;
 }
 
@@ -1420,21 +1425,17 @@ extern "C" int slim_dual_step(int32_t device, const double* Mh, int64_t rows, in
   const int N = (int)rows;
   TrsvParams T{};
   T.L = c->Lbuf[0];
-  T.Dinv = c->Dinv[0];
-  T.flags = c->tflags;
-  T.ticket = c->tickets + 1;
-  T.epoch = 1;
+  T.Linv = c->Linv[0];
   T.N = N;
   T.T = (N + TB - 1) / TB;
   T.rstart = W.newp * (int)ell;
   T.rend = T.rstart + (int)ell;
   T.i0 = T.rstart / TB;
   T.r = c->rvec;
-  T.t = c->tvec;
   T.w = c->wvec;
   T.ctl = nullptr;
-  cudaMemsetAsync(T.ticket, 0, sizeof(int), c->sx);
-  launch_trsv(T, c->sx);
+  T.C = trsv_cluster_size(T.T);
+  if (launch_trsv(T, c->sx) != cudaSuccess) return fail_out(SLIM_ECUDA);
   launch_mtw_dense<double>(c->spart, 1, W, (const double*)c->A, n, (int)n, c->wvec, c->ctl, c->sx);
   if (cudaStreamSynchronize(c->sx) != cudaSuccess || cudaGetLastError() != cudaSuccess)
     return fail_out(SLIM_ECUDA);

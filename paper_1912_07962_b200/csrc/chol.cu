@@ -645,159 +645,6 @@ __global__ void __launch_bounds__(256, 2) k_chol_tiles(const __grid_constant__ C
   if (tr) tr[3] = globaltimer_ns();
 }
 
-// ---------------------------------------------------------------------------
-// Triangular solves  t = L^{-1} y  (y = r on the new block's rows, zero
-// elsewhere; t is zero above tile row i0),  w = L^{-T} t.
-// One launch; tickets 0..nf-1 run the forward tile rows i0..T-1 in order,
-// the rest run the backward tile rows T-1..0.  Every tile the task needs is
-// already final (the factorization finished before this launch), so it is
-// prefetched into shared memory while the task waits for the solved
-// segment it multiplies; the critical path per tile row is one flag hop,
-// one 64x64 product from shared memory and the blocked diagonal solve.
-// ---------------------------------------------------------------------------
-
-__device__ __forceinline__ void load_vec_cg(double* s, const double* g, int tid) {
-  if (tid < TB) s[tid] = __ldcg(g + tid);
-}
-
-// forward diagonal solve in place: v <- L_ii^{-1} v (blocked by 8)
-__device__ void diag_solve_fwd(double* v, const double* Ld, const double* Dv, double* u, int tid) {
-  const int warp = tid >> 5, lane = tid & 31;
-  for (int q = 0; q < 8; ++q) {
-    // warp i computes u_i = v[8q+i] - sum_{k < 8q} L[8q+i][k] v[k]
-    const int row = 8 * q + warp;
-    double s = 0.0;
-    for (int k = lane; k < 8 * q; k += 32) s += Ld[row * TS + k] * v[k];
-    s = warp_sum(s);
-    if (lane == 0) u[warp] = v[row] - s;
-    __syncthreads();
-    if (tid < 8) {
-      double t = 0.0;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) t += Dv[q * 64 + tid * 8 + k] * u[k];
-      v[8 * q + tid] = t;
-    }
-    __syncthreads();
-  }
-}
-
-// backward diagonal solve in place: v <- L_ii^{-T} v
-__device__ void diag_solve_bwd(double* v, const double* Ld, const double* Dv, double* u, int tid) {
-  const int warp = tid >> 5, lane = tid & 31;
-  for (int q = 7; q >= 0; --q) {
-    const int col = 8 * q + warp;
-    double s = 0.0;
-    for (int k = 8 * q + 8 + lane; k < TB; k += 32) s += Ld[k * TS + col] * v[k];
-    s = warp_sum(s);
-    if (lane == 0) u[warp] = v[col] - s;
-    __syncthreads();
-    if (tid < 8) {
-      double t = 0.0;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) t += Dv[q * 64 + k * 8 + tid] * u[k];
-      v[8 * q + tid] = t;
-    }
-    __syncthreads();
-  }
-}
-
-__global__ void __launch_bounds__(256, 2) k_trsv(TrsvParams P) {
-  extern __shared__ __align__(16) double smem[];
-  double* Ld = smem;                   // diagonal tile
-  double* Lb0 = Ld + TB * TS;          // off-diagonal tile, double-buffered
-  double* Lb1 = Lb0 + TB * TS;
-  double* Dv = Lb1 + TB * TS;          // 512
-  double* vec = Dv + 512;              // 64 accumulator
-  double* tv = vec + TB;               // 64 incoming segment
-  double* part = tv + TB;              // 4 x 64 partial sums
-  double* u = part + 4 * TB;           // 8 scratch
-  __shared__ int s_task;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (P.ctl != nullptr && P.ctl->diverged_at != 0) return;
-  if (tid == 0) s_task = atomicAdd(P.ticket, 1);
-  __syncthreads();
-  const int T = P.T, i0 = P.i0, nf = T - i0;
-  const int t = s_task;
-  if (t >= nf + T) return;
-  const bool fwd = t < nf;
-  const int i = fwd ? i0 + t : T - 1 - (t - nf);
-  int* fflag = P.flags;
-  int* bflag = P.flags + T;
-
-  // prefetch the diagonal tile and its small inverses (group 0)
-  load_tile_async(Ld, P.L + tile_off(i, i), tid);
-  load_dinv_async(Dv, P.Dinv + (int64_t)i * 512, tid);
-  cp_async_commit();
-  // the contributing tiles, in the order their solved segments arrive
-  const int jfirst = fwd ? i0 : T - 1;
-  const int jcount = fwd ? (i - i0) : (T - 1 - i);
-  auto tile_of = [&](int jj) { return fwd ? tile_off(i, jj) : tile_off(jj, i); };
-  if (jcount > 0) load_tile_async(Lb0, P.L + tile_of(jfirst), tid);
-  cp_async_commit();
-
-  if (fwd) {
-    if (tid < TB) {
-      const int pr = i * TB + tid;
-      vec[tid] = (pr >= P.rstart && pr < P.rend) ? P.r[pr - P.rstart] : 0.0;
-    }
-  } else {
-    if (i >= i0) {
-      if (tid == 0) wait_flag(fflag + i, P.epoch);
-      __syncthreads();
-      load_vec_cg(vec, P.t + (int64_t)i * TB, tid);
-    } else if (tid < TB) {
-      vec[tid] = 0.0;
-    }
-  }
-  for (int s = 0; s < jcount; ++s) {
-    const int jj = fwd ? jfirst + s : jfirst - s;
-    double* cur = (s & 1) ? Lb1 : Lb0;
-    double* nxt = (s & 1) ? Lb0 : Lb1;
-    if (s + 1 < jcount) {
-      const int jn = fwd ? jj + 1 : jj - 1;
-      load_tile_async(nxt, P.L + tile_of(jn), tid);
-    }
-    cp_async_commit();
-    if (tid == 0) wait_flag((fwd ? fflag : bflag) + jj, P.epoch);
-    __syncthreads();
-    load_vec_cg(tv, (fwd ? P.t : P.w) + (int64_t)jj * TB, tid);
-    cp_async_wait_1();  // everything but the newest prefetch has landed
-    __syncthreads();
-    if (fwd) {
-      // vec[a] -= sum_b L_ij[a][b] t_j[b]; warp w owns rows 8w..8w+7
-      const double t0 = tv[2 * lane], t1 = tv[2 * lane + 1];
-#pragma unroll
-      for (int rr = 0; rr < 8; ++rr) {
-        const int a = warp * 8 + rr;
-        const double2 lv = *reinterpret_cast<const double2*>(cur + a * TS + 2 * lane);
-        const double d = warp_sum(lv.x * t0 + lv.y * t1);
-        if (lane == 0) vec[a] -= d;
-      }
-    } else {
-      // vec[a] -= sum_b L_ji[b][a] w_j[b]
-      const int g = tid >> 6, a = tid & 63;
-      double sacc = 0.0;
-#pragma unroll
-      for (int b = 0; b < 16; ++b) sacc += cur[(16 * g + b) * TS + a] * tv[16 * g + b];
-      part[g * TB + a] = sacc;
-      __syncthreads();
-      if (tid < TB)
-        vec[tid] -= ((part[tid] + part[TB + tid]) + (part[2 * TB + tid] + part[3 * TB + tid]));
-    }
-    __syncthreads();
-  }
-  cp_async_wait_all();
-  __syncthreads();
-  if (fwd) diag_solve_fwd(vec, Ld, Dv, u, tid);
-  else diag_solve_bwd(vec, Ld, Dv, u, tid);
-  if (tid < TB) (fwd ? P.t : P.w)[(int64_t)i * TB + tid] = vec[tid];
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    st_release((fwd ? fflag : bflag) + i, P.epoch);
-  }
-}
-
 size_t chol_smem_bytes() { return (size_t)SMB_TOTAL; }
 
 // Ticket order.  A system's tasks are its fresh tiles (tile_fresh), grouped
@@ -836,7 +683,6 @@ std::vector<int2> chol_task_map(const SysShape* sh, int nb, int W, int ell) {
   }
   return out;
 }
-size_t trsv_smem_bytes() { return (size_t)(3 * TB * TS + 512 + 2 * TB + 4 * TB + 8) * sizeof(double); }
 
 void launch_assemble(const CholParams& P, cudaStream_t s) {
   k_assemble<<<P.tile_base[P.nb], 256, 0, s>>>(P);
@@ -847,22 +693,9 @@ void launch_chol(const CholParams& P, cudaStream_t s) {
   if (!configured) {
     cudaFuncSetAttribute(k_chol_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)chol_smem_bytes());
-    cudaFuncSetAttribute(k_trsv, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)trsv_smem_bytes());
     configured = true;
   }
   k_chol_tiles<<<P.ntasks, 256, chol_smem_bytes(), s>>>(P);
-}
-
-void launch_trsv(const TrsvParams& P, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_trsv, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)trsv_smem_bytes());
-    configured = true;
-  }
-  const int ntask = (P.T - P.i0) + P.T;
-  k_trsv<<<ntask, 256, trsv_smem_bytes(), s>>>(P);
 }
 
 }  // namespace slim

@@ -27,6 +27,7 @@ struct CholMat {
   CUtensorMap map;      // TMA view of L: (tiles * 64) x 64 fp64, box 16 x 64, SW128
   double* L;            // lower tiles, tile_off(i, j)
   double* Dinv;         // T x 512: inverses of the 8x8 diagonal blocks of L_jj
+  double* Linv;         // T x 4096: inverses of the diagonal tiles (k_diag_inv)
   int* flags;           // T (T + 1) / 2 epoch flags
   int N, T, nw, epoch;
   double alpha;
@@ -64,16 +65,14 @@ struct CholParams {
 };
 
 struct TrsvParams {
-  const double* L;
-  const double* Dinv;
-  int* flags;        // 2 T epoch flags (forward, backward)
-  int* ticket;
-  int epoch;
-  int N, T, i0, rstart, rend;  // y = r on rows [rstart, rend), zero elsewhere
-  const double* r;   // newest-block residual (ell)
-  double* t;         // T * 64 forward result
-  double* w;         // T * 64 backward result (window order)
-  const Ctl* ctl;    // nullable; skip when diverged
+  const double* L;     // factor tiles, tile_off(i, j)
+  const double* Linv;  // T x 64 x 64: inverses of the diagonal tiles (row-major)
+  int N, T, i0, rstart, rend;  // y = r on rows [rstart, rend), zero elsewhere;
+                               // t is zero above tile row i0
+  const double* r;     // newest-block residual (ell)
+  double* w;           // T * 64 result w = G^{-1} y (window order)
+  const Ctl* ctl;      // nullable; skip when diverged
+  int C;               // cluster size = grid (tile row i belongs to CTA i mod C)
 };
 
 // window description shared by the x-chain / Gram kernels
@@ -115,12 +114,15 @@ void launch_chol(const CholParams& P, cudaStream_t s);
 // (P.tile_base[b] = first CTA of system b, P.tile_base[nb] = total)
 void launch_assemble(const CholParams& P, cudaStream_t s);
 std::vector<int2> chol_task_map(const SysShape* sh, int nb, int W, int ell);
-void launch_trsv(const TrsvParams& P, cudaStream_t s);
+// inverses of the diagonal tiles of every system of the batch (after launch_chol)
+void launch_diag_inv(const CholParams& P, cudaStream_t s);
+// one cluster of P.C CTAs (trsv_cluster_size(T))
+cudaError_t launch_trsv(const TrsvParams& P, cudaStream_t s);
+int trsv_cluster_size(int T);
+size_t trsv_smem_bytes(int T, int C);
 
 __global__ void k_chol_tiles(const __grid_constant__ CholParams P);
-__global__ void k_trsv(TrsvParams P);
 
 size_t chol_smem_bytes();
-size_t trsv_smem_bytes();
 
 }  // namespace slim

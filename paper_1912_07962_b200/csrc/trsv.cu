@@ -1,0 +1,360 @@
+// trsv.cu -- the triangular solves of the slimLS x-chain,
+//     t = L^{-1} y,   w = L^{-T} t       (w = G^{-1} y, innersolve.py:320)
+// with y = r on the new block's rows and zero elsewhere, plus the inverses
+// of the 64x64 diagonal tiles of L they use.
+//
+// Design (B200): the solve is a dependent chain over tile rows, so its cost
+// is the latency of one hop (segment t_k known -> segment t_{k+1} known)
+// times the number of tile rows.  One thread-block cluster (C <= 16 CTAs)
+// runs the whole solve; tile row i belongs to CTA i mod C.  A segment is
+// published by writing it into the owner's shared memory and setting a
+// flag in every CTA of the cluster (st.release.cluster over DSMEM, ~0.1 us,
+// instead of a global flag round trip through L2).  When segment k lands,
+// the owner of row k + 1 runs the critical step first -- one 64x64 product
+// with the tile it staged in advance, one 64x64 product with the
+// precomputed inverse of L_{k+1,k+1} -- and publishes; only then does every
+// CTA stream the segment's contributions into its other rows.  The solve
+// occupies C SMs for its duration, so it does not starve the factorization
+// batch running beside it.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace slim {
+
+// ---- cluster / DSMEM helpers ----
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t map_to_cta(uint32_t a, uint32_t cta) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(cta));
+  return r;
+}
+__device__ __forceinline__ double ld_remote_f64(uint32_t a) {
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_remote_release(uint32_t a, int v) {
+  asm volatile("st.release.cluster.shared::cluster.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_local_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cluster.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(smem_addr(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void stage_tile(double* s, const double* g, int tid) {
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const int c = tid + it * 256;  // 2048 16-byte chunks
+    const int row = c >> 5, cc = (c & 31) * 2;
+    cp_async16(s + row * TS + cc, g + row * TB + cc);
+  }
+}
+
+// v[a] -= sum_b M[a][b] x[b]   (M in shared memory, row stride TS)
+__device__ __forceinline__ void gemv_sub_smem(double* v, const double* M, const double* x, int tid) {
+  const int a = tid >> 2, q = tid & 3;
+  double s = 0.0;
+#pragma unroll
+  for (int m = 0; m < 16; ++m) s = fma(M[a * TS + q + 4 * m], x[q + 4 * m], s);
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  s += __shfl_xor_sync(0xffffffffu, s, 2);
+  if (q == 0) v[a] -= s;
+}
+// out[a] = sum_b M[a][b] x[b]
+__device__ __forceinline__ void gemv_smem(double* out, const double* M, const double* x, int tid) {
+  const int a = tid >> 2, q = tid & 3;
+  double s = 0.0;
+#pragma unroll
+  for (int m = 0; m < 16; ++m) s = fma(M[a * TS + q + 4 * m], x[q + 4 * m], s);
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  s += __shfl_xor_sync(0xffffffffu, s, 2);
+  if (q == 0) out[a] = s;
+}
+// out[a] (=|-=) sum_b M[b][a] x[b]; part: 4 x 64 scratch; ends with a barrier
+template <bool SUB>
+__device__ __forceinline__ void gemvT_smem(double* out, const double* M, const double* x, double* part,
+                                           int tid) {
+  const int a = tid & 63, g = tid >> 6;
+  double s = 0.0;
+#pragma unroll
+  for (int b = 0; b < 16; ++b) s = fma(M[(16 * g + b) * TS + a], x[16 * g + b], s);
+  part[g * TB + a] = s;
+  __syncthreads();
+  if (tid < TB) {
+    const double t = (part[tid] + part[TB + tid]) + (part[2 * TB + tid] + part[3 * TB + tid]);
+    out[tid] = SUB ? out[tid] - t : t;
+  }
+  __syncthreads();
+}
+// v[a] -= sum_b Lg[a][b] x[b], Lg a row-major tile in global memory (L2):
+// thread (a, q) reads columns 8 m + 2 q, +1 (m < 8), so the four threads of a
+// row read 64 contiguous bytes per instruction (two full sectors)
+__device__ __forceinline__ void gemv_sub_global(double* v, const double* Lg, const double* x, int tid) {
+  const int a = tid >> 2, q = tid & 3;
+  const double2* row = reinterpret_cast<const double2*>(Lg + a * TB);
+  double2 l[8];
+#pragma unroll
+  for (int m = 0; m < 8; ++m) l[m] = __ldcg(row + 4 * m + q);
+  double s = 0.0;
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    s = fma(l[m].x, x[8 * m + 2 * q], s);
+    s = fma(l[m].y, x[8 * m + 2 * q + 1], s);
+  }
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  s += __shfl_xor_sync(0xffffffffu, s, 2);
+  if (q == 0) v[a] -= s;
+}
+// v[a] -= sum_b Lg[b][a] x[b] (transposed, global); ends with a barrier
+__device__ __forceinline__ void gemvT_sub_global(double* v, const double* Lg, const double* x,
+                                                 double* part, int tid) {
+  const int a = tid & 63, g = tid >> 6;
+  double l[16];
+#pragma unroll
+  for (int b = 0; b < 16; ++b) l[b] = __ldcg(Lg + (16 * g + b) * TB + a);
+  double s = 0.0;
+#pragma unroll
+  for (int b = 0; b < 16; ++b) s = fma(l[b], x[16 * g + b], s);
+  part[g * TB + a] = s;
+  __syncthreads();
+  if (tid < TB) v[tid] -= (part[tid] + part[TB + tid]) + (part[2 * TB + tid] + part[3 * TB + tid]);
+  __syncthreads();
+}
+
+size_t trsv_smem_bytes(int T, int C) {
+  const int nown = (T + C - 1) / C;
+  return sizeof(double) * (size_t)(3 * nown * TB + 2 * TB * TS + TB + 4 * TB) + sizeof(int) * 2 * (size_t)T;
+}
+
+__global__ void __launch_bounds__(256, 1) k_trsv_cluster(TrsvParams P) {
+  extern __shared__ __align__(16) double sm[];
+  const int C = P.C, T = P.T, i0 = P.i0;
+  const int me = (int)cluster_rank();
+  const int tid = threadIdx.x;
+  const int nown = (T + C - 1) / C;
+  double* acc = sm;              // per own row: forward, then backward accumulator
+  double* tv = acc + nown * TB;  // own forward segments t_i
+  double* wv = tv + nown * TB;   // own backward segments w_i
+  double* Lc = wv + nown * TB;   // staged critical tile
+  double* Li = Lc + TB * TS;     // staged inverse of the critical diagonal tile
+  double* seg = Li + TB * TS;    // the segment being applied
+  double* part = seg + TB;       // 4 x 64 partial sums
+  int* ff = reinterpret_cast<int*>(part + 4 * TB);  // forward segment flags (T)
+  int* bf = ff + T;                                 // backward segment flags (T)
+
+  const bool skip = P.ctl != nullptr && P.ctl->diverged_at != 0;  // uniform over the cluster
+  for (int e = tid; e < 2 * T; e += 256) ff[e] = 0;
+  const int mine = me < T ? (T - 1 - me) / C + 1 : 0;  // own rows me, me + C, ...
+  for (int e = tid; e < mine * TB; e += 256) {
+    const int q = e >> 6, a = e & 63;
+    const int p = (me + q * C) * TB + a;
+    acc[e] = (p >= P.rstart && p < P.rend) ? P.r[p - P.rstart] : 0.0;
+  }
+  cluster_barrier();  // every CTA's flags are zero before anyone publishes
+  if (!skip && mine > 0) {
+    const int last = me + (mine - 1) * C;                   // largest own row
+    const int ffirst = me >= i0 ? me : me + ((i0 - me + C - 1) / C) * C;  // first own row >= i0
+    // critical-step staging: forward rows ffirst, ffirst + C, ..., last, then
+    // backward rows last, last - C, ..., me
+    auto stage_fwd = [&](int i) {
+      if (i > i0) stage_tile(Lc, P.L + tile_off(i, i - 1), tid);
+      stage_tile(Li, P.Linv + (int64_t)i * TB * TB, tid);
+      cp_async_commit();
+    };
+    auto stage_bwd = [&](int i, bool keep_inv) {
+      if (i < T - 1) stage_tile(Lc, P.L + tile_off(i + 1, i), tid);
+      if (!keep_inv) stage_tile(Li, P.Linv + (int64_t)i * TB * TB, tid);
+      cp_async_commit();
+    };
+    auto publish = [&](int* flags, int i) {
+      __syncthreads();
+      if (tid < C) st_remote_release(map_to_cta(smem_addr(flags + i), (uint32_t)tid), 1);
+    };
+    auto fetch = [&](const int* flags, const double* own_store, int k) {
+      while (ld_local_acquire(flags + k) == 0) {
+      }
+      const int owner = k % C;
+      if (tid < TB) {
+        const double* src = own_store + (k / C) * TB + tid;
+        seg[tid] = owner == me ? *src : ld_remote_f64(map_to_cta(smem_addr(src), (uint32_t)owner));
+      }
+      __syncthreads();
+    };
+    const bool has_fwd = ffirst <= last;
+    if (has_fwd) stage_fwd(ffirst);
+    else stage_bwd(last, false);
+
+    // ---------------- forward: t = L^{-1} y ----------------
+    if (has_fwd && ffirst == i0) {
+      cp_async_wait_all();
+      __syncthreads();
+      gemv_smem(tv + (i0 / C) * TB, Li, acc + (i0 / C) * TB, tid);
+      publish(ff, i0);
+      if (i0 + C <= last) stage_fwd(i0 + C);
+      else stage_bwd(last, true);
+    }
+    for (int k = i0; k < last && has_fwd; ++k) {
+      fetch(ff, tv, k);
+      const int i = k + 1;
+      if (i % C == me) {  // critical: finish row k + 1
+        double* a = acc + (i / C) * TB;
+        cp_async_wait_all();
+        __syncthreads();
+        gemv_sub_smem(a, Lc, seg, tid);
+        __syncthreads();
+        gemv_smem(tv + (i / C) * TB, Li, a, tid);
+        publish(ff, i);
+        if (i + C <= last) stage_fwd(i + C);
+        else stage_bwd(last, true);
+      }
+      // the segment's other contributions: own rows i' > k + 1
+      for (int ip = me + ((k + 2 - me + C - 1) / C) * C; ip <= last; ip += C)
+        gemv_sub_global(acc + (ip / C) * TB, P.L + tile_off(ip, k), seg, tid);
+      __syncthreads();
+    }
+    // ---------------- backward: w = L^{-T} t ----------------
+    for (int q = 0; q < mine; ++q) {
+      const int i = me + q * C;
+      for (int a = tid; a < TB; a += 256) acc[q * TB + a] = i >= i0 ? tv[q * TB + a] : 0.0;
+    }
+    __syncthreads();
+    auto finish_bwd = [&](int i) {  // w_i = Linv_i^T acc_i, publish, stage the next
+      double* w = wv + (i / C) * TB;
+      gemvT_smem<false>(w, Li, acc + (i / C) * TB, part, tid);
+      if (tid < TB) P.w[(int64_t)i * TB + tid] = w[tid];
+      publish(bf, i);
+      if (i - C >= 0) stage_bwd(i - C, false);
+    };
+    if (last == T - 1) {
+      cp_async_wait_all();
+      __syncthreads();
+      finish_bwd(T - 1);
+    }
+    for (int k = T - 1; k > me; --k) {
+      fetch(bf, wv, k);
+      const int i = k - 1;
+      if (i % C == me) {  // critical: finish row k - 1
+        cp_async_wait_all();
+        __syncthreads();
+        gemvT_smem<true>(acc + (i / C) * TB, Lc, seg, part, tid);
+        finish_bwd(i);
+      }
+      // other own rows i' < k - 1
+      for (int ip = me; ip < k - 1; ip += C)
+        gemvT_sub_global(acc + (ip / C) * TB, P.L + tile_off(k, ip), seg, part, tid);
+      __syncthreads();
+    }
+  }
+  cp_async_wait_all();
+  cluster_barrier();  // no CTA leaves while its segments may still be read
+}
+
+// ---------------------------------------------------------------------------
+// Inverses of the diagonal tiles (after the factorization of a batch): one
+// CTA per (system, tile column j).  Warp q builds block column q of
+// X = L_jj^{-1} by 8x8 blocked substitution from the diagonal-block inverses
+// the POTRF stored (X_qq = Dinv_q, X_pq = -Dinv_p sum_{q<=m<p} L_pm X_mq).
+// ---------------------------------------------------------------------------
+constexpr size_t DIAG_INV_SMEM = sizeof(double) * (2 * TB * (TB + 1) + 512 + 512);
+
+__global__ void __launch_bounds__(256) k_diag_inv(CholParams P) {
+  extern __shared__ double dsm[];
+  double (*Ls)[TB + 1] = reinterpret_cast<double (*)[TB + 1]>(dsm);
+  double (*Xs)[TB + 1] = reinterpret_cast<double (*)[TB + 1]>(dsm + TB * (TB + 1));
+  double* Dv = dsm + 2 * TB * (TB + 1);
+  double (*Ss)[64] = reinterpret_cast<double (*)[64]>(Dv + 512);
+  int b = 0, j = blockIdx.x;
+  while (b + 1 < P.nb && j >= P.m[b].T) j -= P.m[b++].T;
+  const CholMat& M = P.m[b];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const double* Lg = M.L + tile_off(j, j);
+  for (int e = tid; e < TB * TB; e += 256) {
+    Ls[e >> 6][e & 63] = __ldcg(Lg + e);
+    Xs[e >> 6][e & 63] = 0.0;
+  }
+  for (int e = tid; e < 512; e += 256) Dv[e] = __ldcg(M.Dinv + (int64_t)j * 512 + e);
+  __syncthreads();
+  const int q = warp;
+  const int rr = lane >> 2, cc = 2 * (lane & 3);  // this lane: entries (rr, cc), (rr, cc + 1)
+  Xs[8 * q + rr][8 * q + cc] = Dv[q * 64 + rr * 8 + cc];
+  Xs[8 * q + rr][8 * q + cc + 1] = Dv[q * 64 + rr * 8 + cc + 1];
+  __syncwarp();
+  for (int p = q + 1; p < 8; ++p) {
+    double s0 = 0.0, s1 = 0.0;
+    for (int m = q; m < p; ++m)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double l = Ls[8 * p + rr][8 * m + u];
+        s0 = fma(l, Xs[8 * m + u][8 * q + cc], s0);
+        s1 = fma(l, Xs[8 * m + u][8 * q + cc + 1], s1);
+      }
+    Ss[q][rr * 8 + cc] = s0;
+    Ss[q][rr * 8 + cc + 1] = s1;
+    __syncwarp();
+    double x0 = 0.0, x1 = 0.0;
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const double d = Dv[p * 64 + rr * 8 + v];
+      x0 = fma(d, Ss[q][v * 8 + cc], x0);
+      x1 = fma(d, Ss[q][v * 8 + cc + 1], x1);
+    }
+    Xs[8 * p + rr][8 * q + cc] = -x0;
+    Xs[8 * p + rr][8 * q + cc + 1] = -x1;
+    __syncwarp();
+  }
+  __syncthreads();
+  double* dst = M.Linv + (int64_t)j * TB * TB;
+  for (int e = tid; e < TB * TB; e += 256) dst[e] = Xs[e >> 6][e & 63];
+}
+
+void launch_diag_inv(const CholParams& P, cudaStream_t s) {
+  int n = 0;
+  for (int b = 0; b < P.nb; ++b) n += P.m[b].T;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_diag_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DIAG_INV_SMEM);
+    configured = true;
+  }
+  k_diag_inv<<<n, 256, DIAG_INV_SMEM, s>>>(P);
+}
+
+int trsv_cluster_size(int T) {
+  int C = 1;
+  while (C * 2 <= T && C * 2 <= 16) C *= 2;
+  return C;
+}
+
+cudaError_t launch_trsv(const TrsvParams& P, cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_trsv_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(k_trsv_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(P.C, 1, 1);
+  cfg.blockDim = dim3(256, 1, 1);
+  cfg.dynamicSmemBytes = trsv_smem_bytes(P.T, P.C);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = P.C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_trsv_cluster, P);
+}
+
+}  // namespace slim
