@@ -86,8 +86,8 @@ def batch_size(n_sys: int) -> int:
     """Systems per batched factorization (same rule as slim_create)."""
     env = os.environ.get("SLIM_BATCH")
     if env:
-        return max(1, min(8, int(env)))
-    return 8 if n_sys <= 6144 else (4 if n_sys <= 10240 else 2)
+        return max(1, min(16, int(env)))
+    return 8 if n_sys <= 2048 else (16 if n_sys <= 6144 else 4)
 
 
 def _peaks():

@@ -245,6 +245,7 @@ struct slim_ctx {
   int* tflags = nullptr;
   int* errflag = nullptr;
   double* rvec = nullptr;
+  RowSplit rsplit{}, dsplit{};  // residual (sx) and Gram-diagonal (sg) row-dot scratch
   double* tvec = nullptr;
   double* wvec = nullptr;
   double* spart = nullptr;
@@ -331,6 +332,10 @@ static void free_all(slim_ctx* c) {
   for (double* p : c->Lbuf) cudaFree(p);
   for (double* p : c->Dinv) cudaFree(p);
   for (double* p : c->Linv) cudaFree(p);
+  for (RowSplit* rs : {&c->rsplit, &c->dsplit}) {
+    if (rs->part) cudaFree(rs->part);
+    if (rs->cnt) cudaFree(rs->cnt);
+  }
   for (int* p : c->cflags) cudaFree(p);
   for (auto& kv : c->maps) cudaFree(kv.second.dev);
   if (c->sf) cudaStreamDestroy(c->sf);
@@ -406,7 +411,7 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
     // systems per batched factorization: enough to overlap the per-column
     // critical paths of mid-size systems; large systems fill the GPU alone
     const int64_t Nmax0 = (d->memory_r + 1) * d->block_rows;
-    c->D = Nmax0 <= 6144 ? 8 : (Nmax0 <= 10240 ? 4 : 2);
+    c->D = Nmax0 <= 2048 ? 8 : (Nmax0 <= 6144 ? 16 : 4);
     if (const char* env = getenv("SLIM_BATCH")) c->D = std::max(1, std::min(MAX_BATCH, atoi(env)));
     if (const char* env = getenv("SLIM_TRSV_CLUSTER")) c->trsv_C = std::max(1, std::min(16, atoi(env)));
   }
@@ -451,6 +456,14 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
   ALLOC(c, c->errflag, sizeof(int));
   CK(c, cudaMemset(c->errflag, 0, sizeof(int)));
   ALLOC(c, c->rvec, sizeof(double) * ell);
+  if (c->layout != SLIM_CSR_PERBLOCK) {
+    for (RowSplit* rs : {&c->rsplit, &c->dsplit}) {
+      rs->nch = rowdot_chunks((int)ell, c->n);
+      ALLOC(c, rs->part, sizeof(double) * ell * rs->nch);
+      ALLOC(c, rs->cnt, sizeof(int) * ell);
+      CK(c, cudaMemset(rs->cnt, 0, sizeof(int) * ell));
+    }
+  }
   ALLOC(c, c->tvec, sizeof(double) * c->Tmax * TB);
   ALLOC(c, c->wvec, sizeof(double) * c->Tmax * TB);
   // M^T w: split the window rows over CTAs when n alone cannot fill the GPU
@@ -464,7 +477,8 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
     }
   }
   if (c->layout != SLIM_CSR_PERBLOCK) {
-    const int64_t cols_ctas = (c->n + 255) / 256;
+    const int64_t vw = (c->layout == SLIM_GEN_SPLITMIX64 || c->vdt == SLIM_F32) ? 4 : 2;
+    const int64_t cols_ctas = (c->n + 256 * vw - 1) / (256 * vw);
     int ns = (int)std::max<int64_t>(1, std::min<int64_t>(32, (4 * 148) / std::max<int64_t>(1, cols_ctas)));
     ns = (int)std::min<int64_t>(ns, Nmax);
     c->nsplit_mtw = ns;
@@ -909,7 +923,7 @@ static int enqueue_gram(slim_ctx* c, const Window& W, int64_t k, int64_t real_bl
       launch_gram_reduce(panel, W, c->gpart, kcs, c->sg);
       // the self-product diagonal (row sums of squares) exactly in fp64
       launch_gram_diag_fp64(panel + (int64_t)slot_new * c->ell * c->ell, c->ell, c->gring + off,
-                            (int)c->ell, (int)c->n, c->sg);
+                            (int)c->ell, (int)c->n, c->dsplit, c->sg);
       c->launches += 2;
     } else {
       launch_gram_dense<float>(panel, c->gpart, c->nsplit_gram, W, c->gring, c->n,
@@ -1031,14 +1045,14 @@ static int enqueue_residual(slim_ctx* c, int64_t newblk, int64_t real_blk) {
   const int64_t brow = use_b ? real_blk * c->ell : 0;
   if (c->layout == SLIM_GEN_SPLITMIX64) {
     launch_residual_dense<float>(c->rvec, c->gring, c->n, row0, brow, (int)c->ell, (int)c->n, c->x,
-                                 bvec, c->ctl, c->sx);
+                                 bvec, c->ctl, c->rsplit, c->sx);
   } else if (c->layout == SLIM_DENSE_ROWMAJOR) {
     if (c->vdt == SLIM_F64)
       launch_residual_dense<double>(c->rvec, (const double*)c->A, c->n, row0, brow, (int)c->ell,
-                                    (int)c->n, c->x, bvec, c->ctl, c->sx);
+                                    (int)c->n, c->x, bvec, c->ctl, c->rsplit, c->sx);
     else
       launch_residual_dense<float>(c->rvec, (const float*)c->A, c->n, row0, brow, (int)c->ell,
-                                   (int)c->n, c->x, bvec, c->ctl, c->sx);
+                                   (int)c->n, c->x, bvec, c->ctl, c->rsplit, c->sx);
   } else {
     if (c->vdt == SLIM_F64)
       launch_residual_csr<double>(c->rvec, c->rowptr, c->col, (const double*)c->val, row0, brow,

@@ -12,7 +12,7 @@ constexpr int TB = 64;
 // 32-byte bank groups -> 2 wavefronts per 256-byte warp load (optimal).
 constexpr int TS = 68;
 constexpr int MAX_WINDOW = 32;   // r + 1 limit carried in kernel params
-constexpr int MAX_BATCH = 8;     // systems factored by one interleaved launch
+constexpr int MAX_BATCH = 16;    // systems factored by one interleaved launch
 constexpr int MAX_REFS = 8;      // error references tracked on device
 
 // ---- DMMA: D(8x8) += A(8x4, row) * B(4x8, col), fp64, IEEE FMA semantics ----

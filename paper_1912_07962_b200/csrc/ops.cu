@@ -24,21 +24,70 @@ namespace slim {
 // residual
 // ---------------------------------------------------------------------------
 
-template <typename T>
-__global__ void __launch_bounds__(256) k_residual_dense(double* r, const T* __restrict__ A,
-                                                        int64_t lda, int64_t row0, int64_t brow0,
-                                                        int ell, int n,
-                                                        const double* __restrict__ x,
-                                                        const double* __restrict__ b,
-                                                        const Ctl* ctl) {
-  if (ctl->diverged_at != 0) return;
-  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (row >= ell) return;
+// Row dots of one sampled block, split over column chunks so the whole GPU
+// streams the block (one warp per row leaves most SMs idle):
+//   residual:  r[row] = A[row0 + row, :] . x - b[brow0 + row]
+//   diagonal:  out[row * ld + row] = A[row, :] . A[row, :]     (SQUARE)
+// CTA (chunk, row) writes a partial; the last CTA of a row (counter) adds
+// the partials in chunk order, so the result is deterministic.
+template <typename T, bool SQUARE>
+__global__ void __launch_bounds__(256) k_rowdot(const T* __restrict__ A, int64_t lda, int64_t row0,
+                                                int n, const double* __restrict__ x, RowSplit rs,
+                                                double* __restrict__ out, int64_t ld_out,
+                                                const double* __restrict__ b, int64_t brow0,
+                                                const Ctl* ctl) {
+  if (ctl != nullptr && ctl->diverged_at != 0) return;
+  constexpr int V = 16 / sizeof(T);
+  const int chunk = blockIdx.x, row = blockIdx.y, tid = threadIdx.x;
+  const int nch = rs.nch;
+  const int csz = ((n + nch - 1) / nch + V - 1) / V * V;
+  const int c0 = chunk * csz, c1 = min(n, c0 + csz);
   const T* a = A + (row0 + row) * lda;
-  double s = 0.0;
-  for (int c = lane; c < n; c += 32) s += to_f64(a[c]) * x[c];
-  s = warp_sum(s);
-  if (lane == 0) r[row] = s - b[brow0 + row];
+  double s0 = 0.0, s1 = 0.0;
+  if (rs.vec) {
+#pragma unroll 2
+    for (int c = c0 + V * tid; c < c1; c += V * 256) {
+      T v[V];
+      *reinterpret_cast<uint4*>(v) = *reinterpret_cast<const uint4*>(a + c);
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        const double ve = to_f64(v[e]);
+        if (e & 1) s1 = fma(ve, SQUARE ? ve : x[c + e], s1);
+        else s0 = fma(ve, SQUARE ? ve : x[c + e], s0);
+      }
+    }
+  } else {
+    for (int c = c0 + tid; c < c1; c += 256) {
+      const double ve = to_f64(a[c]);
+      s0 = fma(ve, SQUARE ? ve : x[c], s0);
+    }
+  }
+  double sv = warp_sum(s0 + s1);
+  __shared__ double ws[8];
+  __shared__ bool last;
+  if ((tid & 31) == 0) ws[tid >> 5] = sv;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += ws[w];
+    rs.part[(int64_t)row * nch + chunk] = t;
+    __threadfence();
+    last = atomicAdd(&rs.cnt[row], 1) == nch - 1;
+    if (last) {
+      __threadfence();
+      double tot = 0.0;
+      for (int z = 0; z < nch; ++z) tot += __ldcg(&rs.part[(int64_t)row * nch + z]);
+      if (SQUARE) out[(int64_t)row * ld_out + row] = tot;
+      else out[row] = tot - b[brow0 + row];
+      rs.cnt[row] = 0;  // ready for the next launch (stream-ordered)
+    }
+  }
+}
+
+int rowdot_chunks(int ell, int64_t n) {
+  int nch = (int)((4 * 148 + ell - 1) / ell);
+  nch = (int)std::min<int64_t>(nch, std::max<int64_t>(1, n / 2048));
+  return std::max(1, std::min(nch, 64));
 }
 
 // ---------------------------------------------------------------------------
@@ -260,26 +309,40 @@ __global__ void k_gram_reduce(double* __restrict__ panel, Window W, const double
 // s = M^T w (alpha applied in k_finish)
 // ---------------------------------------------------------------------------
 
-template <typename T>
+// part[y, c] = sum over the window rows of split y of A[row, c] w[row]:
+// each thread owns V = 16 / sizeof(T) adjacent columns (one 16-byte load
+// per row), rows unrolled so several loads are in flight per thread
+template <typename T, int V>
 __global__ void __launch_bounds__(256) k_mtw_dense(double* __restrict__ part, Window W,
                                                    const T* __restrict__ A, int64_t lda, int n,
                                                    const double* __restrict__ w, int rows_per_split,
                                                    const Ctl* ctl) {
   if (ctl->diverged_at != 0) return;
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) * V;
   if (c >= n) return;
   const int ell = W.ell, N = W.nw * ell;
   const int pbeg = blockIdx.y * rows_per_split, pend = min(N, pbeg + rows_per_split);
-  double s = 0.0;
+  double s[V];
+#pragma unroll
+  for (int e = 0; e < V; ++e) s[e] = 0.0;
   for (int p = pbeg; p < pend;) {
     const int P = p / ell;
     const int a0 = p - P * ell;
     const int cnt = min(ell - a0, pend - p);
     const T* base = A + ((int64_t)W.blk[P] * ell + a0) * lda + c;
-    for (int q = 0; q < cnt; ++q) s += to_f64(base[(int64_t)q * lda]) * w[p + q];
+#pragma unroll 4
+    for (int q = 0; q < cnt; ++q) {
+      T v[V];
+      if (V > 1) *reinterpret_cast<uint4*>(v) = *reinterpret_cast<const uint4*>(base + (int64_t)q * lda);
+      else v[0] = base[(int64_t)q * lda];
+      const double wq = w[p + q];
+#pragma unroll
+      for (int e = 0; e < V; ++e) s[e] = fma(to_f64(v[e]), wq, s[e]);
+    }
     p += cnt;
   }
-  part[(int64_t)blockIdx.y * n + c] = s;
+#pragma unroll
+  for (int e = 0; e < V; ++e) part[(int64_t)blockIdx.y * n + c + e] = s[e];
 }
 
 template <typename T>
@@ -538,8 +601,10 @@ static inline unsigned cdiv(int64_t a, int64_t b) { return (unsigned)((a + b - 1
 template <typename T>
 void launch_residual_dense(double* r, const T* A, int64_t lda, int64_t row0, int64_t brow0,
                            int ell, int n, const double* x, const double* b, const Ctl* ctl,
-                           cudaStream_t s) {
-  k_residual_dense<T><<<cdiv(ell, 8), 256, 0, s>>>(r, A, lda, row0, brow0, ell, n, x, b, ctl);
+                           RowSplit rs, cudaStream_t s) {
+  constexpr int V = 16 / sizeof(T);
+  rs.vec = (n % V == 0 && lda % V == 0) ? 1 : 0;
+  k_rowdot<T, false><<<dim3(rs.nch, ell), 256, 0, s>>>(A, lda, row0, n, x, rs, r, 0, b, brow0, ctl);
 }
 void launch_gen_block(float* dst, float* hi, float* lo, uint64_t seed, int64_t row0, int ell,
                       int n_local, int64_t n_total, int64_t col0, cudaStream_t s) {
@@ -586,24 +651,11 @@ void launch_gram_dense(double* panel, double* part, int nsplit, const Window& W,
 // exact fp64 diagonal of A_k A_k^T (row sums of squares) into the panel: the
 // tensor core accumulates in truncating fp32, which biases these large
 // all-positive sums; every other entry has mixed signs and small partials
-__global__ void __launch_bounds__(256) k_gram_diag_fp64(double* __restrict__ panel_diag, int64_t ld,
-                                                        const float* __restrict__ A, int ell,
-                                                        int n) {
-  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (row >= ell) return;
-  const float* a = A + (int64_t)row * n;
-  double s = 0.0;
-  for (int c = lane; c < n; c += 32) {
-    const double v = (double)a[c];
-    s += v * v;
-  }
-  s = warp_sum(s);
-  if (lane == 0) panel_diag[(int64_t)row * ld + row] = s;
-}
-
 void launch_gram_diag_fp64(double* panel_diag, int64_t ld, const float* A, int ell, int n,
-                           cudaStream_t s) {
-  k_gram_diag_fp64<<<cdiv(ell, 8), 256, 0, s>>>(panel_diag, ld, A, ell, n);
+                           RowSplit rs, cudaStream_t s) {
+  rs.vec = (n % 4 == 0) ? 1 : 0;
+  k_rowdot<float, true><<<dim3(rs.nch, ell), 256, 0, s>>>(A, n, 0, n, nullptr, rs, panel_diag, ld,
+                                                           nullptr, 0, nullptr);
 }
 
 void launch_gram_reduce(double* panel, const Window& W, const double* part, int nsplit,
@@ -617,8 +669,14 @@ void launch_mtw_dense(double* part, int nsplit, const Window& W, const T* A, int
                       const double* w, const Ctl* ctl, cudaStream_t s) {
   const int N = W.nw * W.ell;
   const int rps = (N + nsplit - 1) / nsplit;
-  dim3 grid(cdiv(n, 256), nsplit);
-  k_mtw_dense<T><<<grid, 256, 0, s>>>(part, W, A, lda, n, w, rps, ctl);
+  constexpr int V = 16 / sizeof(T);
+  if (n % V == 0 && lda % V == 0) {
+    dim3 grid(cdiv(n, 256 * V), nsplit);
+    k_mtw_dense<T, V><<<grid, 256, 0, s>>>(part, W, A, lda, n, w, rps, ctl);
+  } else {
+    dim3 grid(cdiv(n, 256), nsplit);
+    k_mtw_dense<T, 1><<<grid, 256, 0, s>>>(part, W, A, lda, n, w, rps, ctl);
+  }
 }
 template <typename T>
 void launch_mtw_csc(double* s_out, const Window& W, const int* colptr, int n, const int* cscrow,
@@ -654,7 +712,8 @@ void launch_build_csc(int* colptr, int* cscrow, T* cscval, const int64_t* rowptr
 
 #define SLIM_INST(T)                                                                              \
   template void launch_residual_dense<T>(double*, const T*, int64_t, int64_t, int64_t, int, int, \
-                                         const double*, const double*, const Ctl*, cudaStream_t); \
+                                         const double*, const double*, const Ctl*, RowSplit,      \
+                                         cudaStream_t);                                           \
   template void launch_residual_csr<T>(double*, const int64_t*, const int*, const T*, int64_t,    \
                                        int64_t, int, const double*, const double*, const Ctl*,   \
                                        cudaStream_t);                                            \

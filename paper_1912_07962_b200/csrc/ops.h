@@ -41,10 +41,19 @@ void launch_record(const RecordParams& R, cudaStream_t s);
 // out[i] = sum_q in[q][i] in rank order (in-process shard group)
 void launch_group_sum(double* out, const double* const* in, int nin, int64_t count, cudaStream_t s);
 
+// scratch of a column-split row-dot launch: nch partials per row and a
+// per-row arrival counter (zero between launches)
+struct RowSplit {
+  double* part;  // ell x nch
+  int* cnt;      // ell
+  int nch;
+  int vec;       // set by the launcher: 16-byte loads
+};
+int rowdot_chunks(int ell, int64_t n);
 template <typename T>
 void launch_residual_dense(double* r, const T* A, int64_t lda, int64_t row0, int64_t brow0,
                            int ell, int n, const double* x, const double* b, const Ctl* ctl,
-                           cudaStream_t s);
+                           RowSplit rs, cudaStream_t s);
 void launch_gen_block(float* dst, float* hi, float* lo, uint64_t seed, int64_t row0, int ell,
                       int n_local, int64_t n_total, int64_t col0, cudaStream_t s);
 void launch_gen_apply(double* out, uint64_t seed, int64_t m, int n_local, int64_t n_total,
@@ -75,7 +84,7 @@ void launch_finish(const FinishParams& F, cudaStream_t s);
 void launch_gram_reduce(double* panel, const Window& W, const double* part, int nsplit,
                         cudaStream_t s);
 void launch_gram_diag_fp64(double* panel_diag, int64_t ld, const float* A, int ell, int n,
-                           cudaStream_t s);
+                           RowSplit rs, cudaStream_t s);
 int finish_grid(int n);
 void launch_stamp_start(Ctl* ctl, cudaStream_t s);
 
