@@ -314,9 +314,17 @@ def run_ours(args, world, rank, local, dist):
     def sampler():
         return slim.Sampler(scheme, M, seed)
 
-    # upload + kernel warm-up (untimed)
+    # upload + kernel warm-up (untimed).  The device-timed leg starts with the
+    # whole operator in HBM (uploaded up front, no host streaming); the e2e
+    # leg below measures the streamed default on a fresh operator.
+    prev = os.environ.get("SLIM_HOST_STREAMING")
+    os.environ["SLIM_HOST_STREAMING"] = "0"
     slim.run("slimls", op, sampler(), slim.Schedule("constant", alpha),
              epochs=min(r + 2, M) / M, r=r, device=dev, shard=shard)
+    if prev is None:
+        os.environ.pop("SLIM_HOST_STREAMING")
+    else:
+        os.environ["SLIM_HOST_STREAMING"] = prev
     timing = {"start_step": wprime + 1}
     _barrier(dist)
     with ClockSampler(dev) as clk:
@@ -364,18 +372,27 @@ def run_ours(args, world, rank, local, dist):
         if args.config == 5:
             op2 = op.with_rhs(b)  # fresh operator object: no cached device state
         h2d = _operator_bytes(op2) + 2 * xt.nbytes + total * 16
-        t0 = time.perf_counter()
-        tr2 = slim.run("slimls", op2, sampler(), slim.Schedule("constant", alpha),
-                       epochs=total / M, r=r, references={"x_true": xt}, record_every=1,
-                       device=dev)
-        wall = time.perf_counter() - t0
+        walls = []
+        while True:  # short runs are repeated on fresh operators, median reported
+            t0 = time.perf_counter()
+            tr2 = slim.run("slimls", op2, sampler(), slim.Schedule("constant", alpha),
+                           epochs=total / M, r=r, references={"x_true": xt}, record_every=1,
+                           device=dev)
+            walls.append(time.perf_counter() - t0)
+            if len(walls) == 3 or sum(walls) > 2.0:
+                break
+            op2 = op2.with_rhs(op2.rhs)  # same arrays, no cached device state
+        wall = float(np.median(walls))
+        print("e2e walls (s): " + " ".join(f"{w:.4f}" for w in walls), file=sys.stderr)
         del op2
         wall = _max_over_ranks(dist, wall)
         d2h = (total + 1) * (5 + 1) * 8 + xt.nbytes
         e2e = {"value": world * total / wall, "unit": "it/s",
                "h2d_bytes_per_step": int(h2d / total), "d2h_bytes_per_step": int(d2h / total),
-               "what": f"public run() on a fresh host operator: operator upload (+ per-block CSC "
-                       f"build for CSR) + {total} steps + history/x download, wall clock"}
+               "what": f"public run() on a fresh host operator: operator upload (streamed "
+                       f"block by block in first-use order, + per-block CSC build for CSR) + "
+                       f"{total} steps + history/x download, wall clock, median of "
+                       f"{len(walls)} fresh operators"}
         assert tr2.status == "ok"
     if rank != 0:
         return

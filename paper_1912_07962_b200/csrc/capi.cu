@@ -25,6 +25,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <chrono>
 #include <map>
 #include <string>
 #include <vector>
@@ -208,6 +209,16 @@ struct slim_ctx {
   std::vector<char> h_have;
   bool op_ready = false;
   bool rhs_set = false;
+  // host streaming: the operator stays in (pageable) host memory and each
+  // block is copied to HBM on stream su right before the batch that first
+  // samples it, overlapped with the factorizations of earlier batches
+  bool streaming = false;
+  const char* hs_dense = nullptr;           // dense rows
+  std::vector<const int64_t*> hs_rowptr;    // CSR: per block (ell + 1 entries, any base)
+  std::vector<const int32_t*> hs_col;
+  std::vector<const char*> hs_val;
+  std::vector<char> resident;               // per block: copied to HBM
+  cudaStream_t su = nullptr;
   // column sharding: exchange of partial sums (nullptr = single context)
   Comm* comm = nullptr;
   double* zero_b = nullptr;  // ell zeros: ranks != 0 do not subtract b
@@ -259,7 +270,7 @@ struct slim_ctx {
   int64_t iters_cap = 0;
   int64_t epoch_base = 0;
   cudaStream_t sx = nullptr, sg = nullptr, sf = nullptr;
-  cudaEvent_t ev_g[NEV], ev_f[NEV], ev_x[NEV];
+  cudaEvent_t ev_g[NEV], ev_f[NEV], ev_x[NEV], ev_u[NEV];
   int64_t* pin_div = nullptr;
   // profiling
   bool prof = false;
@@ -341,7 +352,9 @@ static void free_all(slim_ctx* c) {
   if (c->sf) cudaStreamDestroy(c->sf);
   if (c->sx) cudaStreamDestroy(c->sx);
   if (c->sg) cudaStreamDestroy(c->sg);
+  if (c->su) cudaStreamDestroy(c->su);
   for (int q = 0; q < NEV; ++q) {
+    if (c->ev_u[q]) cudaEventDestroy(c->ev_u[q]);
     if (c->ev_g[q]) cudaEventDestroy(c->ev_g[q]);
     if (c->ev_f[q]) cudaEventDestroy(c->ev_f[q]);
     if (c->ev_x[q]) cudaEventDestroy(c->ev_x[q]);
@@ -398,6 +411,15 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
   c->gen_n_total = d->gen_n_total;
   c->col_offset = d->col_offset;
   *out = c;
+  // SLIM_TRACE_CREATE=1: host time of the setup phases (stderr)
+  const bool trace = getenv("SLIM_TRACE_CREATE") != nullptr;
+  auto t_begin = std::chrono::steady_clock::now();
+  auto tick = [&](const char* what) {
+    if (!trace) return;
+    cudaDeviceSynchronize();
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_begin).count();
+    fprintf(stderr, "slim_create %-10s %8.2f ms\n", what, ms);
+  };
   CK(c, cudaSetDevice(c->dev));
   // the small latency-critical kernels (x-chain, Gram panels) get the
   // higher priority so their CTAs are dispatched ahead of pending tiles of a
@@ -407,6 +429,7 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
   CK(c, cudaStreamCreateWithPriority(&c->sx, cudaStreamNonBlocking, prio_hi));
   CK(c, cudaStreamCreateWithPriority(&c->sg, cudaStreamNonBlocking, prio_hi));
   CK(c, cudaStreamCreateWithPriority(&c->sf, cudaStreamNonBlocking, prio_lo));
+  CK(c, cudaStreamCreateWithPriority(&c->su, cudaStreamNonBlocking, prio_hi));
   {
     // systems per batched factorization: enough to overlap the per-column
     // critical paths of mid-size systems; large systems fill the GPU alone
@@ -419,9 +442,11 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
     CK(c, cudaEventCreateWithFlags(&c->ev_g[q], cudaEventDisableTiming));
     CK(c, cudaEventCreateWithFlags(&c->ev_f[q], cudaEventDisableTiming));
     CK(c, cudaEventCreateWithFlags(&c->ev_x[q], cudaEventDisableTiming));
+    CK(c, cudaEventCreateWithFlags(&c->ev_u[q], cudaEventDisableTiming));
   }
   CK(c, cudaEventCreate(&c->run_a));
   CK(c, cudaEventCreate(&c->run_b));
+  tick("streams");
   CK(c, cudaHostAlloc((void**)&c->pin_div, sizeof(int64_t), cudaHostAllocDefault));
   *c->pin_div = 0;
 
@@ -436,6 +461,7 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
   ALLOC(c, c->b, sizeof(double) * c->m);
   ALLOC(c, c->ctl, sizeof(Ctl));
   ALLOC(c, c->panels, sizeof(double) * (size_t)c->S * c->panel_stride);
+  tick("panels");
   c->Lbuf.assign(2 * c->D, nullptr);
   c->Lmap.resize(2 * c->D);
   c->Dinv.assign(2 * c->D, nullptr);
@@ -450,6 +476,7 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
     ALLOC(c, c->cflags[q], sizeof(int) * ntiles);
     CK(c, cudaMemset(c->cflags[q], 0, sizeof(int) * ntiles));
   }
+  tick("factors");
   ALLOC(c, c->tickets, sizeof(int) * 2);
   ALLOC(c, c->tflags, sizeof(int) * 2 * c->Tmax);
   CK(c, cudaMemset(c->tflags, 0, sizeof(int) * 2 * c->Tmax));
@@ -495,6 +522,7 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
   Ctl h{};
   h.div_limit_sq = 1e24;
   CK(c, cudaMemcpy(c->ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice));
+  tick("done");
   return SLIM_OK;
 }
 
@@ -516,7 +544,12 @@ int slim_upload_dense(slim_ctx* c, const void* a, const double* b) {
   CK(c, cudaSetDevice(c->dev));
   const size_t bytes = (size_t)c->m * c->n * c->vsize;
   if (!c->A) ALLOC(c, c->A, bytes);
-  CK(c, cudaMemcpy(c->A, a, bytes, cudaMemcpyHostToDevice));
+  if (c->streaming) {  // rows are copied block by block inside slim_run
+    c->hs_dense = (const char*)a;
+    c->resident.assign(c->M, 0);
+  } else {
+    CK(c, cudaMemcpy(c->A, a, bytes, cudaMemcpyHostToDevice));
+  }
   CK(c, cudaMemcpy(c->b, b, sizeof(double) * c->m, cudaMemcpyHostToDevice));
   c->op_ready = true;
   return SLIM_OK;
@@ -563,6 +596,28 @@ int slim_upload_csr_block(slim_ctx* c, int64_t block, const int64_t* rowptr, con
   if (c->layout != SLIM_CSR_PERBLOCK) FAIL(c, SLIM_EINVAL, "context layout is not CSR");
   if (block < 1 || block > c->M)
     FAIL(c, SLIM_ERANGE, "block index %lld out of range 1..%lld", (long long)block, (long long)c->M);
+  if (c->streaming) {
+    // only the pointers are kept; slim_finalize_operator sizes the device
+    // arrays and slim_run copies the block when it is first sampled
+    if (c->hs_rowptr.empty()) {
+      c->hs_rowptr.assign(c->M, nullptr);
+      c->hs_col.assign(c->M, nullptr);
+      c->hs_val.assign(c->M, nullptr);
+      c->h_have.assign(c->M, 0);
+      c->h_b.assign(c->m, 0.0);
+    }
+    if (rowptr[c->ell] > rowptr[0] && (!col || !val)) FAIL(c, SLIM_EINVAL, "null argument");
+    for (int64_t i = 0; i < c->ell; ++i)
+      if (rowptr[i + 1] < rowptr[i])
+        FAIL(c, SLIM_EINVAL, "rowptr of block %lld not monotone at row %lld", (long long)block, (long long)i);
+    c->hs_rowptr[block - 1] = rowptr;
+    c->hs_col[block - 1] = col;
+    c->hs_val[block - 1] = (const char*)val;
+    for (int64_t i = 0; i < c->ell; ++i) c->h_b[(block - 1) * c->ell + i] = b_block[i];
+    c->h_have[block - 1] = 1;
+    c->op_ready = false;
+    return SLIM_OK;
+  }
   // staged on the host; the whole operator is pushed by slim_finalize_operator
   if (c->h_have.empty()) {
     c->h_have.assign(c->M, 0);
@@ -626,6 +681,88 @@ static int assemble_staged_csr(slim_ctx* c) {
   return slim_upload_csr(c, rp.data(), colv.data(), valv.data(), bb.data());
 }
 
+// streamed CSR: device arrays sized from the registered blocks, the global
+// row pointers and b uploaded; values, columns and the per-block CSC follow
+// block by block (ensure_blocks)
+static int size_streamed_csr(slim_ctx* c) {
+  const int64_t ell = c->ell, M = c->M;
+  for (int64_t bk = 0; bk < M; ++bk)
+    if (!c->h_have[bk]) FAIL(c, SLIM_EINVAL, "block %lld was never uploaded", (long long)bk + 1);
+  c->h_blkbase.assign(M + 1, 0);
+  for (int64_t bk = 0; bk < M; ++bk) {
+    const int64_t nb = c->hs_rowptr[bk][ell] - c->hs_rowptr[bk][0];
+    if (nb > 0x7fffffffLL) FAIL(c, SLIM_EINVAL, "block %lld has more than 2^31 nonzeros", (long long)bk + 1);
+    c->h_blkbase[bk + 1] = c->h_blkbase[bk] + nb;
+  }
+  const int64_t nnz = c->h_blkbase[M];
+  std::vector<int64_t> rp(c->m + 1);
+  for (int64_t bk = 0; bk < M; ++bk) {
+    const int64_t* r = c->hs_rowptr[bk];
+    for (int64_t i = 0; i < ell; ++i) rp[bk * ell + i] = c->h_blkbase[bk] + (r[i] - r[0]);
+  }
+  rp[c->m] = nnz;
+  for (void** pp : {(void**)&c->rowptr, (void**)&c->col, (void**)&c->val, (void**)&c->colptr,
+                    (void**)&c->cscrow, (void**)&c->cscval, (void**)&c->blkbase})
+    if (*pp) cudaFree(*pp), *pp = nullptr;
+  c->nnz = nnz;
+  ALLOC(c, c->rowptr, sizeof(int64_t) * (c->m + 1));
+  ALLOC(c, c->col, sizeof(int) * (size_t)std::max<int64_t>(1, nnz));
+  ALLOC(c, c->val, c->vsize * (size_t)std::max<int64_t>(1, nnz));
+  ALLOC(c, c->colptr, sizeof(int) * (size_t)M * (c->n + 1));
+  ALLOC(c, c->cscrow, sizeof(int) * (size_t)std::max<int64_t>(1, nnz));
+  ALLOC(c, c->cscval, c->vsize * (size_t)std::max<int64_t>(1, nnz));
+  ALLOC(c, c->blkbase, sizeof(int64_t) * (M + 1));
+  CK(c, cudaMemcpy(c->rowptr, rp.data(), sizeof(int64_t) * (c->m + 1), cudaMemcpyHostToDevice));
+  CK(c, cudaMemcpy(c->blkbase, c->h_blkbase.data(), sizeof(int64_t) * (M + 1), cudaMemcpyHostToDevice));
+  CK(c, cudaMemcpy(c->b, c->h_b.data(), sizeof(double) * c->m, cudaMemcpyHostToDevice));
+  c->h_have.clear();
+  c->h_b.clear();
+  c->resident.assign(M, 0);
+  c->op_ready = true;
+  return SLIM_OK;
+}
+
+// copy the not-yet-resident blocks among blks[0..cnt) (0-based row blocks)
+// to HBM on stream su (and build their CSC); pageable host memory, so the
+// host thread pays the copy while the device works on earlier batches
+static int ensure_blocks(slim_ctx* c, const int64_t* blks, int cnt, int* copied = nullptr) {
+  if (copied) *copied = 0;
+  if (!c->streaming || c->resident.empty()) return SLIM_OK;
+  for (int q = 0; q < cnt; ++q) {
+    const int64_t bk = blks[q];
+    if (c->resident[bk]) continue;
+    if (copied) ++*copied;
+    if (c->layout == SLIM_DENSE_ROWMAJOR) {
+      const size_t rb = (size_t)c->ell * c->n * c->vsize;
+      CK(c, cudaMemcpyAsync((char*)c->A + bk * rb, c->hs_dense + bk * rb, rb, cudaMemcpyHostToDevice, c->su));
+    } else {
+      const int64_t* r = c->hs_rowptr[bk];
+      const int64_t nb = r[c->ell] - r[0], base = c->h_blkbase[bk];
+      const int32_t* col = c->hs_col[bk] + r[0];
+      for (int64_t e = 0; e < nb; ++e)
+        if (col[e] < 0 || col[e] >= c->n)
+          FAIL(c, SLIM_EINVAL, "column index %d out of range in block %lld", col[e], (long long)bk + 1);
+      if (nb > 0) {
+        CK(c, cudaMemcpyAsync(c->col + base, col, sizeof(int) * nb, cudaMemcpyHostToDevice, c->su));
+        CK(c, cudaMemcpyAsync((char*)c->val + c->vsize * base, c->hs_val[bk] + c->vsize * r[0],
+                              c->vsize * nb, cudaMemcpyHostToDevice, c->su));
+      }
+      if (c->vdt == SLIM_F64)
+        launch_build_csc<double>(c->colptr, c->cscrow, (double*)c->cscval, c->rowptr, c->col,
+                                 (const double*)c->val, c->blkbase, c->m, (int)c->ell, (int)c->n,
+                                 c->M, c->su, bk, 1);
+      else
+        launch_build_csc<float>(c->colptr, c->cscrow, (float*)c->cscval, c->rowptr, c->col,
+                                (const float*)c->val, c->blkbase, c->m, (int)c->ell, (int)c->n,
+                                c->M, c->su, bk, 1);
+      CKLAUNCH(c);
+      c->launches += 5;
+    }
+    c->resident[bk] = 1;
+  }
+  return SLIM_OK;
+}
+
 int slim_finalize_operator(slim_ctx* c) {
   if (!c) FAIL(c, SLIM_EINVAL, "null argument");
   CK(c, cudaSetDevice(c->dev));
@@ -637,6 +774,11 @@ int slim_finalize_operator(slim_ctx* c) {
   if (c->layout == SLIM_GEN_SPLITMIX64) {
     if (!c->rhs_set) FAIL(c, SLIM_ESTATE, "generated operator needs its right-hand side (slim_set_rhs)");
     c->op_ready = true;
+    return SLIM_OK;
+  }
+  if (c->streaming && !c->hs_rowptr.empty()) {
+    int rc = size_streamed_csr(c);
+    if (rc) return rc;
     return SLIM_OK;
   }
   if (!c->h_have.empty()) {
@@ -737,7 +879,12 @@ int slim_set_profiling(slim_ctx* c, int32_t enable) {
 
 int slim_set_host_streaming(slim_ctx* c, int32_t enable) {
   if (!c) FAIL(c, SLIM_EINVAL, "null argument");
-  if (enable) FAIL(c, SLIM_EINVAL, "host streaming is not available in this build");
+  if (enable && c->layout == SLIM_GEN_SPLITMIX64)
+    FAIL(c, SLIM_EINVAL, "the generated layout has no host operator to stream");
+  if (enable && c->comm) FAIL(c, SLIM_EINVAL, "host streaming is single-context only");
+  if ((c->A || c->rowptr || !c->h_have.empty()) && (enable != 0) != c->streaming)
+    FAIL(c, SLIM_ESTATE, "set host streaming before uploading the operator");
+  c->streaming = enable != 0;
   return SLIM_OK;
 }
 
@@ -1233,6 +1380,19 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
       launches_at_k0 = c->launches;
       a_recorded = true;
     }
+    // ---- host streaming: the batch's first-sampled blocks into HBM (su)
+    if (c->streaming && !c->resident.empty()) {
+      int64_t blks[MAX_BATCH];
+      for (int b = 0; b < nb; ++b) blks[b] = idx[kb0 + b - 1] - 1;
+      int copied = 0;
+      int rc = ensure_blocks(c, blks, nb, &copied);
+      if (rc) return rc;
+      if (copied) {
+        CK(c, cudaEventRecord(c->ev_u[B % NEV], c->su));
+        CK(c, cudaStreamWaitEvent(c->sg, c->ev_u[B % NEV], 0));
+        CK(c, cudaStreamWaitEvent(c->sx, c->ev_u[B % NEV], 0));
+      }
+    }
     // ---- Gram panels (sg): the ring slots they overwrite were last read by
     // the factorization (and, for generated blocks, the x-chain) of batch B - 2
     if (B >= 2) CK(c, cudaStreamWaitEvent(c->sg, c->ev_f[(B - 2) % NEV], 0));
@@ -1373,6 +1533,11 @@ extern "C" int slim_block_residual(slim_ctx* c, int64_t block, const double* x, 
   if (c->layout == SLIM_GEN_SPLITMIX64) {
     launch_gen_block(c->gring, nullptr, nullptr, c->gen_seed, (block - 1) * c->ell, (int)c->ell,
                      (int)c->n, c->gen_n_total, c->col_offset, c->sx);
+  } else if (c->streaming && !c->resident.empty()) {
+    const int64_t bk = block - 1;
+    int rs = ensure_blocks(c, &bk, 1);
+    if (rs) return rs;
+    CK(c, cudaStreamSynchronize(c->su));
   }
   int rc = enqueue_residual(c, c->layout == SLIM_GEN_SPLITMIX64 ? 0 : block - 1, block - 1);
   if (rc) return rc;

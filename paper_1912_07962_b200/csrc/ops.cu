@@ -505,8 +505,8 @@ __global__ void k_group_sum(double* __restrict__ out, GroupIn in, int nin, int64
 // ---------------------------------------------------------------------------
 
 __global__ void k_csc_count(int* __restrict__ colptr, const int64_t* __restrict__ rowptr,
-                            const int* __restrict__ col, int64_t m, int ell, int n) {
-  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+                            const int* __restrict__ col, int64_t row0, int64_t m, int ell, int n) {
+  const int64_t row = row0 + (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= m) return;
   const int64_t b = row / ell;
@@ -537,9 +537,9 @@ __global__ void __launch_bounds__(256) k_csc_scan(int* __restrict__ colptr, int 
 template <typename T>
 __global__ void k_csc_fill(int* __restrict__ colptr, const int64_t* __restrict__ rowptr,
                            const int* __restrict__ col, const T* __restrict__ val,
-                           int* __restrict__ cscrow, T* __restrict__ cscval, int64_t m, int ell,
-                           int n) {
-  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+                           int* __restrict__ cscrow, T* __restrict__ cscval, int64_t row0,
+                           int64_t m, int ell, int n) {
+  const int64_t row = row0 + (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= m) return;
   const int64_t b = row / ell;
@@ -701,13 +701,18 @@ void launch_group_sum(double* out, const double* const* in, int nin, int64_t cou
 template <typename T>
 void launch_build_csc(int* colptr, int* cscrow, T* cscval, const int64_t* rowptr, const int* col,
                       const T* val, const int64_t* blkbase, int64_t m, int ell, int n,
-                      int64_t nblocks, cudaStream_t s) {
-  cudaMemsetAsync(colptr, 0, sizeof(int) * (size_t)nblocks * (n + 1), s);
-  k_csc_count<<<cdiv(m, 8), 256, 0, s>>>(colptr, rowptr, col, m, ell, n);
-  k_csc_scan<<<(unsigned)nblocks, 256, 0, s>>>(colptr, n);
-  k_csc_fill<T><<<cdiv(m, 8), 256, 0, s>>>(colptr, rowptr, col, val, cscrow, cscval, m, ell, n);
-  k_csc_shift<<<(unsigned)nblocks, 256, 0, s>>>(colptr, n);
-  k_csc_sort<T><<<cdiv(nblocks * n, 256), 256, 0, s>>>(colptr, cscrow, cscval, blkbase, nblocks, n);
+                      int64_t nblocks, cudaStream_t s, int64_t blk0, int64_t nblk) {
+  if (nblk < 0) nblk = nblocks - blk0;
+  if (nblk <= 0) return;
+  int* cp = colptr + blk0 * (int64_t)(n + 1);
+  const int64_t row0 = blk0 * ell, row1 = (blk0 + nblk) * (int64_t)ell;
+  cudaMemsetAsync(cp, 0, sizeof(int) * (size_t)nblk * (n + 1), s);
+  k_csc_count<<<cdiv(row1 - row0, 8), 256, 0, s>>>(colptr, rowptr, col, row0, row1, ell, n);
+  k_csc_scan<<<(unsigned)nblk, 256, 0, s>>>(cp, n);
+  k_csc_fill<T><<<cdiv(row1 - row0, 8), 256, 0, s>>>(colptr, rowptr, col, val, cscrow, cscval, row0,
+                                                      row1, ell, n);
+  k_csc_shift<<<(unsigned)nblk, 256, 0, s>>>(cp, n);
+  k_csc_sort<T><<<cdiv(nblk * n, 256), 256, 0, s>>>(cp, cscrow, cscval, blkbase + blk0, nblk, n);
 }
 
 #define SLIM_INST(T)                                                                              \
@@ -726,7 +731,8 @@ void launch_build_csc(int* colptr, int* cscrow, T* cscval, const int64_t* rowptr
   template void launch_mtw_csc<T>(double*, const Window&, const int*, int, const int*, const T*,  \
                                   const int64_t*, const double*, const Ctl*, cudaStream_t);      \
   template void launch_build_csc<T>(int*, int*, T*, const int64_t*, const int*, const T*,         \
-                                    const int64_t*, int64_t, int, int, int64_t, cudaStream_t);
+                                    const int64_t*, int64_t, int, int, int64_t, cudaStream_t,     \
+                                    int64_t, int64_t);
 
 SLIM_INST(double)
 SLIM_INST(float)

@@ -79,7 +79,7 @@ void launch_mtw_csc(double* s_out, const Window& W, const int* colptr, int n, co
 template <typename T>
 void launch_build_csc(int* colptr, int* cscrow, T* cscval, const int64_t* rowptr, const int* col,
                       const T* val, const int64_t* blkbase, int64_t m, int ell, int n,
-                      int64_t nblocks, cudaStream_t s);
+                      int64_t nblocks, cudaStream_t s, int64_t blk0 = 0, int64_t nblk = -1);
 void launch_finish(const FinishParams& F, cudaStream_t s);
 void launch_gram_reduce(double* panel, const Window& W, const double* part, int nsplit,
                         cudaStream_t s);

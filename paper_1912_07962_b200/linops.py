@@ -18,6 +18,8 @@ from __future__ import annotations
 import ctypes as C
 from dataclasses import dataclass
 
+import os
+
 import numpy as np
 
 from . import _lib
@@ -436,13 +438,36 @@ def device_operator(op, r: int, device: int = 0) -> DeviceOperator:
         dop.call("slim_finalize_operator")
         cache[key] = dop
         return dop
+    # host streaming (default): the operator is registered by pointer and each
+    # block is copied to HBM inside slim_run right before the batch that first
+    # samples it, overlapped with the device work of earlier batches; the
+    # host arrays are kept alive by the device operator
+    streaming = os.environ.get("SLIM_HOST_STREAMING", "1") != "0"
     a = _dense_source(src)
     if a is not None:
         dtype = np.float32 if a.dtype == np.float32 else np.float64
         dop = DeviceOperator(n_rows=m, n_cols=n, ell=ell, r=r, layout=_lib.SLIM_DENSE_ROWMAJOR,
                              dtype=dtype, device=device)
         a_c = np.ascontiguousarray(a, dtype=dtype)
+        if streaming:
+            dop.call("slim_set_host_streaming", 1)
+            dop.host_refs = (a_c, b)
         dop.call("slim_upload_dense", _lib.vptr(a_c), _lib.dptr(b))
+    elif streaming and isinstance(src, SparseBlockOperator):
+        dop = DeviceOperator(n_rows=m, n_cols=n, ell=ell, r=r, layout=_lib.SLIM_CSR_PERBLOCK,
+                             dtype=src.dtype, device=device)
+        dop.call("slim_set_host_streaming", 1)
+        refs = [b]
+        for i in range(1, src.n_blocks + 1):
+            ip, ix, d, _ = src.csr_block(i)
+            ip = np.ascontiguousarray(ip, dtype=np.int64)
+            ix = np.ascontiguousarray(ix, dtype=np.int32)
+            d = np.ascontiguousarray(d, dtype=src.dtype)
+            bb = b[(i - 1) * ell:i * ell]
+            dop.call("slim_upload_csr_block", i, _lib.i64ptr(ip), _lib.i32ptr(ix), _lib.vptr(d),
+                     _lib.dptr(bb))
+            refs.append((ip, ix, d))
+        dop.host_refs = refs
     else:
         if isinstance(src, SparseBlockOperator):
             rowptr, col, val = src.global_csr()

@@ -405,3 +405,54 @@ def test_sharded_generated(slim):
     from paper_1912_07962_b200 import problems
     op, b, xt = problems.generated_dense(n=1536, m=64 * 30, ell=64, seed=9)
     _sharded_vs_single(slim, op, xt, "cyclic", 0, 100.0, 8, 20, 2)
+
+
+# ---------------------------------------------------------------------------
+# host streaming: blocks copied to HBM inside the run, in first-use order
+# ---------------------------------------------------------------------------
+
+
+def _run_fresh(slim, make_op, monkeypatch, streaming, scheme, seed, alpha, r, K, refs):
+    monkeypatch.setenv("SLIM_HOST_STREAMING", "1" if streaming else "0")
+    op = make_op()
+    return slim.run("slimls", op, slim.Sampler(scheme, op.n_blocks, seed),
+                    slim.Schedule("constant", alpha), epochs=K / op.n_blocks, r=r,
+                    references=refs)
+
+
+def test_host_streaming_csr_bit_identical(slim, monkeypatch):
+    """Streamed CSR (values, columns and per-block CSC built inside the run)
+    gives the same bits as the operator uploaded and converted up front."""
+    from paper_1912_07962_b200 import problems
+    prob = problems.tomo2d(grid=48, n_views=40, rays=68, seed=4)
+    mk = lambda: slim.SparseBlockOperator([prob.op.csr_block(i) for i in range(1, 41)], prob.b)
+    a = _run_fresh(slim, mk, monkeypatch, True, "random_cyclic", 5, 1000.0, 6, 70,
+                   {"x_true": prob.x_true})
+    b = _run_fresh(slim, mk, monkeypatch, False, "random_cyclic", 5, 1000.0, 6, 70,
+                   {"x_true": prob.x_true})
+    np.testing.assert_array_equal(a.x_final, b.x_final)
+    np.testing.assert_array_equal(a.residual_norms, b.residual_norms)
+
+
+def test_host_streaming_dense_bit_identical(slim, monkeypatch):
+    c = gc.dense_case("cfg1_reduced")
+    mk = lambda: slim.DenseBlockOperator(c["A"], int(c["ell"]), c["b"])
+    a = _run_fresh(slim, mk, monkeypatch, True, "uniform_iid", 3, 50.0, 4, 60, c["refs"])
+    b = _run_fresh(slim, mk, monkeypatch, False, "uniform_iid", 3, 50.0, 4, 60, c["refs"])
+    np.testing.assert_array_equal(a.x_final, b.x_final)
+
+
+def test_host_streaming_rejects_bad_column(slim, monkeypatch):
+    from paper_1912_07962_b200 import problems
+    prob = problems.tomo2d(grid=16, n_views=6, rays=23, seed=1)
+    parts = [tuple(np.array(p) if isinstance(p, np.ndarray) else p for p in prob.op.csr_block(i))
+             for i in range(1, 7)]
+    ip, ix, d, shp = parts[3]
+    ix = ix.copy()
+    ix[0] = 10_000  # out of range, only seen when block 4 is first sampled
+    parts[3] = (ip, ix, d, shp)
+    monkeypatch.setenv("SLIM_HOST_STREAMING", "1")
+    op = slim.SparseBlockOperator(parts, prob.b)
+    with pytest.raises(ValueError, match="column index"):
+        slim.run("slimls", op, slim.Sampler("cyclic", 6, 0), slim.Schedule("constant", 10.0),
+                 epochs=1.0, r=1)

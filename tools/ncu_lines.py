@@ -1,6 +1,7 @@
 """Attribute ncu warp-stall samples of a kernel to CUDA source lines.
 
-usage: python tools/ncu_lines.py <report.ncu-rep> <object .o or cubin> <mangled kernel> <source.cu>
+usage: python tools/ncu_lines.py <report.ncu-rep> <object .o or cubin> <mangled kernel> [<source.cu>]
+Lines are reported as file:line (inlined headers included).
 """
 import csv
 import glob
@@ -26,9 +27,9 @@ def sass_lines(obj, kernel):
             continue
         if not inside:
             continue
-        m = re.search(r'line (\d+)', ln)
+        m = re.search(r'File "([^"]+)", line (\d+)', ln)
         if "//## File" in ln and m:
-            cur = int(m.group(1))
+            cur = (m.group(1), int(m.group(2)))
             continue
         if re.match(r"\s+/\*[0-9a-f]{4,}\*/\s+[^.\s]", ln):
             res.append(cur)
@@ -36,7 +37,7 @@ def sass_lines(obj, kernel):
 
 
 def main():
-    rep, obj, kernel, src = sys.argv[1:5]
+    rep, obj, kernel = sys.argv[1:4]
     lines = sass_lines(obj, kernel)
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True,
                          text=True).stdout.splitlines()
@@ -53,11 +54,18 @@ def main():
         for i in stall_cols:
             d[1][h[i]] = d[1].get(h[i], 0) + int(r[i])
     total = sum(v[0] for v in agg.values()) or 1
-    text = open(src).read().splitlines()
+    texts = {}
     for ln, (n, st) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:int(os.environ.get("TOP", 25))]:
         top = sorted(st.items(), key=lambda kv: -kv[1])[:3]
-        s = text[ln - 1].strip()[:70] if ln and ln <= len(text) else "?"
-        print(f"{100 * n / total:5.1f}%  L{ln}: {s}   " +
+        s, where = "?", "?"
+        if ln:
+            f, no = ln
+            if f not in texts:
+                texts[f] = open(f).read().splitlines() if os.path.exists(f) else []
+            t = texts[f]
+            s = t[no - 1].strip()[:64] if no <= len(t) else "?"
+            where = f"{os.path.basename(f)}:{no}"
+        print(f"{100 * n / total:5.1f}%  {where}: {s}   " +
               " ".join(f"{k[6:]}={100 * v / max(1, n):.0f}%" for k, v in top))
 
 
