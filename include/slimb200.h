@@ -120,9 +120,16 @@ int slim_run(slim_ctx* ctx, const int64_t* block_idx, const double* alphas, int6
              int64_t record_every, double* hist, int64_t* n_rows, int32_t* status,
              int64_t* diverged_at, double* iterates);
 
-/* Stream mode (for e2e / host-resident operators): the same as slim_run,
- * but each step's block is copied host->device inside the run from the
- * pinned host operator registered with slim_upload_* (HOST staging).    */
+/* Host streaming (replaces the per-step fetch_block of a
+ * host operator, linops.py:192-206, 270-279).  Call before uploading: with
+ * enable = 1, slim_upload_dense / slim_upload_csr_block only REGISTER the
+ * host pointers (they must stay valid while the context may still copy
+ * them); slim_finalize_operator sizes the device arrays; slim_run copies
+ * each block to HBM on its own stream right before the batch that first
+ * samples it (per-block CSC built there), overlapped with earlier device
+ * work.  Column indices are validated when a block is copied (SLIM_EINVAL).
+ * Results are bit-identical to an operator uploaded up front.  Not for the
+ * generated layout or sharded contexts.                                  */
 int slim_set_host_streaming(slim_ctx* ctx, int32_t enable);
 
 /* ---- column sharding -------------------------------------
