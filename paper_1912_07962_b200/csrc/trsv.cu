@@ -97,35 +97,109 @@ __device__ __forceinline__ void gemvT_smem(double* out, const double* M, const d
   }
   __syncthreads();
 }
-// v[a] -= sum_b Lg[a][b] x[b], Lg a row-major tile in global memory (L2):
-// thread (a, q) reads columns 8 m + 2 q, +1 (m < 8), so the four threads of a
-// row read 64 contiguous bytes per instruction (two full sectors)
-__device__ __forceinline__ void gemv_sub_global(double* v, const double* Lg, const double* x, int tid) {
-  const int a = tid >> 2, q = tid & 3;
-  const double2* row = reinterpret_cast<const double2*>(Lg + a * TB);
-  double2 l[8];
-#pragma unroll
-  for (int m = 0; m < 8; ++m) l[m] = __ldcg(row + 4 * m + q);
-  double s = 0.0;
-#pragma unroll
-  for (int m = 0; m < 8; ++m) {
-    s = fma(l[m].x, x[8 * m + 2 * q], s);
-    s = fma(l[m].y, x[8 * m + 2 * q + 1], s);
-  }
-  s += __shfl_xor_sync(0xffffffffu, s, 1);
-  s += __shfl_xor_sync(0xffffffffu, s, 2);
-  if (q == 0) v[a] -= s;
+// ---- bulk-copy ring of the non-critical tiles ----
+constexpr int RS = 3;  // 32 KB slots
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(n));
 }
-// v[a] -= sum_b Lg[b][a] x[b] (transposed, global); ends with a barrier
-__device__ __forceinline__ void gemvT_sub_global(double* v, const double* Lg, const double* x,
-                                                 double* part, int tid) {
-  const int a = tid & 63, g = tid >> 6;
-  double l[16];
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nW_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra W_%=;\n}\n" ::"r"(smem_addr(b)),
+      "r"(parity)
+      : "memory");
+}
+// one 32 KB tile (contiguous, tile-major) global -> shared, completing on b
+__device__ __forceinline__ void bulk_tile(double* dst, const double* src, uint64_t* b) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)),
+               "r"(TB * TB * 8)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(TB * TB * 8), "r"(smem_addr(b))
+      : "memory");
+}
+
+// The non-critical tiles a CTA consumes, in consumption order:
+// forward  k = i0 .. last - 1, own rows ip >= k + 2 ascending: tile (ip, k);
+// backward k = T - 1 .. me + 1, own rows ip <= k - 2 ascending: tile (k, ip).
+struct TileSeq {
+  int dir, k, ip;
+};
+struct SeqCtx {
+  int me, C, T, i0, last;
+  bool has_fwd;
+  __device__ int first_own_ge(int v) const { return v <= me ? me : me + ((v - me + C - 1) / C) * C; }
+  // move s to the next valid position (itself if valid); false when exhausted
+  __device__ bool norm(TileSeq& s) const {
+    while (true) {
+      if (s.dir == 0) {
+        if (!has_fwd || s.k >= last) {
+          s.dir = 1;
+          s.k = T - 1;
+          s.ip = me;
+          continue;
+        }
+        if (s.ip <= last) return true;
+        ++s.k;
+        s.ip = first_own_ge(s.k + 2);
+      } else {
+        if (s.k <= me) return false;
+        if (s.ip <= s.k - 2) return true;
+        --s.k;
+        s.ip = me;
+      }
+    }
+  }
+  __device__ const double* tile(const double* L, const TileSeq& s) const {
+    return L + (s.dir == 0 ? tile_off(s.ip, s.k) : tile_off(s.k, s.ip));
+  }
+  __device__ void advance(TileSeq& s) const { s.ip += C; }
+};
+
+// v[8w + r] -= sum_b M[8w + r][b] x[b] for the 64x64 row-major (unpadded)
+// tile M: warp w reads one 512-byte row per instruction (conflict-free) and
+// a butterfly reduces its 8 row partials across the lanes in 9 shuffles
+__device__ __forceinline__ void gemv_sub_ring(double* v, const double* M, const double* x, int tid) {
+  const int w = tid >> 5, lane = tid & 31;
+  const double2 xv = *reinterpret_cast<const double2*>(x + 2 * lane);
+  double p[8];
 #pragma unroll
-  for (int b = 0; b < 16; ++b) l[b] = __ldcg(Lg + (16 * g + b) * TB + a);
+  for (int r = 0; r < 8; ++r) {
+    const double2 l = *reinterpret_cast<const double2*>(M + (8 * w + r) * TB + 2 * lane);
+    p[r] = fma(l.x, xv.x, l.y * xv.y);
+  }
+  const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const double mine = h16 ? p[i + 4] : p[i];
+    const double other = __shfl_xor_sync(0xffffffffu, h16 ? p[i] : p[i + 4], 16);
+    p[i] = mine + other;
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const double mine = h8 ? p[i + 2] : p[i];
+    const double other = __shfl_xor_sync(0xffffffffu, h8 ? p[i] : p[i + 2], 8);
+    p[i] = mine + other;
+  }
+  {
+    const double mine = h4 ? p[1] : p[0];
+    const double other = __shfl_xor_sync(0xffffffffu, h4 ? p[0] : p[1], 4);
+    p[0] = mine + other;
+  }
+  p[0] += __shfl_xor_sync(0xffffffffu, p[0], 2);
+  p[0] += __shfl_xor_sync(0xffffffffu, p[0], 1);
+  if ((lane & 3) == 0) v[8 * w + (h16 ? 4 : 0) + (h8 ? 2 : 0) + (h4 ? 1 : 0)] -= p[0];
+}
+// v[a] -= sum_b M[b][a] x[b] (unpadded tile, transposed); ends with a barrier
+__device__ __forceinline__ void gemvT_sub_ring(double* v, const double* M, const double* x, double* part,
+                                               int tid) {
+  const int a = tid & 63, g = tid >> 6;
   double s = 0.0;
 #pragma unroll
-  for (int b = 0; b < 16; ++b) s = fma(l[b], x[16 * g + b], s);
+  for (int b = 0; b < 16; ++b) s = fma(M[(16 * g + b) * TB + a], x[16 * g + b], s);
   part[g * TB + a] = s;
   __syncthreads();
   if (tid < TB) v[tid] -= (part[tid] + part[TB + tid]) + (part[2 * TB + tid] + part[3 * TB + tid]);
@@ -134,22 +208,25 @@ __device__ __forceinline__ void gemvT_sub_global(double* v, const double* Lg, co
 
 size_t trsv_smem_bytes(int T, int C) {
   const int nown = (T + C - 1) / C;
-  return sizeof(double) * (size_t)(3 * nown * TB + 2 * TB * TS + TB + 4 * TB) + sizeof(int) * 2 * (size_t)T;
+  return sizeof(double) * (size_t)(RS * TB * TB + 3 * nown * TB + 2 * TB * TS + TB + 4 * TB) +
+         sizeof(int) * 2 * (size_t)T;
 }
 
 __global__ void __launch_bounds__(256, 1) k_trsv_cluster(TrsvParams P) {
-  extern __shared__ __align__(16) double sm[];
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t full[RS];
   const int C = P.C, T = P.T, i0 = P.i0;
   const int me = (int)cluster_rank();
   const int tid = threadIdx.x;
   const int nown = (T + C - 1) / C;
-  double* acc = sm;              // per own row: forward, then backward accumulator
-  double* tv = acc + nown * TB;  // own forward segments t_i
-  double* wv = tv + nown * TB;   // own backward segments w_i
-  double* Lc = wv + nown * TB;   // staged critical tile
-  double* Li = Lc + TB * TS;     // staged inverse of the critical diagonal tile
-  double* seg = Li + TB * TS;    // the segment being applied
-  double* part = seg + TB;       // 4 x 64 partial sums
+  double* ring = sm;                  // RS x 4096: streamed non-critical tiles
+  double* acc = ring + RS * TB * TB;  // per own row: forward, then backward accumulator
+  double* tv = acc + nown * TB;       // own forward segments t_i
+  double* wv = tv + nown * TB;        // own backward segments w_i
+  double* Lc = wv + nown * TB;        // staged critical tile
+  double* Li = Lc + TB * TS;          // staged inverse of the critical diagonal tile
+  double* seg = Li + TB * TS;         // the segment being applied
+  double* part = seg + TB;            // 4 x 64 partial sums
   int* ff = reinterpret_cast<int*>(part + 4 * TB);  // forward segment flags (T)
   int* bf = ff + T;                                 // backward segment flags (T)
 
@@ -161,12 +238,43 @@ __global__ void __launch_bounds__(256, 1) k_trsv_cluster(TrsvParams P) {
     const int p = (me + q * C) * TB + a;
     acc[e] = (p >= P.rstart && p < P.rend) ? P.r[p - P.rstart] : 0.0;
   }
+  const int last = me + (mine - 1) * C;                                  // largest own row
+  const int ffirst = me >= i0 ? me : me + ((i0 - me + C - 1) / C) * C;  // first own row >= i0
+  const bool has_fwd = mine > 0 && ffirst <= last;
+  const SeqCtx sc{me, C, T, i0, last, has_fwd};
+  TileSeq prod{0, i0, sc.first_own_ge(i0 + 2)};
+  bool prod_ok = false;
+  if (tid == 0) {
+    for (int q = 0; q < RS; ++q) mbar_init(&full[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (!skip && mine > 0) {
+      prod_ok = sc.norm(prod);
+      for (int q = 0; q < RS && prod_ok; ++q) {  // the ring runs ahead from the start
+        bulk_tile(ring + q * TB * TB, sc.tile(P.L, prod), &full[q]);
+        sc.advance(prod);
+        prod_ok = sc.norm(prod);
+      }
+    }
+  }
   cluster_barrier();  // every CTA's flags are zero before anyone publishes
   if (!skip && mine > 0) {
-    const int last = me + (mine - 1) * C;                   // largest own row
-    const int ffirst = me >= i0 ? me : me + ((i0 - me + C - 1) / C) * C;  // first own row >= i0
-    // critical-step staging: forward rows ffirst, ffirst + C, ..., last, then
-    // backward rows last, last - C, ..., me
+    uint32_t qc = 0;  // tiles consumed
+    // consume the next ring tile (tile qc of the sequence), then refill its slot
+    auto consume = [&](double* v, bool transposed) {
+      const int slot = qc % RS;
+      mbar_wait(&full[slot], (qc / RS) & 1);
+      const double* M = ring + slot * TB * TB;
+      if (transposed) gemvT_sub_ring(v, M, seg, part, tid);
+      else gemv_sub_ring(v, M, seg, tid);
+      __syncthreads();  // every warp is done with the slot
+      if (tid == 0 && prod_ok) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads -> async write
+        bulk_tile(ring + slot * TB * TB, sc.tile(P.L, prod), &full[slot]);
+        sc.advance(prod);
+        prod_ok = sc.norm(prod);
+      }
+      ++qc;
+    };
     auto stage_fwd = [&](int i) {
       if (i > i0) stage_tile(Lc, P.L + tile_off(i, i - 1), tid);
       stage_tile(Li, P.Linv + (int64_t)i * TB * TB, tid);
@@ -191,7 +299,6 @@ __global__ void __launch_bounds__(256, 1) k_trsv_cluster(TrsvParams P) {
       }
       __syncthreads();
     };
-    const bool has_fwd = ffirst <= last;
     if (has_fwd) stage_fwd(ffirst);
     else stage_bwd(last, false);
 
@@ -218,9 +325,8 @@ __global__ void __launch_bounds__(256, 1) k_trsv_cluster(TrsvParams P) {
         if (i + C <= last) stage_fwd(i + C);
         else stage_bwd(last, true);
       }
-      // the segment's other contributions: own rows i' > k + 1
-      for (int ip = me + ((k + 2 - me + C - 1) / C) * C; ip <= last; ip += C)
-        gemv_sub_global(acc + (ip / C) * TB, P.L + tile_off(ip, k), seg, tid);
+      // the segment's other contributions: own rows i' > k + 1, streamed
+      for (int ip = sc.first_own_ge(k + 2); ip <= last; ip += C) consume(acc + (ip / C) * TB, false);
       __syncthreads();
     }
     // ---------------- backward: w = L^{-T} t ----------------
@@ -250,9 +356,8 @@ __global__ void __launch_bounds__(256, 1) k_trsv_cluster(TrsvParams P) {
         gemvT_smem<true>(acc + (i / C) * TB, Lc, seg, part, tid);
         finish_bwd(i);
       }
-      // other own rows i' < k - 1
-      for (int ip = me; ip < k - 1; ip += C)
-        gemvT_sub_global(acc + (ip / C) * TB, P.L + tile_off(k, ip), seg, part, tid);
+      // other own rows i' < k - 1, streamed
+      for (int ip = me; ip < k - 1; ip += C) consume(acc + (ip / C) * TB, true);
       __syncthreads();
     }
   }
@@ -336,12 +441,22 @@ int trsv_cluster_size(int T) {
 }
 
 cudaError_t launch_trsv(const TrsvParams& P, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
+  static int max_dyn = 0;
+  if (max_dyn == 0) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, k_trsv_cluster);
+    max_dyn = optin - (int)fa.sharedSizeBytes;
     cudaFuncSetAttribute(k_trsv_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(k_trsv_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    configured = true;
+    cudaError_t e = cudaFuncSetAttribute(k_trsv_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn);
+    if (e != cudaSuccess) {
+      max_dyn = 0;
+      return e;
+    }
   }
+  if ((int)trsv_smem_bytes(P.T, P.C) > max_dyn) return cudaErrorInvalidValue;  // T beyond ~330 tiles
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(P.C, 1, 1);
   cfg.blockDim = dim3(256, 1, 1);
