@@ -243,6 +243,7 @@ struct slim_ctx {
   int D = D_DEFAULT;                 // batch size
   int trsv_C = 0;                    // triangular-solve cluster size (0 = by T)
   std::vector<double*> Lbuf, Dinv, Linv;  // 2 D factor buffers (+ 8x8 and 64x64 diagonal inverses)
+  void* factor_slab = nullptr;            // one allocation behind Lbuf / Dinv / Linv / cflags
   std::vector<CUtensorMap> Lmap;     // TMA views of the factor buffers
   std::vector<int*> cflags;
   int* tickets = nullptr;  // [0] chol ticket, [1] trsv ticket
@@ -340,14 +341,11 @@ static void free_all(slim_ctx* c) {
     if (p) cudaFree(p);
   for (int q = 0; q < MAX_REFS; ++q)
     if (c->refs[q]) cudaFree(c->refs[q]);
-  for (double* p : c->Lbuf) cudaFree(p);
-  for (double* p : c->Dinv) cudaFree(p);
-  for (double* p : c->Linv) cudaFree(p);
+  if (c->factor_slab) cudaFree(c->factor_slab);
   for (RowSplit* rs : {&c->rsplit, &c->dsplit}) {
     if (rs->part) cudaFree(rs->part);
     if (rs->cnt) cudaFree(rs->cnt);
   }
-  for (int* p : c->cflags) cudaFree(p);
   for (auto& kv : c->maps) cudaFree(kv.second.dev);
   if (c->sf) cudaStreamDestroy(c->sf);
   if (c->sx) cudaStreamDestroy(c->sx);
@@ -452,7 +450,7 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
 
   const int64_t ell = c->ell, W = c->r + 1;
   c->S = (int)(c->r + 2 * c->D);
-  c->panel_stride = (int64_t)c->S * ell * ell;
+  c->panel_stride = (int64_t)W * ell * ell;  // a panel holds one product block per window position
   const int64_t Nmax = W * ell;
   c->Tmax = (int)((Nmax + TB - 1) / TB);
   const int64_t ntiles = (int64_t)c->Tmax * (c->Tmax + 1) / 2;
@@ -467,14 +465,25 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
   c->Dinv.assign(2 * c->D, nullptr);
   c->Linv.assign(2 * c->D, nullptr);
   c->cflags.assign(2 * c->D, nullptr);
-  for (int q = 0; q < 2 * c->D; ++q) {
-    ALLOC(c, c->Lbuf[q], sizeof(double) * (size_t)ntiles * TB * TB);
-    if (!tma_map_f64_sw128(&c->Lmap[q], c->Lbuf[q], ntiles * TB, TB, 16, TB))
-      FAIL(c, SLIM_ECUDA, "TMA descriptor for the factor buffer could not be encoded");
-    ALLOC(c, c->Dinv[q], sizeof(double) * (size_t)c->Tmax * 512);
-    ALLOC(c, c->Linv[q], sizeof(double) * (size_t)c->Tmax * TB * TB);
-    ALLOC(c, c->cflags[q], sizeof(int) * ntiles);
-    CK(c, cudaMemset(c->cflags[q], 0, sizeof(int) * ntiles));
+  {
+    // one slab for all 2D factor buffers (one allocation, one memset)
+    const size_t lb = sizeof(double) * (size_t)ntiles * TB * TB;
+    const size_t db = sizeof(double) * (size_t)c->Tmax * 512;
+    const size_t ib = sizeof(double) * (size_t)c->Tmax * TB * TB;
+    const size_t fb = ((sizeof(int) * (size_t)ntiles + 255) / 256) * 256;
+    const size_t per = lb + db + ib;
+    ALLOC(c, c->factor_slab, (per + fb) * 2 * c->D);
+    char* base = (char*)c->factor_slab;
+    char* flags = base + per * 2 * c->D;
+    CK(c, cudaMemset(flags, 0, fb * 2 * c->D));
+    for (int q = 0; q < 2 * c->D; ++q) {
+      c->Lbuf[q] = (double*)(base + per * q);
+      c->Dinv[q] = (double*)(base + per * q + lb);
+      c->Linv[q] = (double*)(base + per * q + lb + db);
+      c->cflags[q] = (int*)(flags + fb * q);
+      if (!tma_map_f64_sw128(&c->Lmap[q], c->Lbuf[q], ntiles * TB, TB, 16, TB))
+        FAIL(c, SLIM_ECUDA, "TMA descriptor for the factor buffer could not be encoded");
+    }
   }
   tick("factors");
   ALLOC(c, c->tickets, sizeof(int) * 2);
@@ -1069,7 +1078,7 @@ static int enqueue_gram(slim_ctx* c, const Window& W, int64_t k, int64_t real_bl
                                kcs, c->sg));
       launch_gram_reduce(panel, W, c->gpart, kcs, c->sg);
       // the self-product diagonal (row sums of squares) exactly in fp64
-      launch_gram_diag_fp64(panel + (int64_t)slot_new * c->ell * c->ell, c->ell, c->gring + off,
+      launch_gram_diag_fp64(panel + (int64_t)W.newp * c->ell * c->ell, c->ell, c->gring + off,
                             (int)c->ell, (int)c->n, c->dsplit, c->sg);
       c->launches += 2;
     } else {

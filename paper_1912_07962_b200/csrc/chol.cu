@@ -282,7 +282,8 @@ __device__ __forceinline__ void init_acc(const CholParams& P, const MatRT& M, in
 // G = alpha * (Gram ring) + I, identity padding, written tile-major into the
 // factor buffers (one CTA per 64x64 tile of every system of the batch).
 // Entry (p, q) is the product of two window blocks; the ring keeps it in the
-// panel of the newer of the two, with the newer block's rows contiguous.
+// panel of the newer of the two (ring slot), at the older one's window
+// position (fixed for a block's lifetime), newer block's rows contiguous.
 // Pass 1 reads the entries whose row block is the newer one with threads
 // along p, pass 2 the others with threads along q (both coalesced); the
 // tile is transposed through shared memory into row-major order.
@@ -332,7 +333,7 @@ __global__ void __launch_bounds__(256) k_assemble(CholParams P) {
         const int qb = q / ell, c = q - qb * ell;
         if (Mp.age[qb] < Mp.age[pb]) continue;  // column block newer: pass 2
         const double* pan = P.panels + (int64_t)Mp.slot[pb] * P.panel_stride;
-        v = alpha * pan[((int64_t)Mp.slot[qb] * ell + c) * ell + a] + (p == q ? 1.0 : 0.0);
+        v = alpha * pan[((int64_t)qb * ell + c) * ell + a] + (p == q ? 1.0 : 0.0);
       } else {
         v = P.G[(int64_t)p * P.ldg + q];
       }
@@ -350,7 +351,7 @@ __global__ void __launch_bounds__(256) k_assemble(CholParams P) {
         if (p >= N || q > p) continue;
         const int pb = p / ell, a = p - pb * ell;
         if (!(Mp.age[qb] < Mp.age[pb])) continue;
-        sh[ps][ll] = alpha * pan[((int64_t)Mp.slot[pb] * ell + a) * ell + c];
+        sh[ps][ll] = alpha * pan[((int64_t)pb * ell + a) * ell + c];
       }
     }
   }

@@ -48,7 +48,7 @@ struct CholParams {
   int* error;           // set to 1 on a non-positive pivot
   // ring mode: initial tiles gathered from the incremental Gram panels
   const double* panels;
-  int64_t panel_stride;  // S * ell * ell
+  int64_t panel_stride;  // (r + 1) * ell * ell: one product block per window position
   int ell, S;
   int W;                 // window positions (r + 1)
   // tiles a system shares with the previous batch's last system (step

@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(128) k_gram_csr(double* __restrict__ panel, Wi
     }
   }
   __syncwarp();
-  double* out = panel + ((int64_t)W.slot[P] * ell + a) * ell;
+  double* out = panel + ((int64_t)P * ell + a) * ell;  // panels are indexed by window position
   for (int j = lane; j < ell; j += 32) out[j] = acc[j];
 }
 
@@ -302,7 +302,7 @@ __global__ void k_gram_reduce(double* __restrict__ panel, Window W, const double
   double s = 0.0;
   for (int z = 0; z < nsplit; ++z) s += part[(int64_t)z * N * ell + idx];
   const int P = p / ell, a = p - P * ell;
-  panel[((int64_t)W.slot[P] * ell + a) * ell + j] = s;
+  panel[((int64_t)P * ell + a) * ell + j] = s;
 }
 
 // ---------------------------------------------------------------------------
