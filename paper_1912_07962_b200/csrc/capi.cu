@@ -454,6 +454,17 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
   const int64_t Nmax = W * ell;
   c->Tmax = (int)((Nmax + TB - 1) / TB);
   const int64_t ntiles = (int64_t)c->Tmax * (c->Tmax + 1) / 2;
+  {
+    // the triangular-solve cluster keeps per-row vectors in shared memory
+    int optin = 0;
+    CK(c, cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->dev));
+    const int C = trsv_cluster_size(c->Tmax);
+    if (trsv_smem_bytes(c->Tmax, C) + 2048 > (size_t)optin)
+      FAIL(c, SLIM_EINVAL,
+           "dual system of (r+1) ell = %lld rows exceeds this build's limit (about 36000 rows: "
+           "the triangular-solve cluster holds its row vectors in shared memory)",
+           (long long)Nmax);
+  }
   ALLOC(c, c->x, sizeof(double) * c->n);
   CK(c, cudaMemset(c->x, 0, sizeof(double) * c->n));
   ALLOC(c, c->b, sizeof(double) * c->m);

@@ -456,7 +456,7 @@ cudaError_t launch_trsv(const TrsvParams& P, cudaStream_t s) {
       return e;
     }
   }
-  if ((int)trsv_smem_bytes(P.T, P.C) > max_dyn) return cudaErrorInvalidValue;  // T beyond ~330 tiles
+  if ((int)trsv_smem_bytes(P.T, P.C) > max_dyn) return cudaErrorInvalidValue;  // T beyond ~576 tiles
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(P.C, 1, 1);
   cfg.blockDim = dim3(256, 1, 1);
