@@ -1309,9 +1309,35 @@ static int enqueue_chol_batch(slim_ctx* c, const Window* Ws, int nb, int set, co
   CKLAUNCH(c);
   if (P.ntasks > 0) {
     CK(c, cudaMemsetAsync(P.ticket, 0, sizeof(int), c->sf));
+    // SLIM_CHOL_TRACE=<file>: timeline of launch SLIM_CHOL_TRACE_LAUNCH (default 3)
+    // of this context -- ticket, system, i, j, 4 globaltimer stamps (debug)
+    static int trace_count = 0;
+    const char* tpath = getenv("SLIM_CHOL_TRACE");
+    const int twant = getenv("SLIM_CHOL_TRACE_LAUNCH") ? atoi(getenv("SLIM_CHOL_TRACE_LAUNCH")) : 3;
+    unsigned long long* dtr = nullptr;
+    if (tpath && ++trace_count == twant) {
+      CK(c, cudaMalloc(&dtr, sizeof(unsigned long long) * 4 * (size_t)P.ntasks));
+      CK(c, cudaMemsetAsync(dtr, 0, sizeof(unsigned long long) * 4 * (size_t)P.ntasks, c->sf));
+      P.trace = dtr;
+    }
     launch_chol(P, c->sf);
     c->launches += 1;
     CKLAUNCH(c);
+    if (dtr) {
+      CK(c, cudaStreamSynchronize(c->sf));
+      std::vector<unsigned long long> h(4 * (size_t)P.ntasks);
+      std::vector<int2> hm(P.ntasks);
+      CK(c, cudaMemcpy(h.data(), dtr, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost));
+      CK(c, cudaMemcpy(hm.data(), P.map, sizeof(int2) * hm.size(), cudaMemcpyDeviceToHost));
+      cudaFree(dtr);
+      if (FILE* f = fopen(tpath, "w")) {
+        fprintf(f, "ticket,sys,i,j,t0,t1,t2,t3,T\n");
+        for (int t = 0; t < P.ntasks; ++t)
+          fprintf(f, "%d,%d,%d,%d,%llu,%llu,%llu,%llu,%d\n", t, hm[t].x, hm[t].y >> 16, hm[t].y & 0xffff,
+                  h[4 * t], h[4 * t + 1], h[4 * t + 2], h[4 * t + 3], P.m[hm[t].x].T);
+        fclose(f);
+      }
+    }
   }
   launch_diag_inv(P, c->sf);  // the x-chain's diagonal solves are 64x64 products
   c->launches += 1;

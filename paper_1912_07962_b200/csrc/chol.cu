@@ -551,7 +551,10 @@ __device__ void forward_tile(const CholParams& P, int b, int i, int j, const dou
 // dependencies carry smaller tickets, so spinning on them cannot deadlock.
 __global__ void __launch_bounds__(256, 2) k_chol_tiles(const __grid_constant__ CholParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);  // SW128 tiles
+  // 1024-byte alignment for the SW128 TMA boxes by pointer arithmetic on the
+  // shared array (a round trip through an integer would make every fragment
+  // load a generic LD instead of LDS)
+  uint8_t* base = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   uint8_t* stage = base + SMB_ST;
   double* Sg = reinterpret_cast<double*>(base + SMB_SG);
   double* Dv = reinterpret_cast<double*>(base + SMB_DV);
