@@ -179,14 +179,18 @@ __global__ void __launch_bounds__(128) k_gram_csr(double* __restrict__ panel, Wi
   extern __shared__ __align__(16) double gacc[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ell = W.ell;
-  const int grow_w = blockIdx.x * 4 + warp;
-  if (grow_w >= W.nw * ell) return;
+  // one window row per CTA; its nonzeros are split in 4 contiguous quarters
+  // (one per warp: 4x shorter chains of dependent CSC lookups), the four
+  // partial rows are added in warp order (deterministic)
+  const int grow_w = blockIdx.x;
   const int P = grow_w / ell, a = grow_w - P * ell;
   double* acc = gacc + (size_t)warp * ell;
   for (int j = lane; j < ell; j += 32) acc[j] = 0.0;
   __syncwarp();
   const int64_t grow = (int64_t)W.blk[P] * ell + a;
-  const int64_t lo = rowptr[grow], hi = rowptr[grow + 1];
+  const int64_t rlo = rowptr[grow], rhi = rowptr[grow + 1];
+  const int64_t q4 = (rhi - rlo + 3) / 4;
+  const int64_t lo = rlo + warp * q4, hi = min(rhi, lo + q4);
   const unsigned full = 0xffffffffu;
   const unsigned lt = (1u << lane) - 1u;
   for (int64_t base = lo; base < hi; base += 32) {
@@ -229,9 +233,10 @@ __global__ void __launch_bounds__(128) k_gram_csr(double* __restrict__ panel, Wi
       __syncwarp();
     }
   }
-  __syncwarp();
+  __syncthreads();
   double* out = panel + ((int64_t)P * ell + a) * ell;  // panels are indexed by window position
-  for (int j = lane; j < ell; j += 32) out[j] = acc[j];
+  for (int j = threadIdx.x; j < ell; j += 128)
+    out[j] = (gacc[j] + gacc[ell + j]) + (gacc[2 * ell + j] + gacc[3 * ell + j]);
 }
 
 // Dense: DMMA tile GEMM, 64 window rows x 64 new rows per CTA, split-K over
@@ -634,7 +639,7 @@ void launch_gram_csr(double* panel, const Window& W, const int64_t* rowptr, cons
       configured = true;
     }
   }
-  k_gram_csr<T><<<cdiv((int64_t)W.nw * W.ell, 4), 128, smem, s>>>(
+  k_gram_csr<T><<<(unsigned)((int64_t)W.nw * W.ell), 128, smem, s>>>(
       panel, W, rowptr, col, val, colptr_new, cscrow, cscval, base_new);
 }
 template <typename T>
