@@ -1137,6 +1137,10 @@ static int enqueue_x_chain(slim_ctx* c, const Window& W, int64_t k, int d, doubl
   T.w = c->wvec;
   T.ctl = c->ctl;
   T.C = c->trsv_C > 0 ? std::min(c->trsv_C, T.T) : trsv_cluster_size(T.T);
+  {
+    static const int rs = getenv("SLIM_TRSV_RING") ? std::max(1, std::min(3, atoi(getenv("SLIM_TRSV_RING")))) : 3;
+    T.rs = rs;
+  }
   CK(c, launch_trsv(T, s));
   CKLAUNCH(c);
   c->launches += 3;  // trsv, M^T w, finish
@@ -1243,12 +1247,12 @@ static const slim_ctx::TaskMap* task_map(slim_ctx* c, const std::vector<SysShape
   const double t3 = (double)TB * TB * TB;
   double flops = 0.0;
   for (const int2& e : h) {
-    const int i = e.y >> 16, j = e.y & 0xffff;
+    const int i = e.y >> 16, j = e.y & 0x7fff;
     if (i == j) {
       flops += t3 * j + t3 / 3.0;
       if (j + 1 < sh[e.x].T) flops += 2.0 * t3 * j + t3;
     } else {
-      flops += 2.0 * t3 * j + t3;
+      flops += ((e.y & 0x8000) ? 2.0 : 1.0) * (2.0 * t3 * j + t3);  // dual: rows i, i + 1
     }
   }
   slim_ctx::TaskMap tm{nullptr, (int)h.size(), flops};
@@ -1660,6 +1664,7 @@ extern "C" int slim_dual_step(int32_t device, const double* Mh, int64_t rows, in
   T.w = c->wvec;
   T.ctl = nullptr;
   T.C = trsv_cluster_size(T.T);
+  T.rs = 3;
   if (launch_trsv(T, c->sx) != cudaSuccess) return fail_out(SLIM_ECUDA);
   launch_mtw_dense<double>(c->spart, 1, W, (const double*)c->A, n, (int)n, c->wvec, c->ctl, c->sx);
   if (cudaStreamSynchronize(c->sx) != cudaSuccess || cudaGetLastError() != cudaSuccess)

@@ -247,20 +247,23 @@ __device__ void trsm_tile_warp(double* As, const double* Bs, const double* Dv, i
 // tile Cholesky kernel
 // ---------------------------------------------------------------------------
 // K chunks of 16 fp64 (one 128-byte swizzle row per tile row) stream through a
-// 4-stage TMA ring: a stage holds the 64x16 slices of both operand tiles.
+// 3-stage TMA ring: a stage holds the 64x16 slices of up to three operand
+// tiles (A, B, and the second A of a dual task).
 constexpr int KC = 16;
-constexpr int NSTAGE = 4;
+constexpr int NSTAGE = 3;
 constexpr int BOX_BYTES = TB * KC * 8;         // 8 KB
-constexpr int STAGE_BYTES = 2 * BOX_BYTES;     // 16 KB
+constexpr int STAGE_BYTES = 3 * BOX_BYTES;     // 24 KB
 
 // dynamic shared layout (bytes, from a 1024-aligned base):
 //   stage ring [NSTAGE][STAGE_BYTES] | Sg[TB*TS] | Dv[512] | rdiag[64]
-// the 64 x TS work tile X overlays the stage ring once the operands are consumed
+// the 64 x TS work tiles X (two for a dual task) overlay the stage ring once
+// the operands are consumed; two CTAs fit an SM (2 x 112 KB)
 constexpr int SMB_ST = 0;
 constexpr int SMB_SG = NSTAGE * STAGE_BYTES;
 constexpr int SMB_DV = SMB_SG + TB * TS * 8;
 constexpr int SMB_RD = SMB_DV + 512 * 8;
 constexpr int SMB_TOTAL = SMB_RD + 64 * 8 + 1024;  // + alignment slack
+static_assert(2 * TB * TS * 8 <= SMB_SG, "two work tiles must fit over the stage ring");
 
 // the tile (i, j) of G was assembled in place by k_assemble (tile-major)
 __device__ __forceinline__ void init_acc(const CholParams& P, const MatRT& M, int i, int j,
@@ -402,15 +405,19 @@ __device__ __forceinline__ void fence_proxy_async() {
 }
 
 
-// C_(ra, j) -= sum_{k in [kb, ke)} L_(ra,k) L_(j,k)^T   into accA, and when
-// PAIR also C_(j,j) -= L_(j,k) L_(j,k)^T into accB.  Thread 0 issues one 2D
-// TMA box per operand per K chunk (64 rows x 16 fp64, SWIZZLE_128B) three
-// chunks ahead; every warp releases a stage with one mbarrier arrival, so
-// there is no CTA-wide barrier in the loop.  Dependency flags are probed
-// once in parallel; only k-steps past the ready prefix make thread 0 wait.
-template <bool PAIR>
+// C_(ra, j) -= sum_{k in [kb, ke)} L_(ra,k) L_(j,k)^T into accA, and
+//   MODE 1 (pair): also C_(j,j)    -= L_(j,k)    L_(j,k)^T into accB,
+//   MODE 2 (dual): also C_(ra+1,j) -= L_(ra+1,k) L_(j,k)^T into accB
+// (the B operand L_(j,k) shared: 16 independent DMMAs per 8 fragment loads).
+// Thread 0 issues one 2D TMA box per operand per K chunk (64 rows x 16 fp64,
+// SWIZZLE_128B) two chunks ahead; every warp releases a stage with one
+// mbarrier arrival, so there is no CTA-wide barrier in the loop.  Dependency
+// flags are probed once; only k-steps past the ready prefix make thread 0 wait.
+template <int MODE>
 __device__ void accumulate(const MatRT& P, int ra, int j, int kb, int ke, uint8_t* stage,
                            Pipe& pipe, double (&accA)[8][2], double (&accB)[8][2], int tid) {
+  constexpr bool TWO = MODE != 0;
+  constexpr int NBOX = MODE == 2 ? 3 : 2;
   const int warp = tid >> 5, lane = tid & 31;
   const int nchunk = (TB / KC) * (ke - kb);
   if (nchunk <= 0) return;
@@ -421,11 +428,13 @@ __device__ void accumulate(const MatRT& P, int ra, int j, int kb, int ke, uint8_
   if (tid == 0) {
     const int* fa = P.flags + ra * (ra + 1) / 2;
     const int* fb = P.flags + j * (j + 1) / 2;
+    const int* fc = P.flags + (ra + 1) * (ra + 2) / 2;
     for (int k = kb; k < ke; ++k) {
-      int va, vb;
+      int va, vb, vc = P.epoch;
       asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(va) : "l"(fa + k) : "memory");
       asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(vb) : "l"(fb + k) : "memory");
-      if (va < P.epoch || vb < P.epoch) {
+      if (MODE == 2) asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(vc) : "l"(fc + k) : "memory");
+      if (va < P.epoch || vb < P.epoch || vc < P.epoch) {
         kready = k;
         break;
       }
@@ -441,12 +450,15 @@ __device__ void accumulate(const MatRT& P, int ra, int j, int kb, int ke, uint8_
     if (c == 0 && k >= kready) {
       wait_flag(P.flags + (ra * (ra + 1) / 2 + k), P.epoch);
       wait_flag(P.flags + (j * (j + 1) / 2 + k), P.epoch);
+      if (MODE == 2) wait_flag(P.flags + ((ra + 1) * (ra + 2) / 2 + k), P.epoch);
       fence_proxy_async();
     }
     uint8_t* dst = stage + st * STAGE_BYTES;
-    bar_expect(&pipe.full[st], STAGE_BYTES);
+    bar_expect(&pipe.full[st], NBOX * BOX_BYTES);
     tma2d(dst, P.map, &pipe.full[st], KC * c, (ra * (ra + 1) / 2 + k) * TB);
     tma2d(dst + BOX_BYTES, P.map, &pipe.full[st], KC * c, (j * (j + 1) / 2 + k) * TB);
+    if (MODE == 2)
+      tma2d(dst + 2 * BOX_BYTES, P.map, &pipe.full[st], KC * c, ((ra + 1) * (ra + 2) / 2 + k) * TB);
   };
   if (tid == 0)
     for (int u = 0; u < NSTAGE - 1 && u < nchunk; ++u) issue(u);
@@ -468,13 +480,14 @@ __device__ void accumulate(const MatRT& P, int ra, int j, int kb, int ke, uint8_
     __syncwarp();
     const uint8_t* sa = stage + st * STAGE_BYTES;
     const uint8_t* sb = sa + BOX_BYTES;
+    const uint8_t* sd = MODE == 2 ? sa + 2 * BOX_BYTES : sb;  // second A operand
 #pragma unroll
     for (int k4 = 0; k4 < KC / 4; ++k4) {
       double a[2], ad[2], b[4];
 #pragma unroll
       for (int rb = 0; rb < 2; ++rb) {
         a[rb] = -*reinterpret_cast<const double*>(sa + arow + rb * 8 * 128 + colofs[k4]);
-        if (PAIR) ad[rb] = -*reinterpret_cast<const double*>(sb + arow + rb * 8 * 128 + colofs[k4]);
+        if (TWO) ad[rb] = -*reinterpret_cast<const double*>(sd + arow + rb * 8 * 128 + colofs[k4]);
       }
 #pragma unroll
       for (int cb = 0; cb < 4; ++cb)
@@ -482,7 +495,7 @@ __device__ void accumulate(const MatRT& P, int ra, int j, int kb, int ke, uint8_
 #pragma unroll
       for (int f = 0; f < 8; ++f) {
         dmma8x8x4(accA[f], a[f >> 2], b[f & 3]);
-        if (PAIR) dmma8x8x4(accB[f], ad[f >> 2], b[f & 3]);
+        if (TWO) dmma8x8x4(accB[f], ad[f >> 2], b[f & 3]);
       }
     }
     // the next TMA into this stage is an async-proxy write: the warp's
@@ -550,7 +563,7 @@ __device__ void forward_tile(const CholParams& P, int b, int i, int j, const dou
 // tiles arrive through forward_tile or k_assemble.  Every task's
 // dependencies carry smaller tickets, so spinning on them cannot deadlock.
 __global__ void __launch_bounds__(256, 2) k_chol_tiles(const __grid_constant__ CholParams P) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  extern __shared__ __align__(16) uint8_t smem_raw[];  // 1024-aligned by hand below
   // 1024-byte alignment for the SW128 TMA boxes by pointer arithmetic on the
   // shared array (a round trip through an integer would make every fragment
   // load a generic LD instead of LDS)
@@ -587,7 +600,8 @@ __global__ void __launch_bounds__(256, 2) k_chol_tiles(const __grid_constant__ C
   if (tid == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(M.map) : "memory");
   __syncthreads();
   Pipe pipe{s_full, s_empty, 0u};
-  const int i = e.y >> 16, j = e.y & 0xffff;
+  const int i = e.y >> 16, j = e.y & 0x7fff;
+  const bool dual = (e.y & 0x8000) != 0;  // off-diagonal rows i and i + 1 of column j
   const int T = M.T;
   unsigned long long* tr = (P.trace != nullptr && tid == 0) ? P.trace + 4 * (int64_t)s_task : nullptr;
   if (tr) tr[0] = globaltimer_ns();
@@ -599,10 +613,10 @@ __global__ void __launch_bounds__(256, 2) k_chol_tiles(const __grid_constant__ C
     init_acc(P, M, j, j, warp, lane, accB);
     if (has_sub) {
       init_acc(P, M, j + 1, j, warp, lane, accA);
-      accumulate<true>(M, j + 1, j, 0, j - 1 > 0 ? j - 1 : 0, stage, pipe, accA, accB, tid);
+      accumulate<1>(M, j + 1, j, 0, j - 1 > 0 ? j - 1 : 0, stage, pipe, accA, accB, tid);
     }
     // last update of the diagonal alone, then factor it right away
-    if (j >= 1) accumulate<false>(M, j, j, has_sub ? j - 1 : 0, j, stage, pipe, accB, accB, tid);
+    if (j >= 1) accumulate<0>(M, j, j, has_sub ? j - 1 : 0, j, stage, pipe, accB, accB, tid);
     if (tr) tr[1] = globaltimer_ns();
     acc_to_smem(Sg, accB, warp, lane);
     __syncthreads();
@@ -615,7 +629,7 @@ __global__ void __launch_bounds__(256, 2) k_chol_tiles(const __grid_constant__ C
     }
     publish(M, j, j, tid);
     if (has_sub) {
-      if (j >= 1) accumulate<false>(M, j + 1, j, j - 1, j, stage, pipe, accA, accA, tid);
+      if (j >= 1) accumulate<0>(M, j + 1, j, j - 1, j, stage, pipe, accA, accA, tid);
       __syncthreads();  // every warp is done reading the stages X overlays
       acc_to_smem(X, accA, warp, lane);
       __syncthreads();
@@ -626,10 +640,36 @@ __global__ void __launch_bounds__(256, 2) k_chol_tiles(const __grid_constant__ C
       forward_tile(P, e.x, j + 1, j, X, nullptr, tid);
     }
     forward_tile(P, e.x, j, j, Sg, Dv, tid);
+  } else if (dual) {
+    // ---------------- off-diagonal tiles (i, j) and (i + 1, j) ----------
+    double* X2 = X + TB * TS;  // second work tile, also over the drained stages
+    init_acc(P, M, i, j, warp, lane, accA);
+    init_acc(P, M, i + 1, j, warp, lane, accB);
+    accumulate<2>(M, i, j, 0, j, stage, pipe, accA, accB, tid);
+    if (tr) tr[1] = globaltimer_ns();
+    if (tid == 0) wait_flag(M.flags + (j * (j + 1) / 2 + j), M.epoch);
+    if (tr) tr[2] = globaltimer_ns();
+    __syncthreads();
+    load_tile_async(Sg, M.L + tile_off(j, j), tid);
+    load_dinv_async(Dv, M.Dinv + (int64_t)j * 512, tid);
+    cp_async_commit();
+    acc_to_smem(X, accA, warp, lane);
+    acc_to_smem(X2, accB, warp, lane);
+    cp_async_wait_all();
+    __syncthreads();
+    trsm_tile_warp(X, Sg, Dv, warp, lane);
+    trsm_tile_warp(X2, Sg, Dv, warp, lane);
+    __syncthreads();
+    store_tile(M.L + tile_off(i, j), X, tid);
+    store_tile(M.L + tile_off(i + 1, j), X2, tid);
+    publish(M, i, j, tid);
+    if (tid == 0) st_release(M.flags + ((i + 1) * (i + 2) / 2 + j), M.epoch);  // fenced by publish
+    forward_tile(P, e.x, i, j, X, nullptr, tid);
+    forward_tile(P, e.x, i + 1, j, X2, nullptr, tid);
   } else {
     // ---------------- off-diagonal tile (i, j), i > j -----------------
     init_acc(P, M, i, j, warp, lane, accA);
-    accumulate<false>(M, i, j, 0, j, stage, pipe, accA, accA, tid);
+    accumulate<0>(M, i, j, 0, j, stage, pipe, accA, accA, tid);
     if (tr) tr[1] = globaltimer_ns();
     if (tid == 0) wait_flag(M.flags + (j * (j + 1) / 2 + j), M.epoch);
     if (tr) tr[2] = globaltimer_ns();
@@ -656,7 +696,9 @@ size_t chol_smem_bytes() { return (size_t)SMB_TOTAL; }
 // stand-alone (j + 1, j) (column j not fresh but that row is), the first
 // off-diagonal tile (j + 2, j), the pair of column j + 1 (one column ahead
 // of the bulk, so the critical diagonal chain is never queued behind it) and
-// the rest of column j.  Encoded as (i << 16) | j with i == j for pair tasks.
+// the rest of column j, consecutive fresh rows paired into dual tasks.
+// Encoded as (i << 16) | j with i == j for pair tasks; bit 15 of the low half
+// marks a dual task (rows i and i + 1).
 // The batch is merged group-major, system-minor: a tile a system shares
 // with an earlier system of the batch is produced by that system's task in
 // the same or an earlier group, so every dependency holds a smaller ticket
@@ -681,8 +723,16 @@ std::vector<int2> chol_task_map(const SysShape* sh, int nb, int W, int ell) {
       if (!col_fresh && j + 1 < T && fresh(b, j + 1, j)) out.push_back(make_int2(b, ((j + 1) << 16) | j));
       if (j + 2 < T && fresh(b, j + 2, j)) out.push_back(make_int2(b, ((j + 2) << 16) | j));
       if (j + 1 < T && fresh(b, j + 1, j + 1)) out.push_back(make_int2(b, ((j + 1) << 16) | (j + 1)));
-      for (int i = j + 3; i < T; ++i)
-        if (fresh(b, i, j)) out.push_back(make_int2(b, (i << 16) | j));
+      // the rest of column j, fresh rows in consecutive pairs (dual tasks)
+      for (int i = j + 3; i < T; ++i) {
+        if (!fresh(b, i, j)) continue;
+        if (i + 1 < T && fresh(b, i + 1, j)) {
+          out.push_back(make_int2(b, (i << 16) | 0x8000 | j));
+          ++i;
+        } else {
+          out.push_back(make_int2(b, (i << 16) | j));
+        }
+      }
     }
   }
   return out;

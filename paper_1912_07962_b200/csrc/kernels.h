@@ -73,6 +73,7 @@ struct TrsvParams {
   double* w;           // T * 64 result w = G^{-1} y (window order)
   const Ctl* ctl;      // nullable; skip when diverged
   int C;               // cluster size = grid (tile row i belongs to CTA i mod C)
+  int rs;              // bulk-copy ring slots (1..3)
 };
 
 // window description shared by the x-chain / Gram kernels
@@ -119,7 +120,7 @@ void launch_diag_inv(const CholParams& P, cudaStream_t s);
 // one cluster of P.C CTAs (trsv_cluster_size(T))
 cudaError_t launch_trsv(const TrsvParams& P, cudaStream_t s);
 int trsv_cluster_size(int T);
-size_t trsv_smem_bytes(int T, int C);
+size_t trsv_smem_bytes(int T, int C, int rs = 3);
 
 __global__ void k_chol_tiles(const __grid_constant__ CholParams P);
 

@@ -98,7 +98,7 @@ __device__ __forceinline__ void gemvT_smem(double* out, const double* M, const d
   __syncthreads();
 }
 // ---- bulk-copy ring of the non-critical tiles ----
-constexpr int RS = 3;  // 32 KB slots
+constexpr int RS_MAX = 3;  // 32 KB slots (P.rs in use)
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(n));
 }
@@ -206,15 +206,16 @@ __device__ __forceinline__ void gemvT_sub_ring(double* v, const double* M, const
   __syncthreads();
 }
 
-size_t trsv_smem_bytes(int T, int C) {
+size_t trsv_smem_bytes(int T, int C, int rs) {
   const int nown = (T + C - 1) / C;
-  return sizeof(double) * (size_t)(RS * TB * TB + 3 * nown * TB + 2 * TB * TS + TB + 4 * TB) +
+  return sizeof(double) * (size_t)(rs * TB * TB + 3 * nown * TB + 2 * TB * TS + TB + 4 * TB) +
          sizeof(int) * 2 * (size_t)T;
 }
 
 __global__ void __launch_bounds__(256, 1) k_trsv_cluster(TrsvParams P) {
   extern __shared__ __align__(128) double sm[];
-  __shared__ __align__(8) uint64_t full[RS];
+  __shared__ __align__(8) uint64_t full[RS_MAX];
+  const int RS = P.rs;
   const int C = P.C, T = P.T, i0 = P.i0;
   const int me = (int)cluster_rank();
   const int tid = threadIdx.x;
@@ -456,11 +457,11 @@ cudaError_t launch_trsv(const TrsvParams& P, cudaStream_t s) {
       return e;
     }
   }
-  if ((int)trsv_smem_bytes(P.T, P.C) > max_dyn) return cudaErrorInvalidValue;  // T beyond ~576 tiles
+  if ((int)trsv_smem_bytes(P.T, P.C, P.rs) > max_dyn) return cudaErrorInvalidValue;  // T beyond ~576 tiles
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(P.C, 1, 1);
   cfg.blockDim = dim3(256, 1, 1);
-  cfg.dynamicSmemBytes = trsv_smem_bytes(P.T, P.C);
+  cfg.dynamicSmemBytes = trsv_smem_bytes(P.T, P.C, P.rs);
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;

@@ -34,12 +34,13 @@ static int check(int r, int ell, int D, int nsteps, bool alpha_change_mid) {
     std::vector<std::map<long long, int>> prod(nb);
     auto key = [](int i, int j) { return ((long long)i << 20) | j; };
     for (int t = 0; t < (int)map.size(); ++t) {
-      const int b = map[t].x, i = map[t].y >> 16, j = map[t].y & 0xffff;
+      const int b = map[t].x, i = map[t].y >> 16, j = map[t].y & 0x7fff;
       if (i == j) {
         prod[b][key(j, j)] = t;
         if (j + 1 < sh[b].T) prod[b][key(j + 1, j)] = t;
       } else {
         prod[b][key(i, j)] = t;
+        if (map[t].y & 0x8000) prod[b][key(i + 1, j)] = t;  // dual task: rows i, i + 1
       }
     }
     auto fresh = [&](int b, int i, int j) { return tile_fresh(sh[b].full, sh[b].pnew, W, ell, i, j); };
@@ -65,7 +66,8 @@ static int check(int r, int ell, int D, int nsteps, bool alpha_change_mid) {
           }
         }
     for (int t = 0; t < (int)map.size(); ++t) {
-      const int b = map[t].x, i = map[t].y >> 16, j = map[t].y & 0xffff;
+      const int b = map[t].x, i = map[t].y >> 16, j = map[t].y & 0x7fff;
+      const bool dual = (map[t].y & 0x8000) != 0;
       std::vector<std::pair<int, int>> deps;
       if (i == j) {
         for (int k = 0; k < j; ++k) {
@@ -73,8 +75,14 @@ static int check(int r, int ell, int D, int nsteps, bool alpha_change_mid) {
           if (j + 1 < sh[b].T) deps.push_back({j + 1, k});
         }
       } else {
-        for (int k = 0; k < j; ++k) deps.push_back({i, k}), deps.push_back({j, k});
+        for (int k = 0; k < j; ++k) {
+          deps.push_back({i, k}), deps.push_back({j, k});
+          if (dual) deps.push_back({i + 1, k});
+        }
         deps.push_back({j, j});
+        if (dual && i + 1 >= sh[b].T) {
+          if (bad++ < 5) printf("dual task past the last row: b=%d (%d,%d)\n", b, i, j);
+        }
       }
       for (auto& d : deps) {
         const int p = producer(b, d.first, d.second);
