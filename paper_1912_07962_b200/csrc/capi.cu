@@ -44,6 +44,7 @@ constexpr int D_DEFAULT = 8;  // systems per batched factorization
 
 struct ProfPair {
   cudaEvent_t a, b;
+  int steps = 1;  // steps covered by the pair (a fused x-chain covers a batch)
 };
 
 }  // namespace
@@ -1528,7 +1529,7 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
     float ms = 0.f;
     for (auto& pp : pgr) cudaEventElapsedTime(&ms, pp.a, pp.b), c->t_ms[0] += ms, c->t_n[0]++;
     for (auto& pp : pch) cudaEventElapsedTime(&ms, pp.a, pp.b), c->t_ms[1] += ms, c->t_n[1]++;
-    for (auto& pp : pxc) cudaEventElapsedTime(&ms, pp.a, pp.b), c->t_ms[2] += ms, c->t_n[2]++;
+    for (auto& pp : pxc) cudaEventElapsedTime(&ms, pp.a, pp.b), c->t_ms[2] += ms, c->t_n[2] += pp.steps;
     for (auto& pp : pgr) c->prof_gram.push_back(pp);
     for (auto& pp : pch) c->prof_chol.push_back(pp);
     for (auto& pp : pxc) c->prof_x.push_back(pp);

@@ -212,26 +212,47 @@ size_t trsv_smem_bytes(int T, int C, int rs) {
          sizeof(int) * 2 * (size_t)T;
 }
 
-__global__ void __launch_bounds__(256, 1) k_trsv_cluster(TrsvParams P) {
-  extern __shared__ __align__(128) double sm[];
-  __shared__ __align__(8) uint64_t full[RS_MAX];
+// shared-memory carve-up of one solve (dynamic part)
+struct TrsvSmem {
+  double *ring, *acc, *tv, *wv, *Lc, *Li, *seg, *part;
+  int *ff, *bf;
+};
+__device__ __forceinline__ TrsvSmem trsv_carve(double* sm, int RS, int T, int C) {
+  const int nown = (T + C - 1) / C;
+  TrsvSmem S;
+  S.ring = sm;                       // RS x 4096: streamed non-critical tiles
+  S.acc = S.ring + RS * TB * TB;     // per own row: forward, then backward accumulator
+  S.tv = S.acc + nown * TB;          // own forward segments t_i
+  S.wv = S.tv + nown * TB;           // own backward segments w_i
+  S.Lc = S.wv + nown * TB;           // staged critical tile
+  S.Li = S.Lc + TB * TS;             // staged inverse of the critical diagonal tile
+  S.seg = S.Li + TB * TS;            // the segment being applied
+  S.part = S.seg + TB;               // 4 x 64 partial sums
+  S.ff = reinterpret_cast<int*>(S.part + 4 * TB);  // forward segment flags (T)
+  S.bf = S.ff + T;                                 // backward segment flags (T)
+  return S;
+}
+
+// One solve w = L^{-T} L^{-1} y by the whole cluster (every CTA calls it).
+// `full` are the ring's mbarriers and qbase the ring tiles consumed by
+// earlier solves of the same launch (the barrier phases continue).  Starts
+// with a cluster barrier (flags zeroed everywhere), ends with the CTA's own
+// copies drained; the caller separates consecutive solves by a cluster barrier.
+__device__ void trsv_body(const TrsvParams& P, const TrsvSmem& S, uint64_t* full, uint32_t& qbase,
+                          int me, int tid) {
   const int RS = P.rs;
   const int C = P.C, T = P.T, i0 = P.i0;
-  const int me = (int)cluster_rank();
-  const int tid = threadIdx.x;
-  const int nown = (T + C - 1) / C;
-  double* ring = sm;                  // RS x 4096: streamed non-critical tiles
-  double* acc = ring + RS * TB * TB;  // per own row: forward, then backward accumulator
-  double* tv = acc + nown * TB;       // own forward segments t_i
-  double* wv = tv + nown * TB;        // own backward segments w_i
-  double* Lc = wv + nown * TB;        // staged critical tile
-  double* Li = Lc + TB * TS;          // staged inverse of the critical diagonal tile
-  double* seg = Li + TB * TS;         // the segment being applied
-  double* part = seg + TB;            // 4 x 64 partial sums
-  int* ff = reinterpret_cast<int*>(part + 4 * TB);  // forward segment flags (T)
-  int* bf = ff + T;                                 // backward segment flags (T)
+  double* const ring = S.ring;
+  double* const acc = S.acc;
+  double* const tv = S.tv;
+  double* const wv = S.wv;
+  double* const Lc = S.Lc;
+  double* const Li = S.Li;
+  double* const seg = S.seg;
+  double* const part = S.part;
+  int* const ff = S.ff;
+  int* const bf = S.bf;
 
-  const bool skip = P.ctl != nullptr && P.ctl->diverged_at != 0;  // uniform over the cluster
   for (int e = tid; e < 2 * T; e += 256) ff[e] = 0;
   const int mine = me < T ? (T - 1 - me) / C + 1 : 0;  // own rows me, me + C, ...
   for (int e = tid; e < mine * TB; e += 256) {
@@ -245,25 +266,26 @@ __global__ void __launch_bounds__(256, 1) k_trsv_cluster(TrsvParams P) {
   const SeqCtx sc{me, C, T, i0, last, has_fwd};
   TileSeq prod{0, i0, sc.first_own_ge(i0 + 2)};
   bool prod_ok = false;
-  if (tid == 0) {
-    for (int q = 0; q < RS; ++q) mbar_init(&full[q], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if (!skip && mine > 0) {
+  if (tid == 0 && mine > 0) {
+    // slots were last read (generic proxy) by the previous solve: order those
+    // reads before the async-proxy refills
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    prod_ok = sc.norm(prod);
+    for (int q = 0; q < RS && prod_ok; ++q) {  // the ring runs ahead from the start
+      const uint32_t slot = (qbase + q) % RS;
+      bulk_tile(ring + slot * TB * TB, sc.tile(P.L, prod), &full[slot]);
+      sc.advance(prod);
       prod_ok = sc.norm(prod);
-      for (int q = 0; q < RS && prod_ok; ++q) {  // the ring runs ahead from the start
-        bulk_tile(ring + q * TB * TB, sc.tile(P.L, prod), &full[q]);
-        sc.advance(prod);
-        prod_ok = sc.norm(prod);
-      }
     }
   }
   cluster_barrier();  // every CTA's flags are zero before anyone publishes
-  if (!skip && mine > 0) {
-    uint32_t qc = 0;  // tiles consumed
-    // consume the next ring tile (tile qc of the sequence), then refill its slot
+  if (mine > 0) {
+    uint32_t qc = 0;  // tiles consumed by this solve
+    // consume the next ring tile (tile qbase + qc of the launch), then refill its slot
     auto consume = [&](double* v, bool transposed) {
-      const int slot = qc % RS;
-      mbar_wait(&full[slot], (qc / RS) & 1);
+      const uint32_t q = qbase + qc;
+      const int slot = q % RS;
+      mbar_wait(&full[slot], (q / RS) & 1);
       const double* M = ring + slot * TB * TB;
       if (transposed) gemvT_sub_ring(v, M, seg, part, tid);
       else gemv_sub_ring(v, M, seg, tid);
@@ -361,8 +383,26 @@ __global__ void __launch_bounds__(256, 1) k_trsv_cluster(TrsvParams P) {
       for (int ip = me; ip < k - 1; ip += C) consume(acc + (ip / C) * TB, true);
       __syncthreads();
     }
+    qbase += qc;
   }
   cp_async_wait_all();
+}
+
+__global__ void __launch_bounds__(256, 1) k_trsv_cluster(TrsvParams P) {
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t full[RS_MAX];
+  const int me = (int)cluster_rank();
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int q = 0; q < P.rs; ++q) mbar_init(&full[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const bool skip = P.ctl != nullptr && P.ctl->diverged_at != 0;  // uniform over the cluster
+  if (!skip) {
+    uint32_t qbase = 0;
+    trsv_body(P, trsv_carve(sm, P.rs, P.T, P.C), full, qbase, me, tid);
+  }
   cluster_barrier();  // no CTA leaves while its segments may still be read
 }
 
