@@ -242,11 +242,15 @@ struct slim_ctx {
   double* panels = nullptr;
   int64_t panel_stride = 0;
   int D = D_DEFAULT;                 // batch size
+  bool serial = false;               // debug (SLIM_SERIAL): factorizations wait for the x-chain
   int trsv_C = 0;                    // triangular-solve cluster size (0 = by T)
   std::vector<double*> Lbuf, Dinv, Linv;  // 2 D factor buffers (+ 8x8 and 64x64 diagonal inverses)
   void* factor_slab = nullptr;            // one allocation behind Lbuf / Dinv / Linv / cflags
   std::vector<CUtensorMap> Lmap;     // TMA views of the factor buffers
   std::vector<int*> cflags;
+  std::vector<int8_t*> Qbuf;         // int8 digit slices of the factors (tensor-core updates)
+  std::vector<CUtensorMap> Qmap;
+  std::vector<int*> rexp;            // row scale exponents per factor buffer
   int* tickets = nullptr;  // [0] chol ticket, [1] trsv ticket
   struct TaskMap {
     int2* dev;
@@ -435,6 +439,7 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
     const int64_t Nmax0 = (d->memory_r + 1) * d->block_rows;
     c->D = Nmax0 <= 2048 ? 8 : (Nmax0 <= 6144 ? 16 : 4);
     if (const char* env = getenv("SLIM_BATCH")) c->D = std::max(1, std::min(MAX_BATCH, atoi(env)));
+    c->serial = getenv("SLIM_SERIAL") != nullptr;  // debug: no factorization / x-chain overlap
     if (const char* env = getenv("SLIM_TRSV_CLUSTER")) c->trsv_C = std::max(1, std::min(16, atoi(env)));
   }
   for (int q = 0; q < NEV; ++q) {
@@ -455,6 +460,9 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
   const int64_t Nmax = W * ell;
   c->Tmax = (int)((Nmax + TB - 1) / TB);
   const int64_t ntiles = (int64_t)c->Tmax * (c->Tmax + 1) / 2;
+  if (chol_use_i8() && c->Tmax > CHOL_I8_TMAX)  // int32 digit-product sums stay exact
+    FAIL(c, SLIM_EINVAL, "dual system of %lld rows exceeds the tensor-core factorization's limit "
+         "(%d rows)", (long long)Nmax, CHOL_I8_TMAX * TB);
   {
     // the triangular-solve cluster keeps per-row vectors in shared memory
     int optin = 0;
@@ -477,13 +485,19 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
   c->Dinv.assign(2 * c->D, nullptr);
   c->Linv.assign(2 * c->D, nullptr);
   c->cflags.assign(2 * c->D, nullptr);
+  c->Qbuf.assign(2 * c->D, nullptr);
+  c->Qmap.resize(2 * c->D);
+  c->rexp.assign(2 * c->D, nullptr);
   {
     // one slab for all 2D factor buffers (one allocation, one memset)
     const size_t lb = sizeof(double) * (size_t)ntiles * TB * TB;
     const size_t db = sizeof(double) * (size_t)c->Tmax * 512;
     const size_t ib = sizeof(double) * (size_t)c->Tmax * TB * TB;
     const size_t fb = ((sizeof(int) * (size_t)ntiles + 255) / 256) * 256;
-    const size_t per = lb + db + ib;
+    // int8 digit slices (same bytes as the fp64 tiles) + row exponents
+    const size_t qb = chol_use_i8() ? lb : 0;
+    const size_t eb = chol_use_i8() ? ((sizeof(int) * (size_t)c->Tmax * TB + 1023) / 1024) * 1024 : 0;
+    const size_t per = lb + db + ib + qb + eb;
     ALLOC(c, c->factor_slab, (per + fb) * 2 * c->D);
     char* base = (char*)c->factor_slab;
     char* flags = base + per * 2 * c->D;
@@ -495,6 +509,10 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
       c->cflags[q] = (int*)(flags + fb * q);
       if (!tma_map_f64_sw128(&c->Lmap[q], c->Lbuf[q], ntiles * TB, TB, 16, TB))
         FAIL(c, SLIM_ECUDA, "TMA descriptor for the factor buffer could not be encoded");
+      c->Qbuf[q] = qb ? (int8_t*)(base + per * q + lb + db + ib) : nullptr;
+      c->rexp[q] = eb ? (int*)(base + per * q + lb + db + ib + qb) : nullptr;
+      if (qb && !tma_map_q(&c->Qmap[q], c->Qbuf[q], ntiles))
+        FAIL(c, SLIM_ECUDA, "TMA descriptor for the sliced factor buffer could not be encoded");
     }
   }
   tick("factors");
@@ -1280,6 +1298,9 @@ static int enqueue_chol_batch(slim_ctx* c, const Window* Ws, int nb, int set, co
     M.Dinv = c->Dinv[buf];
     M.Linv = c->Linv[buf];
     M.flags = c->cflags[buf];
+    M.Q = c->Qbuf[buf];
+    M.qmap = c->Qmap[buf];
+    M.rexp = c->rexp[buf];
     M.N = N;
     M.T = (N + TB - 1) / TB;
     M.nw = Ws[b].nw;
@@ -1307,6 +1328,7 @@ static int enqueue_chol_batch(slim_ctx* c, const Window* Ws, int nb, int set, co
   P.W = (int)(c->r + 1);
   P.prevL = prev >= 0 ? c->Lbuf[prev] : nullptr;
   P.prevDinv = prev >= 0 ? c->Dinv[prev] : nullptr;
+  P.prevQ = prev >= 0 ? c->Qbuf[prev] : nullptr;
   P.tile_base[0] = 0;
   for (int b = 0; b < nb; ++b) P.tile_base[b + 1] = P.tile_base[b] + sh[b].T * (sh[b].T + 1) / 2;
   launch_assemble(P, c->sf);
@@ -1461,6 +1483,7 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
     // ---- batched factorization (sf): buffer set reused from batch B - 2
     CK(c, cudaStreamWaitEvent(c->sf, c->ev_g[B % NEV], 0));
     if (B >= 2) CK(c, cudaStreamWaitEvent(c->sf, c->ev_x[(B - 2) % NEV], 0));
+    if (B >= 1 && c->serial) CK(c, cudaStreamWaitEvent(c->sf, c->ev_x[(B - 1) % NEV], 0));
     ProfPair pc{};
     if (prof_b) pc = take(c->prof_chol, pch), cudaEventRecord(pc.a, c->sf);
     {
@@ -1696,10 +1719,16 @@ static int potrf_impl(int32_t device, const double* G, int64_t N, double* L_out,
   if (!G || !L_out || N < 1) FAIL((slim_ctx*)nullptr, SLIM_EINVAL, "bad argument");
   if (cudaSetDevice(device) != cudaSuccess) FAIL((slim_ctx*)nullptr, SLIM_ECUDA, "cudaSetDevice");
   const int T = (int)((N + TB - 1) / TB);
+  if (chol_use_i8() && T > CHOL_I8_TMAX)
+    FAIL((slim_ctx*)nullptr, SLIM_EINVAL, "N = %lld exceeds the tensor-core factorization's limit (%d)",
+         (long long)N, CHOL_I8_TMAX * TB);
   const int64_t ntiles = (int64_t)T * (T + 1) / 2;
   double *dG = nullptr, *dL = nullptr, *dD = nullptr;
-  int *flags = nullptr, *ticket = nullptr, *err = nullptr;
+  int *flags = nullptr, *ticket = nullptr, *err = nullptr, *rx = nullptr;
+  int8_t* dQ = nullptr;
   auto cleanup = [&]() {
+    cudaFree(dQ);
+    cudaFree(rx);
     cudaFree(dG);
     cudaFree(dL);
     cudaFree(dD);
@@ -1711,7 +1740,9 @@ static int potrf_impl(int32_t device, const double* G, int64_t N, double* L_out,
       cudaMalloc(&dL, sizeof(double) * ntiles * TB * TB) != cudaSuccess ||
       cudaMalloc(&dD, sizeof(double) * T * 512) != cudaSuccess ||
       cudaMalloc(&flags, sizeof(int) * ntiles) != cudaSuccess ||
-      cudaMalloc(&ticket, sizeof(int)) != cudaSuccess || cudaMalloc(&err, sizeof(int)) != cudaSuccess) {
+      cudaMalloc(&ticket, sizeof(int)) != cudaSuccess || cudaMalloc(&err, sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&dQ, (size_t)ntiles * TB * TB * 8) != cudaSuccess ||
+      cudaMalloc(&rx, sizeof(int) * T * TB) != cudaSuccess) {
     cleanup();
     FAIL((slim_ctx*)nullptr, SLIM_ENOMEM, "device allocation failed");
   }
@@ -1724,6 +1755,12 @@ static int potrf_impl(int32_t device, const double* G, int64_t N, double* L_out,
     cleanup();
     FAIL((slim_ctx*)nullptr, SLIM_ECUDA, "TMA descriptor could not be encoded");
   }
+  if (chol_use_i8() && !tma_map_q(&P.m[0].qmap, dQ, ntiles)) {
+    cleanup();
+    FAIL((slim_ctx*)nullptr, SLIM_ECUDA, "TMA descriptor could not be encoded");
+  }
+  P.m[0].Q = chol_use_i8() ? dQ : nullptr;
+  P.m[0].rexp = chol_use_i8() ? rx : nullptr;
   P.m[0].L = dL;
   P.m[0].Dinv = dD;
   P.m[0].flags = flags;

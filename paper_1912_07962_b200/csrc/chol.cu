@@ -29,6 +29,8 @@
 // 8x8 blocks are inverted, so the backward error stays that of a
 // substitution (the 8x8 blocks of a Cholesky factor are well conditioned).
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "common.cuh"
@@ -309,12 +311,37 @@ __global__ void __launch_bounds__(256) k_assemble(CholParams P) {
   const int N = Mp.N, ell = P.ell;
   const int tid = threadIdx.x;
   const int64_t toff = tile_off(I, J);
+  if (I == J && Mp.rexp != nullptr && tid < TB) {
+    // row scales of the int8 digit slices: 2^e >= sqrt(G_pp) >= |L_pk|
+    // (every system, fresh or not: the same G_pp gives the same exponent)
+    const int p = I * TB + tid;
+    double gpp = 1.0;
+    if (p < N) {
+      if (P.panels != nullptr) {
+        const int pb = p / ell, a = p - pb * ell;
+        const double* pan = P.panels + (int64_t)Mp.slot[pb] * P.panel_stride;
+        gpp = Mp.alpha * pan[((int64_t)pb * ell + a) * ell + a] + 1.0;
+      } else {
+        gpp = P.G[(int64_t)p * P.ldg + p];
+      }
+    }
+    // 2^e >= 1.004 sqrt(gpp): |L_pk| 2^(7 - e) < 127.5, so the leading digit
+    // rounds into [-127, 127]
+    int e = 0;
+    frexp(1.004 * sqrt(fmax(gpp, 1e-300)), &e);
+    Mp.rexp[p] = e;
+  }
   if (!tile_fresh(Mp.full, Mp.pnew, P.W, ell, I, J)) {
     for (int bb = b - 1; bb >= 0; --bb)
       if (tile_fresh(P.m[bb].full, P.m[bb].pnew, P.W, ell, I, J)) return;  // produced in-batch
     const double2* src = reinterpret_cast<const double2*>(P.prevL + toff);
     double2* dst = reinterpret_cast<double2*>(Mp.L + toff);
     for (int e = tid; e < TB * TB / 2; e += 256) dst[e] = __ldcg(src + e);
+    if (Mp.Q != nullptr && P.prevQ != nullptr) {  // same byte count as the fp64 tile
+      const double2* qs = reinterpret_cast<const double2*>(P.prevQ + toff * 8);
+      double2* qd = reinterpret_cast<double2*>(Mp.Q + toff * 8);
+      for (int e = tid; e < TB * TB / 2; e += 256) qd[e] = __ldcg(qs + e);
+    }
     if (I == J)
       for (int e = tid; e < 512; e += 256) Mp.Dinv[(int64_t)J * 512 + e] = __ldcg(P.prevDinv + (int64_t)J * 512 + e);
     if (tid == 0) Mp.flags[I * (I + 1) / 2 + J] = Mp.epoch;  // next kernel: stream-ordered
@@ -689,7 +716,344 @@ __global__ void __launch_bounds__(256, 2) k_chol_tiles(const __grid_constant__ C
   if (tr) tr[3] = globaltimer_ns();
 }
 
-size_t chol_smem_bytes() { return (size_t)SMB_TOTAL; }
+// ===========================================================================
+// Tile updates on the 5th-generation tensor cores (tcgen05 kind::i8).
+//
+// The left-looking update C = G_ij - sum_k L_ik L_jk^T dominates the
+// factorization (all but O(T^2) of its flops).  tcgen05 has no fp64 kind, so
+// the update is computed EXACTLY in integer arithmetic from digit slices:
+// every entry of L row p is written as
+//     L_pk = 2^(e_p - 7) sum_{a=1..8} d_a 2^(-7 (a-1)),
+// d_1 in [-127, 127], d_a in [-64, 64] for a > 1, with 2^(e_p) >= 1.004
+// sqrt(G_pp) >= 1.004 |L_pk| (row scales known before the factorization
+// starts, k_assemble), so the representation error is below 2^-57 2^(e_p).
+// Then
+//     sum_k L_ik L_jk = 2^(e_i + e_j - 14) sum_{t=0..7} 2^(-7 t) P_t,
+//     P_t = sum_{a + b = t + 2} D_a(i) D_b(j)^T        (int32, exact)
+// where the 36 digit products with a + b <= 9 are kept; the dropped ones
+// weigh < 2^-56 of sqrt(G_ii G_jj) per k, the size of fp64 rounding (the
+// Cholesky backward-error bound is componentwise in sqrt(G_ii G_jj), so this
+// row scaling is the natural one).  Each P_t is one TMEM accumulator
+// (M = 128 rows of two output tiles x N = 64: 8 x 64 = all 512 columns), the
+// int32 sums are exact (|P_t| <= (2 * 127 * 64 + 6 * 64^2) 64 T < 2^31 for
+// T <= 800, checked at context creation), and
+// the eight are combined in fp64 once per task.  POTRF, TRSM and the 8x8
+// inverses stay in fp64 (DMMA), on O(T^2) tiles.
+//
+// A sliced tile (32 KB, the size of its fp64 tile) is stored as
+// [k half h][digit quad dq][row][4 digits x 32 k] so that one K = 32 MMA
+// step of a digit pair is one 32-byte column of a SWIZZLE_128B row.
+// ===========================================================================
+namespace oz {
+constexpr int BOX = 64 * 128;            // 64 rows x 128 B
+constexpr int ST_A = 4 * BOX;            // [dq][row tile 0 / 1][64][128 B]
+constexpr int ST_B = 2 * BOX;            // [dq][64][128 B]
+constexpr int STAGE = ST_A + ST_B;       // 48 KB: one k half of three tiles
+constexpr int NST = 4;
+constexpr int SMEM = NST * STAGE + 1024;
+// work tiles over the drained stage ring
+constexpr int W_X = 0;                               // 128 x TS fp64
+constexpr int W_SG = W_X + 2 * TB * TS * 8;          // L_jj, 64 x TS fp64
+constexpr int W_DV = W_SG + TB * TS * 8;             // 8x8 inverses (512)
+constexpr int W_RD = W_DV + 512 * 8;                 // 64 reciprocal pivots
+static_assert(W_RD + 64 * 8 <= NST * STAGE, "work tiles must fit over the stage ring");
+constexpr uint32_t IDESC = (2u << 4) |               // D format S32
+                           (1u << 7) | (1u << 10) |  // A, B signed 8-bit
+                           ((uint32_t)(TB >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, int (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ double pow2(int e) {  // exact 2^e, |e| < 1000
+  return __longlong_as_double((long long)(e + 1023) << 52);
+}
+}  // namespace oz
+
+// digit slices of the 64x64 fp64 tile X (smem, stride TS) with row
+// exponents rex[0..63] into the sliced tile Qt (global): thread = (row,
+// 16 consecutive k); v = L 2^(7 - e) lies in (-127.5, 127.5), and
+// d_a = rint(v), v <- (v - d_a) 128 is exact in fp64
+__device__ void slice_store(const double* X, const int* rex, int8_t* Qt, int tid) {
+  const int r = tid >> 2, kq = tid & 3, kh = kq >> 1, kk0 = (kq & 1) * 16;
+  const double sc = oz::pow2(7 - __ldcg(rex + r));
+  uint32_t w[8][4];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) w[a][q] = 0u;
+#pragma unroll
+  for (int cc = 0; cc < 16; ++cc) {
+    double v = X[r * TS + 16 * kq + cc] * sc;
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      const double d = rint(v);
+      v = (v - d) * 128.0;
+      w[a][cc >> 2] |= ((uint32_t)(int)d & 0xffu) << (8 * (cc & 3));
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+    const int dq = a >> 2, dd = a & 3;
+    uint4 u;
+    u.x = w[a][0];
+    u.y = w[a][1];
+    u.z = w[a][2];
+    u.w = w[a][3];
+    *reinterpret_cast<uint4*>(Qt + ((kh * 2 + dq) * 64 + r) * 128 + dd * 32 + kk0) = u;
+  }
+}
+
+__device__ __forceinline__ int8_t* qtile(const CholMat& M, int i, int j) {
+  return M.Q + tile_off(i, j) * 8;
+}
+
+// store tile (i, j) of system b (fp64 + digit slices) and publish it
+__device__ void store_publish_i8(const CholMat& M, int i, int j, const double* X, const double* Dv,
+                                 int tid) {
+  store_tile(M.L + tile_off(i, j), X, tid);
+  if (i != j) slice_store(X, M.rexp + i * TB, qtile(M, i, j), tid);  // diagonal tiles are never operands
+  if (Dv != nullptr) {
+    const double2 v = *reinterpret_cast<const double2*>(Dv + 2 * tid);
+    *reinterpret_cast<double2*>(M.Dinv + (int64_t)j * 512 + 2 * tid) = v;
+  }
+  fence_proxy_async();  // consumers read the slices with TMA (async proxy)
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    st_release(M.flags + (i * (i + 1) / 2 + j), M.epoch);
+  }
+}
+
+// later systems of the batch that share tile (i, j) bit for bit
+__device__ void forward_tile_i8(const CholParams& P, int b, int i, int j, const double* X,
+                                const double* Dv, int tid) {
+  for (int bb = b + 1; bb < P.nb; ++bb) {
+    const CholMat& M2 = P.m[bb];
+    if (tile_fresh(M2.full, M2.pnew, P.W, P.ell, i, j)) break;  // recomputed from here on
+    store_publish_i8(M2, i, j, X, Dv, tid);
+  }
+}
+
+// One task per CTA (same ticket map as k_chol_tiles): output rows ra (and
+// ra + 1 for pair / dual tasks) of tile column j.  Warp 0 lane 0 streams the
+// digit slices of L_(ra, k), L_(ra+1, k), L_(j, k) for k < j through a 4-stage
+// TMA ring (48 KB per k half); warp 1 lane 0 issues the 36 digit-pair MMAs
+// per stage into the eight TMEM accumulators; then all eight warps combine
+// the accumulators with G in fp64 and finish the tiles (POTRF / TRSM, DMMA).
+__global__ void __launch_bounds__(256, 1) k_chol_i8(const __grid_constant__ CholParams P) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* base = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* stage = base;
+  double* X = reinterpret_cast<double*>(base + oz::W_X);
+  double* X2 = X + TB * TS;
+  double* Sg = reinterpret_cast<double*>(base + oz::W_SG);
+  double* Dv = reinterpret_cast<double*>(base + oz::W_DV);
+  double* rdiag = reinterpret_cast<double*>(base + oz::W_RD);
+  __shared__ int s_task;
+  __shared__ uint32_t s_tmem;
+  __shared__ int s_ecol[TB];
+  __shared__ __align__(8) uint64_t s_full[oz::NST], s_empty[oz::NST], s_accf;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    s_task = atomicAdd(P.ticket, 1);
+    for (int q = 0; q < oz::NST; ++q) {
+      bar_init(&s_full[q], 1);
+      bar_init(&s_empty[q], 1);
+    }
+    bar_init(&s_accf, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (s_task >= P.ntasks) return;
+  const int2 e = P.map[s_task];
+  const CholMat& M = P.m[e.x];
+  const int i = e.y >> 16, j = e.y & 0x7fff;
+  const bool pair = i == j;
+  const int T = M.T;
+  const bool two = pair ? (j + 1 < T) : ((e.y & 0x8000) != 0);
+  const int ra = i;  // first output row tile (the diagonal for a pair task)
+  unsigned long long* tr = (P.trace != nullptr && tid == 0) ? P.trace + 4 * (int64_t)s_task : nullptr;
+  if (tr) tr[0] = globaltimer_ns();
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        su32(&s_tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid < TB) s_ecol[tid] = __ldcg(M.rexp + j * TB + tid);
+  if (tid == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(&M.qmap) : "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = s_tmem;
+  const int nchunk = 2 * j;  // k tiles 0 .. j-1, two k halves each
+
+  if (tid == 0 && nchunk > 0) {
+    // ---------------- TMA producer ----------------
+    const int* fa = M.flags + ra * (ra + 1) / 2;
+    const int* fa2 = M.flags + (ra + 1) * (ra + 2) / 2;
+    const int* fb = M.flags + j * (j + 1) / 2;
+    int kready = j;
+    for (int k = 0; k < j; ++k) {
+      int va, vb = M.epoch, vc = M.epoch;
+      asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(va) : "l"(fa + k) : "memory");
+      if (two) asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(vb) : "l"(fa2 + k) : "memory");
+      if (!pair) asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(vc) : "l"(fb + k) : "memory");
+      if (va < M.epoch || vb < M.epoch || vc < M.epoch) {
+        kready = k;
+        break;
+      }
+    }
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    fence_proxy_async();
+    const uint32_t bytes = (two ? 4 : 2) * oz::BOX + (pair ? 0 : 2 * oz::BOX);
+    for (int u = 0; u < nchunk; ++u) {
+      const int st = u % oz::NST;
+      bar_wait(&s_empty[st], ((u / oz::NST) & 1) ^ 1);
+      const int k = u >> 1, kh = u & 1;
+      if (kh == 0 && k >= kready) {
+        wait_flag(fa + k, M.epoch);
+        if (two) wait_flag(fa2 + k, M.epoch);
+        if (!pair) wait_flag(fb + k, M.epoch);
+        fence_proxy_async();
+      }
+      uint8_t* dst = stage + st * oz::STAGE;
+      bar_expect(&s_full[st], bytes);
+      const int ya = (ra * (ra + 1) / 2 + k) * 256 + kh * 128;
+      const int ya2 = ((ra + 1) * (ra + 2) / 2 + k) * 256 + kh * 128;
+      const int yb = (j * (j + 1) / 2 + k) * 256 + kh * 128;
+#pragma unroll
+      for (int dq = 0; dq < 2; ++dq) {
+        tma2d(dst + dq * 2 * oz::BOX, &M.qmap, &s_full[st], 0, ya + dq * 64);
+        if (two) tma2d(dst + dq * 2 * oz::BOX + oz::BOX, &M.qmap, &s_full[st], 0, ya2 + dq * 64);
+        if (!pair) tma2d(dst + oz::ST_A + dq * oz::BOX, &M.qmap, &s_full[st], 0, yb + dq * 64);
+      }
+    }
+  } else if (warp == 1 && lane == 0 && nchunk > 0) {
+    // ---------------- MMA issuer ----------------
+    for (int u = 0; u < nchunk; ++u) {
+      const int st = u % oz::NST;
+      bar_wait(&s_full[st], (u / oz::NST) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t a0 = su32(stage + st * oz::STAGE);
+      const uint32_t b0 = pair ? a0 : a0 + oz::ST_A;
+      const uint32_t bdq = pair ? 2 * oz::BOX : oz::BOX;
+      const uint64_t ad = oz::sw128_desc(a0), bd = oz::sw128_desc(b0);
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+#pragma unroll
+        for (int a = 1; a <= t + 1; ++a) {
+          const int b = t + 2 - a;
+          const uint32_t aoff = ((a - 1) >> 2) * 2 * oz::BOX + ((a - 1) & 3) * 32;
+          const uint32_t boff = ((b - 1) >> 2) * bdq + ((b - 1) & 3) * 32;
+          oz::mma_i8(tmem + 64 * t, ad + (aoff >> 4), bd + (boff >> 4), (u > 0 || a > 1) ? 1u : 0u);
+        }
+      oz::mma_commit(&s_empty[st]);
+    }
+    oz::mma_commit(&s_accf);
+  }
+  __syncwarp();
+
+  // ---------------- combine: X = G - 2^(e_r + e_c - 14) sum_t 2^(-7t) P_t ----------------
+  {
+    if (nchunk > 0) bar_wait(&s_accf, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int q = warp & 3, h = warp >> 2;
+    const int R = 32 * q + lane, sel = R >> 6, r = R & 63;
+    double s[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) s[c] = 0.0;
+    if (nchunk > 0) {
+#pragma unroll 1
+      for (int t = 7; t >= 0; --t) {
+        int v[32];
+        oz::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + 64 * t + 32 * h, v);
+#pragma unroll
+        for (int c = 0; c < 32; ++c) s[c] = fma(s[c], 0.0078125, (double)v[c]);
+      }
+    }
+    if (sel == 0 || two) {
+      const int er = __ldcg(M.rexp + (ra + sel) * TB + r);
+      const double* g = M.L + tile_off(ra + sel, j) + r * TB + 32 * h;
+      double* x = X + R * TS + 32 * h;
+#pragma unroll
+      for (int c = 0; c < 32; c += 2) {
+        const double2 gv = __ldcg(reinterpret_cast<const double2*>(g + c));
+        x[c] = gv.x - s[c] * oz::pow2(er + s_ecol[32 * h + c] - 14);
+        x[c + 1] = gv.y - s[c + 1] * oz::pow2(er + s_ecol[32 * h + c + 1] - 14);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  if (tr) tr[1] = globaltimer_ns();
+
+  if (pair) {
+    potrf_tile_blocked(X, Dv, rdiag, tid, P.error);
+    if (tr) tr[2] = globaltimer_ns();
+    store_publish_i8(M, j, j, X, Dv, tid);
+    if (two) {
+      trsm_tile_warp(X2, X, Dv, warp, lane);
+      __syncthreads();
+      store_publish_i8(M, j + 1, j, X2, nullptr, tid);
+      forward_tile_i8(P, e.x, j + 1, j, X2, nullptr, tid);
+    }
+    forward_tile_i8(P, e.x, j, j, X, Dv, tid);
+  } else {
+    if (tid == 0) wait_flag(M.flags + (j * (j + 1) / 2 + j), M.epoch);
+    if (tr) tr[2] = globaltimer_ns();
+    __syncthreads();
+    load_tile_async(Sg, M.L + tile_off(j, j), tid);
+    load_dinv_async(Dv, M.Dinv + (int64_t)j * 512, tid);
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+    trsm_tile_warp(X, Sg, Dv, warp, lane);
+    if (two) trsm_tile_warp(X2, Sg, Dv, warp, lane);
+    __syncthreads();
+    store_publish_i8(M, ra, j, X, nullptr, tid);
+    if (two) store_publish_i8(M, ra + 1, j, X2, nullptr, tid);
+    forward_tile_i8(P, e.x, ra, j, X, nullptr, tid);
+    if (two) forward_tile_i8(P, e.x, ra + 1, j, X2, nullptr, tid);
+  }
+  if (tr) tr[3] = globaltimer_ns();
+}
+
+bool chol_use_i8() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SLIM_CHOL");
+    v = (e != nullptr && std::string(e) == "dmma") ? 0 : 1;
+  }
+  return v == 1;
+}
+
+size_t chol_smem_bytes() { return chol_use_i8() ? (size_t)oz::SMEM : (size_t)SMB_TOTAL; }
 
 // Ticket order.  A system's tasks are its fresh tiles (tile_fresh), grouped
 // by column: pair(0) opens group -1; group j holds, in this order, the
@@ -745,11 +1109,14 @@ void launch_assemble(const CholParams& P, cudaStream_t s) {
 void launch_chol(const CholParams& P, cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(k_chol_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)chol_smem_bytes());
+    cudaFuncSetAttribute(k_chol_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMB_TOTAL);
+    cudaFuncSetAttribute(k_chol_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)oz::SMEM);
     configured = true;
   }
-  k_chol_tiles<<<P.ntasks, 256, chol_smem_bytes(), s>>>(P);
+  if (chol_use_i8())
+    k_chol_i8<<<P.ntasks, 256, oz::SMEM, s>>>(P);
+  else
+    k_chol_tiles<<<P.ntasks, 256, SMB_TOTAL, s>>>(P);
 }
 
 }  // namespace slim

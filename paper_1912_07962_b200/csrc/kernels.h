@@ -28,6 +28,12 @@ struct CholMat {
   double* L;            // lower tiles, tile_off(i, j)
   double* Dinv;         // T x 512: inverses of the 8x8 diagonal blocks of L_jj
   double* Linv;         // T x 4096: inverses of the diagonal tiles (k_diag_inv)
+  // int8 digit slices of L for the tensor-core updates (chol.cu, k_chol_i8):
+  // tile t at Q + t * 32 KB, [k half][digit quad][row][4 digits x 32 k];
+  // qmap views them as (tiles * 256) rows of 128 B, box 64 rows, SW128
+  int8_t* Q;
+  CUtensorMap qmap;
+  int* rexp;            // T * 64: row scale exponents, 2^rexp >= sqrt(G_rr)
   int* flags;           // T (T + 1) / 2 epoch flags
   int N, T, nw, epoch;
   double alpha;
@@ -55,6 +61,7 @@ struct CholParams {
   // k0 - 1) are copied from its factor buffer by k_assemble
   const double* prevL;
   const double* prevDinv;
+  const int8_t* prevQ;   // digit slices of the previous batch's last system
   // dense mode (panels == nullptr, nb == 1): G is the full SPD matrix, row-major
   const double* G;
   int64_t ldg;
@@ -123,7 +130,15 @@ int trsv_cluster_size(int T);
 size_t trsv_smem_bytes(int T, int C, int rs = 3);
 
 __global__ void k_chol_tiles(const __grid_constant__ CholParams P);
+__global__ void k_chol_i8(const __grid_constant__ CholParams P);
 
 size_t chol_smem_bytes();
+// factorization kernel: true = int8 tensor-core updates (default), false =
+// fp64 DMMA updates (SLIM_CHOL=dmma, kept for A/B measurements)
+bool chol_use_i8();
+// int8 updates: |P_t| <= (2 * 127 * 64 + 6 * 64^2) * 64 T < 2^31
+constexpr int CHOL_I8_TMAX = 800;
+// TMA view of a sliced factor buffer (tiles * 256 rows x 128 B, box 64 rows)
+bool tma_map_q(CUtensorMap* m, const int8_t* base, int64_t ntiles);
 
 }  // namespace slim
