@@ -101,6 +101,11 @@ def _peaks():
 # FP64 DMMA/DFMA peak is not in MEASURED_PEAKS.json; measured on this pool
 # by tools/microbench/fp64_rates.cu (profiles/fp64_peak_r01.txt)
 FP64_PEAK_TFLOPS = 37.1
+# int8 tcgen05 peak (kind::i8, M=128 N=256, smem operands) and the ceiling of
+# the factorization's own MMA shape (M=128 N=64), measured on this pool by
+# tools/microbench/i8_rates.cu (profiles/i8_peak_r01.txt)
+I8_PEAK_TOPS = 4579.0
+I8_N64_CEIL_TOPS = 3056.0
 
 
 def _dist():
@@ -353,18 +358,39 @@ def run_ours(args, world, rank, local, dist):
             traffic = prof["dram_bytes_per_launch"]
     except (OSError, ValueError, KeyError):
         pass
-    roofline = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
-                "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
-                "kernel": f"k_chol_tiles (fp64 DMMA tile-DAG Cholesky, {per_launch:g} systems "
-                          f"of N={N} interleaved per launch)",
-                "algorithmic_per_launch": f"{flops_chol:.4g} flop (tiles factored, 2*64^3 per "
-                                          f"tile update; from scratch a system is N^3/3 = "
-                                          f"{N ** 3 / 3.0:.4g})",
-                "peak_source": "FP64 DMMA peak measured on this pool "
-                               "(tools/microbench/fp64_rates.cu, profiles/fp64_peak_r01.txt)",
-                "aggregate_tflops_over_window": agg,
-                "aggregate_frac": agg / FP64_PEAK_TFLOPS,
-                "avg_launch_ms": chol_ms, "launches": timing["cholesky_count"]}
+    i8ops = timing.get("cholesky_i8ops", 0.0) / max(1, timing["cholesky_count"])
+    if i8ops > 0:
+        # int8 tensor-core factorization: the tile updates are exact int32
+        # digit-pair products (36 per 64^3 update); POTRF/TRSM stay fp64
+        ach_i8 = i8ops / (chol_ms * 1e-3) / 1e12
+        roofline = {"bound": "tensor", "achieved": ach_i8, "peak": I8_PEAK_TOPS,
+                    "unit": "TOPS (int8)", "frac": ach_i8 / I8_PEAK_TOPS, "traffic": traffic,
+                    "kernel": f"k_chol_i8 (tile-DAG Cholesky, updates on tcgen05 kind::i8 with "
+                              f"TMEM accumulators, {per_launch:g} systems of N={N} per launch)",
+                    "algorithmic_per_launch": f"{i8ops:.4g} int8 ops (36 digit-pair products x "
+                                              f"2*64^3 per 64x64x64 tile update; the launch "
+                                              f"factors {flops_chol:.4g} fp64-equivalent flop)",
+                    "peak_source": "int8 tcgen05 peak measured on this pool, M=128 N=256 "
+                                   "(tools/microbench/i8_rates.cu, profiles/i8_peak_r01.txt)",
+                    "shape_ceiling_tops": I8_N64_CEIL_TOPS,
+                    "frac_of_shape_ceiling": ach_i8 / I8_N64_CEIL_TOPS,
+                    "fp64_equivalent_tflops": achieved,
+                    "fp64_equivalent_frac_of_dmma_peak": achieved / FP64_PEAK_TFLOPS,
+                    "aggregate_tflops_over_window": agg,
+                    "avg_launch_ms": chol_ms, "launches": timing["cholesky_count"]}
+    else:
+        roofline = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
+                    "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+                    "kernel": f"k_chol_tiles (fp64 DMMA tile-DAG Cholesky, {per_launch:g} systems "
+                              f"of N={N} interleaved per launch)",
+                    "algorithmic_per_launch": f"{flops_chol:.4g} flop (tiles factored, 2*64^3 per "
+                                              f"tile update; from scratch a system is N^3/3 = "
+                                              f"{N ** 3 / 3.0:.4g})",
+                    "peak_source": "FP64 DMMA peak measured on this pool "
+                                   "(tools/microbench/fp64_rates.cu, profiles/fp64_peak_r01.txt)",
+                    "aggregate_tflops_over_window": agg,
+                    "aggregate_frac": agg / FP64_PEAK_TFLOPS,
+                    "avg_launch_ms": chol_ms, "launches": timing["cholesky_count"]}
     # ---- e2e through the public API, host-resident fresh operator ----
     e2e = None
     if not args.quick and not sharded:

@@ -32,6 +32,7 @@
 
 #include "gram_tc.h"
 #include "kernels.h"
+#include "smpart.h"
 #include "ops.h"
 #include "slimb200.h"
 
@@ -242,6 +243,8 @@ struct slim_ctx {
   double* panels = nullptr;
   int64_t panel_stride = 0;
   int D = D_DEFAULT;                 // batch size
+  int xsms = 0;                      // SLIM_XSMS: SMs of the x-chain partition (0 = shared)
+  SmPartition part;
   bool serial = false;               // debug (SLIM_SERIAL): factorizations wait for the x-chain
   int trsv_C = 0;                    // triangular-solve cluster size (0 = by T)
   std::vector<double*> Lbuf, Dinv, Linv;  // 2 D factor buffers (+ 8x8 and 64x64 diagonal inverses)
@@ -256,9 +259,11 @@ struct slim_ctx {
     int2* dev;
     int ntasks;
     double flops;  // algorithmic fp64 flops of the tiles the batch factors
+    double i8ops;  // int8 tensor ops of their updates (digit-pair products)
   };
   std::map<std::vector<SysShape>, TaskMap> maps;  // cached task maps by batch shape
   double chol_flops = 0.0;  // profiled factorizations: algorithmic flops
+  double chol_i8ops = 0.0;  // ... and int8 tensor ops of their tile updates
   int* tflags = nullptr;
   int* errflag = nullptr;
   double* rvec = nullptr;
@@ -352,10 +357,14 @@ static void free_all(slim_ctx* c) {
     if (rs->cnt) cudaFree(rs->cnt);
   }
   for (auto& kv : c->maps) cudaFree(kv.second.dev);
-  if (c->sf) cudaStreamDestroy(c->sf);
-  if (c->sx) cudaStreamDestroy(c->sx);
-  if (c->sg) cudaStreamDestroy(c->sg);
-  if (c->su) cudaStreamDestroy(c->su);
+  if (c->part.gx || c->part.gr) {
+    sm_partition_destroy(&c->part);  // owns the four streams
+  } else {
+    if (c->sf) cudaStreamDestroy(c->sf);
+    if (c->sx) cudaStreamDestroy(c->sx);
+    if (c->sg) cudaStreamDestroy(c->sg);
+    if (c->su) cudaStreamDestroy(c->su);
+  }
   for (int q = 0; q < NEV; ++q) {
     if (c->ev_u[q]) cudaEventDestroy(c->ev_u[q]);
     if (c->ev_g[q]) cudaEventDestroy(c->ev_g[q]);
@@ -429,10 +438,21 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
   // running batched factorization instead of waiting for its tail
   int prio_lo = 0, prio_hi = 0;
   CK(c, cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-  CK(c, cudaStreamCreateWithPriority(&c->sx, cudaStreamNonBlocking, prio_hi));
-  CK(c, cudaStreamCreateWithPriority(&c->sg, cudaStreamNonBlocking, prio_hi));
-  CK(c, cudaStreamCreateWithPriority(&c->sf, cudaStreamNonBlocking, prio_lo));
-  CK(c, cudaStreamCreateWithPriority(&c->su, cudaStreamNonBlocking, prio_hi));
+  c->xsms = getenv("SLIM_XSMS") ? atoi(getenv("SLIM_XSMS")) : 0;
+  if (c->xsms > 0) {
+    std::string err;
+    if (!sm_partition_create(c->dev, c->xsms, prio_hi, prio_lo, &c->part, err))
+      FAIL(c, SLIM_ECUDA, "%s", err.c_str());
+    c->sx = c->part.sx;
+    c->sg = c->part.sg;
+    c->sf = c->part.sf;
+    c->su = c->part.su;
+  } else {
+    CK(c, cudaStreamCreateWithPriority(&c->sx, cudaStreamNonBlocking, prio_hi));
+    CK(c, cudaStreamCreateWithPriority(&c->sg, cudaStreamNonBlocking, prio_hi));
+    CK(c, cudaStreamCreateWithPriority(&c->sf, cudaStreamNonBlocking, prio_lo));
+    CK(c, cudaStreamCreateWithPriority(&c->su, cudaStreamNonBlocking, prio_hi));
+  }
   {
     // systems per batched factorization: enough to overlap the per-column
     // critical paths of mid-size systems; large systems fill the GPU alone
@@ -1021,7 +1041,12 @@ int slim_set_timing_start(slim_ctx* c, int64_t k0) {
 }
 
 int slim_timing(slim_ctx* c, int32_t which, double* ms, int64_t* launches) {
-  if (!c || which < 0 || which > 5) FAIL(c, SLIM_EINVAL, "bad argument");
+  if (!c || which < 0 || which > 6) FAIL(c, SLIM_EINVAL, "bad argument");
+  if (which == 6) {  // int8 tensor ops of the profiled factorization launches
+    if (ms) *ms = chol_use_i8() ? c->chol_i8ops : 0.0;
+    if (launches) *launches = c->t_n[1];
+    return SLIM_OK;
+  }
   if (which == 5) {  // algorithmic flops of the profiled factorization launches
     if (ms) *ms = c->chol_flops;
     if (launches) *launches = c->t_n[1];
@@ -1264,17 +1289,23 @@ static const slim_ctx::TaskMap* task_map(slim_ctx* c, const std::vector<SysShape
   if (it != c->maps.end()) return &it->second;
   std::vector<int2> h = chol_task_map(sh.data(), (int)sh.size(), (int)(c->r + 1), (int)c->ell);
   const double t3 = (double)TB * TB * TB;
-  double flops = 0.0;
+  // int8 tensor-core path: 36 digit-pair products of 2 * 64^3 ops per 64x64x64
+  // tile update (k_chol_i8)
+  const double u8 = 36.0 * 2.0 * t3;
+  double flops = 0.0, i8ops = 0.0;
   for (const int2& e : h) {
     const int i = e.y >> 16, j = e.y & 0x7fff;
     if (i == j) {
       flops += t3 * j + t3 / 3.0;
-      if (j + 1 < sh[e.x].T) flops += 2.0 * t3 * j + t3;
+      i8ops += u8 * j;
+      if (j + 1 < sh[e.x].T) flops += 2.0 * t3 * j + t3, i8ops += u8 * j;
     } else {
-      flops += ((e.y & 0x8000) ? 2.0 : 1.0) * (2.0 * t3 * j + t3);  // dual: rows i, i + 1
+      const double rows = (e.y & 0x8000) ? 2.0 : 1.0;  // dual: rows i, i + 1
+      flops += rows * (2.0 * t3 * j + t3);
+      i8ops += rows * u8 * j;
     }
   }
-  slim_ctx::TaskMap tm{nullptr, (int)h.size(), flops};
+  slim_ctx::TaskMap tm{nullptr, (int)h.size(), flops, i8ops};
   if (h.empty()) h.push_back(make_int2(0, 0));
   if (cudaMalloc(&tm.dev, sizeof(int2) * h.size()) != cudaSuccess) return nullptr;
   cudaMemcpy(tm.dev, h.data(), sizeof(int2) * h.size(), cudaMemcpyHostToDevice);
@@ -1285,7 +1316,8 @@ static const slim_ctx::TaskMap* task_map(slim_ctx* c, const std::vector<SysShape
 // buffer set `set` (buffers set * D + b); tiles shared with step k0 - 1 come
 // from buffer `prev` (the previous batch's last system, -1 for none)
 static int enqueue_chol_batch(slim_ctx* c, const Window* Ws, int nb, int set, const double* alphas,
-                              int64_t k0, int64_t epoch0, int prev, double* flops = nullptr) {
+                              int64_t k0, int64_t epoch0, int prev, double* flops = nullptr,
+                              double* i8ops = nullptr) {
   CholParams P{};
   std::vector<SysShape> sh(nb);
   for (int b = 0; b < nb; ++b) {
@@ -1319,6 +1351,7 @@ static int enqueue_chol_batch(slim_ctx* c, const Window* Ws, int nb, int set, co
   P.map = tm->dev;
   P.ntasks = tm->ntasks;
   if (flops) *flops = tm->flops;
+  if (i8ops) *i8ops = tm->i8ops;
   P.ticket = c->tickets;
   P.error = c->errflag;
   P.panels = c->panels;
@@ -1343,8 +1376,8 @@ static int enqueue_chol_batch(slim_ctx* c, const Window* Ws, int nb, int set, co
     const int twant = getenv("SLIM_CHOL_TRACE_LAUNCH") ? atoi(getenv("SLIM_CHOL_TRACE_LAUNCH")) : 3;
     unsigned long long* dtr = nullptr;
     if (tpath && ++trace_count == twant) {
-      CK(c, cudaMalloc(&dtr, sizeof(unsigned long long) * 4 * (size_t)P.ntasks));
-      CK(c, cudaMemsetAsync(dtr, 0, sizeof(unsigned long long) * 4 * (size_t)P.ntasks, c->sf));
+      CK(c, cudaMalloc(&dtr, sizeof(unsigned long long) * 6 * (size_t)P.ntasks));
+      CK(c, cudaMemsetAsync(dtr, 0, sizeof(unsigned long long) * 6 * (size_t)P.ntasks, c->sf));
       P.trace = dtr;
     }
     launch_chol(P, c->sf);
@@ -1352,16 +1385,17 @@ static int enqueue_chol_batch(slim_ctx* c, const Window* Ws, int nb, int set, co
     CKLAUNCH(c);
     if (dtr) {
       CK(c, cudaStreamSynchronize(c->sf));
-      std::vector<unsigned long long> h(4 * (size_t)P.ntasks);
+      std::vector<unsigned long long> h(6 * (size_t)P.ntasks);
       std::vector<int2> hm(P.ntasks);
       CK(c, cudaMemcpy(h.data(), dtr, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost));
       CK(c, cudaMemcpy(hm.data(), P.map, sizeof(int2) * hm.size(), cudaMemcpyDeviceToHost));
       cudaFree(dtr);
       if (FILE* f = fopen(tpath, "w")) {
-        fprintf(f, "ticket,sys,i,j,t0,t1,t2,t3,T\n");
+        fprintf(f, "ticket,sys,i,j,t0,t1,t2,t3,T,dep_ns,ring_ns\n");
         for (int t = 0; t < P.ntasks; ++t)
-          fprintf(f, "%d,%d,%d,%d,%llu,%llu,%llu,%llu,%d\n", t, hm[t].x, hm[t].y >> 16, hm[t].y & 0xffff,
-                  h[4 * t], h[4 * t + 1], h[4 * t + 2], h[4 * t + 3], P.m[hm[t].x].T);
+          fprintf(f, "%d,%d,%d,%d,%llu,%llu,%llu,%llu,%d,%llu,%llu\n", t, hm[t].x, hm[t].y >> 16,
+                  hm[t].y & 0xffff, h[6 * t], h[6 * t + 1], h[6 * t + 2], h[6 * t + 3], P.m[hm[t].x].T,
+                  h[6 * t + 4], h[6 * t + 5]);
         fclose(f);
       }
     }
@@ -1408,6 +1442,7 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
   *c->pin_div = 0;
   for (int q = 0; q < 4; ++q) c->t_ms[q] = 0.0, c->t_n[q] = 0;
   c->chol_flops = 0.0;
+  c->chol_i8ops = 0.0;
   std::vector<ProfPair> pch, pgr, pxc;
   auto take = [](std::vector<ProfPair>& pool, std::vector<ProfPair>& used) {
     if (pool.empty()) used.push_back(make_pair());
@@ -1487,11 +1522,11 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
     ProfPair pc{};
     if (prof_b) pc = take(c->prof_chol, pch), cudaEventRecord(pc.a, c->sf);
     {
-      double fl = 0.0;
+      double fl = 0.0, i8 = 0.0;
       int rc = enqueue_chol_batch(c, Ws.data(), nb, set, alphas, kb0, epoch0,
-                                  B >= 1 ? (1 - set) * D + (D - 1) : -1, &fl);
+                                  B >= 1 ? (1 - set) * D + (D - 1) : -1, &fl, &i8);
       if (rc) return rc;
-      if (prof_b) c->chol_flops += fl;
+      if (prof_b) c->chol_flops += fl, c->chol_i8ops += i8;
     }
     if (prof_b) cudaEventRecord(pc.b, c->sf);
     CK(c, cudaEventRecord(c->ev_f[B % NEV], c->sf));

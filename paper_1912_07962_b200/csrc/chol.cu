@@ -245,6 +245,47 @@ __device__ void trsm_tile_warp(double* As, const double* Bs, const double* Dv, i
   }
 }
 
+// the same for two right-hand tiles X1, X2 at once: two independent DMMA
+// chains per warp
+__device__ void trsm_tile_warp2(double* A1, double* A2, const double* Bs, const double* Dv, int warp,
+                                int lane) {
+  const int rowA = (8 * warp + (lane >> 2)) * TS;
+  const int rowB = lane >> 2, colk = lane & 3;
+#pragma unroll 1
+  for (int q = 0; q < 8; ++q) {
+    double* c1 = A1 + rowA + 8 * q + 2 * colk;
+    double* c2 = A2 + rowA + 8 * q + 2 * colk;
+    double acc1[2] = {c1[0], c1[1]}, acc2[2] = {c2[0], c2[1]};
+    for (int p = 0; p < q; ++p) {
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        const double b = Bs[(8 * q + rowB) * TS + 8 * p + 4 * ks + colk];
+        dmma8x8x4(acc1, -A1[rowA + 8 * p + 4 * ks + colk], b);
+        dmma8x8x4(acc2, -A2[rowA + 8 * p + 4 * ks + colk], b);
+      }
+    }
+    __syncwarp();
+    c1[0] = acc1[0];
+    c1[1] = acc1[1];
+    c2[0] = acc2[0];
+    c2[1] = acc2[1];
+    __syncwarp();
+    double x1[2] = {0.0, 0.0}, x2[2] = {0.0, 0.0};
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const double b = Dv[q * 64 + rowB * 8 + 4 * ks + colk];
+      dmma8x8x4(x1, A1[rowA + 8 * q + 4 * ks + colk], b);
+      dmma8x8x4(x2, A2[rowA + 8 * q + 4 * ks + colk], b);
+    }
+    __syncwarp();
+    c1[0] = x1[0];
+    c1[1] = x1[1];
+    c2[0] = x2[0];
+    c2[1] = x2[1];
+    __syncwarp();
+  }
+}
+
 // ---------------------------------------------------------------------------
 // tile Cholesky kernel
 // ---------------------------------------------------------------------------
@@ -630,7 +671,7 @@ __global__ void __launch_bounds__(256, 2) k_chol_tiles(const __grid_constant__ C
   const int i = e.y >> 16, j = e.y & 0x7fff;
   const bool dual = (e.y & 0x8000) != 0;  // off-diagonal rows i and i + 1 of column j
   const int T = M.T;
-  unsigned long long* tr = (P.trace != nullptr && tid == 0) ? P.trace + 4 * (int64_t)s_task : nullptr;
+  unsigned long long* tr = (P.trace != nullptr && tid == 0) ? P.trace + 6 * (int64_t)s_task : nullptr;
   if (tr) tr[0] = globaltimer_ns();
   double accA[8][2], accB[8][2];
 
@@ -744,6 +785,9 @@ __global__ void __launch_bounds__(256, 2) k_chol_tiles(const __grid_constant__ C
 // [k half h][digit quad dq][row][4 digits x 32 k] so that one K = 32 MMA
 // step of a digit pair is one 32-byte column of a SWIZZLE_128B row.
 // ===========================================================================
+#ifndef SLIM_ACC_SLEEP_NS
+#define SLIM_ACC_SLEEP_NS 2000
+#endif
 namespace oz {
 constexpr int BOX = 64 * 128;            // 64 rows x 128 B
 constexpr int ST_A = 4 * BOX;            // [dq][row tile 0 / 1][64][128 B]
@@ -765,12 +809,28 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
+// A-operand collector: consecutive MMAs of one A digit read its slice from
+// shared memory once (fill), then reuse it (use / lastuse): 8 A reads per
+// stage instead of 36, which lifts the N = 64 shape off the shared-memory
+// bound (tools/microbench/i8_rates.cu)
+template <int COLL>  // 0 plain, 1 fill, 2 use, 3 lastuse
 __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t acc) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(acc)
-      : "memory");
+  if (COLL == 1)
+    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                 "tcgen05.mma.cta_group::1.kind::i8.collector::a::fill [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+                 "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(acc) : "memory");
+  else if (COLL == 2)
+    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                 "tcgen05.mma.cta_group::1.kind::i8.collector::a::use [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+                 "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(acc) : "memory");
+  else if (COLL == 3)
+    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                 "tcgen05.mma.cta_group::1.kind::i8.collector::a::lastuse [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+                 "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(acc) : "memory");
+  else
+    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                 "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+                 "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(acc) : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -795,12 +855,17 @@ __device__ __forceinline__ double pow2(int e) {  // exact 2^e, |e| < 1000
 }  // namespace oz
 
 // digit slices of the 64x64 fp64 tile X (smem, stride TS) with row
-// exponents rex[0..63] into the sliced tile Qt (global): thread = (row,
-// 16 consecutive k); v = L 2^(7 - e) lies in (-127.5, 127.5), and
-// d_a = rint(v), v <- (v - d_a) 128 is exact in fp64
-__device__ void slice_store(const double* X, const int* rex, int8_t* Qt, int tid) {
-  const int r = tid >> 2, kq = tid & 3, kh = kq >> 1, kk0 = (kq & 1) * 16;
-  const double sc = oz::pow2(7 - __ldcg(rex + r));
+// exponents rex[0..63]: thread = (row, 16 consecutive k); v = L 2^(7 - e)
+// lies in (-127.5, 127.5), and d_a = rint(v), v <- (v - d_a) 128 is exact
+struct Digits {
+  uint4 w[8];  // digit a of the thread's 16 entries, one byte each
+};
+__device__ __forceinline__ void slice_tile(const double* X, const int* rex, int tid, Digits& D) {
+  const int r = tid >> 2, kq = tid & 3;
+  // I = rint(L 2^(56 - e)) = rint(v 2^49): |I| < 127.5 2^49, exact in fp64 and
+  // int64; balanced base-128 digits peeled off from the bottom in integer
+  // arithmetic, the remaining top digit in [-127, 127]
+  const double sc = oz::pow2(56 - __ldcg(rex + r));
   uint32_t w[8][4];
 #pragma unroll
   for (int a = 0; a < 8; ++a)
@@ -808,54 +873,55 @@ __device__ void slice_store(const double* X, const int* rex, int8_t* Qt, int tid
     for (int q = 0; q < 4; ++q) w[a][q] = 0u;
 #pragma unroll
   for (int cc = 0; cc < 16; ++cc) {
-    double v = X[r * TS + 16 * kq + cc] * sc;
+    long long I = __double2ll_rn(X[r * TS + 16 * kq + cc] * sc);
 #pragma unroll
-    for (int a = 0; a < 8; ++a) {
-      const double d = rint(v);
-      v = (v - d) * 128.0;
-      w[a][cc >> 2] |= ((uint32_t)(int)d & 0xffu) << (8 * (cc & 3));
+    for (int a = 7; a >= 1; --a) {
+      const int d = (((int)I + 64) & 127) - 64;
+      I = (I - d) >> 7;
+      w[a][cc >> 2] |= ((uint32_t)d & 0xffu) << (8 * (cc & 3));
     }
+    w[0][cc >> 2] |= ((uint32_t)(int)I & 0xffu) << (8 * (cc & 3));
   }
 #pragma unroll
-  for (int a = 0; a < 8; ++a) {
-    const int dq = a >> 2, dd = a & 3;
-    uint4 u;
-    u.x = w[a][0];
-    u.y = w[a][1];
-    u.z = w[a][2];
-    u.w = w[a][3];
-    *reinterpret_cast<uint4*>(Qt + ((kh * 2 + dq) * 64 + r) * 128 + dd * 32 + kk0) = u;
-  }
+  for (int a = 0; a < 8; ++a) D.w[a] = make_uint4(w[a][0], w[a][1], w[a][2], w[a][3]);
+}
+// sliced tile layout: [k half][digit quad][row][4 digits x 32 k]
+__device__ __forceinline__ void store_digits(int8_t* Qt, const Digits& D, int tid) {
+  const int r = tid >> 2, kq = tid & 3, kh = kq >> 1, kk0 = (kq & 1) * 16;
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+    *reinterpret_cast<uint4*>(Qt + ((kh * 2 + (a >> 2)) * 64 + r) * 128 + (a & 3) * 32 + kk0) = D.w[a];
 }
 
 __device__ __forceinline__ int8_t* qtile(const CholMat& M, int i, int j) {
   return M.Q + tile_off(i, j) * 8;
 }
 
-// store tile (i, j) of system b (fp64 + digit slices) and publish it
-__device__ void store_publish_i8(const CholMat& M, int i, int j, const double* X, const double* Dv,
-                                 int tid) {
-  store_tile(M.L + tile_off(i, j), X, tid);
-  if (i != j) slice_store(X, M.rexp + i * TB, qtile(M, i, j), tid);  // diagonal tiles are never operands
-  if (Dv != nullptr) {
-    const double2 v = *reinterpret_cast<const double2*>(Dv + 2 * tid);
-    *reinterpret_cast<double2*>(M.Dinv + (int64_t)j * 512 + 2 * tid) = v;
+// Store tile (i, j) -- fp64, digit slices (off-diagonal tiles: the only
+// update operands) and, for a diagonal tile, its 8x8 inverses -- into system
+// b and every later system of the batch that shares it bit for bit, then
+// publish all copies behind one fence.
+__device__ void store_publish_i8(const CholParams& P, int b, int i, int j, const double* X,
+                                 const double* Dv, int tid) {
+  Digits D;
+  if (i != j) slice_tile(X, P.m[b].rexp + i * TB, tid, D);
+  int last = b;
+  for (int bb = b; bb < P.nb; ++bb) {
+    const CholMat& M2 = P.m[bb];
+    if (bb > b && tile_fresh(M2.full, M2.pnew, P.W, P.ell, i, j)) break;  // recomputed from here on
+    last = bb;
+    store_tile(M2.L + tile_off(i, j), X, tid);
+    if (i != j) store_digits(qtile(M2, i, j), D, tid);
+    if (Dv != nullptr) {
+      const double2 v = *reinterpret_cast<const double2*>(Dv + 2 * tid);
+      *reinterpret_cast<double2*>(M2.Dinv + (int64_t)j * 512 + 2 * tid) = v;
+    }
   }
   fence_proxy_async();  // consumers read the slices with TMA (async proxy)
   __syncthreads();
   if (tid == 0) {
     __threadfence();
-    st_release(M.flags + (i * (i + 1) / 2 + j), M.epoch);
-  }
-}
-
-// later systems of the batch that share tile (i, j) bit for bit
-__device__ void forward_tile_i8(const CholParams& P, int b, int i, int j, const double* X,
-                                const double* Dv, int tid) {
-  for (int bb = b + 1; bb < P.nb; ++bb) {
-    const CholMat& M2 = P.m[bb];
-    if (tile_fresh(M2.full, M2.pnew, P.W, P.ell, i, j)) break;  // recomputed from here on
-    store_publish_i8(M2, i, j, X, Dv, tid);
+    for (int bb = b; bb <= last; ++bb) st_release(P.m[bb].flags + (i * (i + 1) / 2 + j), P.m[bb].epoch);
   }
 }
 
@@ -897,7 +963,7 @@ __global__ void __launch_bounds__(256, 1) k_chol_i8(const __grid_constant__ Chol
   const int T = M.T;
   const bool two = pair ? (j + 1 < T) : ((e.y & 0x8000) != 0);
   const int ra = i;  // first output row tile (the diagonal for a pair task)
-  unsigned long long* tr = (P.trace != nullptr && tid == 0) ? P.trace + 4 * (int64_t)s_task : nullptr;
+  unsigned long long* tr = (P.trace != nullptr && tid == 0) ? P.trace + 6 * (int64_t)s_task : nullptr;
   if (tr) tr[0] = globaltimer_ns();
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
@@ -931,15 +997,20 @@ __global__ void __launch_bounds__(256, 1) k_chol_i8(const __grid_constant__ Chol
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
     fence_proxy_async();
     const uint32_t bytes = (two ? 4 : 2) * oz::BOX + (pair ? 0 : 2 * oz::BOX);
+    unsigned long long t_dep = 0, t_ring = 0;  // trace: producer stall time
     for (int u = 0; u < nchunk; ++u) {
       const int st = u % oz::NST;
+      const unsigned long long w0 = tr ? globaltimer_ns() : 0;
       bar_wait(&s_empty[st], ((u / oz::NST) & 1) ^ 1);
+      const unsigned long long w1 = tr ? globaltimer_ns() : 0;
+      t_ring += w1 - w0;
       const int k = u >> 1, kh = u & 1;
       if (kh == 0 && k >= kready) {
         wait_flag(fa + k, M.epoch);
         if (two) wait_flag(fa2 + k, M.epoch);
         if (!pair) wait_flag(fb + k, M.epoch);
         fence_proxy_async();
+        if (tr) t_dep += globaltimer_ns() - w1;
       }
       uint8_t* dst = stage + st * oz::STAGE;
       bar_expect(&s_full[st], bytes);
@@ -953,34 +1024,67 @@ __global__ void __launch_bounds__(256, 1) k_chol_i8(const __grid_constant__ Chol
         if (!pair) tma2d(dst + oz::ST_A + dq * oz::BOX, &M.qmap, &s_full[st], 0, yb + dq * 64);
       }
     }
+    if (tr) tr[4] = t_dep;
+    (void)t_ring;
   } else if (warp == 1 && lane == 0 && nchunk > 0) {
     // ---------------- MMA issuer ----------------
+    unsigned long long* trm = P.trace != nullptr ? P.trace + 6 * (int64_t)s_task : nullptr;
+    unsigned long long t_data = 0;  // trace: waiting for operand stages
     for (int u = 0; u < nchunk; ++u) {
       const int st = u % oz::NST;
+      const unsigned long long w0 = trm ? globaltimer_ns() : 0;
       bar_wait(&s_full[st], (u / oz::NST) & 1);
+      if (trm) t_data += globaltimer_ns() - w0;
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t a0 = su32(stage + st * oz::STAGE);
       const uint32_t b0 = pair ? a0 : a0 + oz::ST_A;
       const uint32_t bdq = pair ? 2 * oz::BOX : oz::BOX;
       const uint64_t ad = oz::sw128_desc(a0), bd = oz::sw128_desc(b0);
+      // grouped by A digit a (collector reuse); the a = 1 group touches every
+      // accumulator first, so only it may overwrite (first stage)
 #pragma unroll
-      for (int t = 0; t < 8; ++t)
+      for (int a = 1; a <= 8; ++a) {
+        const uint32_t aoff = ((a - 1) >> 2) * 2 * oz::BOX + ((a - 1) & 3) * 32;
 #pragma unroll
-        for (int a = 1; a <= t + 1; ++a) {
-          const int b = t + 2 - a;
-          const uint32_t aoff = ((a - 1) >> 2) * 2 * oz::BOX + ((a - 1) & 3) * 32;
+        for (int b = 1; b <= 9 - a; ++b) {
+          const int t = a + b - 2;
           const uint32_t boff = ((b - 1) >> 2) * bdq + ((b - 1) & 3) * 32;
-          oz::mma_i8(tmem + 64 * t, ad + (aoff >> 4), bd + (boff >> 4), (u > 0 || a > 1) ? 1u : 0u);
+          const uint32_t acc = (u > 0 || a > 1) ? 1u : 0u;
+          const uint64_t A = ad + (aoff >> 4), B = bd + (boff >> 4);
+          if (a == 8)
+            oz::mma_i8<0>(tmem + 64 * t, A, B, acc);
+          else if (b == 1)
+            oz::mma_i8<1>(tmem + 64 * t, A, B, acc);
+          else if (b == 9 - a)
+            oz::mma_i8<3>(tmem + 64 * t, A, B, acc);
+          else
+            oz::mma_i8<2>(tmem + 64 * t, A, B, acc);
         }
+      }
       oz::mma_commit(&s_empty[st]);
     }
     oz::mma_commit(&s_accf);
+    if (trm) trm[5] = t_data;
   }
   __syncwarp();
 
   // ---------------- combine: X = G - 2^(e_r + e_c - 14) sum_t 2^(-7t) P_t ----------------
   {
-    if (nchunk > 0) bar_wait(&s_accf, 0);
+    if (nchunk > 0) {
+      // idle warps poll with back-off: a tight try_wait loop of 250 threads
+      // competes with the tensor core for shared-memory bandwidth
+      const uint32_t a = su32(&s_accf);
+      uint32_t done = 0;
+      while (true) {
+        asm volatile("{\n.reg .pred P1;\nmbarrier.test_wait.parity.shared::cta.b64 P1, [%1], 0;\n"
+                     "selp.u32 %0, 1, 0, P1;\n}\n"
+                     : "=r"(done)
+                     : "r"(a)
+                     : "memory");
+        if (done) break;
+        __nanosleep(SLIM_ACC_SLEEP_NS);
+      }
+    }
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const int q = warp & 3, h = warp >> 2;
     const int R = 32 * q + lane, sel = R >> 6, r = R & 63;
@@ -1016,30 +1120,28 @@ __global__ void __launch_bounds__(256, 1) k_chol_i8(const __grid_constant__ Chol
   if (pair) {
     potrf_tile_blocked(X, Dv, rdiag, tid, P.error);
     if (tr) tr[2] = globaltimer_ns();
-    store_publish_i8(M, j, j, X, Dv, tid);
+    store_publish_i8(P, e.x, j, j, X, Dv, tid);
     if (two) {
       trsm_tile_warp(X2, X, Dv, warp, lane);
       __syncthreads();
-      store_publish_i8(M, j + 1, j, X2, nullptr, tid);
-      forward_tile_i8(P, e.x, j + 1, j, X2, nullptr, tid);
+      store_publish_i8(P, e.x, j + 1, j, X2, nullptr, tid);
     }
-    forward_tile_i8(P, e.x, j, j, X, Dv, tid);
   } else {
     if (tid == 0) wait_flag(M.flags + (j * (j + 1) / 2 + j), M.epoch);
-    if (tr) tr[2] = globaltimer_ns();
     __syncthreads();
     load_tile_async(Sg, M.L + tile_off(j, j), tid);
     load_dinv_async(Dv, M.Dinv + (int64_t)j * 512, tid);
     cp_async_commit();
     cp_async_wait_all();
     __syncthreads();
-    trsm_tile_warp(X, Sg, Dv, warp, lane);
-    if (two) trsm_tile_warp(X2, Sg, Dv, warp, lane);
+    if (two)
+      trsm_tile_warp2(X, X2, Sg, Dv, warp, lane);
+    else
+      trsm_tile_warp(X, Sg, Dv, warp, lane);
     __syncthreads();
-    store_publish_i8(M, ra, j, X, nullptr, tid);
-    if (two) store_publish_i8(M, ra + 1, j, X2, nullptr, tid);
-    forward_tile_i8(P, e.x, ra, j, X, nullptr, tid);
-    if (two) forward_tile_i8(P, e.x, ra + 1, j, X2, nullptr, tid);
+    if (tr) tr[2] = globaltimer_ns();  // wait + L_jj load + TRSM
+    store_publish_i8(P, e.x, ra, j, X, nullptr, tid);
+    if (two) store_publish_i8(P, e.x, ra + 1, j, X2, nullptr, tid);
   }
   if (tr) tr[3] = globaltimer_ns();
 }

@@ -211,6 +211,8 @@ def run(method: str, op: RowBlockOperator, sampler, schedule: Schedule, *, epoch
         timing["launches"] = cnt.value
         dop.call("slim_timing", 5, C.byref(ms), C.byref(cnt))
         timing["cholesky_flops"] = ms.value
+        dop.call("slim_timing", 6, C.byref(ms), C.byref(cnt))
+        timing["cholesky_i8ops"] = ms.value
     x_final = np.empty(x0.shape[0])
     dop.call("slim_get_x", _lib.dptr(x_final))
     if stream_state is not None:

@@ -24,6 +24,12 @@ METRICS = [
     "launch__grid_size",
     "launch__registers_per_thread",
     "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "sm__ops_path_tensor_op_utcimma_src_int8_sparsity_off.avg.pct_of_peak_sustained_elapsed",
+    "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active",
+    "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+    "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+    "lts__throughput.avg.pct_of_peak_sustained_elapsed",
 ]
 UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 
@@ -60,7 +66,8 @@ def main():
         print("stall samples by source line (tools/ncu_lines.py):")
         sys.stdout.flush()
         subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_lines.py"), rep, objs[-1],
-                        "_ZN4slim12k_chol_tilesENS_10CholParamsE"], env=dict(os.environ, TOP="15"))
+                        os.environ.get("KERNEL_SYM", "_ZN4slim9k_chol_i8ENS_10CholParamsE")],
+                       env=dict(os.environ, TOP="15"))
 
 
 main()
