@@ -252,7 +252,7 @@ struct slim_ctx {
   std::vector<CUtensorMap> Lmap;     // TMA views of the factor buffers
   std::vector<int*> cflags;
   std::vector<int8_t*> Qbuf;         // int8 digit slices of the factors (tensor-core updates)
-  std::vector<CUtensorMap> Qmap;
+  std::vector<CUtensorMap> QmapA, QmapB;
   std::vector<int*> rexp;            // row scale exponents per factor buffer
   int* tickets = nullptr;  // [0] chol ticket, [1] trsv ticket
   struct TaskMap {
@@ -506,7 +506,8 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
   c->Linv.assign(2 * c->D, nullptr);
   c->cflags.assign(2 * c->D, nullptr);
   c->Qbuf.assign(2 * c->D, nullptr);
-  c->Qmap.resize(2 * c->D);
+  c->QmapA.resize(2 * c->D);
+  c->QmapB.resize(2 * c->D);
   c->rexp.assign(2 * c->D, nullptr);
   {
     // one slab for all 2D factor buffers (one allocation, one memset)
@@ -515,7 +516,7 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
     const size_t ib = sizeof(double) * (size_t)c->Tmax * TB * TB;
     const size_t fb = ((sizeof(int) * (size_t)ntiles + 255) / 256) * 256;
     // int8 digit slices (same bytes as the fp64 tiles) + row exponents
-    const size_t qb = chol_use_i8() ? lb : 0;
+    const size_t qb = chol_use_i8() ? q_bytes(c->Tmax) : 0;
     const size_t eb = chol_use_i8() ? ((sizeof(int) * (size_t)c->Tmax * TB + 1023) / 1024) * 1024 : 0;
     const size_t per = lb + db + ib + qb + eb;
     ALLOC(c, c->factor_slab, (per + fb) * 2 * c->D);
@@ -531,7 +532,8 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
         FAIL(c, SLIM_ECUDA, "TMA descriptor for the factor buffer could not be encoded");
       c->Qbuf[q] = qb ? (int8_t*)(base + per * q + lb + db + ib) : nullptr;
       c->rexp[q] = eb ? (int*)(base + per * q + lb + db + ib + qb) : nullptr;
-      if (qb && !tma_map_q(&c->Qmap[q], c->Qbuf[q], ntiles))
+      if (qb && (!tma_map_q(&c->QmapA[q], c->Qbuf[q], c->Tmax, 128) ||
+                 !tma_map_q(&c->QmapB[q], c->Qbuf[q], c->Tmax, 64)))
         FAIL(c, SLIM_ECUDA, "TMA descriptor for the sliced factor buffer could not be encoded");
     }
   }
@@ -1331,7 +1333,9 @@ static int enqueue_chol_batch(slim_ctx* c, const Window* Ws, int nb, int set, co
     M.Linv = c->Linv[buf];
     M.flags = c->cflags[buf];
     M.Q = c->Qbuf[buf];
-    M.qmap = c->Qmap[buf];
+    M.qmapA = c->QmapA[buf];
+    M.qmapB = c->QmapB[buf];
+    M.qT = c->Tmax;
     M.rexp = c->rexp[buf];
     M.N = N;
     M.T = (N + TB - 1) / TB;
@@ -1776,7 +1780,7 @@ static int potrf_impl(int32_t device, const double* G, int64_t N, double* L_out,
       cudaMalloc(&dD, sizeof(double) * T * 512) != cudaSuccess ||
       cudaMalloc(&flags, sizeof(int) * ntiles) != cudaSuccess ||
       cudaMalloc(&ticket, sizeof(int)) != cudaSuccess || cudaMalloc(&err, sizeof(int)) != cudaSuccess ||
-      cudaMalloc(&dQ, (size_t)ntiles * TB * TB * 8) != cudaSuccess ||
+      cudaMalloc(&dQ, q_bytes(T)) != cudaSuccess ||
       cudaMalloc(&rx, sizeof(int) * T * TB) != cudaSuccess) {
     cleanup();
     FAIL((slim_ctx*)nullptr, SLIM_ENOMEM, "device allocation failed");
@@ -1790,7 +1794,8 @@ static int potrf_impl(int32_t device, const double* G, int64_t N, double* L_out,
     cleanup();
     FAIL((slim_ctx*)nullptr, SLIM_ECUDA, "TMA descriptor could not be encoded");
   }
-  if (chol_use_i8() && !tma_map_q(&P.m[0].qmap, dQ, ntiles)) {
+  P.m[0].qT = T;
+  if (chol_use_i8() && (!tma_map_q(&P.m[0].qmapA, dQ, T, 128) || !tma_map_q(&P.m[0].qmapB, dQ, T, 64))) {
     cleanup();
     FAIL((slim_ctx*)nullptr, SLIM_ECUDA, "TMA descriptor could not be encoded");
   }

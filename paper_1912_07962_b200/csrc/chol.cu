@@ -40,6 +40,12 @@ namespace slim {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+// byte offset of row r of digit block kd = (k half, digit) of sliced tile
+// (i, k): [k][k half][digit][tile row i < qT][64 rows][32 B]
+__host__ __device__ __forceinline__ int64_t q_off(int qT, int i, int k, int kd, int r) {
+  return ((((int64_t)k * 16 + kd) * qT + i) * 64 + r) * 32;
+}
+
 // per-CTA view of its system, in registers (indexing the kernel-parameter
 // array with the runtime system id would turn every field access into a
 // dynamically indexed constant load)
@@ -378,10 +384,11 @@ __global__ void __launch_bounds__(256) k_assemble(CholParams P) {
     const double2* src = reinterpret_cast<const double2*>(P.prevL + toff);
     double2* dst = reinterpret_cast<double2*>(Mp.L + toff);
     for (int e = tid; e < TB * TB / 2; e += 256) dst[e] = __ldcg(src + e);
-    if (Mp.Q != nullptr && P.prevQ != nullptr) {  // same byte count as the fp64 tile
-      const double2* qs = reinterpret_cast<const double2*>(P.prevQ + toff * 8);
-      double2* qd = reinterpret_cast<double2*>(Mp.Q + toff * 8);
-      for (int e = tid; e < TB * TB / 2; e += 256) qd[e] = __ldcg(qs + e);
+    if (Mp.Q != nullptr && P.prevQ != nullptr && I != J) {  // 16 (k half, digit) blocks of 2 KB
+      for (int e = tid; e < 16 * 128; e += 256) {
+        const int64_t off = q_off(Mp.qT, I, J, e >> 7, 0) + (int64_t)(e & 127) * 16;
+        *reinterpret_cast<uint4*>(Mp.Q + off) = __ldcg(reinterpret_cast<const uint4*>(P.prevQ + off));
+      }
     }
     if (I == J)
       for (int e = tid; e < 512; e += 256) Mp.Dinv[(int64_t)J * 512 + e] = __ldcg(P.prevDinv + (int64_t)J * 512 + e);
@@ -464,6 +471,13 @@ __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* map, uint64_
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4}], [%2];" ::"r"(su32(dst)),
       "l"(map), "r"(su32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void tma3d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(su32(dst)),
+      "l"(map), "r"(su32(bar)), "r"(x), "r"(y), "r"(z)
       : "memory");
 }
 // generic-proxy writes of other CTAs (acquired through a flag) made visible
@@ -789,9 +803,10 @@ __global__ void __launch_bounds__(256, 2) k_chol_tiles(const __grid_constant__ C
 #define SLIM_ACC_SLEEP_NS 2000
 #endif
 namespace oz {
-constexpr int BOX = 64 * 128;            // 64 rows x 128 B
-constexpr int ST_A = 4 * BOX;            // [dq][row tile 0 / 1][64][128 B]
-constexpr int ST_B = 2 * BOX;            // [dq][64][128 B]
+constexpr int DIG_A = 128 * 32;          // one digit of the A operand: 128 rows x 32 B
+constexpr int DIG_B = 64 * 32;           // one digit of B: 64 rows x 32 B
+constexpr int ST_A = 8 * DIG_A;          // [digit][rows of tiles i, i + 1][32 B]
+constexpr int ST_B = 8 * DIG_B;          // [digit][64 rows][32 B]
 constexpr int STAGE = ST_A + ST_B;       // 48 KB: one k half of three tiles
 constexpr int NST = 4;
 constexpr int SMEM = NST * STAGE + 1024;
@@ -801,36 +816,37 @@ constexpr int W_SG = W_X + 2 * TB * TS * 8;          // L_jj, 64 x TS fp64
 constexpr int W_DV = W_SG + TB * TS * 8;             // 8x8 inverses (512)
 constexpr int W_RD = W_DV + 512 * 8;                 // 64 reciprocal pivots
 static_assert(W_RD + 64 * 8 <= NST * STAGE, "work tiles must fit over the stage ring");
-constexpr uint32_t IDESC = (2u << 4) |               // D format S32
-                           (1u << 7) | (1u << 10) |  // A, B signed 8-bit
-                           ((uint32_t)(TB >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+// kind::i8, S32 accumulate, signed A and B, M = 128, N = 64 n
+__host__ __device__ constexpr uint32_t idesc(int n) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(8 * n) << 17) | ((uint32_t)(128 >> 4) << 24);
 }
-// A-operand collector: consecutive MMAs of one A digit read its slice from
-// shared memory once (fill), then reuse it (use / lastuse): 8 A reads per
-// stage instead of 36, which lifts the N = 64 shape off the shared-memory
-// bound (tools/microbench/i8_rates.cu)
-template <int COLL>  // 0 plain, 1 fill, 2 use, 3 lastuse
-__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t acc) {
+
+// K-major SWIZZLE_32B operand: rows of 32 B (K = 32 int8), 8-row groups 256 B apart
+__device__ __forceinline__ uint64_t sw32_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(256 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)6 << 61);
+}
+// One MMA per (A digit a, run of up to four B digits b0 .. b0 + n - 1): the
+// B digits are stacked along N (64 rows each), and D starts at accumulator
+// t = a + b0 - 2, so the product with B digit b lands in TMEM column block
+// a + b - 2 -- its own accumulator.  12 MMAs (N up to 256) per stage instead
+// of 36 with N = 64 (which cap at 2/3 of the tensor peak); the two MMAs of
+// one A digit share it through the A-operand collector.
+template <int COLL>  // 0 plain, 1 fill, 3 lastuse
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idsc,
+                                       uint32_t acc) {
   if (COLL == 1)
     asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
                  "tcgen05.mma.cta_group::1.kind::i8.collector::a::fill [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-                 "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(acc) : "memory");
-  else if (COLL == 2)
-    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                 "tcgen05.mma.cta_group::1.kind::i8.collector::a::use [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-                 "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(acc) : "memory");
+                 "l"(adesc), "l"(bdesc), "r"(idsc), "r"(acc) : "memory");
   else if (COLL == 3)
     asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
                  "tcgen05.mma.cta_group::1.kind::i8.collector::a::lastuse [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-                 "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(acc) : "memory");
+                 "l"(adesc), "l"(bdesc), "r"(idsc), "r"(acc) : "memory");
   else
     asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
                  "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-                 "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(acc) : "memory");
+                 "l"(adesc), "l"(bdesc), "r"(idsc), "r"(acc) : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -885,16 +901,12 @@ __device__ __forceinline__ void slice_tile(const double* X, const int* rex, int 
 #pragma unroll
   for (int a = 0; a < 8; ++a) D.w[a] = make_uint4(w[a][0], w[a][1], w[a][2], w[a][3]);
 }
-// sliced tile layout: [k half][digit quad][row][4 digits x 32 k]
-__device__ __forceinline__ void store_digits(int8_t* Qt, const Digits& D, int tid) {
+// digit a of the thread's 16 entries (row r, k = 16 kq ..) into sliced tile (i, k)
+__device__ __forceinline__ void store_digits(const CholMat& M, int i, int k, const Digits& D, int tid) {
   const int r = tid >> 2, kq = tid & 3, kh = kq >> 1, kk0 = (kq & 1) * 16;
 #pragma unroll
   for (int a = 0; a < 8; ++a)
-    *reinterpret_cast<uint4*>(Qt + ((kh * 2 + (a >> 2)) * 64 + r) * 128 + (a & 3) * 32 + kk0) = D.w[a];
-}
-
-__device__ __forceinline__ int8_t* qtile(const CholMat& M, int i, int j) {
-  return M.Q + tile_off(i, j) * 8;
+    *reinterpret_cast<uint4*>(M.Q + q_off(M.qT, i, k, kh * 8 + a, r) + kk0) = D.w[a];
 }
 
 // Store tile (i, j) -- fp64, digit slices (off-diagonal tiles: the only
@@ -911,7 +923,7 @@ __device__ void store_publish_i8(const CholParams& P, int b, int i, int j, const
     if (bb > b && tile_fresh(M2.full, M2.pnew, P.W, P.ell, i, j)) break;  // recomputed from here on
     last = bb;
     store_tile(M2.L + tile_off(i, j), X, tid);
-    if (i != j) store_digits(qtile(M2, i, j), D, tid);
+    if (i != j) store_digits(M2, i, j, D, tid);
     if (Dv != nullptr) {
       const double2 v = *reinterpret_cast<const double2*>(Dv + 2 * tid);
       *reinterpret_cast<double2*>(M2.Dinv + (int64_t)j * 512 + 2 * tid) = v;
@@ -971,7 +983,10 @@ __global__ void __launch_bounds__(256, 1) k_chol_i8(const __grid_constant__ Chol
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid < TB) s_ecol[tid] = __ldcg(M.rexp + j * TB + tid);
-  if (tid == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(&M.qmap) : "memory");
+  if (tid == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&M.qmapA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&M.qmapB) : "memory");
+  }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -996,7 +1011,6 @@ __global__ void __launch_bounds__(256, 1) k_chol_i8(const __grid_constant__ Chol
     }
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
     fence_proxy_async();
-    const uint32_t bytes = (two ? 4 : 2) * oz::BOX + (pair ? 0 : 2 * oz::BOX);
     unsigned long long t_dep = 0, t_ring = 0;  // trace: producer stall time
     for (int u = 0; u < nchunk; ++u) {
       const int st = u % oz::NST;
@@ -1013,16 +1027,11 @@ __global__ void __launch_bounds__(256, 1) k_chol_i8(const __grid_constant__ Chol
         if (tr) t_dep += globaltimer_ns() - w1;
       }
       uint8_t* dst = stage + st * oz::STAGE;
-      bar_expect(&s_full[st], bytes);
-      const int ya = (ra * (ra + 1) / 2 + k) * 256 + kh * 128;
-      const int ya2 = ((ra + 1) * (ra + 2) / 2 + k) * 256 + kh * 128;
-      const int yb = (j * (j + 1) / 2 + k) * 256 + kh * 128;
-#pragma unroll
-      for (int dq = 0; dq < 2; ++dq) {
-        tma2d(dst + dq * 2 * oz::BOX, &M.qmap, &s_full[st], 0, ya + dq * 64);
-        if (two) tma2d(dst + dq * 2 * oz::BOX + oz::BOX, &M.qmap, &s_full[st], 0, ya2 + dq * 64);
-        if (!pair) tma2d(dst + oz::ST_A + dq * oz::BOX, &M.qmap, &s_full[st], 0, yb + dq * 64);
-      }
+      bar_expect(&s_full[st], oz::STAGE);
+      // A: tile rows ra, ra + 1, all 8 digits (a single task's spare row is
+      // loaded and ignored); B: tile row j
+      tma3d(dst, &M.qmapA, &s_full[st], 0, ra * TB, (k * 2 + kh) * 8);
+      tma3d(dst + oz::ST_A, &M.qmapB, &s_full[st], 0, j * TB, (k * 2 + kh) * 8);
     }
     if (tr) tr[4] = t_dep;
     (void)t_ring;
@@ -1037,28 +1046,24 @@ __global__ void __launch_bounds__(256, 1) k_chol_i8(const __grid_constant__ Chol
       if (trm) t_data += globaltimer_ns() - w0;
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t a0 = su32(stage + st * oz::STAGE);
-      const uint32_t b0 = pair ? a0 : a0 + oz::ST_A;
-      const uint32_t bdq = pair ? 2 * oz::BOX : oz::BOX;
-      const uint64_t ad = oz::sw128_desc(a0), bd = oz::sw128_desc(b0);
-      // grouped by A digit a (collector reuse); the a = 1 group touches every
-      // accumulator first, so only it may overwrite (first stage)
+      const uint64_t ad = oz::sw32_desc(a0), bd = oz::sw32_desc(a0 + oz::ST_A);
+      // accumulators are first touched by the a = 1 MMAs: only they may
+      // overwrite (first stage)
 #pragma unroll
       for (int a = 1; a <= 8; ++a) {
-        const uint32_t aoff = ((a - 1) >> 2) * 2 * oz::BOX + ((a - 1) & 3) * 32;
+        const uint64_t A = ad + (((a - 1) * oz::DIG_A) >> 4);
 #pragma unroll
-        for (int b = 1; b <= 9 - a; ++b) {
-          const int t = a + b - 2;
-          const uint32_t boff = ((b - 1) >> 2) * bdq + ((b - 1) & 3) * 32;
+        for (int b0 = 1; b0 <= 9 - a; b0 += 4) {
+          const int n = (10 - a - b0) < 4 ? (10 - a - b0) : 4;
+          const uint64_t B = bd + (((b0 - 1) * oz::DIG_B) >> 4);
           const uint32_t acc = (u > 0 || a > 1) ? 1u : 0u;
-          const uint64_t A = ad + (aoff >> 4), B = bd + (boff >> 4);
-          if (a == 8)
-            oz::mma_i8<0>(tmem + 64 * t, A, B, acc);
-          else if (b == 1)
-            oz::mma_i8<1>(tmem + 64 * t, A, B, acc);
-          else if (b == 9 - a)
-            oz::mma_i8<3>(tmem + 64 * t, A, B, acc);
+          const uint32_t d = tmem + 64 * (a + b0 - 2);
+          if (a > 4)
+            oz::mma_i8<0>(d, A, B, oz::idesc(n), acc);
+          else if (b0 == 1)
+            oz::mma_i8<1>(d, A, B, oz::idesc(n), acc);
           else
-            oz::mma_i8<2>(tmem + 64 * t, A, B, acc);
+            oz::mma_i8<3>(d, A, B, oz::idesc(n), acc);
         }
       }
       oz::mma_commit(&s_empty[st]);

@@ -279,15 +279,17 @@ bool tma_map_f64_sw128(CUtensorMap* m, const double* base, int64_t rows, int64_t
   return r == CUDA_SUCCESS;
 }
 
-bool tma_map_q(CUtensorMap* m, const int8_t* base, int64_t ntiles) {
+bool tma_map_q(CUtensorMap* m, const int8_t* base, int qT, int box_rows) {
   auto enc = get_encode();
   if (!enc) return false;
-  cuuint64_t dims[2] = {128, (cuuint64_t)ntiles * 256};
-  cuuint64_t strides[1] = {128};
-  cuuint32_t box[2] = {128, 64};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)base, dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+  // dim0: 32 B of one digit (K = 32 int8), dim1: rows over all tile rows of a
+  // column (qT * 64), dim2: (column, k half, digit) blocks
+  cuuint64_t dims[3] = {32, (cuuint64_t)qT * 64, (cuuint64_t)qT * 16};
+  cuuint64_t strides[2] = {32, (cuuint64_t)qT * 64 * 32};
+  cuuint32_t box[3] = {32, (cuuint32_t)box_rows, 8};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)base, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }

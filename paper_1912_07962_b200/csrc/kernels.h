@@ -28,11 +28,13 @@ struct CholMat {
   double* L;            // lower tiles, tile_off(i, j)
   double* Dinv;         // T x 512: inverses of the 8x8 diagonal blocks of L_jj
   double* Linv;         // T x 4096: inverses of the diagonal tiles (k_diag_inv)
-  // int8 digit slices of L for the tensor-core updates (chol.cu, k_chol_i8):
-  // tile t at Q + t * 32 KB, [k half][digit quad][row][4 digits x 32 k];
-  // qmap views them as (tiles * 256) rows of 128 B, box 64 rows, SW128
+  // int8 digit slices of L for the tensor-core updates (chol.cu, k_chol_i8),
+  // by tile column: [k][k half][digit][tile row i < qT][64 rows][32 B], so the
+  // A operand of a task (tile rows i, i + 1, all 8 digits) is one 3D TMA box;
+  // qmapA boxes 128 rows x 8 digits, qmapB 64 rows x 8 digits (SWIZZLE_32B)
   int8_t* Q;
-  CUtensorMap qmap;
+  CUtensorMap qmapA, qmapB;
+  int qT;               // tile rows per column in Q (the buffer's Tmax)
   int* rexp;            // T * 64: row scale exponents, 2^rexp >= sqrt(G_rr)
   int* flags;           // T (T + 1) / 2 epoch flags
   int N, T, nw, epoch;
@@ -138,7 +140,10 @@ size_t chol_smem_bytes();
 bool chol_use_i8();
 // int8 updates: |P_t| <= (2 * 127 * 64 + 6 * 64^2) * 64 T < 2^31
 constexpr int CHOL_I8_TMAX = 800;
-// TMA view of a sliced factor buffer (tiles * 256 rows x 128 B, box 64 rows)
-bool tma_map_q(CUtensorMap* m, const int8_t* base, int64_t ntiles);
+// TMA views of a sliced factor buffer with qT tile rows per column (box
+// rows = 128 for the A operand, 64 for B; 8 digits per box)
+bool tma_map_q(CUtensorMap* m, const int8_t* base, int qT, int box_rows);
+// bytes of a sliced factor buffer
+inline size_t q_bytes(int qT) { return (size_t)qT * qT * 32768; }
 
 }  // namespace slim

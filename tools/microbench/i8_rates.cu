@@ -335,6 +335,114 @@ void run_pipe(int sms, size_t buf_mb) {
   cudaFree(buf);
 }
 
+// K-major SWIZZLE_32B descriptor: rows of 32 B (one K = 32 int8 chunk), 8-row
+// core groups 256 B apart
+__device__ __forceinline__ uint64_t sw32_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(256 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)6 << 61);
+}
+__device__ __forceinline__ constexpr uint32_t idesc_n(int n) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+// Digit-stacked stage: A [digit][128 rows][32 B] (32 KB), B [digit][64 rows][32 B]
+// (16 KB); per A digit a, ONE MMA against B digits b0..b0+n-1 stacked along N
+// (N = 64 n <= 256) writes their products straight into accumulators
+// t = a + b0 - 2 .. (D column offset 64 t): 12 MMAs per stage instead of 36.
+// STACK=false: the same SW32 layout with the 36 N=64 MMAs (layout control).
+template <bool STACK, bool RING>
+__global__ void __launch_bounds__(128, 1) stacked_pattern(int* out, int iters) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
+  __shared__ uint32_t s_tmem;
+  __shared__ __align__(8) uint64_t bar, ring[4];
+  for (int i = threadIdx.x; i < 4 * 49152 / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(sm)[i] = make_uint4(0x01fe03fdu * (i + 1), 0x7f80017fu ^ i, 0x11223344u + i, 0x55667788u - i);
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        (uint32_t)__cvta_generic_to_shared(&s_tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&bar)));
+    for (int q = 0; q < 4; ++q)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&ring[q])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = s_tmem;
+  if (threadIdx.x == 0) {
+    for (int it = 0; it < iters; ++it) {
+      if (RING && it >= 4)
+        asm volatile("{\n.reg .pred P1;\nW4:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n@!P1 bra W4;\n}\n" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(&ring[it & 3])), "r"(((it >> 2) - 1) & 1)
+                     : "memory");
+      const uint32_t a0 = (uint32_t)__cvta_generic_to_shared(sm + (it & 3) * 49152);
+      const uint64_t ad = sw32_desc(a0), bd = sw32_desc(a0 + 32768);
+#define SMMA(N, T, AO, BO)                                                                           \
+  asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"                                         \
+               "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + 64 * (T)), \
+               "l"(ad + ((AO) >> 4)), "l"(bd + ((BO) >> 4)), "r"(idesc_n(N)), "r"(1u)             \
+               : "memory")
+      if (STACK) {
+#pragma unroll
+        for (int a = 1; a <= 8; ++a)
+#pragma unroll
+          for (int b0 = 1; b0 <= 9 - a; b0 += 4) {
+            const int n = (9 - a - b0 + 1) < 4 ? (9 - a - b0 + 1) : 4;
+            SMMA(64 * n, a + b0 - 2, (a - 1) * 4096, (b0 - 1) * 2048);
+          }
+      } else {
+#pragma unroll
+        for (int a = 1; a <= 8; ++a)
+#pragma unroll
+          for (int b = 1; b <= 9 - a; ++b) SMMA(64, a + b - 2, (a - 1) * 4096, (b - 1) * 2048);
+      }
+#undef SMMA
+      if (RING)
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(&ring[it & 3])) : "memory");
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+        (uint32_t)__cvta_generic_to_shared(&bar)) : "memory");
+    asm volatile("{\n.reg .pred P1;\nW5:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n@!P1 bra W5;\n}\n" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&bar)) : "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  if (threadIdx.x == 0 && iters < 0) out[0] = 1;
+}
+
+template <bool STACK, bool RING>
+void run_stacked(int sms) {
+  const int iters = 4000;
+  const size_t smem = 4 * 49152 + 1024;
+  cudaFuncSetAttribute(stacked_pattern<STACK, RING>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int* d;
+  cudaMalloc(&d, 4);
+  stacked_pattern<STACK, RING><<<sms, 128, smem>>>(d, 10);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  float best = 1e30f;
+  for (int rep = 0; rep < 5; ++rep) {
+    cudaEventRecord(a);
+    stacked_pattern<STACK, RING><<<sms, 128, smem>>>(d, iters);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    if (ms < best) best = ms;
+  }
+  const double ops = 2.0 * 128 * 64 * 32 * 36.0 * iters * sms;
+  printf("SW32 digit layout, %s%s: %8.1f TOPS (digit-pair ops), %.3f us per k-tile  %s\n",
+         STACK ? "12 digit-stacked MMAs (N up to 256)" : "36 N=64 MMAs", RING ? ", ring commit/wait" : "",
+         ops / best / 1e9, best * 1e3 / iters * 2, cudaGetErrorString(cudaGetLastError()));
+}
+
 template <int N, bool REUSE = false>
 void run(int sms) {
   const int iters = 20000;
@@ -384,5 +492,9 @@ int main() {
   run_pipe<2, true, true>(sms, 48);
   run_pipe<2>(sms, 4096);
   run_pipe<3>(sms, 48);
+  run_stacked<false, false>(sms);
+  run_stacked<true, false>(sms);
+  run_stacked<false, true>(sms);
+  run_stacked<true, true>(sms);
   return 0;
 }
