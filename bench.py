@@ -405,7 +405,7 @@ def run_ours(args, world, rank, local, dist):
                            epochs=total / M, r=r, references={"x_true": xt}, record_every=1,
                            device=dev)
             walls.append(time.perf_counter() - t0)
-            if len(walls) == 3 or sum(walls) > 2.0:
+            if len(walls) == 5 or sum(walls) > 2.0:
                 break
             op2 = op2.with_rhs(op2.rhs)  # same arrays, no cached device state
         wall = float(np.median(walls))
