@@ -19,6 +19,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <condition_variable>
 #include <mutex>
 #include <cmath>
@@ -28,6 +29,7 @@
 #include <chrono>
 #include <map>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "gram_tc.h"
@@ -786,6 +788,103 @@ static int size_streamed_csr(slim_ctx* c) {
 // copy the not-yet-resident blocks among blks[0..cnt) (0-based row blocks)
 // to HBM on stream su (and build their CSC); pageable host memory, so the
 // host thread pays the copy while the device works on earlier batches
+// Process-wide pinned staging ring for streamed uploads: the worker copies a
+// block into a pinned slot on the host (no driver lock held) and the DMA from
+// the slot is truly asynchronous; a slot is reused once its copy completed.
+// Allocated once per process (like a caching host allocator).
+struct PinRing {
+  static constexpr size_t SLOT = 4u << 20;
+  static constexpr int NSLOT = 8;
+  char* buf = nullptr;
+  cudaEvent_t ev[NSLOT] = {};
+  bool used[NSLOT] = {};
+  int next = 0;
+  std::mutex m;
+  bool ok = false;
+  bool init() {  // under m
+    if (buf) return ok;
+    if (cudaMallocHost(&buf, SLOT * NSLOT) != cudaSuccess) {
+      buf = reinterpret_cast<char*>(1);
+      return ok = false;
+    }
+    for (int q = 0; q < NSLOT; ++q)
+      if (cudaEventCreateWithFlags(&ev[q], cudaEventDisableTiming) != cudaSuccess) return ok = false;
+    return ok = true;
+  }
+};
+static PinRing g_pin;
+
+// host -> device copy of `bytes` through the pinned ring (pageable fallback)
+static cudaError_t staged_copy(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_pin.m);
+  if (!g_pin.init()) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
+  const char* sp = static_cast<const char*>(src);
+  char* dp = static_cast<char*>(dst);
+  while (bytes > 0) {
+    const size_t n = std::min(bytes, PinRing::SLOT);
+    const int q = g_pin.next;
+    g_pin.next = (q + 1) % PinRing::NSLOT;
+    if (g_pin.used[q]) {
+      cudaError_t e = cudaEventSynchronize(g_pin.ev[q]);
+      if (e != cudaSuccess) return e;
+    }
+    char* slot = g_pin.buf + (size_t)q * PinRing::SLOT;
+    memcpy(slot, sp, n);
+    cudaError_t e = cudaMemcpyAsync(dp, slot, n, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaEventRecord(g_pin.ev[q], s)) != cudaSuccess) return e;
+    g_pin.used[q] = true;
+    sp += n, dp += n, bytes -= n;
+  }
+  return cudaSuccess;
+}
+
+// copy one row block (0-based) to HBM on su (+ its CSC build); thread-safe
+// with respect to the context's error string (the message goes to err)
+static int copy_block(slim_ctx* c, int64_t bk, std::string& err, int64_t* launches, bool build_csc = true) {
+  char msg[160];
+  if (c->layout == SLIM_DENSE_ROWMAJOR) {
+    const size_t rb = (size_t)c->ell * c->n * c->vsize;
+    if (staged_copy((char*)c->A + bk * rb, c->hs_dense + bk * rb, rb, c->su) != cudaSuccess) {
+      err = "block upload failed";
+      return SLIM_ECUDA;
+    }
+    return SLIM_OK;
+  }
+  const int64_t* r = c->hs_rowptr[bk];
+  const int64_t nb = r[c->ell] - r[0], base = c->h_blkbase[bk];
+  const int32_t* col = c->hs_col[bk] + r[0];
+  for (int64_t e = 0; e < nb; ++e)
+    if (col[e] < 0 || col[e] >= c->n) {
+      snprintf(msg, sizeof msg, "column index %d out of range in block %lld", col[e], (long long)bk + 1);
+      err = msg;
+      return SLIM_EINVAL;
+    }
+  if (nb > 0) {
+    if (staged_copy(c->col + base, col, sizeof(int) * nb, c->su) != cudaSuccess ||
+        staged_copy((char*)c->val + c->vsize * base, c->hs_val[bk] + c->vsize * r[0], c->vsize * nb, c->su) !=
+            cudaSuccess) {
+      err = "block upload failed";
+      return SLIM_ECUDA;
+    }
+  }
+  if (!build_csc) return SLIM_OK;  // the caller builds a whole batch's CSC at once
+  if (c->vdt == SLIM_F64)
+    launch_build_csc<double>(c->colptr, c->cscrow, (double*)c->cscval, c->rowptr, c->col,
+                             (const double*)c->val, c->blkbase, c->m, (int)c->ell, (int)c->n, c->M,
+                             c->su, bk, 1);
+  else
+    launch_build_csc<float>(c->colptr, c->cscrow, (float*)c->cscval, c->rowptr, c->col,
+                            (const float*)c->val, c->blkbase, c->m, (int)c->ell, (int)c->n, c->M,
+                            c->su, bk, 1);
+  if (cudaGetLastError() != cudaSuccess) {
+    err = "CSC build launch failed";
+    return SLIM_ECUDA;
+  }
+  *launches += 5;
+  return SLIM_OK;
+}
+
 static int ensure_blocks(slim_ctx* c, const int64_t* blks, int cnt, int* copied = nullptr) {
   if (copied) *copied = 0;
   if (!c->streaming || c->resident.empty()) return SLIM_OK;
@@ -793,32 +892,9 @@ static int ensure_blocks(slim_ctx* c, const int64_t* blks, int cnt, int* copied 
     const int64_t bk = blks[q];
     if (c->resident[bk]) continue;
     if (copied) ++*copied;
-    if (c->layout == SLIM_DENSE_ROWMAJOR) {
-      const size_t rb = (size_t)c->ell * c->n * c->vsize;
-      CK(c, cudaMemcpyAsync((char*)c->A + bk * rb, c->hs_dense + bk * rb, rb, cudaMemcpyHostToDevice, c->su));
-    } else {
-      const int64_t* r = c->hs_rowptr[bk];
-      const int64_t nb = r[c->ell] - r[0], base = c->h_blkbase[bk];
-      const int32_t* col = c->hs_col[bk] + r[0];
-      for (int64_t e = 0; e < nb; ++e)
-        if (col[e] < 0 || col[e] >= c->n)
-          FAIL(c, SLIM_EINVAL, "column index %d out of range in block %lld", col[e], (long long)bk + 1);
-      if (nb > 0) {
-        CK(c, cudaMemcpyAsync(c->col + base, col, sizeof(int) * nb, cudaMemcpyHostToDevice, c->su));
-        CK(c, cudaMemcpyAsync((char*)c->val + c->vsize * base, c->hs_val[bk] + c->vsize * r[0],
-                              c->vsize * nb, cudaMemcpyHostToDevice, c->su));
-      }
-      if (c->vdt == SLIM_F64)
-        launch_build_csc<double>(c->colptr, c->cscrow, (double*)c->cscval, c->rowptr, c->col,
-                                 (const double*)c->val, c->blkbase, c->m, (int)c->ell, (int)c->n,
-                                 c->M, c->su, bk, 1);
-      else
-        launch_build_csc<float>(c->colptr, c->cscrow, (float*)c->cscval, c->rowptr, c->col,
-                                (const float*)c->val, c->blkbase, c->m, (int)c->ell, (int)c->n,
-                                c->M, c->su, bk, 1);
-      CKLAUNCH(c);
-      c->launches += 5;
-    }
+    std::string err;
+    const int rc = copy_block(c, bk, err, &c->launches);
+    if (rc) FAIL(c, rc, "%s", err.c_str());
     c->resident[bk] = 1;
   }
   return SLIM_OK;
@@ -1410,6 +1486,26 @@ static int enqueue_chol_batch(slim_ctx* c, const Window* Ws, int nb, int set, co
   return SLIM_OK;
 }
 
+// worker-thread state of a streamed run (joined on every exit path)
+struct Uploader {
+  bool active = false;
+  std::thread th;
+  std::vector<std::vector<int64_t>> blocks;  // per batch: first-use blocks
+  std::vector<cudaEvent_t> ev;               // per batch: copies enqueued (nullptr: none)
+  std::atomic<int64_t> done{0};              // batches whose uploads are enqueued
+  int rc = SLIM_OK;
+  std::string msg;
+  int64_t launches = 0;
+  void join() {
+    if (th.joinable()) th.join();
+  }
+  ~Uploader() {
+    join();
+    for (cudaEvent_t e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+};
+
 extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, int64_t K,
                         int64_t record_every, double* hist, int64_t* n_rows, int32_t* status,
                         int64_t* diverged_at, double* iterates) {
@@ -1473,6 +1569,59 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
   std::vector<Window> Ws(D);
   const int64_t nbatch = (K + D - 1) / D;
   bool stop = false;
+  // ---- host streaming: the index trace is known up front, so one worker
+  // thread issues every first-use block upload of the run (host->HBM copy +
+  // CSC build on su), batch by batch, while this thread enqueues the
+  // pipeline; pageable copies no longer stall the enqueue of device work
+  Uploader up;
+  if (c->streaming && !c->resident.empty()) {
+    up.blocks.resize(nbatch);
+    up.ev.assign(nbatch, nullptr);
+    std::vector<char> seen(c->resident.begin(), c->resident.end());
+    for (int64_t B = 0; B < nbatch; ++B) {
+      const int64_t kb0 = B * D + 1;
+      const int nb = (int)std::min<int64_t>(D, K - kb0 + 1);
+      for (int b = 0; b < nb; ++b) {
+        const int64_t bk = idx[kb0 + b - 1] - 1;
+        if (!seen[bk]) seen[bk] = 1, up.blocks[B].push_back(bk);
+      }
+      if (!up.blocks[B].empty()) CK(c, cudaEventCreateWithFlags(&up.ev[B], cudaEventDisableTiming));
+    }
+    up.active = true;
+    up.th = std::thread([c, &up, nbatch]() {
+      cudaSetDevice(c->dev);
+      for (int64_t B = 0; B < nbatch; ++B) {
+        const bool csr = c->layout == SLIM_CSR_PERBLOCK;
+        BlkList L{};
+        for (int64_t bk : up.blocks[B]) {
+          const int rc = copy_block(c, bk, up.msg, &up.launches, !csr);
+          if (rc) {
+            up.rc = rc;
+            up.done.store(nbatch + 1, std::memory_order_release);
+            return;
+          }
+          c->resident[bk] = 1;
+          L.id[L.n++] = (int)bk;
+        }
+        if (csr && L.n > 0) {  // the batch's CSC in one launch per phase
+          if (c->vdt == SLIM_F64)
+            launch_build_csc_list<double>(c->colptr, c->cscrow, (double*)c->cscval, c->rowptr, c->col,
+                                          (const double*)c->val, c->blkbase, (int)c->ell, (int)c->n, L, c->su);
+          else
+            launch_build_csc_list<float>(c->colptr, c->cscrow, (float*)c->cscval, c->rowptr, c->col,
+                                         (const float*)c->val, c->blkbase, (int)c->ell, (int)c->n, L, c->su);
+          up.launches += 5;
+        }
+        if (up.ev[B] && cudaEventRecord(up.ev[B], c->su) != cudaSuccess) {
+          up.rc = SLIM_ECUDA;
+          up.msg = "upload event record failed";
+          up.done.store(nbatch + 1, std::memory_order_release);
+          return;
+        }
+        up.done.store(B + 1, std::memory_order_release);
+      }
+    });
+  }
   for (int64_t B = 0; B < nbatch && !stop; ++B) {
     const int64_t kb0 = B * D + 1;
     const int nb = (int)std::min<int64_t>(D, K - kb0 + 1);
@@ -1492,17 +1641,18 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
       launches_at_k0 = c->launches;
       a_recorded = true;
     }
-    // ---- host streaming: the batch's first-sampled blocks into HBM (su)
-    if (c->streaming && !c->resident.empty()) {
-      int64_t blks[MAX_BATCH];
-      for (int b = 0; b < nb; ++b) blks[b] = idx[kb0 + b - 1] - 1;
-      int copied = 0;
-      int rc = ensure_blocks(c, blks, nb, &copied);
-      if (rc) return rc;
-      if (copied) {
-        CK(c, cudaEventRecord(c->ev_u[B % NEV], c->su));
-        CK(c, cudaStreamWaitEvent(c->sg, c->ev_u[B % NEV], 0));
-        CK(c, cudaStreamWaitEvent(c->sx, c->ev_u[B % NEV], 0));
+    // ---- host streaming: the batch's first-sampled blocks, uploaded by the
+    // worker thread (below); wait until it has enqueued them, then order the
+    // batch's Gram panels and x-chain after the copies
+    if (up.active) {
+      while (up.done.load(std::memory_order_acquire) <= B) std::this_thread::yield();
+      if (up.rc) {
+        up.join();
+        FAIL(c, up.rc, "%s", up.msg.c_str());
+      }
+      if (up.ev[B]) {
+        CK(c, cudaStreamWaitEvent(c->sg, up.ev[B], 0));
+        CK(c, cudaStreamWaitEvent(c->sx, up.ev[B], 0));
       }
     }
     // ---- Gram panels (sg): the ring slots they overwrite were last read by
@@ -1572,6 +1722,11 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
       CK(c, cudaMemcpyAsync(c->pin_div, &c->ctl->diverged_at, sizeof(int64_t),
                             cudaMemcpyDeviceToHost, c->sx));
     }
+  }
+  if (up.active) {  // every upload enqueued (a run stopped early still finishes its copies)
+    up.join();
+    c->launches += up.launches;
+    if (up.rc) FAIL(c, up.rc, "%s", up.msg.c_str());
   }
   CK(c, cudaEventRecord(c->ev_f[0], c->sf));
   CK(c, cudaStreamWaitEvent(c->sx, c->ev_f[0], 0));

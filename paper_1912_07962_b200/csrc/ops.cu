@@ -597,6 +597,94 @@ __global__ void k_csc_sort(const int* __restrict__ colptr, int* __restrict__ csc
   }
 }
 
+// The same build for an arbitrary list of blocks (a streamed batch's
+// first-use blocks): one launch per phase for the whole list.
+template <typename T>
+__global__ void k_csc_count_list(int* __restrict__ colptr, const int64_t* __restrict__ rowptr,
+                                 const int* __restrict__ col, BlkList L, int ell, int n) {
+  const int64_t lr = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (lr >= (int64_t)L.n * ell) return;
+  const int64_t b = L.id[lr / ell];
+  const int64_t row = b * ell + lr % ell;
+  int* cp = colptr + b * (int64_t)(n + 1);
+  for (int64_t e = rowptr[row] + lane; e < rowptr[row + 1]; e += 32) atomicAdd(cp + col[e] + 1, 1);
+}
+template <typename T>
+__global__ void k_csc_fill_list(int* __restrict__ colptr, const int64_t* __restrict__ rowptr,
+                                const int* __restrict__ col, const T* __restrict__ val,
+                                int* __restrict__ cscrow, T* __restrict__ cscval, BlkList L, int ell,
+                                int n) {
+  const int64_t lr = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (lr >= (int64_t)L.n * ell) return;
+  const int64_t b = L.id[lr / ell];
+  const int rloc = (int)(lr % ell);
+  const int64_t row = b * ell + rloc;
+  const int64_t base = rowptr[b * ell];
+  int* cp = colptr + b * (int64_t)(n + 1);
+  for (int64_t e = rowptr[row] + lane; e < rowptr[row + 1]; e += 32) {
+    const int pos = atomicAdd(cp + col[e], 1);
+    cscrow[base + pos] = rloc;
+    cscval[base + pos] = val[e];
+  }
+}
+__global__ void __launch_bounds__(256) k_csc_scan_list(int* __restrict__ colptr, BlkList L, int n) {
+  using Scan = cub::BlockScan<int, 256>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int carry;
+  int* cp = colptr + L.id[blockIdx.x] * (int64_t)(n + 1);
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 1; base <= n; base += 256) {
+    const int idx = base + threadIdx.x;
+    int v = (idx <= n) ? cp[idx] : 0;
+    int incl, agg;
+    Scan(tmp).InclusiveSum(v, incl, agg);
+    const int c0 = carry;
+    if (idx <= n) cp[idx] = incl + c0;
+    __syncthreads();
+    if (threadIdx.x == 0) carry = c0 + agg;
+    __syncthreads();
+  }
+}
+__global__ void __launch_bounds__(256) k_csc_shift_list(int* __restrict__ colptr, BlkList L, int n) {
+  int* cp = colptr + L.id[blockIdx.x] * (int64_t)(n + 1);
+  for (int hi = n + 1; hi > 0; hi -= 256) {
+    const int c = hi - 256 + (int)threadIdx.x;
+    int v = 0;
+    if (c >= 1) v = cp[c - 1];
+    __syncthreads();
+    if (c >= 1) cp[c] = v;
+    else if (c == 0) cp[0] = 0;
+    __syncthreads();
+  }
+}
+template <typename T>
+__global__ void k_csc_sort_list(const int* __restrict__ colptr, int* __restrict__ cscrow,
+                                T* __restrict__ cscval, const int64_t* __restrict__ blkbase, BlkList L,
+                                int n) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (int64_t)L.n * n) return;
+  const int64_t b = L.id[gid / n];
+  const int c = (int)(gid % n);
+  const int* cp = colptr + b * (int64_t)(n + 1);
+  const int64_t base = blkbase[b];
+  const int lo = cp[c], hi = cp[c + 1];
+  for (int e = lo + 1; e < hi; ++e) {
+    const int rk = cscrow[base + e];
+    const T vk = cscval[base + e];
+    int q = e - 1;
+    while (q >= lo && cscrow[base + q] > rk) {
+      cscrow[base + q + 1] = cscrow[base + q];
+      cscval[base + q + 1] = cscval[base + q];
+      --q;
+    }
+    cscrow[base + q + 1] = rk;
+    cscval[base + q + 1] = vk;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
@@ -720,6 +808,21 @@ void launch_build_csc(int* colptr, int* cscrow, T* cscval, const int64_t* rowptr
   k_csc_sort<T><<<cdiv(nblk * n, 256), 256, 0, s>>>(cp, cscrow, cscval, blkbase + blk0, nblk, n);
 }
 
+template <typename T>
+void launch_build_csc_list(int* colptr, int* cscrow, T* cscval, const int64_t* rowptr, const int* col,
+                           const T* val, const int64_t* blkbase, int ell, int n, const BlkList& L,
+                           cudaStream_t s) {
+  if (L.n <= 0) return;
+  for (int q = 0; q < L.n; ++q)
+    cudaMemsetAsync(colptr + (int64_t)L.id[q] * (n + 1), 0, sizeof(int) * (size_t)(n + 1), s);
+  const int64_t rows = (int64_t)L.n * ell;
+  k_csc_count_list<T><<<cdiv(rows, 8), 256, 0, s>>>(colptr, rowptr, col, L, ell, n);
+  k_csc_scan_list<<<(unsigned)L.n, 256, 0, s>>>(colptr, L, n);
+  k_csc_fill_list<T><<<cdiv(rows, 8), 256, 0, s>>>(colptr, rowptr, col, val, cscrow, cscval, L, ell, n);
+  k_csc_shift_list<<<(unsigned)L.n, 256, 0, s>>>(colptr, L, n);
+  k_csc_sort_list<T><<<cdiv((int64_t)L.n * n, 256), 256, 0, s>>>(colptr, cscrow, cscval, blkbase, L, n);
+}
+
 #define SLIM_INST(T)                                                                              \
   template void launch_residual_dense<T>(double*, const T*, int64_t, int64_t, int64_t, int, int, \
                                          const double*, const double*, const Ctl*, RowSplit,      \
@@ -737,7 +840,9 @@ void launch_build_csc(int* colptr, int* cscrow, T* cscval, const int64_t* rowptr
                                   const int64_t*, const double*, const Ctl*, cudaStream_t);      \
   template void launch_build_csc<T>(int*, int*, T*, const int64_t*, const int*, const T*,         \
                                     const int64_t*, int64_t, int, int, int64_t, cudaStream_t,     \
-                                    int64_t, int64_t);
+                                    int64_t, int64_t);                                            \
+  template void launch_build_csc_list<T>(int*, int*, T*, const int64_t*, const int*, const T*,    \
+                                         const int64_t*, int, int, const BlkList&, cudaStream_t);
 
 SLIM_INST(double)
 SLIM_INST(float)

@@ -76,6 +76,15 @@ template <typename T>
 void launch_mtw_csc(double* s_out, const Window& W, const int* colptr, int n, const int* cscrow,
                     const T* cscval, const int64_t* blkbase, const double* w, const Ctl* ctl,
                     cudaStream_t s);
+// block list for the batched per-block CSC build of a streamed batch
+struct BlkList {
+  int n;
+  int id[MAX_BATCH];
+};
+template <typename T>
+void launch_build_csc_list(int* colptr, int* cscrow, T* cscval, const int64_t* rowptr, const int* col,
+                           const T* val, const int64_t* blkbase, int ell, int n, const BlkList& L,
+                           cudaStream_t s);
 template <typename T>
 void launch_build_csc(int* colptr, int* cscrow, T* cscval, const int64_t* rowptr, const int* col,
                       const T* val, const int64_t* blkbase, int64_t m, int ell, int n,
