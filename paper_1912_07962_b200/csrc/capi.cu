@@ -1456,8 +1456,8 @@ static int enqueue_chol_batch(slim_ctx* c, const Window* Ws, int nb, int set, co
     const int twant = getenv("SLIM_CHOL_TRACE_LAUNCH") ? atoi(getenv("SLIM_CHOL_TRACE_LAUNCH")) : 3;
     unsigned long long* dtr = nullptr;
     if (tpath && ++trace_count == twant) {
-      CK(c, cudaMalloc(&dtr, sizeof(unsigned long long) * 6 * (size_t)P.ntasks));
-      CK(c, cudaMemsetAsync(dtr, 0, sizeof(unsigned long long) * 6 * (size_t)P.ntasks, c->sf));
+      CK(c, cudaMalloc(&dtr, sizeof(unsigned long long) * 8 * (size_t)P.ntasks));
+      CK(c, cudaMemsetAsync(dtr, 0, sizeof(unsigned long long) * 8 * (size_t)P.ntasks, c->sf));
       P.trace = dtr;
     }
     launch_chol(P, c->sf);
@@ -1465,17 +1465,17 @@ static int enqueue_chol_batch(slim_ctx* c, const Window* Ws, int nb, int set, co
     CKLAUNCH(c);
     if (dtr) {
       CK(c, cudaStreamSynchronize(c->sf));
-      std::vector<unsigned long long> h(6 * (size_t)P.ntasks);
+      std::vector<unsigned long long> h(8 * (size_t)P.ntasks);
       std::vector<int2> hm(P.ntasks);
       CK(c, cudaMemcpy(h.data(), dtr, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost));
       CK(c, cudaMemcpy(hm.data(), P.map, sizeof(int2) * hm.size(), cudaMemcpyDeviceToHost));
       cudaFree(dtr);
       if (FILE* f = fopen(tpath, "w")) {
-        fprintf(f, "ticket,sys,i,j,t0,t1,t2,t3,T,dep_ns,ring_ns\n");
+        fprintf(f, "ticket,sys,i,j,t0,t1,t2,t3,T,dep_ns,ring_ns,slice_ns,store_ns\n");
         for (int t = 0; t < P.ntasks; ++t)
-          fprintf(f, "%d,%d,%d,%d,%llu,%llu,%llu,%llu,%d,%llu,%llu\n", t, hm[t].x, hm[t].y >> 16,
-                  hm[t].y & 0xffff, h[6 * t], h[6 * t + 1], h[6 * t + 2], h[6 * t + 3], P.m[hm[t].x].T,
-                  h[6 * t + 4], h[6 * t + 5]);
+          fprintf(f, "%d,%d,%d,%d,%llu,%llu,%llu,%llu,%d,%llu,%llu,%llu,%llu\n", t, hm[t].x, hm[t].y >> 16,
+                  hm[t].y & 0xffff, h[8 * t], h[8 * t + 1], h[8 * t + 2], h[8 * t + 3], P.m[hm[t].x].T,
+                  h[8 * t + 4], h[8 * t + 5], h[8 * t + 6], h[8 * t + 7]);
         fclose(f);
       }
     }

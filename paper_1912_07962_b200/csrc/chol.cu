@@ -685,7 +685,7 @@ __global__ void __launch_bounds__(256, 2) k_chol_tiles(const __grid_constant__ C
   const int i = e.y >> 16, j = e.y & 0x7fff;
   const bool dual = (e.y & 0x8000) != 0;  // off-diagonal rows i and i + 1 of column j
   const int T = M.T;
-  unsigned long long* tr = (P.trace != nullptr && tid == 0) ? P.trace + 6 * (int64_t)s_task : nullptr;
+  unsigned long long* tr = (P.trace != nullptr && tid == 0) ? P.trace + 8 * (int64_t)s_task : nullptr;
   if (tr) tr[0] = globaltimer_ns();
   double accA[8][2], accB[8][2];
 
@@ -914,9 +914,12 @@ __device__ __forceinline__ void store_digits(const CholMat& M, int i, int k, con
 // b and every later system of the batch that shares it bit for bit, then
 // publish all copies behind one fence.
 __device__ void store_publish_i8(const CholParams& P, int b, int i, int j, const double* X,
-                                 const double* Dv, int tid) {
+                                 const double* Dv, int tid, unsigned long long* tr = nullptr) {
   Digits D;
+  const unsigned long long s0 = tr ? globaltimer_ns() : 0;
   if (i != j) slice_tile(X, P.m[b].rexp + i * TB, tid, D);
+  if (tr) tr[6] += globaltimer_ns() - s0;
+  const unsigned long long s1 = tr ? globaltimer_ns() : 0;
   int last = b;
   for (int bb = b; bb < P.nb; ++bb) {
     const CholMat& M2 = P.m[bb];
@@ -935,6 +938,7 @@ __device__ void store_publish_i8(const CholParams& P, int b, int i, int j, const
     __threadfence();
     for (int bb = b; bb <= last; ++bb) st_release(P.m[bb].flags + (i * (i + 1) / 2 + j), P.m[bb].epoch);
   }
+  if (tr) tr[7] += globaltimer_ns() - s1;
 }
 
 // One task per CTA (same ticket map as k_chol_tiles): output rows ra (and
@@ -975,7 +979,7 @@ __global__ void __launch_bounds__(256, 1) k_chol_i8(const __grid_constant__ Chol
   const int T = M.T;
   const bool two = pair ? (j + 1 < T) : ((e.y & 0x8000) != 0);
   const int ra = i;  // first output row tile (the diagonal for a pair task)
-  unsigned long long* tr = (P.trace != nullptr && tid == 0) ? P.trace + 6 * (int64_t)s_task : nullptr;
+  unsigned long long* tr = (P.trace != nullptr && tid == 0) ? P.trace + 8 * (int64_t)s_task : nullptr;
   if (tr) tr[0] = globaltimer_ns();
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
@@ -1037,7 +1041,7 @@ __global__ void __launch_bounds__(256, 1) k_chol_i8(const __grid_constant__ Chol
     (void)t_ring;
   } else if (warp == 1 && lane == 0 && nchunk > 0) {
     // ---------------- MMA issuer ----------------
-    unsigned long long* trm = P.trace != nullptr ? P.trace + 6 * (int64_t)s_task : nullptr;
+    unsigned long long* trm = P.trace != nullptr ? P.trace + 8 * (int64_t)s_task : nullptr;
     unsigned long long t_data = 0;  // trace: waiting for operand stages
     for (int u = 0; u < nchunk; ++u) {
       const int st = u % oz::NST;
@@ -1125,11 +1129,11 @@ __global__ void __launch_bounds__(256, 1) k_chol_i8(const __grid_constant__ Chol
   if (pair) {
     potrf_tile_blocked(X, Dv, rdiag, tid, P.error);
     if (tr) tr[2] = globaltimer_ns();
-    store_publish_i8(P, e.x, j, j, X, Dv, tid);
+    store_publish_i8(P, e.x, j, j, X, Dv, tid, tr);
     if (two) {
       trsm_tile_warp(X2, X, Dv, warp, lane);
       __syncthreads();
-      store_publish_i8(P, e.x, j + 1, j, X2, nullptr, tid);
+      store_publish_i8(P, e.x, j + 1, j, X2, nullptr, tid, tr);
     }
   } else {
     if (tid == 0) wait_flag(M.flags + (j * (j + 1) / 2 + j), M.epoch);
@@ -1145,8 +1149,8 @@ __global__ void __launch_bounds__(256, 1) k_chol_i8(const __grid_constant__ Chol
       trsm_tile_warp(X, Sg, Dv, warp, lane);
     __syncthreads();
     if (tr) tr[2] = globaltimer_ns();  // wait + L_jj load + TRSM
-    store_publish_i8(P, e.x, ra, j, X, nullptr, tid);
-    if (two) store_publish_i8(P, e.x, ra + 1, j, X2, nullptr, tid);
+    store_publish_i8(P, e.x, ra, j, X, nullptr, tid, tr);
+    if (two) store_publish_i8(P, e.x, ra + 1, j, X2, nullptr, tid, tr);
   }
   if (tr) tr[3] = globaltimer_ns();
 }

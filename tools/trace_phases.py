@@ -25,6 +25,9 @@ for k in ("pair", "dual", "single"):
     if not m.any():
         continue
     extra = ""
+    if "slice_ns" in d.dtype.names:
+        extra += (f"  [finish: slicing {np.mean(d['slice_ns'][ok][m]) / 1e3:5.2f} us, stores+publish "
+                  f"{np.mean(d['store_ns'][ok][m]) / 1e3:5.2f} us]")
     if "dep_ns" in d.dtype.names:
         extra = (f"  [producer: dep wait {np.mean(d['dep_ns'][ok][m]) / 1e3:6.2f} us, MMA waits for data "
                  f"{np.mean(d['ring_ns'][ok][m]) / 1e3:6.2f} us]")
