@@ -28,6 +28,7 @@ is the max over ranks, value = all ranks' steps / that time.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -400,6 +401,7 @@ def run_ours(args, world, rank, local, dist):
         h2d = _operator_bytes(op2) + 2 * xt.nbytes + total * 16
         walls = []
         while True:  # short runs are repeated on fresh operators, median reported
+            gc.collect()  # the previous operator's context is released here, untimed
             t0 = time.perf_counter()
             tr2 = slim.run("slimls", op2, sampler(), slim.Schedule("constant", alpha),
                            epochs=total / M, r=r, references={"x_true": xt}, record_every=1,

@@ -322,9 +322,92 @@ static void set_err(slim_ctx* c, const char* msg) {
   g_err = msg;
 }
 
+// Process-wide caching device allocator for context buffers: a run() on a
+// fresh operator creates a context with ~GBs of factor buffers; recycling
+// same-size blocks of destroyed contexts (after a device sync) replaces a
+// cudaMalloc / cudaFree pair of GBs per call.  Bounded: beyond kCap cached
+// bytes the oldest cached blocks are released.
+struct DevCache {
+  static constexpr size_t kCap = (size_t)48 << 30;
+  std::mutex m;
+  std::multimap<std::pair<int, size_t>, void*> freelist;  // (device, bytes) -> block
+  std::map<void*, std::pair<int, size_t>> live;
+  std::vector<std::pair<void*, std::pair<int, size_t>>> order;  // cached blocks, oldest first
+  size_t cached = 0;
+};
+static DevCache g_dcache;
+
+static cudaError_t cache_malloc(void** p, size_t bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_dcache.m);
+  auto it = g_dcache.freelist.find({dev, bytes});
+  if (it != g_dcache.freelist.end()) {
+    *p = it->second;
+    g_dcache.freelist.erase(it);
+    for (size_t q = 0; q < g_dcache.order.size(); ++q)
+      if (g_dcache.order[q].first == *p) {
+        g_dcache.order.erase(g_dcache.order.begin() + q);
+        break;
+      }
+    g_dcache.cached -= bytes;
+    g_dcache.live[*p] = {dev, bytes};
+    return cudaSuccess;
+  }
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e == cudaErrorMemoryAllocation && g_dcache.cached > 0) {  // release the cache and retry
+    cudaGetLastError();
+    for (auto& kv : g_dcache.freelist) cudaFree(kv.second);
+    g_dcache.freelist.clear();
+    g_dcache.order.clear();
+    g_dcache.cached = 0;
+    e = cudaMalloc(p, bytes);
+  }
+  if (e == cudaSuccess) g_dcache.live[*p] = {dev, bytes};
+  return e;
+}
+
+// the caller has synchronized the device (no pending work uses p)
+static void cache_free(void* p) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_dcache.m);
+  auto it = g_dcache.live.find(p);
+  if (it == g_dcache.live.end()) {
+    cudaFree(p);
+    return;
+  }
+  const auto key = it->second;
+  g_dcache.live.erase(it);
+  g_dcache.freelist.insert({key, p});
+  g_dcache.order.push_back({p, key});
+  g_dcache.cached += key.second;
+  while (g_dcache.cached > DevCache::kCap && !g_dcache.order.empty()) {
+    auto victim = g_dcache.order.front();
+    g_dcache.order.erase(g_dcache.order.begin());
+    auto range = g_dcache.freelist.equal_range(victim.second);
+    for (auto f = range.first; f != range.second; ++f)
+      if (f->second == victim.first) {
+        g_dcache.freelist.erase(f);
+        break;
+      }
+    g_dcache.cached -= victim.second.second;
+    cudaFree(victim.first);
+  }
+}
+
+// free a context block right away (implicitly synchronizing, like cudaFree)
+static void cache_release(void* p) {
+  if (!p) return;
+  {
+    std::lock_guard<std::mutex> lk(g_dcache.m);
+    g_dcache.live.erase(p);
+  }
+  cudaFree(p);
+}
+
 static int dev_alloc(slim_ctx* c, void** p, size_t bytes) {
   if (bytes == 0) bytes = 16;
-  cudaError_t e = cudaMalloc(p, bytes);
+  cudaError_t e = cache_malloc(p, bytes);
   if (e != cudaSuccess)
     FAIL(c, SLIM_ENOMEM, "cudaMalloc(%zu bytes) failed: %s", bytes, cudaGetErrorString(e));
   return SLIM_OK;
@@ -346,17 +429,17 @@ const char* slim_last_error(const slim_ctx* ctx) {
 static void free_all(slim_ctx* c) {
   delete c->comm;
   c->comm = nullptr;
+  cudaSetDevice(c->dev);
+  cudaDeviceSynchronize();  // no pending work may touch recycled blocks
   void* ptrs[] = {c->gring_hi, c->gring_lo, c->zero_b, c->norms, c->gring, c->A, c->b, c->rowptr, c->col, c->val, c->colptr, c->cscrow, c->cscval,
                   c->blkbase, c->x, c->ctl, c->panels, c->tickets, c->tflags, c->errflag,
                   c->rvec, c->tvec, c->wvec, c->spart, c->fpart, c->gpart, c->hist, c->iters_dev};
-  for (void* p : ptrs)
-    if (p) cudaFree(p);
-  for (int q = 0; q < MAX_REFS; ++q)
-    if (c->refs[q]) cudaFree(c->refs[q]);
-  if (c->factor_slab) cudaFree(c->factor_slab);
+  for (void* p : ptrs) cache_free(p);
+  for (int q = 0; q < MAX_REFS; ++q) cache_free(c->refs[q]);
+  cache_free(c->factor_slab);
   for (RowSplit* rs : {&c->rsplit, &c->dsplit}) {
-    if (rs->part) cudaFree(rs->part);
-    if (rs->cnt) cudaFree(rs->cnt);
+    cache_free(rs->part);
+    cache_free(rs->cnt);
   }
   for (auto& kv : c->maps) cudaFree(kv.second.dev);
   if (c->part.gx || c->part.gr) {
@@ -636,9 +719,9 @@ int slim_upload_csr(slim_ctx* c, const int64_t* rowptr, const int32_t* col, cons
   for (int64_t bk = 0; bk < c->M; ++bk)
     if (c->h_blkbase[bk + 1] - c->h_blkbase[bk] > 0x7fffffffLL)
       FAIL(c, SLIM_EINVAL, "block %lld has more than 2^31 nonzeros", (long long)bk + 1);
-  if (c->rowptr) cudaFree(c->rowptr), c->rowptr = nullptr;
-  if (c->col) cudaFree(c->col), c->col = nullptr;
-  if (c->val) cudaFree(c->val), c->val = nullptr;
+  if (c->rowptr) cache_release(c->rowptr), c->rowptr = nullptr;
+  if (c->col) cache_release(c->col), c->col = nullptr;
+  if (c->val) cache_release(c->val), c->val = nullptr;
   c->nnz = nnz;
   ALLOC(c, c->rowptr, sizeof(int64_t) * (c->m + 1));
   ALLOC(c, c->col, sizeof(int) * nnz);
@@ -766,7 +849,7 @@ static int size_streamed_csr(slim_ctx* c) {
   rp[c->m] = nnz;
   for (void** pp : {(void**)&c->rowptr, (void**)&c->col, (void**)&c->val, (void**)&c->colptr,
                     (void**)&c->cscrow, (void**)&c->cscval, (void**)&c->blkbase})
-    if (*pp) cudaFree(*pp), *pp = nullptr;
+    if (*pp) cache_release(*pp), *pp = nullptr;
   c->nnz = nnz;
   ALLOC(c, c->rowptr, sizeof(int64_t) * (c->m + 1));
   ALLOC(c, c->col, sizeof(int) * (size_t)std::max<int64_t>(1, nnz));
@@ -923,10 +1006,10 @@ int slim_finalize_operator(slim_ctx* c) {
     if (rc) return rc;
   }
   if (!c->rowptr) FAIL(c, SLIM_ESTATE, "no CSR operator uploaded");
-  if (c->colptr) cudaFree(c->colptr), c->colptr = nullptr;
-  if (c->cscrow) cudaFree(c->cscrow), c->cscrow = nullptr;
-  if (c->cscval) cudaFree(c->cscval), c->cscval = nullptr;
-  if (c->blkbase) cudaFree(c->blkbase), c->blkbase = nullptr;
+  if (c->colptr) cache_release(c->colptr), c->colptr = nullptr;
+  if (c->cscrow) cache_release(c->cscrow), c->cscrow = nullptr;
+  if (c->cscval) cache_release(c->cscval), c->cscval = nullptr;
+  if (c->blkbase) cache_release(c->blkbase), c->blkbase = nullptr;
   ALLOC(c, c->colptr, sizeof(int) * (size_t)c->M * (c->n + 1));
   ALLOC(c, c->cscrow, sizeof(int) * (size_t)std::max<int64_t>(1, c->nnz));
   ALLOC(c, c->cscval, c->vsize * (size_t)std::max<int64_t>(1, c->nnz));
@@ -1525,12 +1608,12 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
   const int cols = SLIM_HIST_FIXED + c->nref;
   const int64_t rows_cap = K / record_every + 2;
   if (rows_cap > c->hist_rows_cap) {
-    if (c->hist) cudaFree(c->hist), c->hist = nullptr;
+    if (c->hist) cache_release(c->hist), c->hist = nullptr;
     ALLOC(c, c->hist, sizeof(double) * rows_cap * (SLIM_HIST_FIXED + MAX_REFS));
     c->hist_rows_cap = rows_cap;
   }
   if (iterates && rows_cap > c->iters_cap) {
-    if (c->iters_dev) cudaFree(c->iters_dev), c->iters_dev = nullptr;
+    if (c->iters_dev) cache_release(c->iters_dev), c->iters_dev = nullptr;
     ALLOC(c, c->iters_dev, sizeof(double) * rows_cap * c->n);
     c->iters_cap = rows_cap;
   }
