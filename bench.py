@@ -279,13 +279,13 @@ def run_reference(args, world, rank, dist):
     print(json.dumps(line), flush=True)
 
 
-def _config_dict(cfg_id, op, world, sharded=False):
+def _config_dict(cfg_id, op, world, sharded=False, factor="replicated"):
     cfg = CONFIGS[cfg_id]
     return {"workload": cfg["workload"], "n": op.n_cols, "m": op.n_rows, "ell": op.block_rows,
             "r": cfg["r"], "lambda": 1.0 / cfg["alpha"],
             "dual_system_N": (cfg["r"] + 1) * op.block_rows,
-            "parallelism": (f"columns{world}" if sharded else f"replicas{world}") if world > 1
-            else "single",
+            "parallelism": (f"columns{world}" + ("-rr" if factor == "round_robin" else "")
+                            if sharded else f"replicas{world}") if world > 1 else "single",
             "l2": "per-iteration working set > 126 MB L2 (no flush)"}
 
 
@@ -312,7 +312,7 @@ def run_ours(args, world, rank, local, dist):
         import torch
 
         torch.cuda.set_device(dev)
-        shard = NcclShard.from_torch(op.n_cols)
+        shard = NcclShard.from_torch(op.n_cols, round_robin=args.factor == "round_robin")
         seed = SAMPLER_SEED  # one solve: every shard walks the same index trace
     else:
         shard = None
@@ -331,7 +331,7 @@ def run_ours(args, world, rank, local, dist):
         os.environ.pop("SLIM_HOST_STREAMING")
     else:
         os.environ["SLIM_HOST_STREAMING"] = prev
-    timing = {"start_step": wprime + 1}
+    timing = {"start_step": wprime + 1, "probe_reps": 24}
     _barrier(dist)
     with ClockSampler(dev) as clk:
         traj = slim.run("slimls", op, sampler(), slim.Schedule("constant", alpha),
@@ -392,6 +392,19 @@ def run_ours(args, world, rank, local, dist):
                     "aggregate_tflops_over_window": agg,
                     "aggregate_frac": agg / FP64_PEAK_TFLOPS,
                     "avg_launch_ms": chol_ms, "launches": timing["cholesky_count"]}
+    # ---- operator-streaming kernels alone (K1, K5, CSR K2), cold L2 ----
+    hbm_peak = float(_peaks().get("hbm_gbs", 0.0)) or 7700.0
+    streaming = {"peak_gbs": hbm_peak,
+                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if _peaks().get("hbm_gbs")
+                 else "B200_PROFILING.md fallback",
+                 "how": "probe after the timed run: 24 launches, each on a different window of "
+                        "resident blocks, L2 flushed (256 MB memset) between launches, one CUDA "
+                        "event pair per launch on the x-chain stream; bytes = operator bytes the "
+                        "launch must read once + vectors read/written (algorithmic)"}
+    for name, (us, nbytes) in timing.get("streaming", {}).items():
+        gbs = nbytes / (us * 1e-6) / 1e9
+        streaming[name] = {"us_per_launch": us, "bytes_per_launch": nbytes, "achieved_gbs": gbs,
+                           "frac": gbs / hbm_peak}
     # ---- e2e through the public API, host-resident fresh operator ----
     e2e = None
     if not args.quick and not sharded:
@@ -422,6 +435,10 @@ def run_ours(args, world, rank, local, dist):
                        f"{total} steps + history/x download, wall clock, median of "
                        f"{len(walls)} fresh operators"}
         assert tr2.status == "ok"
+    # ---- device projector: tomography operators traced in HBM ----
+    projector = None
+    if args.config in (2, 3, 4) and not sharded:
+        projector = _projector_leg(args, dev, b, xt, r, alpha, scheme, total, M, sampler)
     if rank != 0:
         return
     cb = None
@@ -431,8 +448,9 @@ def run_ours(args, world, rank, local, dist):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_win / args.steps,
             "higher_is_better": True, "scaling": "strong" if sharded else "weak",
             "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": _config_dict(args.config, op, world, sharded),
-            "rows_per_s": value * ell, "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
+            "data": "synthetic", "config": _config_dict(args.config, op, world, sharded, args.factor),
+            "rows_per_s": value * ell, "roofline": roofline, "streaming": streaming,
+            "cpu_baseline": cb, "e2e": e2e, "device_projector": projector,
             "gpu_launches": int(timing["launches"]), "clocks": clk.summary(),
             "kernel_ms_per_step": {
                 "gram": timing["gram_ms"] / max(1, timing["gram_count"]),
@@ -440,6 +458,61 @@ def run_ours(args, world, rank, local, dist):
                 "x_chain": timing["x_chain_ms"] / max(1, timing["x_chain_count"])},
             "final_rel_err_x_true": float(traj.rel_errors["x_true"][-1])}
     print(json.dumps(line), flush=True)
+
+
+def _projector_leg(args, dev, b, xt, r, alpha, scheme, total, M, sampler):
+    """Device Siddon projector: trace time of the whole operator (count pass,
+    scan, fill, per-block CSC) and e2e through the public API with the
+    operator traced on the device inside the timed region (only b and the
+    geometry cross PCIe)."""
+    import torch
+
+    import paper_1912_07962_b200 as slim
+    from paper_1912_07962_b200 import problems, tomo
+
+    geom, grid, dtype, ell, rmap = problems.projector_config(args.config)
+    builds = []
+    for _ in range(3):
+        gc.collect()
+        op = tomo.ProjectorOperator(geom, grid, dtype=dtype, block_rows=ell, ray_of_row=rmap)
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        dop = op.device_context(r, dev)
+        torch.cuda.synchronize(dev)
+        builds.append(time.perf_counter() - t0)
+        nnz = dop.nnz()
+        del dop, op
+    vb = np.dtype(dtype).itemsize
+    m = b.shape[0]
+    csr_bytes = nnz * (4 + vb) + (m + 1) * 8
+    t_build = float(np.median(builds))
+    out = {"what": "slim_build_projector + slim_finalize_operator on a fresh context: count pass, "
+                   "row-pointer scan, fill pass, per-block CSC; wall clock, median of 3",
+           "nnz": nnz, "build_ms": 1e3 * t_build, "csr_bytes": csr_bytes,
+           "csr_write_gbs": csr_bytes / t_build / 1e9,
+           "rays_per_s": m / t_build}
+    if args.quick:
+        return out
+    walls = []
+    for _ in range(3):
+        gc.collect()
+        t0 = time.perf_counter()
+        op = tomo.ProjectorOperator(geom, grid, dtype=dtype, block_rows=ell, ray_of_row=rmap,
+                                    b=b)
+        tr = slim.run("slimls", op, sampler(), slim.Schedule("constant", alpha),
+                      epochs=total / M, r=r, references={"x_true": xt}, record_every=1,
+                      device=dev)
+        walls.append(time.perf_counter() - t0)
+        assert tr.status == "ok"
+        del op
+    wall = float(np.median(walls))
+    out["e2e"] = {"value": total / wall, "unit": "it/s",
+                  "h2d_bytes_per_step": int((b.nbytes + 2 * xt.nbytes + total * 16) / total),
+                  "d2h_bytes_per_step": int(((total + 1) * 6 * 8 + xt.nbytes) / total),
+                  "what": f"public run() on a fresh ProjectorOperator (geometry + b on the host): "
+                          f"device trace of the operator + CSC + {total} steps + history/x "
+                          f"download, wall clock, median of 3"}
+    return out
 
 
 def _operator_bytes(op) -> int:
@@ -463,6 +536,9 @@ def main():
     ap.add_argument("--shard", default="replicas", choices=["replicas", "columns"],
                     help="N > 1: independent replicas (default) or one column-sharded solve "
                          "(NCCL allreduce of Gram panel / residual / norm partials per step)")
+    ap.add_argument("--factor", default="replicated", choices=["replicated", "round_robin"],
+                    help="--shard columns: every rank factors every system (replicated) or "
+                         "batch B is factored on rank B mod N only (SURVEY 8f.1)")
     ap.add_argument("--quick", action="store_true",
                     help="skip the CPU baseline and the e2e leg (profiling runs)")
     args = ap.parse_args()

@@ -149,6 +149,13 @@ int slim_comm_init(slim_ctx* ctx, const void* nccl_unique_id, int32_t nranks, in
 void* slim_local_group_create(int32_t nranks);
 void slim_local_group_destroy(void* group);
 int slim_comm_init_local(slim_ctx* ctx, void* group, int32_t rank);
+/* column shards only: the batched factorization of batch B
+ * runs on rank B mod P alone; that rank's triangular solves give w and the
+ * other ranks add zeros in an allreduce of w (N doubles per step), so the
+ * replicated factorization cost is divided by P. Results are bit-identical
+ * to the replicated mode except for the first system of each batch, which
+ * is factored without the previous batch's tiles (same arithmetic).       */
+int slim_set_factor_round_robin(slim_ctx* ctx, int32_t enable);
 
 /* ---- secondary seam and kernel-level entry points -------------------- */
 /* innersolve.dual_step (innersolve.py:305-321): stacked dense window
@@ -181,6 +188,14 @@ int slim_set_profiling(slim_ctx* ctx, int32_t enable);
  * from the end of step k0-1's x-chain to the end of the run; which = 4
  * returns the number of kernels launched inside that window.           */
 int slim_set_timing_start(slim_ctx* ctx, int64_t k0);
+/* streaming-kernel probe: `reps` launches of one operator-streaming kernel
+ * (0: residual A_k x - b_k, 1: M_k^T w, 2: the new Gram panel A_k M_k^T;
+ * 2 is not defined for generated blocks), each on a different window of
+ * resident blocks with the L2 flushed in between; returns the mean launch
+ * time (us, CUDA events on the x-chain stream) and the algorithmic bytes
+ * per launch. Scratch only: the solver state (x, panels, factors) is kept. */
+int slim_probe_stream(slim_ctx* ctx, int32_t kernel, int32_t reps, double* us_out,
+                      double* bytes_out);
 
 /* ---- problem setup helpers (host side, not the hot path) ------------- */
 /* Siddon parallel-beam 2D view block (restates tomo.py:219-273): counts
@@ -189,6 +204,26 @@ int slim_siddon2d_view(double angle_deg, int64_t grid, int64_t rays, double spac
                        int64_t* rowptr, int32_t* col, double* val);
 int slim_siddon3d_view(const double* direction, int64_t grid, int64_t side, double spacing,
                        int64_t* rowptr, int32_t* col, double* val);
+
+/* ---- device projector (tomo.py:304-320) --------------- */
+/* Trace the parallel-beam operator on the GPU into a CSR context (no host
+ * copy of the matrix). dims 2: `views` = n_views angles in degrees, `rays`
+ * rays per view (tomo.py:259-273); dims 3: `views` = n_views x 3 unit
+ * directions, `rays` = detector side, rows per view = side^2 (tomo.py:
+ * 285-301). Row i of view v is ray ray_of_row[v * rows_per_view + i] of the
+ * view (NULL = identity; configs[3]'s permuted sub-blocks). Bit-identical to
+ * slim_siddon2d_view / slim_siddon3d_view. Follow with slim_set_rhs and
+ * slim_finalize_operator.                                                 */
+int slim_build_projector(slim_ctx* ctx, int32_t dims, int64_t grid, int64_t rays, int64_t n_views,
+                         const double* views, double spacing, const int32_t* ray_of_row);
+/* stored nonzeros of the context's CSR operator (0 for other layouts)   */
+int slim_nnz(slim_ctx* ctx, int64_t* nnz_out);
+/* out = A x over all rows of a resident CSR operator (or the generated one) */
+int slim_apply(slim_ctx* ctx, const double* x, double* out);
+/* one resident CSR block back to the host: rowptr_out (ell + 1, relative),
+ * then, when non-NULL, its columns and values (the context's value type)  */
+int slim_get_csr_block(slim_ctx* ctx, int64_t block, int64_t* rowptr_out, int32_t* col_out,
+                       void* val_out);
 
 #ifdef __cplusplus
 }

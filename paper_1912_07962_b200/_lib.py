@@ -27,9 +27,10 @@ EXPORTS = (
     "slim_upload_dense", "slim_upload_csr_block", "slim_upload_csr", "slim_finalize_operator",
     "slim_set_rhs", "slim_gen_apply", "slim_set_x", "slim_get_x", "slim_set_references",
     "slim_set_divergence_limit", "slim_run", "slim_set_host_streaming", "slim_nccl_unique_id", "slim_comm_init",
-    "slim_local_group_create", "slim_local_group_destroy", "slim_comm_init_local",
-    "slim_dual_step", "slim_potrf", "slim_potrf_traced", "slim_block_residual", "slim_timing", "slim_set_profiling", "slim_set_timing_start",
+    "slim_local_group_create", "slim_local_group_destroy", "slim_comm_init_local", "slim_set_factor_round_robin",
+    "slim_dual_step", "slim_potrf", "slim_potrf_traced", "slim_block_residual", "slim_timing", "slim_set_profiling", "slim_set_timing_start", "slim_probe_stream",
     "slim_siddon2d_view", "slim_siddon3d_view",
+    "slim_build_projector", "slim_apply", "slim_get_csr_block", "slim_nnz",
 )
 
 
@@ -79,8 +80,14 @@ _SIGS = {
     "slim_timing": (C.c_int, [_P, _I32, _DP, _I64P]),
     "slim_set_profiling": (C.c_int, [_P, _I32]),
     "slim_set_timing_start": (C.c_int, [_P, _I64]),
+    "slim_probe_stream": (C.c_int, [_P, _I32, _I32, _DP, _DP]),
     "slim_siddon2d_view": (C.c_int, [_D, _I64, _I64, _D, _I64P, _I32P, _DP]),
     "slim_siddon3d_view": (C.c_int, [_DP, _I64, _I64, _D, _I64P, _I32P, _DP]),
+    "slim_build_projector": (C.c_int, [_P, _I32, _I64, _I64, _I64, _DP, _D, _I32P]),
+    "slim_apply": (C.c_int, [_P, _DP, _DP]),
+    "slim_nnz": (C.c_int, [_P, _I64P]),
+    "slim_set_factor_round_robin": (C.c_int, [_P, _I32]),
+    "slim_get_csr_block": (C.c_int, [_P, _I64, _I64P, _I32P, C.c_void_p]),
 }
 
 _lock = threading.Lock()

@@ -34,6 +34,7 @@
 
 #include "gram_tc.h"
 #include "kernels.h"
+#include "siddon.h"
 #include "smpart.h"
 #include "ops.h"
 #include "slimb200.h"
@@ -248,6 +249,10 @@ struct slim_ctx {
   int xsms = 0;                      // SLIM_XSMS: SMs of the x-chain partition (0 = shared)
   SmPartition part;
   bool serial = false;               // debug (SLIM_SERIAL): factorizations wait for the x-chain
+  // column shards: batch B's factorization runs only on rank
+  // B mod P; that rank's triangular solves produce w, the others contribute
+  // zeros to an allreduce of w (exact: one nonzero term per entry)
+  bool rr = false;
   int trsv_C = 0;                    // triangular-solve cluster size (0 = by T)
   std::vector<double*> Lbuf, Dinv, Linv;  // 2 D factor buffers (+ 8x8 and 64x64 diagonal inverses)
   void* factor_slab = nullptr;            // one allocation behind Lbuf / Dinv / Linv / cflags
@@ -1097,6 +1102,12 @@ int slim_set_profiling(slim_ctx* c, int32_t enable) {
   return SLIM_OK;
 }
 
+int slim_set_factor_round_robin(slim_ctx* c, int32_t enable) {
+  if (!c) FAIL(c, SLIM_EINVAL, "null argument");
+  c->rr = enable != 0;
+  return SLIM_OK;
+}
+
 int slim_set_host_streaming(slim_ctx* c, int32_t enable) {
   if (!c) FAIL(c, SLIM_EINVAL, "null argument");
   if (enable && c->layout == SLIM_GEN_SPLITMIX64)
@@ -1325,10 +1336,13 @@ static int enqueue_gram(slim_ctx* c, const Window& W, int64_t k, int64_t real_bl
 }
 
 static int enqueue_x_chain(slim_ctx* c, const Window& W, int64_t k, int d, double alpha,
-                           int record, int epoch) {
+                           int record, int epoch, bool own = true) {
   const int ell = (int)c->ell, n = (int)c->n, N = W.nw * ell;
   cudaStream_t s = c->sx;
   (void)k;
+  if (!own) {  // round-robin factorization: another rank solves this step
+    CK(c, cudaMemsetAsync(c->wvec, 0, sizeof(double) * N, s));
+  } else {
   // trsv
   TrsvParams T{};
   T.L = c->Lbuf[d];
@@ -1348,7 +1362,12 @@ static int enqueue_x_chain(slim_ctx* c, const Window& W, int64_t k, int d, doubl
   }
   CK(c, launch_trsv(T, s));
   CKLAUNCH(c);
-  c->launches += 3;  // trsv, M^T w, finish
+  }
+  if (c->rr && c->comm) {
+    int rc = comm_allreduce(c, c->wvec, (size_t)N, s);
+    if (rc) return rc;
+  }
+  c->launches += own ? 3 : 2;  // trsv, M^T w, finish
   // M^T w
   double* s_parts = c->spart;
   int nsplit = 1;
@@ -1753,6 +1772,9 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
     if (prof_b) cudaEventRecord(pg.b, c->sg);
     CK(c, cudaEventRecord(c->ev_g[B % NEV], c->sg));
     // ---- batched factorization (sf): buffer set reused from batch B - 2
+    const bool rr = c->rr && c->comm && c->comm->nranks > 1;
+    const bool own = !rr || B % c->comm->nranks == c->comm->rank;
+    if (own) {
     CK(c, cudaStreamWaitEvent(c->sf, c->ev_g[B % NEV], 0));
     if (B >= 2) CK(c, cudaStreamWaitEvent(c->sf, c->ev_x[(B - 2) % NEV], 0));
     if (B >= 1 && c->serial) CK(c, cudaStreamWaitEvent(c->sf, c->ev_x[(B - 1) % NEV], 0));
@@ -1760,13 +1782,16 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
     if (prof_b) pc = take(c->prof_chol, pch), cudaEventRecord(pc.a, c->sf);
     {
       double fl = 0.0, i8 = 0.0;
+      // tiles shared with the previous batch's last system: only when this
+      // rank factored that batch too
       int rc = enqueue_chol_batch(c, Ws.data(), nb, set, alphas, kb0, epoch0,
-                                  B >= 1 ? (1 - set) * D + (D - 1) : -1, &fl, &i8);
+                                  B >= 1 && !rr ? (1 - set) * D + (D - 1) : -1, &fl, &i8);
       if (rc) return rc;
       if (prof_b) c->chol_flops += fl, c->chol_i8ops += i8;
     }
     if (prof_b) cudaEventRecord(pc.b, c->sf);
     CK(c, cudaEventRecord(c->ev_f[B % NEV], c->sf));
+    }
     // ---- x-chain (sx), one step at a time
     for (int b = 0; b < nb; ++b) {
       const int64_t k = kb0 + b;
@@ -1781,13 +1806,13 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
         if (rc) return rc;
       }
       if (b == 0) {
-        CK(c, cudaStreamWaitEvent(c->sx, c->ev_f[B % NEV], 0));
+        if (own) CK(c, cudaStreamWaitEvent(c->sx, c->ev_f[B % NEV], 0));
         // the x-chain's own time: not the wait for the batch's factors
         if (c->prof && k >= k0) cudaEventRecord(px.a, c->sx);
       }
       const int record = (k % record_every == 0 || k == K) ? 1 : 0;
       {
-        int rc = enqueue_x_chain(c, W, k, set * D + b, alpha, record, (int)(epoch0 + k));
+        int rc = enqueue_x_chain(c, W, k, set * D + b, alpha, record, (int)(epoch0 + k), own);
         if (rc) return rc;
       }
       if (c->prof && k >= k0) cudaEventRecord(px.b, c->sx);
@@ -2115,5 +2140,309 @@ static int potrf_impl(int32_t device, const double* G, int64_t N, double* L_out,
       L_out[p * N + q] = v;
     }
   if (herr) FAIL((slim_ctx*)nullptr, SLIM_ENOTSPD, "matrix is not positive definite");
+  return SLIM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// streaming-kernel probe (bench.py "streaming"): the x-chain / Gram passes that
+// stream the operator, each launch on a different window of resident blocks,
+// L2 flushed between launches (a 256 MB read, so no dirty lines are written
+// back during the probed kernel), one event pair per launch (cold-cache kernel
+// time, like ncu's serialised launch list). Algorithmic bytes per launch as
+// every operator byte the launch must read once, plus the
+// vectors it reads and writes.
+// ---------------------------------------------------------------------------
+extern "C" int slim_probe_stream(slim_ctx* c, int32_t kernel, int32_t reps, double* us_out,
+                                 double* bytes_out) {
+  if (!c || kernel < 0 || kernel > 2 || reps < 1) FAIL(c, SLIM_EINVAL, "bad argument");
+  const bool gen = c->layout == SLIM_GEN_SPLITMIX64;
+  const bool csr = c->layout == SLIM_CSR_PERBLOCK;
+  if (kernel == 2 && gen) FAIL(c, SLIM_EINVAL, "generated blocks: the Gram is the tensor-core kernel");
+  CK(c, cudaSetDevice(c->dev));
+  std::vector<int64_t> res;  // storage blocks with data in HBM
+  if (gen) {
+    for (int64_t s = 0; s < c->S; ++s) res.push_back(s);
+  } else {
+    for (int64_t b = 0; b < c->M; ++b)
+      if (c->resident.empty() || c->resident[b]) res.push_back(b);
+  }
+  if (res.empty()) FAIL(c, SLIM_EINVAL, "no resident blocks (run or upload first)");
+  const int ell = (int)c->ell, n = (int)c->n;
+  const int nw = (int)std::min<int64_t>(c->r + 1, (int64_t)res.size());
+  const int vb = c->vdt == SLIM_F64 ? 8 : 4;
+  const size_t flush_bytes = (size_t)256 << 20;  // > 126 MB L2
+  void* flush = nullptr;
+  double* panel = nullptr;
+  Ctl* ctl = nullptr;
+  auto cleanup = [&]() {
+    if (flush) cudaFree(flush);
+    if (panel) cudaFree(panel);
+    if (ctl) cudaFree(ctl);
+  };
+  if (cudaMalloc(&flush, flush_bytes) != cudaSuccess || cudaMalloc(&ctl, sizeof(Ctl)) != cudaSuccess ||
+      (kernel == 2 && cudaMalloc(&panel, sizeof(double) * (size_t)c->panel_stride) != cudaSuccess)) {
+    cleanup();
+    FAIL(c, SLIM_ENOMEM, "probe scratch allocation failed");
+  }
+  cudaMemset(ctl, 0, sizeof(Ctl));
+  cudaMemset(flush, 0x5a, flush_bytes);
+  cudaStream_t s = c->sx;
+  std::vector<cudaEvent_t> ev(2 * (size_t)reps);
+  for (auto& e : ev) cudaEventCreate(&e);
+  double bytes_sum = 0.0;
+  const int warm = 2;
+  for (int t = -warm; t < reps; ++t) {
+    const int64_t u = (int64_t)(t + warm);
+    Window W{};
+    W.nw = nw;
+    W.ell = ell;
+    W.newp = nw - 1;
+    for (int P = 0; P < nw; ++P) {
+      const int64_t b = res[(size_t)((u * nw + P) % (int64_t)res.size())];
+      W.blk[P] = (int)b;
+      W.slot[P] = gen ? (int)b : P;
+      W.age[P] = nw - 1 - P;
+    }
+    auto blk_nnz = [&](int64_t b) { return (double)(c->h_blkbase[b + 1] - c->h_blkbase[b]); };
+    double bytes = 0.0;
+    launch_flush_read(flush, flush_bytes, (unsigned*)ctl + sizeof(Ctl) / 4 - 1, s);
+    if (t >= 0) cudaEventRecord(ev[2 * t], s);
+    if (kernel == 0) {  // K1: r = A_k x - b_k
+      const int64_t b = W.blk[W.newp];
+      const int64_t row0 = b * c->ell;
+      if (csr) {
+        bytes = blk_nnz(b) * (4 + vb) + 8.0 * (ell + 1) + 16.0 * ell + 8.0 * n;
+        if (vb == 8)
+          launch_residual_csr<double>(c->rvec, c->rowptr, c->col, (const double*)c->val, row0, row0, ell,
+                                      c->x, c->b, ctl, s);
+        else
+          launch_residual_csr<float>(c->rvec, c->rowptr, c->col, (const float*)c->val, row0, row0, ell,
+                                     c->x, c->b, ctl, s);
+      } else {
+        bytes = (double)ell * n * vb + 16.0 * ell + 8.0 * n;
+        if (gen)
+          launch_residual_dense<float>(c->rvec, c->gring, c->n, row0, 0, ell, n, c->x, c->b, ctl,
+                                       c->rsplit, s);
+        else if (vb == 8)
+          launch_residual_dense<double>(c->rvec, (const double*)c->A, c->n, row0, row0, ell, n, c->x,
+                                        c->b, ctl, c->rsplit, s);
+        else
+          launch_residual_dense<float>(c->rvec, (const float*)c->A, c->n, row0, row0, ell, n, c->x,
+                                       c->b, ctl, c->rsplit, s);
+      }
+    } else if (kernel == 1) {  // K5: s = M_k^T w
+      const int N = nw * ell;
+      if (csr) {
+        bytes = 8.0 * N + 8.0 * n;
+        for (int P = 0; P < nw; ++P) bytes += 4.0 * (n + 1) + blk_nnz(W.blk[P]) * (4 + vb);
+        if (vb == 8)
+          launch_mtw_csc<double>(c->spart, W, c->colptr, n, c->cscrow, (const double*)c->cscval,
+                                 c->blkbase, c->wvec, ctl, s);
+        else
+          launch_mtw_csc<float>(c->spart, W, c->colptr, n, c->cscrow, (const float*)c->cscval,
+                                c->blkbase, c->wvec, ctl, s);
+      } else {
+        const int nsplit = std::min(c->nsplit_mtw, N);
+        bytes = (double)N * n * vb + 8.0 * N + 8.0 * nsplit * n;
+        if (gen)
+          launch_mtw_dense<float>(c->spart, nsplit, W, c->gring, c->n, n, c->wvec, ctl, s);
+        else if (vb == 8)
+          launch_mtw_dense<double>(c->spart, nsplit, W, (const double*)c->A, c->n, n, c->wvec, ctl, s);
+        else
+          launch_mtw_dense<float>(c->spart, nsplit, W, (const float*)c->A, c->n, n, c->wvec, ctl, s);
+      }
+    } else {  // K2: the new Gram panel A_k M_k^T
+      const int N = nw * ell;
+      const int64_t nb = W.blk[W.newp];
+      if (csr) {
+        bytes = 8.0 * N * ell + 4.0 * (n + 1) + blk_nnz(nb) * (4 + vb);
+        for (int P = 0; P < nw; ++P) bytes += blk_nnz(W.blk[P]) * (4 + vb) + 8.0 * (ell + 1);
+        const int* cpn = c->colptr + nb * (c->n + 1);
+        if (vb == 8)
+          launch_gram_csr<double>(panel, W, c->rowptr, c->col, (const double*)c->val, cpn, c->cscrow,
+                                  (const double*)c->cscval, c->h_blkbase[nb], s);
+        else
+          launch_gram_csr<float>(panel, W, c->rowptr, c->col, (const float*)c->val, cpn, c->cscrow,
+                                 (const float*)c->cscval, c->h_blkbase[nb], s);
+      } else {
+        bytes = (double)N * n * vb + 8.0 * N * ell * (1 + c->nsplit_gram);
+        if (vb == 8)
+          launch_gram_dense<double>(panel, c->gpart, c->nsplit_gram, W, (const double*)c->A, c->n,
+                                    nb * c->ell, n, s);
+        else
+          launch_gram_dense<float>(panel, c->gpart, c->nsplit_gram, W, (const float*)c->A, c->n,
+                                   nb * c->ell, n, s);
+      }
+    }
+    if (t >= 0) cudaEventRecord(ev[2 * t + 1], s), bytes_sum += bytes;
+  }
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  double ms_sum = 0.0;
+  for (int t = 0; t < reps && e == cudaSuccess; ++t) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev[2 * t], ev[2 * t + 1]);
+    ms_sum += ms;
+  }
+  for (auto& x : ev) cudaEventDestroy(x);
+  cleanup();
+  if (e != cudaSuccess) FAIL(c, SLIM_ECUDA, "probe kernel failed: %s", cudaGetErrorString(e));
+  if (us_out) *us_out = 1e3 * ms_sum / reps;
+  if (bytes_out) *bytes_out = bytes_sum / reps;
+  return SLIM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// device projector: the tomography operator traced on the
+// GPU into this context's CSR arrays (tomo.py:304-320 build_projector, with
+// the views' rows optionally permuted per view as the configs[3] sub-blocks)
+// ---------------------------------------------------------------------------
+namespace slim {
+void view_geometry_2d(double angle_deg, double* g);
+void view_geometry_3d(const double* dir, double* g);
+}  // namespace slim
+
+extern "C" int slim_build_projector(slim_ctx* c, int32_t dims, int64_t grid, int64_t rays,
+                                    int64_t n_views, const double* views, double spacing,
+                                    const int32_t* ray_of_row) {
+  if (!c || !views) FAIL(c, SLIM_EINVAL, "null argument");
+  if (c->layout != SLIM_CSR_PERBLOCK) FAIL(c, SLIM_EINVAL, "context layout is not CSR");
+  if (dims != 2 && dims != 3) FAIL(c, SLIM_EINVAL, "dims must be 2 or 3");
+  if (grid < 1 || rays < 1 || n_views < 1 || !(spacing > 0)) FAIL(c, SLIM_EINVAL, "bad geometry");
+  const int64_t cols = dims == 2 ? grid * grid : grid * grid * grid;
+  const int64_t rpv = dims == 2 ? rays : rays * rays;
+  if (cols > 0x7fffffffLL) FAIL(c, SLIM_EINVAL, "grid too large for int32 columns");
+  if (cols != c->n || c->col_offset != 0)
+    FAIL(c, SLIM_EINVAL, "projector has %lld columns, the context %lld (unsharded)", (long long)cols,
+         (long long)c->n);
+  if (rpv * n_views != c->m)
+    FAIL(c, SLIM_EINVAL, "projector has %lld rows, the context %lld", (long long)(rpv * n_views),
+         (long long)c->m);
+  if (ray_of_row)
+    for (int64_t i = 0; i < c->m; ++i)
+      if (ray_of_row[i] < 0 || ray_of_row[i] >= rpv)
+        FAIL(c, SLIM_EINVAL, "ray_of_row[%lld] = %d out of range", (long long)i, ray_of_row[i]);
+  CK(c, cudaSetDevice(c->dev));
+  std::vector<double> geo((size_t)9 * n_views);
+  for (int64_t v = 0; v < n_views; ++v) {
+    if (dims == 2) view_geometry_2d(views[v], &geo[9 * v]);
+    else view_geometry_3d(views + 3 * v, &geo[9 * v]);
+  }
+  double* dgeo = nullptr;
+  int* dmap = nullptr;
+  int* derr = nullptr;
+  auto cleanup = [&]() {
+    if (dgeo) cudaFree(dgeo);
+    if (dmap) cudaFree(dmap);
+    if (derr) cudaFree(derr);
+  };
+  if (cudaMalloc(&dgeo, sizeof(double) * geo.size()) != cudaSuccess ||
+      cudaMalloc(&derr, sizeof(int)) != cudaSuccess ||
+      (ray_of_row && cudaMalloc(&dmap, sizeof(int) * c->m) != cudaSuccess)) {
+    cleanup();
+    FAIL(c, SLIM_ENOMEM, "projector scratch allocation failed");
+  }
+  cudaMemcpy(dgeo, geo.data(), sizeof(double) * geo.size(), cudaMemcpyHostToDevice);
+  if (dmap) cudaMemcpy(dmap, ray_of_row, sizeof(int) * c->m, cudaMemcpyHostToDevice);
+  cudaMemset(derr, 0, sizeof(int));
+  SiddonSpec S{};
+  S.dims = dims;
+  S.grid = grid;
+  S.rows_per_view = rpv;
+  S.side = rays;
+  S.spacing = spacing;
+  S.views = dgeo;
+  S.ray_of_row = dmap;
+  S.m = c->m;
+  for (void** pp : {(void**)&c->rowptr, (void**)&c->col, (void**)&c->val})
+    if (*pp) cache_release(*pp), *pp = nullptr;
+  c->hs_rowptr.clear();
+  c->h_have.clear();
+  c->resident.clear();
+  c->streaming = false;
+  if (cudaMalloc((void**)&c->rowptr, sizeof(int64_t) * (c->m + 1)) != cudaSuccess) {
+    c->rowptr = nullptr;
+    cleanup();
+    FAIL(c, SLIM_ENOMEM, "row pointer allocation failed");
+  }
+  cudaError_t e = siddon_count(S, c->rowptr, c->sx);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->sx);
+  if (e != cudaSuccess) {
+    cleanup();
+    FAIL(c, SLIM_ECUDA, "projector count pass failed: %s", cudaGetErrorString(e));
+  }
+  // block bases: rowptr[bk * ell], bk = 0..M
+  c->h_blkbase.assign(c->M + 1, 0);
+  CK(c, cudaMemcpy2D(c->h_blkbase.data(), sizeof(int64_t), c->rowptr, sizeof(int64_t) * c->ell,
+                     sizeof(int64_t), c->M + 1, cudaMemcpyDeviceToHost));
+  for (int64_t bk = 0; bk < c->M; ++bk)
+    if (c->h_blkbase[bk + 1] - c->h_blkbase[bk] > 0x7fffffffLL) {
+      cleanup();
+      FAIL(c, SLIM_EINVAL, "block %lld has more than 2^31 nonzeros", (long long)bk + 1);
+    }
+  c->nnz = c->h_blkbase[c->M];
+  ALLOC(c, c->col, sizeof(int) * (size_t)std::max<int64_t>(1, c->nnz));
+  ALLOC(c, c->val, c->vsize * (size_t)std::max<int64_t>(1, c->nnz));
+  e = siddon_fill(S, c->rowptr, c->col, c->val, c->vdt == SLIM_F64, derr, c->sx);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->sx);
+  int herr = 0;
+  if (e == cudaSuccess) e = cudaMemcpy(&herr, derr, sizeof(int), cudaMemcpyDeviceToHost);
+  cleanup();
+  if (e != cudaSuccess) FAIL(c, SLIM_ECUDA, "projector fill pass failed: %s", cudaGetErrorString(e));
+  if (herr) FAIL(c, SLIM_ESTATE, "device projector: inconsistent ray (code %d)", herr);
+  c->op_ready = false;
+  return SLIM_OK;
+}
+
+extern "C" int slim_apply(slim_ctx* c, const double* x, double* out) {
+  if (!c || !x || !out) FAIL(c, SLIM_EINVAL, "null argument");
+  if (c->layout == SLIM_GEN_SPLITMIX64) return slim_gen_apply(c, x, out);
+  if (c->layout != SLIM_CSR_PERBLOCK || !c->rowptr || !c->col)
+    FAIL(c, SLIM_ESTATE, "no resident CSR operator");
+  if (!c->resident.empty())
+    for (char r : c->resident)
+      if (!r) FAIL(c, SLIM_ESTATE, "operator is host-streamed (not all blocks resident)");
+  CK(c, cudaSetDevice(c->dev));
+  double *dx = nullptr, *dy = nullptr;
+  if (cudaMalloc(&dx, sizeof(double) * c->n) != cudaSuccess ||
+      cudaMalloc(&dy, sizeof(double) * c->m) != cudaSuccess) {
+    if (dx) cudaFree(dx);
+    FAIL(c, SLIM_ENOMEM, "apply scratch allocation failed");
+  }
+  cudaMemcpy(dx, x, sizeof(double) * c->n, cudaMemcpyHostToDevice);
+  cudaError_t e = csr_spmv(c->rowptr, c->col, c->val, c->vdt == SLIM_F64, dx, dy, c->m, c->sx);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->sx);
+  if (e == cudaSuccess) e = cudaMemcpy(out, dy, sizeof(double) * c->m, cudaMemcpyDeviceToHost);
+  cudaFree(dx);
+  cudaFree(dy);
+  if (e != cudaSuccess) FAIL(c, SLIM_ECUDA, "apply failed: %s", cudaGetErrorString(e));
+  return SLIM_OK;
+}
+
+extern "C" int slim_get_csr_block(slim_ctx* c, int64_t block, int64_t* rowptr_out, int32_t* col_out,
+                                  void* val_out) {
+  if (!c || !rowptr_out) FAIL(c, SLIM_EINVAL, "null argument");
+  if (c->layout != SLIM_CSR_PERBLOCK || !c->rowptr) FAIL(c, SLIM_ESTATE, "no resident CSR operator");
+  if (block < 1 || block > c->M)
+    FAIL(c, SLIM_ERANGE, "block index %lld out of range 1..%lld", (long long)block, (long long)c->M);
+  if (!c->resident.empty() && !c->resident[block - 1])
+    FAIL(c, SLIM_ESTATE, "block %lld is not resident", (long long)block);
+  CK(c, cudaSetDevice(c->dev));
+  CK(c, cudaDeviceSynchronize());
+  const int64_t r0 = (block - 1) * c->ell;
+  CK(c, cudaMemcpy(rowptr_out, c->rowptr + r0, sizeof(int64_t) * (c->ell + 1), cudaMemcpyDeviceToHost));
+  const int64_t base = rowptr_out[0], nnzb = rowptr_out[c->ell] - base;
+  for (int64_t i = 0; i <= c->ell; ++i) rowptr_out[i] -= base;
+  if (col_out && nnzb)
+    CK(c, cudaMemcpy(col_out, c->col + base, sizeof(int) * nnzb, cudaMemcpyDeviceToHost));
+  if (val_out && nnzb)
+    CK(c, cudaMemcpy(val_out, (const char*)c->val + c->vsize * base, c->vsize * nnzb,
+                     cudaMemcpyDeviceToHost));
+  return SLIM_OK;
+}
+
+extern "C" int slim_nnz(slim_ctx* c, int64_t* nnz_out) {
+  if (!c || !nnz_out) FAIL(c, SLIM_EINVAL, "null argument");
+  *nnz_out = c->layout == SLIM_CSR_PERBLOCK ? (c->h_blkbase.empty() ? c->nnz : c->h_blkbase.back()) : 0;
   return SLIM_OK;
 }

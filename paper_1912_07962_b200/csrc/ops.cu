@@ -28,64 +28,108 @@ namespace slim {
 // streams the block (one warp per row leaves most SMs idle):
 //   residual:  r[row] = A[row0 + row, :] . x - b[brow0 + row]
 //   diagonal:  out[row * ld + row] = A[row, :] . A[row, :]     (SQUARE)
-// CTA (chunk, row) writes a partial; the last CTA of a row (counter) adds
-// the partials in chunk order, so the result is deterministic.
-template <typename T, bool SQUARE>
+// CTA (chunk, group) covers RD_ROWS rows of one column chunk: every thread
+// loads its x values once (16-byte loads) and streams the group's rows with
+// RD_ROWS independent 16-byte loads in flight, so x costs 1/RD_ROWS of the A
+// traffic. Each CTA writes one partial per row; the last CTA of a group
+// (counter) adds the partials in chunk order, so the result is deterministic.
+template <typename T, bool SQUARE, int RD_ROWS>
 __global__ void __launch_bounds__(256) k_rowdot(const T* __restrict__ A, int64_t lda, int64_t row0,
-                                                int n, const double* __restrict__ x, RowSplit rs,
-                                                double* __restrict__ out, int64_t ld_out,
-                                                const double* __restrict__ b, int64_t brow0,
-                                                const Ctl* ctl) {
+                                                int n, int ell, const double* __restrict__ x,
+                                                RowSplit rs, double* __restrict__ out,
+                                                int64_t ld_out, const double* __restrict__ b,
+                                                int64_t brow0, const Ctl* ctl) {
   if (ctl != nullptr && ctl->diverged_at != 0) return;
   constexpr int V = 16 / sizeof(T);
-  const int chunk = blockIdx.x, row = blockIdx.y, tid = threadIdx.x;
+  const int chunk = blockIdx.x, grp = blockIdx.y, tid = threadIdx.x;
+  const int r0 = grp * RD_ROWS, nr = min(RD_ROWS, ell - r0);
   const int nch = rs.nch;
   const int csz = ((n + nch - 1) / nch + V - 1) / V * V;
   const int c0 = chunk * csz, c1 = min(n, c0 + csz);
-  const T* a = A + (row0 + row) * lda;
-  double s0 = 0.0, s1 = 0.0;
-  if (rs.vec) {
-#pragma unroll 2
-    for (int c = c0 + V * tid; c < c1; c += V * 256) {
-      T v[V];
-      *reinterpret_cast<uint4*>(v) = *reinterpret_cast<const uint4*>(a + c);
+  const T* a = A + (row0 + r0) * lda;
+  double acc[RD_ROWS];
 #pragma unroll
-      for (int e = 0; e < V; ++e) {
-        const double ve = to_f64(v[e]);
-        if (e & 1) s1 = fma(ve, SQUARE ? ve : x[c + e], s1);
-        else s0 = fma(ve, SQUARE ? ve : x[c + e], s0);
+  for (int q = 0; q < RD_ROWS; ++q) acc[q] = 0.0;
+  if (rs.vec) {
+#pragma unroll(RD_ROWS == 1 ? 4 : 1)
+    for (int c = c0 + V * tid; c < c1; c += V * 256) {
+      double xv[V];
+      if (!SQUARE) {
+#pragma unroll
+        for (int e = 0; e < V; e += 2) {
+          const double2 t = __ldg(reinterpret_cast<const double2*>(x + c + e));
+          xv[e] = t.x, xv[e + 1] = t.y;
+        }
       }
+      T v[RD_ROWS][V];
+#pragma unroll
+      for (int q = 0; q < RD_ROWS; ++q)
+        if (q < nr)
+          *reinterpret_cast<uint4*>(v[q]) =
+              __ldcs(reinterpret_cast<const uint4*>(a + (int64_t)q * lda + c));
+#pragma unroll
+      for (int q = 0; q < RD_ROWS; ++q)
+        if (q < nr) {
+#pragma unroll
+          for (int e = 0; e < V; ++e) {
+            const double ve = to_f64(v[q][e]);
+            acc[q] = fma(ve, SQUARE ? ve : xv[e], acc[q]);
+          }
+        }
     }
   } else {
     for (int c = c0 + tid; c < c1; c += 256) {
-      const double ve = to_f64(a[c]);
-      s0 = fma(ve, SQUARE ? ve : x[c], s0);
+      const double xc = SQUARE ? 0.0 : x[c];
+#pragma unroll
+      for (int q = 0; q < RD_ROWS; ++q)
+        if (q < nr) {
+          const double ve = to_f64(a[(int64_t)q * lda + c]);
+          acc[q] = fma(ve, SQUARE ? ve : xc, acc[q]);
+        }
     }
   }
-  double sv = warp_sum(s0 + s1);
-  __shared__ double ws[8];
+  __shared__ double ws[8][RD_ROWS];
   __shared__ bool last;
-  if ((tid & 31) == 0) ws[tid >> 5] = sv;
+#pragma unroll
+  for (int q = 0; q < RD_ROWS; ++q) {
+    const double v = warp_sum(acc[q]);
+    if ((tid & 31) == 0) ws[tid >> 5][q] = v;
+  }
   __syncthreads();
-  if (tid == 0) {
+  if (tid < nr) {
     double t = 0.0;
-    for (int w = 0; w < 8; ++w) t += ws[w];
-    rs.part[(int64_t)row * nch + chunk] = t;
+    for (int w = 0; w < 8; ++w) t += ws[w][tid];
+    rs.part[(int64_t)(r0 + tid) * nch + chunk] = t;
     __threadfence();
-    last = atomicAdd(&rs.cnt[row], 1) == nch - 1;
-    if (last) {
-      __threadfence();
+  }
+  __syncthreads();
+  if (tid == 0) last = atomicAdd(&rs.cnt[grp], 1) == nch - 1;
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    if (tid < nr) {
+      const int row = r0 + tid;
       double tot = 0.0;
       for (int z = 0; z < nch; ++z) tot += __ldcg(&rs.part[(int64_t)row * nch + z]);
       if (SQUARE) out[(int64_t)row * ld_out + row] = tot;
       else out[row] = tot - b[brow0 + row];
-      rs.cnt[row] = 0;  // ready for the next launch (stream-ordered)
     }
+    if (tid == 0) rs.cnt[grp] = 0;  // ready for the next launch (stream-ordered)
   }
 }
 
+// rows per CTA: 8 when the blocks are wide enough to give every SM several
+// (chunk, group) CTAs, else 1 (narrow dense blocks, configs[0])
+int rowdot_rows(int ell, int64_t n) {
+  const int64_t ctas8 = (int64_t)((ell + 7) / 8) * std::min<int64_t>(64, std::max<int64_t>(1, n / 2048));
+  return ctas8 >= 2 * 148 ? 8 : 1;
+}
 int rowdot_chunks(int ell, int64_t n) {
-  int nch = (int)((4 * 148 + ell - 1) / ell);
+  const int R = rowdot_rows(ell, n);
+  const int groups = (ell + R - 1) / R;
+  // R = 8: one full wave (3 resident CTAs of 256 threads per SM at ~80
+  // registers), so no second partial wave; R = 1: 4 CTAs per SM
+  int nch = R == 8 ? std::max(1, 3 * 148 / groups) : (int)((4 * 148 + groups - 1) / groups);
   nch = (int)std::min<int64_t>(nch, std::max<int64_t>(1, n / 2048));
   return std::max(1, std::min(nch, 64));
 }
@@ -140,8 +184,11 @@ __global__ void __launch_bounds__(256) k_gen_apply(double* __restrict__ out, uin
   if (lane == 0) out[row] = s;
 }
 
+// one CTA (RES_THREADS) per row, four independent nonzeros in flight per
+// thread; partial sums added in a fixed order (deterministic)
+constexpr int RES_THREADS = 128;
 template <typename T>
-__global__ void __launch_bounds__(256) k_residual_csr(double* r, const int64_t* __restrict__ rowptr,
+__global__ void __launch_bounds__(RES_THREADS) k_residual_csr(double* r, const int64_t* __restrict__ rowptr,
                                                       const int* __restrict__ col,
                                                       const T* __restrict__ val, int64_t row0,
                                                       int64_t brow0, int ell,
@@ -149,13 +196,32 @@ __global__ void __launch_bounds__(256) k_residual_csr(double* r, const int64_t* 
                                                       const double* __restrict__ b,
                                                       const Ctl* ctl) {
   if (ctl->diverged_at != 0) return;
-  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (row >= ell) return;
+  const int row = blockIdx.x, tid = threadIdx.x;
   const int64_t lo = rowptr[row0 + row], hi = rowptr[row0 + row + 1];
-  double s = 0.0;
-  for (int64_t e = lo + lane; e < hi; e += 32) s += to_f64(val[e]) * x[col[e]];
-  s = warp_sum(s);
-  if (lane == 0) r[row] = s - b[brow0 + row];
+  constexpr int S = RES_THREADS;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int64_t e = lo + tid;
+  for (; e + 3 * S < hi; e += 4 * S) {
+    const int k0 = __ldcs(col + e), k1 = __ldcs(col + e + S), k2 = __ldcs(col + e + 2 * S),
+              k3 = __ldcs(col + e + 3 * S);
+    const double v0 = to_f64(__ldcs(val + e)), v1 = to_f64(__ldcs(val + e + S)),
+                 v2 = to_f64(__ldcs(val + e + 2 * S)), v3 = to_f64(__ldcs(val + e + 3 * S));
+    s0 = fma(v0, __ldg(x + k0), s0);
+    s1 = fma(v1, __ldg(x + k1), s1);
+    s2 = fma(v2, __ldg(x + k2), s2);
+    s3 = fma(v3, __ldg(x + k3), s3);
+  }
+  for (; e < hi; e += S) s0 = fma(to_f64(val[e]), x[col[e]], s0);
+  const double sv = warp_sum((s0 + s1) + (s2 + s3));
+  __shared__ double ws[S / 32];
+  if ((tid & 31) == 0) ws[tid >> 5] = sv;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < S / 32; ++w) t += ws[w];
+    r[row] = t - b[brow0 + row];
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -350,7 +416,12 @@ __global__ void __launch_bounds__(256) k_mtw_dense(double* __restrict__ part, Wi
   for (int e = 0; e < V; ++e) part[(int64_t)blockIdx.y * n + c + e] = s[e];
 }
 
-template <typename T>
+// one thread per column; the window's blocks are taken MTW_GROUP at a time
+// with every block's column range and first nonzero loaded before any is
+// used, so a thread waits on ~3 dependent loads per group instead of per
+// block (the kernel was latency-bound at 3 chains x r + 1 blocks). The
+// accumulation order (block, then nonzero) is unchanged.
+template <typename T, int MTW_GROUP>
 __global__ void __launch_bounds__(256) k_mtw_csc(double* __restrict__ s_out, Window W,
                                                  const int* __restrict__ colptr, int n,
                                                  const int* __restrict__ cscrow,
@@ -362,13 +433,40 @@ __global__ void __launch_bounds__(256) k_mtw_csc(double* __restrict__ s_out, Win
   if (c >= n) return;
   const int ell = W.ell;
   double s = 0.0;
-  for (int P = 0; P < W.nw; ++P) {
-    const int b = W.blk[P];
-    const int* cp = colptr + (int64_t)b * (n + 1);
-    const int lo = cp[c], hi = cp[c + 1];
-    const int64_t base = blkbase[b];
-    const double* wp = w + P * ell;
-    for (int e = lo; e < hi; ++e) s += to_f64(cscval[base + e]) * wp[cscrow[base + e]];
+  for (int P0 = 0; P0 < W.nw; P0 += MTW_GROUP) {
+    int lo[MTW_GROUP], hi[MTW_GROUP];
+    int64_t base[MTW_GROUP];
+#pragma unroll
+    for (int q = 0; q < MTW_GROUP; ++q) {
+      lo[q] = hi[q] = 0;
+      base[q] = 0;
+      if (P0 + q < W.nw) {
+        const int bk = W.blk[P0 + q];
+        const int* cp = colptr + (int64_t)bk * (n + 1);
+        lo[q] = __ldcs(cp + c);
+        hi[q] = __ldcs(cp + c + 1);
+        base[q] = __ldg(blkbase + bk);
+      }
+    }
+    double v[MTW_GROUP], wv[MTW_GROUP];
+#pragma unroll
+    for (int q = 0; q < MTW_GROUP; ++q) {
+      v[q] = 0.0, wv[q] = 0.0;
+      if (lo[q] < hi[q]) {
+        const int64_t e = base[q] + lo[q];
+        v[q] = to_f64(__ldcs(cscval + e));
+        wv[q] = __ldg(w + (P0 + q) * ell + __ldcs(cscrow + e));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < MTW_GROUP; ++q) {
+      if (lo[q] < hi[q]) {
+        s += v[q] * wv[q];
+        const double* wp = w + (P0 + q) * ell;
+        for (int e = lo[q] + 1; e < hi[q]; ++e)
+          s += to_f64(cscval[base[q] + e]) * wp[cscrow[base[q] + e]];
+      }
+    }
   }
   s_out[c] = s;
 }
@@ -697,7 +795,12 @@ void launch_residual_dense(double* r, const T* A, int64_t lda, int64_t row0, int
                            RowSplit rs, cudaStream_t s) {
   constexpr int V = 16 / sizeof(T);
   rs.vec = (n % V == 0 && lda % V == 0) ? 1 : 0;
-  k_rowdot<T, false><<<dim3(rs.nch, ell), 256, 0, s>>>(A, lda, row0, n, x, rs, r, 0, b, brow0, ctl);
+  if (rowdot_rows(ell, n) == 8)
+    k_rowdot<T, false, 8><<<dim3(rs.nch, cdiv(ell, 8)), 256, 0, s>>>(A, lda, row0, n, ell, x, rs, r, 0,
+                                                                     b, brow0, ctl);
+  else
+    k_rowdot<T, false, 1><<<dim3(rs.nch, ell), 256, 0, s>>>(A, lda, row0, n, ell, x, rs, r, 0, b,
+                                                            brow0, ctl);
 }
 void launch_gen_block(float* dst, float* hi, float* lo, uint64_t seed, int64_t row0, int ell,
                       int n_local, int64_t n_total, int64_t col0, cudaStream_t s) {
@@ -713,7 +816,7 @@ template <typename T>
 void launch_residual_csr(double* r, const int64_t* rowptr, const int* col, const T* val,
                          int64_t row0, int64_t brow0, int ell, const double* x, const double* b,
                          const Ctl* ctl, cudaStream_t s) {
-  k_residual_csr<T><<<cdiv(ell, 8), 256, 0, s>>>(r, rowptr, col, val, row0, brow0, ell, x, b, ctl);
+  k_residual_csr<T><<<ell, RES_THREADS, 0, s>>>(r, rowptr, col, val, row0, brow0, ell, x, b, ctl);
 }
 template <typename T>
 void launch_gram_csr(double* panel, const Window& W, const int64_t* rowptr, const int* col,
@@ -747,8 +850,12 @@ void launch_gram_dense(double* panel, double* part, int nsplit, const Window& W,
 void launch_gram_diag_fp64(double* panel_diag, int64_t ld, const float* A, int ell, int n,
                            RowSplit rs, cudaStream_t s) {
   rs.vec = (n % 4 == 0) ? 1 : 0;
-  k_rowdot<float, true><<<dim3(rs.nch, ell), 256, 0, s>>>(A, n, 0, n, nullptr, rs, panel_diag, ld,
-                                                           nullptr, 0, nullptr);
+  if (rowdot_rows(ell, n) == 8)
+    k_rowdot<float, true, 8><<<dim3(rs.nch, cdiv(ell, 8)), 256, 0, s>>>(
+        A, n, 0, n, ell, nullptr, rs, panel_diag, ld, nullptr, 0, nullptr);
+  else
+    k_rowdot<float, true, 1><<<dim3(rs.nch, ell), 256, 0, s>>>(A, n, 0, n, ell, nullptr, rs, panel_diag,
+                                                               ld, nullptr, 0, nullptr);
 }
 
 void launch_gram_reduce(double* panel, const Window& W, const double* part, int nsplit,
@@ -775,12 +882,35 @@ template <typename T>
 void launch_mtw_csc(double* s_out, const Window& W, const int* colptr, int n, const int* cscrow,
                     const T* cscval, const int64_t* blkbase, const double* w, const Ctl* ctl,
                     cudaStream_t s) {
-  k_mtw_csc<T><<<cdiv(n, 256), 256, 0, s>>>(s_out, W, colptr, n, cscrow, cscval, blkbase, w, ctl);
+  static const int grp = getenv("SLIM_MTW_GROUP") ? atoi(getenv("SLIM_MTW_GROUP")) : 3;
+  if (grp <= 1)
+    k_mtw_csc<T, 1><<<cdiv(n, 256), 256, 0, s>>>(s_out, W, colptr, n, cscrow, cscval, blkbase, w, ctl);
+  else if (grp == 2)
+    k_mtw_csc<T, 2><<<cdiv(n, 256), 256, 0, s>>>(s_out, W, colptr, n, cscrow, cscval, blkbase, w, ctl);
+  else if (grp <= 4)
+    k_mtw_csc<T, 3><<<cdiv(n, 256), 256, 0, s>>>(s_out, W, colptr, n, cscrow, cscval, blkbase, w, ctl);
+  else
+    k_mtw_csc<T, 6><<<cdiv(n, 256), 256, 0, s>>>(s_out, W, colptr, n, cscrow, cscval, blkbase, w, ctl);
 }
 void launch_finish(const FinishParams& F, cudaStream_t s) {
   k_finish<<<cdiv(F.n, 256), 256, 0, s>>>(F);
 }
 int finish_grid(int n) { return (int)cdiv(n, 256); }
+// L2 flush by reading (the lines it leaves are clean, so the next kernel's
+// DRAM bandwidth is not shared with write-backs)
+__global__ void __launch_bounds__(256) k_flush_read(const uint4* __restrict__ p, int64_t count,
+                                                    unsigned* sink) {
+  unsigned acc = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 v = __ldcg(p + i);
+    acc ^= v.x ^ v.y ^ v.z ^ v.w;
+  }
+  if (acc == 0x9e3779b9u) *sink = acc;  // keeps the loads
+}
+void launch_flush_read(const void* buf, size_t bytes, unsigned* sink, cudaStream_t s) {
+  k_flush_read<<<148 * 8, 256, 0, s>>>((const uint4*)buf, (int64_t)(bytes / 16), sink);
+}
 void launch_stamp_start(Ctl* ctl, cudaStream_t s) { k_stamp_start<<<1, 1, 0, s>>>(ctl); }
 void launch_record(const RecordParams& R, cudaStream_t s) { k_record<<<1, 32, 0, s>>>(R); }
 void launch_group_sum(double* out, const double* const* in, int nin, int64_t count,

@@ -96,5 +96,6 @@ void launch_gram_diag_fp64(double* panel_diag, int64_t ld, const float* A, int e
                            RowSplit rs, cudaStream_t s);
 int finish_grid(int n);
 void launch_stamp_start(Ctl* ctl, cudaStream_t s);
+void launch_flush_read(const void* buf, size_t bytes, unsigned* sink, cudaStream_t s);
 
 }  // namespace slim

@@ -116,26 +116,20 @@ int build_block(int64_t rays, int64_t* rowptr, int32_t* col, double* val, RayFn&
 
 }  // namespace
 
-extern "C" int slim_siddon2d_view(double angle_deg, int64_t grid, int64_t rays, double spacing,
-                                  int64_t* rowptr, int32_t* col, double* val) {
-  if (grid < 1 || rays < 1 || !rowptr || !(spacing > 0)) return SLIM_EINVAL;
-  if (grid * grid > 0x7fffffffLL) return SLIM_EINVAL;
+// per-view geometry, 9 doubles: d[3], then the 2D detector axis or the 3D
+// basis e1[3], e2[3] (tomo.py:260-262 and 276-282); shared by the host
+// builders below and the device projector (siddon.cu)
+namespace slim {
+void view_geometry_2d(double angle_deg, double* g) {
   // np.radians(x) = x * (pi / 180)
   const double theta = angle_deg * (M_PI / 180.0);
-  const double d[2] = {-std::sin(theta), std::cos(theta)};
-  const double axis[2] = {std::cos(theta), std::sin(theta)};
-  auto ray = [&](int64_t j, std::vector<Seg>& segs, std::vector<double>& ts) {
-    const double offset = ((double)j - (double)(rays - 1) / 2.0) * spacing;
-    const double p0[2] = {offset * axis[0], offset * axis[1]};
-    trace_ray(p0, d, 2, grid, segs, ts);
-  };
-  return build_block(rays, rowptr, col, val, ray);
+  for (int q = 0; q < 9; ++q) g[q] = 0.0;
+  g[0] = -std::sin(theta);
+  g[1] = std::cos(theta);
+  g[3] = std::cos(theta);
+  g[4] = std::sin(theta);
 }
-
-extern "C" int slim_siddon3d_view(const double* dir, int64_t grid, int64_t side, double spacing,
-                                  int64_t* rowptr, int32_t* col, double* val) {
-  if (!dir || grid < 1 || side < 1 || !rowptr || !(spacing > 0)) return SLIM_EINVAL;
-  if (grid * grid * grid > 0x7fffffffLL) return SLIM_EINVAL;
+void view_geometry_3d(const double* dir, double* g) {
   const double d[3] = {dir[0], dir[1], dir[2]};
   // e1 = cross(d, z), fallback cross(d, x) for near-axial d; e2 = cross(d, e1)
   auto cross = [](const double* a, const double* b, double* o) {
@@ -151,6 +145,34 @@ extern "C" int slim_siddon3d_view(const double* dir, int64_t grid, int64_t side,
   const double ne = norm3(e1);
   for (int a = 0; a < 3; ++a) e1[a] = e1[a] / ne;
   cross(d, e1, e2);
+  for (int a = 0; a < 3; ++a) g[a] = d[a], g[3 + a] = e1[a], g[6 + a] = e2[a];
+}
+}  // namespace slim
+
+extern "C" int slim_siddon2d_view(double angle_deg, int64_t grid, int64_t rays, double spacing,
+                                  int64_t* rowptr, int32_t* col, double* val) {
+  if (grid < 1 || rays < 1 || !rowptr || !(spacing > 0)) return SLIM_EINVAL;
+  if (grid * grid > 0x7fffffffLL) return SLIM_EINVAL;
+  double g[9];
+  slim::view_geometry_2d(angle_deg, g);
+  const double d[2] = {g[0], g[1]};
+  const double axis[2] = {g[3], g[4]};
+  auto ray = [&](int64_t j, std::vector<Seg>& segs, std::vector<double>& ts) {
+    const double offset = ((double)j - (double)(rays - 1) / 2.0) * spacing;
+    const double p0[2] = {offset * axis[0], offset * axis[1]};
+    trace_ray(p0, d, 2, grid, segs, ts);
+  };
+  return build_block(rays, rowptr, col, val, ray);
+}
+
+extern "C" int slim_siddon3d_view(const double* dir, int64_t grid, int64_t side, double spacing,
+                                  int64_t* rowptr, int32_t* col, double* val) {
+  if (!dir || grid < 1 || side < 1 || !rowptr || !(spacing > 0)) return SLIM_EINVAL;
+  if (grid * grid * grid > 0x7fffffffLL) return SLIM_EINVAL;
+  double g[9];
+  slim::view_geometry_3d(dir, g);
+  const double d[3] = {g[0], g[1], g[2]};
+  const double e1[3] = {g[3], g[4], g[5]}, e2[3] = {g[6], g[7], g[8]};
   auto ray = [&](int64_t j, std::vector<Seg>& segs, std::vector<double>& ts) {
     const int64_t u = j / side, v = j - u * side;
     const double off_u = ((double)u - (double)(side - 1) / 2.0) * spacing;

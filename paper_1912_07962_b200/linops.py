@@ -406,6 +406,12 @@ class DeviceOperator:
         rc = getattr(_lib.lib(), name)(self.ctx, *args)
         _lib.check(rc, self.ctx)
 
+    def nnz(self) -> int:
+        """Stored nonzeros of a CSR operator (0 for dense / generated)."""
+        out = C.c_int64(0)
+        self.call("slim_nnz", C.byref(out))
+        return out.value
+
 
 def _dense_source(op):
     a = getattr(op, "matrix", None)
@@ -424,6 +430,8 @@ def device_operator(op, r: int, device: int = 0) -> DeviceOperator:
         if key not in cache:
             cache[key] = device_operator(src.consume_all(), r, device)
         return cache[key]
+    if hasattr(src, "device_context"):  # tomo.ProjectorOperator: traced on the device
+        return src.device_context(r, device)
     cache = src.__dict__.setdefault("_slim_device_cache", {})
     key = (int(device), int(r), id(getattr(src, "_b", None)))
     dop = cache.get(key)

@@ -101,14 +101,18 @@ class _Shard:
                 dop = device_operator(shard_operator(src, self.col0, self.col1), r, device)
             self._attach(dop)
             cache[key] = dop
+        # factorizations round-robin over the shards (batch B on
+        # rank B mod P), w allreduced from its owner instead of replicated solves
+        dop.call("slim_set_factor_round_robin", 1 if getattr(self, "round_robin", False) else 0)
         return dop
 
 
 class LocalGroup:
     """P column shards on one device, driven by one host thread each."""
 
-    def __init__(self, nranks: int):
+    def __init__(self, nranks: int, round_robin: bool = False):
         self.nranks = int(nranks)
+        self.round_robin = bool(round_robin)
         self.handle = _lib.lib().slim_local_group_create(self.nranks)
         if not self.handle:
             raise ValueError("a local shard group holds 1..8 shards")
@@ -124,7 +128,9 @@ class LocalGroup:
 
     def shard(self, rank: int, n: int) -> "LocalShard":
         c0, c1 = column_ranges(n, self.nranks)[rank]
-        return LocalShard(rank, self.nranks, c0, c1, self)
+        sh = LocalShard(rank, self.nranks, c0, c1, self)
+        sh.round_robin = self.round_robin
+        return sh
 
     def run(self, method, op, make_sampler, schedule, **kw):
         """Run every shard in its own thread; returns (trajectory of rank 0 with
@@ -174,8 +180,9 @@ class NcclShard(_Shard):
     uid: bytes = b""
 
     @classmethod
-    def from_torch(cls, n: int):
-        """Create the shard for this torch.distributed rank (NCCL id broadcast)."""
+    def from_torch(cls, n: int, round_robin: bool = False):
+        """Create the shard for this torch.distributed rank (NCCL id broadcast);
+        ``round_robin``: factorizations distributed over the ranks (8f.1)."""
         import torch.distributed as dist
 
         rank, world = dist.get_rank(), dist.get_world_size()
@@ -186,7 +193,9 @@ class NcclShard(_Shard):
             obj[0] = bytes(buf.raw)
         dist.broadcast_object_list(obj, src=0)
         c0, c1 = column_ranges(n, world)[rank]
-        return cls(rank, world, c0, c1, obj[0])
+        sh = cls(rank, world, c0, c1, obj[0])
+        sh.round_robin = bool(round_robin)
+        return sh
 
     def _attach(self, dop):
         buf = C.create_string_buffer(self.uid, 128)

@@ -178,21 +178,46 @@ def tomo2d(grid=256, n_views=180, rays=362, ellipses=10, seed=2, noise=0.01,
     return _finish_tomo(parts, x_true, noise, seed, dtype)
 
 
+def tomo3d_geometry(n_views=180, side=128, sub_rows=2048, seed=4):
+    """configs[3] directions (xy-plane over [0, pi)) and the per-view seeded
+    ray permutation that defines the sub-blocks (row i of view v is ray
+    ray_of_row[v side^2 + i])."""
+    theta = np.arange(n_views) * (np.pi / n_views)
+    dirs = np.stack([np.cos(theta), np.sin(theta), np.zeros_like(theta)], axis=1)
+    rows = side * side
+    if rows % sub_rows:
+        raise ValueError("detector rows must split evenly into sub-blocks")
+    g = _rng(seed + 7)
+    ray_of_row = np.concatenate([g.permutation(rows) for _ in range(n_views)]).astype(np.int32)
+    return dirs, ray_of_row
+
+
+def projector_config(cfg_id: int):
+    """(geometry, grid, dtype, block_rows, ray_of_row) of a tomography config
+    (bench numbering 2..4 = BASELINE configs[1..3]) for the device projector."""
+    from .tomo import parallel_2d_geometry, parallel_3d_geometry
+
+    if cfg_id == 2:
+        return parallel_2d_geometry(angles_0_pi(180), 362), 256, np.float64, 362, None
+    if cfg_id == 3:
+        return parallel_2d_geometry(angles_0_pi(720), 1448), 1024, np.float32, 1448, None
+    if cfg_id == 4:
+        dirs, rmap = tomo3d_geometry(180, 128, 2048, 4)
+        return parallel_3d_geometry(dirs, 128), 128, np.float32, 2048, rmap
+    raise ValueError(f"config {cfg_id} is not a tomography config")
+
+
 def tomo3d(grid=128, n_views=180, side=128, sub_rows=2048, ellipsoids=20, seed=4,
            noise=0.01, dtype=np.float32, threads=None) -> TomoProblem:
     """configs[3]: directions in the xy-plane over [0, pi); each view's
     side^2 rays split into side^2 / sub_rows contiguous blocks after a
     seeded per-view row permutation (uniform partition, linops.py:64-72)."""
-    theta = np.arange(n_views) * (np.pi / n_views)
-    dirs = np.stack([np.cos(theta), np.sin(theta), np.zeros_like(theta)], axis=1)
+    dirs, ray_of_row = tomo3d_geometry(n_views, side, sub_rows, seed)
     parts = _pmap(lambda d: siddon3d_block(d, grid, side), list(dirs), threads)
-    rows = side * side
-    if rows % sub_rows:
-        raise ValueError("detector rows must split evenly into sub-blocks")
-    g = _rng(seed + 7)
     blocks = []
-    for ip, ix, d, (nr, nc) in parts:
-        perm = g.permutation(nr)
+    rows = side * side
+    for v, (ip, ix, d, (nr, nc)) in enumerate(parts):
+        perm = ray_of_row[v * rows:(v + 1) * rows]
         counts = np.diff(ip)[perm]
         starts = ip[:-1][perm]
         for s in range(0, nr, sub_rows):

@@ -213,6 +213,16 @@ def run(method: str, op: RowBlockOperator, sampler, schedule: Schedule, *, epoch
         timing["cholesky_flops"] = ms.value
         dop.call("slim_timing", 6, C.byref(ms), C.byref(cnt))
         timing["cholesky_i8ops"] = ms.value
+        reps = int(timing.get("probe_reps", 0))
+        if reps > 0:  # operator-streaming kernels alone, cold L2 (bench "streaming")
+            timing["streaming"] = {}
+            us, nbytes = C.c_double(0), C.c_double(0)
+            for kid, name in ((0, "residual"), (1, "mtw"), (2, "gram")):
+                try:
+                    dop.call("slim_probe_stream", kid, reps, C.byref(us), C.byref(nbytes))
+                except ValueError:  # generated blocks: the Gram is the tensor-core kernel
+                    continue
+                timing["streaming"][name] = (us.value, nbytes.value)
     x_final = np.empty(x0.shape[0])
     dop.call("slim_get_x", _lib.dptr(x_final))
     if stream_state is not None:

@@ -368,13 +368,13 @@ def test_generated_tensor_core_gram(slim, tc, monkeypatch):
 # ---------------------------------------------------------------------------
 
 
-def _sharded_vs_single(slim, op, xt, scheme, seed, alpha, r, K, P):
+def _sharded_vs_single(slim, op, xt, scheme, seed, alpha, r, K, P, round_robin=False):
     from paper_1912_07962_b200.parallel import LocalGroup
     M = op.n_blocks
     kw = dict(epochs=K / M, r=r, references={"x_true": xt})
     single = slim.run("slimls", op, slim.Sampler(scheme, M, seed), slim.Schedule("constant", alpha),
                       **kw)
-    group = LocalGroup(P)
+    group = LocalGroup(P, round_robin=round_robin)
     full, per = group.run("slimls", op, lambda: slim.Sampler(scheme, M, seed),
                           slim.Schedule("constant", alpha), **kw)
     err = np.linalg.norm(full.x_final - single.x_final) / np.linalg.norm(single.x_final)
@@ -399,6 +399,23 @@ def test_sharded_csr_tomography(slim, P):
     from paper_1912_07962_b200 import problems
     prob = problems.tomo2d(grid=48, n_views=30, rays=68, seed=6)
     _sharded_vs_single(slim, prob.op, prob.x_true, "random_cyclic", 5, 1000.0, 6, 40, P)
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_sharded_round_robin_tomography(slim, P):
+    """factorizations distributed over the shards (batch B on
+    rank B mod P), w allreduced from its owner."""
+    from paper_1912_07962_b200 import problems
+    prob = problems.tomo2d(grid=48, n_views=30, rays=68, seed=6)
+    _sharded_vs_single(slim, prob.op, prob.x_true, "random_cyclic", 5, 1000.0, 6, 60, P,
+                       round_robin=True)
+
+
+def test_sharded_round_robin_dense(slim):
+    c = gc.dense_case("dense_dual")
+    op = slim.DenseBlockOperator(c["A"], 20, c["b"])
+    _sharded_vs_single(slim, op, c["refs"]["x_true"], "random_cyclic", 11, 100.0, 4, 60, 2,
+                       round_robin=True)
 
 
 def test_sharded_generated(slim):

@@ -30,8 +30,12 @@ def _allreduce(v):
     return t.numpy()
 
 
-def _sharded_run(a_shard, b, ell, idx, alpha, r, rank, xt_shard):
-    """slimLS on one column shard; exchanges by gloo allreduce."""
+def _sharded_run(a_shard, b, ell, idx, alpha, r, rank, xt_shard, round_robin=False, world=1,
+                 batch=1):
+    """slimLS on one column shard; exchanges by gloo allreduce. With
+    ``round_robin`` (slim_set_factor_round_robin) only rank
+    (k - 1) // batch mod world factors step k's system and solves for w; the
+    others add zeros in an allreduce of w."""
     n_p = a_shard.shape[1]
     x = np.zeros(n_p)
     window = []
@@ -47,14 +51,19 @@ def _sharded_run(a_shard, b, ell, idx, alpha, r, rank, xt_shard):
         g[np.diag_indices_from(g)] += 1.0
         y = np.zeros(mat.shape[0])
         y[-ell:] = res
-        w = scipy.linalg.solve(g, y, assume_a="pos")  # replicated
+        if not round_robin:
+            w = scipy.linalg.solve(g, y, assume_a="pos")  # replicated
+        else:
+            own = ((k - 1) // batch) % world == rank
+            w = scipy.linalg.solve(g, y, assume_a="pos") if own else np.zeros_like(y)
+            w = _allreduce(w)  # the owner's w, exactly
         x = x - alpha * (mat.T @ w)  # local
         norms = _allreduce(np.array([x @ x, (x - xt_shard) @ (x - xt_shard)]))
         history.append((float(np.sqrt(res @ res)), float(np.sqrt(norms[1]))))
     return x, history
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, round_robin=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     g = np.random.Generator(np.random.Philox(key=3))
@@ -64,7 +73,8 @@ def _worker(rank, world, port, out):
     b = a @ xt + 0.01 * g.standard_normal(m)
     c0, c1 = column_ranges(n, world)[rank]
     idx = orc.sampler_indices("random_cyclic", m // ell, 11, K)
-    x, hist = _sharded_run(a[:, c0:c1], b, ell, idx, alpha, r, rank, xt[c0:c1])
+    x, hist = _sharded_run(a[:, c0:c1], b, ell, idx, alpha, r, rank, xt[c0:c1],
+                           round_robin=round_robin, world=world, batch=4)
     xs = [None] * world
     dist.all_gather_object(xs, x)
     if rank == 0:
@@ -72,12 +82,14 @@ def _worker(rank, world, port, out):
     dist.destroy_process_group()
 
 
-def test_column_sharded_decomposition_matches_oracle():
+@pytest.mark.parametrize("round_robin", [False, True])
+def test_column_sharded_decomposition_matches_oracle(round_robin):
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(p, world, port, q)) for p in range(world)]
+    procs = [ctx.Process(target=_worker, args=(p, world, port, q, round_robin))
+             for p in range(world)]
     for p in procs:
         p.start()
     x, hist = q.get(timeout=120)
