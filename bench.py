@@ -398,7 +398,7 @@ def run_ours(args, world, rank, local, dist):
                  "peak_source": "MEASURED_PEAKS.json hbm_gbs" if _peaks().get("hbm_gbs")
                  else "B200_PROFILING.md fallback",
                  "how": "probe after the timed run: 24 launches, each on a different window of "
-                        "resident blocks, L2 flushed (256 MB memset) between launches, one CUDA "
+                        "resident blocks, L2 flushed (256 MB read) between launches, one CUDA "
                         "event pair per launch on the x-chain stream; bytes = operator bytes the "
                         "launch must read once + vectors read/written (algorithmic)"}
     for name, (us, nbytes) in timing.get("streaming", {}).items():
