@@ -130,6 +130,7 @@ int rowdot_chunks(int ell, int64_t n) {
   // R = 8: one full wave (3 resident CTAs of 256 threads per SM at ~80
   // registers), so no second partial wave; R = 1: 4 CTAs per SM
   int nch = R == 8 ? std::max(1, 3 * 148 / groups) : (int)((4 * 148 + groups - 1) / groups);
+  if (const char* e = getenv("SLIM_RD_NCH")) nch = std::max(1, atoi(e));  // tuning knob
   nch = (int)std::min<int64_t>(nch, std::max<int64_t>(1, n / 2048));
   return std::max(1, std::min(nch, 64));
 }
