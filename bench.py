@@ -331,7 +331,7 @@ def run_ours(args, world, rank, local, dist):
         os.environ.pop("SLIM_HOST_STREAMING")
     else:
         os.environ["SLIM_HOST_STREAMING"] = prev
-    timing = {"start_step": wprime + 1, "probe_reps": 24}
+    timing = {"start_step": wprime + 1, "probe_reps": 0 if args.bare else 24}
     _barrier(dist)
     with ClockSampler(dev) as clk:
         traj = slim.run("slimls", op, sampler(), slim.Schedule("constant", alpha),
@@ -407,7 +407,7 @@ def run_ours(args, world, rank, local, dist):
                            "frac": gbs / hbm_peak}
     # ---- e2e through the public API, host-resident fresh operator ----
     e2e = None
-    if not args.quick and not sharded:
+    if not args.quick and not args.bare and not sharded:
         op2, b2, _ = (op, b, xt) if args.config == 5 else build_config(args.config)
         if args.config == 5:
             op2 = op.with_rhs(b)  # fresh operator object: no cached device state
@@ -437,12 +437,12 @@ def run_ours(args, world, rank, local, dist):
         assert tr2.status == "ok"
     # ---- device projector: tomography operators traced in HBM ----
     projector = None
-    if args.config in (2, 3, 4) and not sharded:
+    if args.config in (2, 3, 4) and not sharded and not args.bare:
         projector = _projector_leg(args, dev, b, xt, r, alpha, scheme, total, M, sampler)
     if rank != 0:
         return
     cb = None
-    if world == 1 and not args.quick:
+    if world == 1 and not args.quick and not args.bare:
         cb = cpu_sample(args.config, op, b, r, alpha, scheme, SAMPLER_SEED)
     line = {"metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_win / args.steps,
@@ -539,6 +539,9 @@ def main():
     ap.add_argument("--factor", default="replicated", choices=["replicated", "round_robin"],
                     help="--shard columns: every rank factors every system (replicated) or "
                          "batch B is factored on rank B mod N only (SURVEY 8f.1)")
+    ap.add_argument("--bare", action="store_true",
+                    help="only the timed steps (no streaming probe, projector leg, e2e or CPU "
+                         "legs): for ncu launch lists whose kernel shares are the step's")
     ap.add_argument("--quick", action="store_true",
                     help="skip the CPU baseline and the e2e leg (profiling runs)")
     args = ap.parse_args()

@@ -53,6 +53,13 @@ enum slim_layout {
   SLIM_GEN_SPLITMIX64 = 2    /* generated rows, never stored (configs[4])   */
 };
 
+/* step rule of slim_run (slim_set_method) */
+enum slim_method {
+  SLIM_METHOD_SLIMLS = 0,    /* slimls_step, dual solve (solvers.py:213-242) */
+  SLIM_METHOD_SG = 1         /* sg_step: x - alpha A_k^T r (solvers.py:245-250);
+                                needs memory_r = 0                           */
+};
+
 typedef struct slim_ctx slim_ctx;
 
 typedef struct slim_desc {
@@ -156,6 +163,8 @@ int slim_comm_init_local(slim_ctx* ctx, void* group, int32_t rank);
  * to the replicated mode except for the first system of each batch, which
  * is factored without the previous batch's tiles (same arithmetic).       */
 int slim_set_factor_round_robin(slim_ctx* ctx, int32_t enable);
+/* step rule of the following slim_run calls (enum slim_method)           */
+int slim_set_method(slim_ctx* ctx, int32_t method);
 
 /* ---- secondary seam and kernel-level entry points -------------------- */
 /* innersolve.dual_step (innersolve.py:305-321): stacked dense window

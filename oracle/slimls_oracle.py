@@ -224,9 +224,19 @@ def slimls_step(st: _State, index: int, a: np.ndarray, b: np.ndarray, alpha: flo
     return norm_sq <= st.div_limit_sq
 
 
+def sg_step(st: _State, index: int, a: np.ndarray, b: np.ndarray, alpha: float):
+    """``sg_step`` (solvers.py:245-250): x - alpha A_k^T (A_k x - b_k), the
+    memoryless subset of the slimLS chain (no window, no solve)."""
+    residual = a @ st.x - b  # _sampled_residual, solvers.py:180-183
+    st.last_residual_norm = float(np.sqrt(residual @ residual))
+    st.x = st.x - alpha * (a.T @ residual)
+    norm_sq = float(st.x @ st.x)
+    return norm_sq <= st.div_limit_sq
+
+
 def run_slimls(fetch, n_blocks: int, n_cols: int, indices, alphas, *, r: int = 0,
                x0=None, references=None, record_every: int = 1,
-               store_iterates: bool = False) -> OracleTrajectory:
+               store_iterates: bool = False, method: str = "slimls") -> OracleTrajectory:
     """Restatement of ``run`` (solvers.py:480-588) for the slimLS path.
 
     ``fetch(i)`` returns the dense block (a_block (ell, n), b_block (ell,))
@@ -272,7 +282,7 @@ def run_slimls(fetch, n_blocks: int, n_cols: int, indices, alphas, *, r: int = 0
         alpha = float(alphas[k - 1])
         if not alpha > 0:
             raise ValueError(f"schedule produced alpha_{k} = {alpha} <= 0")
-        ok = slimls_step(st, idx, a, b, alpha)
+        ok = (sg_step if method == "sg" else slimls_step)(st, idx, a, b, alpha)
         if not ok:  # solvers.py:563-570
             status, diverged_at = "diverged", k
             now = time.perf_counter()

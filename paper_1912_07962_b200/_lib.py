@@ -20,6 +20,7 @@ SLIM_ECUDA, SLIM_ENCCL, SLIM_ESTATE, SLIM_ENOMEM = 4, 5, 6, 7
 SLIM_F64, SLIM_F32 = 0, 1
 SLIM_DENSE_ROWMAJOR, SLIM_CSR_PERBLOCK, SLIM_GEN_SPLITMIX64 = 0, 1, 2
 SLIM_HIST_FIXED = 5
+SLIM_METHOD_SLIMLS, SLIM_METHOD_SG = 0, 1
 
 # every symbol include/slimb200.h declares (checked by tests/test_capi_exports.py)
 EXPORTS = (
@@ -27,7 +28,7 @@ EXPORTS = (
     "slim_upload_dense", "slim_upload_csr_block", "slim_upload_csr", "slim_finalize_operator",
     "slim_set_rhs", "slim_gen_apply", "slim_set_x", "slim_get_x", "slim_set_references",
     "slim_set_divergence_limit", "slim_run", "slim_set_host_streaming", "slim_nccl_unique_id", "slim_comm_init",
-    "slim_local_group_create", "slim_local_group_destroy", "slim_comm_init_local", "slim_set_factor_round_robin",
+    "slim_local_group_create", "slim_local_group_destroy", "slim_comm_init_local", "slim_set_factor_round_robin", "slim_set_method",
     "slim_dual_step", "slim_potrf", "slim_potrf_traced", "slim_block_residual", "slim_timing", "slim_set_profiling", "slim_set_timing_start", "slim_probe_stream",
     "slim_siddon2d_view", "slim_siddon3d_view",
     "slim_build_projector", "slim_apply", "slim_get_csr_block", "slim_nnz",
@@ -87,6 +88,7 @@ _SIGS = {
     "slim_apply": (C.c_int, [_P, _DP, _DP]),
     "slim_nnz": (C.c_int, [_P, _I64P]),
     "slim_set_factor_round_robin": (C.c_int, [_P, _I32]),
+    "slim_set_method": (C.c_int, [_P, _I32]),
     "slim_get_csr_block": (C.c_int, [_P, _I64, _I64P, _I32P, C.c_void_p]),
 }
 

@@ -253,6 +253,9 @@ struct slim_ctx {
   // B mod P; that rank's triangular solves produce w, the others contribute
   // zeros to an allreduce of w (exact: one nonzero term per entry)
   bool rr = false;
+  // SLIM_METHOD_SG (sg_step, solvers.py:245-250): no Gram panels, no
+  // factorization; the x-chain takes w = r and s = A_k^T r
+  bool sgm = false;
   int trsv_C = 0;                    // triangular-solve cluster size (0 = by T)
   std::vector<double*> Lbuf, Dinv, Linv;  // 2 D factor buffers (+ 8x8 and 64x64 diagonal inverses)
   void* factor_slab = nullptr;            // one allocation behind Lbuf / Dinv / Linv / cflags
@@ -1102,6 +1105,16 @@ int slim_set_profiling(slim_ctx* c, int32_t enable) {
   return SLIM_OK;
 }
 
+int slim_set_method(slim_ctx* c, int32_t method) {
+  if (!c) FAIL(c, SLIM_EINVAL, "null argument");
+  if (method != SLIM_METHOD_SLIMLS && method != SLIM_METHOD_SG)
+    FAIL(c, SLIM_EINVAL, "unknown method %d", method);
+  if (method == SLIM_METHOD_SG && c->r != 0)
+    FAIL(c, SLIM_EINVAL, "sg keeps no window: create the context with memory_r = 0");
+  c->sgm = method == SLIM_METHOD_SG;
+  return SLIM_OK;
+}
+
 int slim_set_factor_round_robin(slim_ctx* c, int32_t enable) {
   if (!c) FAIL(c, SLIM_EINVAL, "null argument");
   c->rr = enable != 0;
@@ -1340,7 +1353,9 @@ static int enqueue_x_chain(slim_ctx* c, const Window& W, int64_t k, int d, doubl
   const int ell = (int)c->ell, n = (int)c->n, N = W.nw * ell;
   cudaStream_t s = c->sx;
   (void)k;
-  if (!own) {  // round-robin factorization: another rank solves this step
+  if (c->sgm) {  // sg: w = r (window of one block), s = A_k^T r
+    CK(c, cudaMemcpyAsync(c->wvec, c->rvec, sizeof(double) * ell, cudaMemcpyDeviceToDevice, s));
+  } else if (!own) {  // round-robin factorization: another rank solves this step
     CK(c, cudaMemsetAsync(c->wvec, 0, sizeof(double) * N, s));
   } else {
   // trsv
@@ -1363,11 +1378,11 @@ static int enqueue_x_chain(slim_ctx* c, const Window& W, int64_t k, int d, doubl
   CK(c, launch_trsv(T, s));
   CKLAUNCH(c);
   }
-  if (c->rr && c->comm) {
+  if (c->rr && c->comm && !c->sgm) {
     int rc = comm_allreduce(c, c->wvec, (size_t)N, s);
     if (rc) return rc;
   }
-  c->launches += own ? 3 : 2;  // trsv, M^T w, finish
+  c->launches += own && !c->sgm ? 3 : 2;  // trsv, M^T w, finish
   // M^T w
   double* s_parts = c->spart;
   int nsplit = 1;
@@ -1766,6 +1781,17 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
     const bool prof_b = c->prof && kb0 >= k0;
     if (prof_b) pg = take(c->prof_gram, pgr), cudaEventRecord(pg.a, c->sg);
     for (int b = 0; b < nb; ++b) {
+      if (c->sgm) {  // sg: no Gram panel; a generated block is still generated
+        if (c->layout == SLIM_GEN_SPLITMIX64) {
+          const int64_t off = (int64_t)Ws[b].slot[Ws[b].newp] * c->ell * c->n;
+          launch_gen_block(c->gring + off, nullptr, nullptr, c->gen_seed,
+                           (idx[kb0 + b - 1] - 1) * c->ell, (int)c->ell, (int)c->n,
+                           c->gen_n_total, c->col_offset, c->sg);
+          CKLAUNCH(c);
+          c->launches += 1;
+        }
+        continue;
+      }
       int rc = enqueue_gram(c, Ws[b], kb0 + b, idx[kb0 + b - 1] - 1);
       if (rc) return rc;
     }
@@ -1773,7 +1799,7 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
     CK(c, cudaEventRecord(c->ev_g[B % NEV], c->sg));
     // ---- batched factorization (sf): buffer set reused from batch B - 2
     const bool rr = c->rr && c->comm && c->comm->nranks > 1;
-    const bool own = !rr || B % c->comm->nranks == c->comm->rank;
+    const bool own = !c->sgm && (!rr || B % c->comm->nranks == c->comm->rank);
     if (own) {
     CK(c, cudaStreamWaitEvent(c->sf, c->ev_g[B % NEV], 0));
     if (B >= 2) CK(c, cudaStreamWaitEvent(c->sf, c->ev_x[(B - 2) % NEV], 0));

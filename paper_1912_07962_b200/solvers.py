@@ -31,7 +31,7 @@ METHODS = (
     "slimls", "sg", "kaczmarz", "block_kaczmarz", "damped_block_kaczmarz",
     "recursive_ls", "olbfgs", "slimtik",
 )
-DEVICE_METHODS = ("slimls", "damped_block_kaczmarz", "slimtik")
+DEVICE_METHODS = ("slimls", "damped_block_kaczmarz", "slimtik", "sg")
 
 
 class DivergenceError(RuntimeError):
@@ -118,9 +118,10 @@ def _validate(method, op, sampler, epochs, r, reg, lam, inner, record_every, sch
         if lam < 0:
             raise ValueError("lambda must be >= 0")
         raise ValueError("slimtik with lam > 0 is not on the B200 slimLS path")
-    if reg is not None and not getattr(reg, "is_identity", False):
+    # sg (solvers.py:245-250) takes no window, regularizer or inner solve
+    if method != "sg" and reg is not None and not getattr(reg, "is_identity", False):
         raise ValueError("only the identity regularizer C = I is on the B200 dual path")
-    if inner not in ("auto", "dual"):
+    if method != "sg" and inner not in ("auto", "dual"):
         raise ValueError(f"inner solve {inner!r} is not on the B200 path; use 'auto' or 'dual'")
     if schedule.kind == "ramp" and schedule.ramp_length is None:
         schedule = schedule.with_ramp_length(r + 1)
@@ -172,14 +173,16 @@ def run(method: str, op: RowBlockOperator, sampler, schedule: Schedule, *, epoch
         raise StreamOrderError(f"single-pass stream expected block {stream_state}, got 1")
 
     x0_full = x0
+    r_dev = 0 if method == "sg" else r  # sg keeps no window (r only sets the ramp length)
     if shard is not None:
         c0, c1 = shard.col0, shard.col1
-        dop = shard.device_operator(op, r, device)
+        dop = shard.device_operator(op, r_dev, device)
         x0 = np.ascontiguousarray(x0[c0:c1])
         dev_refs = [np.ascontiguousarray(v[c0:c1]) for _, v, _ in ref_items]
     else:
-        dop = device_operator(op, r, device)
+        dop = device_operator(op, r_dev, device)
         dev_refs = [v for _, v, _ in ref_items]
+    dop.call("slim_set_method", _lib.SLIM_METHOD_SG if method == "sg" else _lib.SLIM_METHOD_SLIMLS)
     x0c = np.ascontiguousarray(x0)
     dop.call("slim_set_x", _lib.dptr(x0c))
     refp = (C.POINTER(C.c_double) * max(1, len(ref_items)))(*[_lib.dptr(v) for v in dev_refs])

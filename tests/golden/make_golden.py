@@ -63,12 +63,13 @@ def _traj_dict(prefix, traj):
 
 
 def _case(prefix, a, b, ell, *, scheme, seed, sched, epochs, r, x0=None,
-          refs=None, record_every=1, store_iterates=False, single_pass=False):
+          refs=None, record_every=1, store_iterates=False, single_pass=False,
+          method="slimls"):
     op = DenseBlockOperator(a, ell, b)
     if single_pass:
         op = SinglePassAdapter(op)
     sampler = Sampler(scheme, op.n_blocks, seed=seed)
-    traj = run("slimls", op, sampler, sched, epochs=epochs, r=r, x0=x0,
+    traj = run(method, op, sampler, sched, epochs=epochs, r=r, x0=x0,
                references=refs, record_every=record_every,
                store_iterates=store_iterates)
     # the index trace that produced it (fresh sampler, same seed)
@@ -159,6 +160,28 @@ def dense_runs():
                      sched=Schedule("constant", 1.0), epochs=2, r=1,
                      refs={"x_true": np.ones(30)}, record_every=2))
     np.savez_compressed(os.path.join(HERE, "dense_runs.npz"), **out)
+
+
+def sg_runs():
+    """Plain sampled-gradient runs (method "sg", solvers.py:245-250), the
+    memoryless subset of the slimLS chain."""
+    out = {}
+    rng = np.random.default_rng(202)
+    a = rng.standard_normal((90, 40)); xt = rng.standard_normal(40)
+    b = a @ xt + 0.05 * rng.standard_normal(90)
+    out.update(_case("sg_dense", a, b, 6, scheme="random_cyclic", seed=4,
+                     sched=Schedule("constant", 0.01), epochs=3, r=0,
+                     refs={"x_true": xt}, record_every=2, store_iterates=True, method="sg"))
+    out.update(_case("sg_ramp_r3", a, b, 6, scheme="uniform_iid", seed=5,
+                     sched=Schedule("ramp", 0.02), epochs=2, r=3,
+                     x0=rng.standard_normal(40), refs={"x_true": xt}, method="sg"))
+    out.update(_case("sg_decay", a, b, 9, scheme="cyclic", seed=0,
+                     sched=Schedule("decay", 0.02, decay_exponent=0.6), epochs=2, r=0,
+                     refs={"x_true": xt}, record_every=3, method="sg"))
+    out.update(_case("sg_diverge", a, b, 6, scheme="cyclic", seed=0,
+                     sched=Schedule("constant", 50.0), epochs=3, r=0,
+                     refs={"x_true": xt}, method="sg"))
+    np.savez_compressed(os.path.join(HERE, "sg_runs.npz"), **out)
 
 
 def _angles_0_pi(count):
@@ -331,6 +354,7 @@ if __name__ == "__main__":
     tomo_runs()
     projector_golden()
     dual_step_golden()
+    sg_runs()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

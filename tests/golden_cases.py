@@ -13,6 +13,9 @@ DENSE_CASES = ("scalar", "direct_route", "dense_dual", "cfg1_reduced", "ramp", "
                "diverge_late")
 
 
+SG_CASES = ("sg_dense", "sg_ramp_r3", "sg_decay", "sg_diverge")
+
+
 def load(name):
     return np.load(os.path.join(GOLDEN, name), allow_pickle=False)
 
@@ -29,7 +32,7 @@ def cfg1_reduced_matrix():
 
 
 def dense_case(name):
-    d = load("dense_runs.npz")
+    d = load("sg_runs.npz" if name.startswith("sg_") else "dense_runs.npz")
     p = name + "/"
     case = {k[len(p):]: d[k] for k in d.files if k.startswith(p)}
     if name == "cfg1_reduced":

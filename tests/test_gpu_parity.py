@@ -130,7 +130,7 @@ def test_errors_map_to_reference_exceptions(slim):
     with pytest.raises(ValueError, match="memory level"):
         slim.run("slimls", op, smp, slim.Schedule(), epochs=1, r=-1)
     with pytest.raises(ValueError, match="not on the B200"):
-        slim.run("sg", op, smp, slim.Schedule(), epochs=1)
+        slim.run("olbfgs", op, smp, slim.Schedule(), epochs=1)
     sp = slim.SinglePassAdapter(op)
     with pytest.raises(ValueError, match="cyclic"):
         slim.run("slimls", sp, slim.Sampler("uniform_iid", op.n_blocks, 0), slim.Schedule(),

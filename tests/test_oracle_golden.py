@@ -16,7 +16,7 @@ def test_sampler_traces_bit_exact():
         assert np.array_equal(got, d[key]), key
 
 
-@pytest.mark.parametrize("name", gc.DENSE_CASES)
+@pytest.mark.parametrize("name", gc.DENSE_CASES + gc.SG_CASES)
 def test_dense_runs_match_reference(name):
     c = gc.dense_case(name)
     ell = int(c["ell"])
@@ -25,7 +25,8 @@ def test_dense_runs_match_reference(name):
     traj = orc.run_slimls(fetch, m // ell, n, c["indices"], gc.case_alphas(c),
                           r=int(c["r"]), x0=c.get("x0"), references=c["refs"],
                           record_every=int(c["record_every"]),
-                          store_iterates="iterates" in c)
+                          store_iterates="iterates" in c,
+                          method="sg" if name.startswith("sg_") else "slimls")
     assert np.array_equal(traj.ks, c["ks"])
     assert traj.status == str(c["status"])
     assert (traj.diverged_at or -1) == int(c["diverged_at"])
