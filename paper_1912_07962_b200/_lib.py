@@ -13,7 +13,8 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libslimb200.so")
+# SLIM_LIB: an alternate in-tree build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("SLIM_LIB") or os.path.join(_HERE, "libslimb200.so")
 
 SLIM_OK, SLIM_EINVAL, SLIM_ERANGE, SLIM_ENOTSPD = 0, 1, 2, 3
 SLIM_ECUDA, SLIM_ENCCL, SLIM_ESTATE, SLIM_ENOMEM = 4, 5, 6, 7
