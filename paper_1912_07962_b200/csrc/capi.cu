@@ -1486,7 +1486,7 @@ static const slim_ctx::TaskMap* task_map(slim_ctx* c, const std::vector<SysShape
   const double t3 = (double)TB * TB * TB;
   // int8 tensor-core path: 36 digit-pair products of 2 * 64^3 ops per 64x64x64
   // tile update (k_chol_i8)
-  const double u8 = 36.0 * 2.0 * t3;
+  const double u8 = (double)(QD * (QD + 1) / 2) * 2.0 * t3;
   double flops = 0.0, i8ops = 0.0;
   for (const int2& e : h) {
     const int i = e.y >> 16, j = e.y & 0x7fff;

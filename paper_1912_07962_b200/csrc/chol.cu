@@ -43,7 +43,7 @@ constexpr unsigned FULL = 0xffffffffu;
 // byte offset of row r of digit block kd = (k half, digit) of sliced tile
 // (i, k): [k][k half][digit][tile row i < qT][64 rows][32 B]
 __host__ __device__ __forceinline__ int64_t q_off(int qT, int i, int k, int kd, int r) {
-  return ((((int64_t)k * 16 + kd) * qT + i) * 64 + r) * 32;
+  return ((((int64_t)k * 2 * QD + kd) * qT + i) * 64 + r) * 32;
 }
 
 // per-CTA view of its system, in registers (indexing the kernel-parameter
@@ -384,8 +384,8 @@ __global__ void __launch_bounds__(256) k_assemble(CholParams P) {
     const double2* src = reinterpret_cast<const double2*>(P.prevL + toff);
     double2* dst = reinterpret_cast<double2*>(Mp.L + toff);
     for (int e = tid; e < TB * TB / 2; e += 256) dst[e] = __ldcg(src + e);
-    if (Mp.Q != nullptr && P.prevQ != nullptr && I != J) {  // 16 (k half, digit) blocks of 2 KB
-      for (int e = tid; e < 16 * 128; e += 256) {
+    if (Mp.Q != nullptr && P.prevQ != nullptr && I != J) {  // 2 QD (k half, digit) blocks of 2 KB
+      for (int e = tid; e < 2 * QD * 128; e += 256) {
         const int64_t off = q_off(Mp.qT, I, J, e >> 7, 0) + (int64_t)(e & 127) * 16;
         *reinterpret_cast<uint4*>(Mp.Q + off) = __ldcg(reinterpret_cast<const uint4*>(P.prevQ + off));
       }
@@ -782,6 +782,8 @@ __global__ void __launch_bounds__(256, 2) k_chol_tiles(const __grid_constant__ C
 // d_1 in [-127, 127], d_a in [-64, 64] for a > 1, with 2^(e_p) >= 1.004
 // sqrt(G_pp) >= 1.004 |L_pk| (row scales known before the factorization
 // starts, k_assemble), so the representation error is below 2^-57 2^(e_p).
+// (QD = SLIM_QD digits in general, kernels.h; 8 is the default and the only
+// count that keeps the products fp64-class)
 // Then
 //     sum_k L_ik L_jk = 2^(e_i + e_j - 14) sum_{t=0..7} 2^(-7 t) P_t,
 //     P_t = sum_{a + b = t + 2} D_a(i) D_b(j)^T        (int32, exact)
@@ -805,9 +807,9 @@ __global__ void __launch_bounds__(256, 2) k_chol_tiles(const __grid_constant__ C
 namespace oz {
 constexpr int DIG_A = 128 * 32;          // one digit of the A operand: 128 rows x 32 B
 constexpr int DIG_B = 64 * 32;           // one digit of B: 64 rows x 32 B
-constexpr int ST_A = 8 * DIG_A;          // [digit][rows of tiles i, i + 1][32 B]
-constexpr int ST_B = 8 * DIG_B;          // [digit][64 rows][32 B]
-constexpr int STAGE = ST_A + ST_B;       // 48 KB: one k half of three tiles
+constexpr int ST_A = QD * DIG_A;         // [digit][rows of tiles i, i + 1][32 B]
+constexpr int ST_B = QD * DIG_B;         // [digit][64 rows][32 B]
+constexpr int STAGE = ST_A + ST_B;       // 6 QD KB: one k half of three tiles
 #ifndef SLIM_OZ_NST
 #define SLIM_OZ_NST 3
 #endif
@@ -880,24 +882,24 @@ __device__ __forceinline__ double pow2(int e) {  // exact 2^e, |e| < 1000
 // exponents rex[0..63]: thread = (row, 16 consecutive k); v = L 2^(7 - e)
 // lies in (-127.5, 127.5), and d_a = rint(v), v <- (v - d_a) 128 is exact
 struct Digits {
-  uint4 w[8];  // digit a of the thread's 16 entries, one byte each
+  uint4 w[QD];  // digit a of the thread's 16 entries, one byte each
 };
 __device__ __forceinline__ void slice_tile(const double* X, const int* rex, int tid, Digits& D) {
   const int r = tid >> 2, kq = tid & 3;
-  // I = rint(L 2^(56 - e)) = rint(v 2^49): |I| < 127.5 2^49, exact in fp64 and
-  // int64; balanced base-128 digits peeled off from the bottom in integer
-  // arithmetic, the remaining top digit in [-127, 127]
-  const double sc = oz::pow2(56 - __ldcg(rex + r));
-  uint32_t w[8][4];
+  // I = rint(L 2^(7 QD - e)) = rint(v 2^(7 (QD - 1))): |I| < 127.5 2^(7 (QD - 1)),
+  // exact in fp64 and int64; balanced base-128 digits peeled off from the
+  // bottom in integer arithmetic, the remaining top digit in [-127, 127]
+  const double sc = oz::pow2(7 * QD - __ldcg(rex + r));
+  uint32_t w[QD][4];
 #pragma unroll
-  for (int a = 0; a < 8; ++a)
+  for (int a = 0; a < QD; ++a)
 #pragma unroll
     for (int q = 0; q < 4; ++q) w[a][q] = 0u;
 #pragma unroll
   for (int cc = 0; cc < 16; ++cc) {
     long long I = __double2ll_rn(X[r * TS + 16 * kq + cc] * sc);
 #pragma unroll
-    for (int a = 7; a >= 1; --a) {
+    for (int a = QD - 1; a >= 1; --a) {
       const int d = (((int)I + 64) & 127) - 64;
       I = (I - d) >> 7;
       w[a][cc >> 2] |= ((uint32_t)d & 0xffu) << (8 * (cc & 3));
@@ -905,14 +907,14 @@ __device__ __forceinline__ void slice_tile(const double* X, const int* rex, int 
     w[0][cc >> 2] |= ((uint32_t)(int)I & 0xffu) << (8 * (cc & 3));
   }
 #pragma unroll
-  for (int a = 0; a < 8; ++a) D.w[a] = make_uint4(w[a][0], w[a][1], w[a][2], w[a][3]);
+  for (int a = 0; a < QD; ++a) D.w[a] = make_uint4(w[a][0], w[a][1], w[a][2], w[a][3]);
 }
 // digit a of the thread's 16 entries (row r, k = 16 kq ..) into sliced tile (i, k)
 __device__ __forceinline__ void store_digits(const CholMat& M, int i, int k, const Digits& D, int tid) {
   const int r = tid >> 2, kq = tid & 3, kh = kq >> 1, kk0 = (kq & 1) * 16;
 #pragma unroll
-  for (int a = 0; a < 8; ++a)
-    *reinterpret_cast<uint4*>(M.Q + q_off(M.qT, i, k, kh * 8 + a, r) + kk0) = D.w[a];
+  for (int a = 0; a < QD; ++a)
+    *reinterpret_cast<uint4*>(M.Q + q_off(M.qT, i, k, kh * QD + a, r) + kk0) = D.w[a];
 }
 
 // Store tile (i, j) -- fp64, digit slices (off-diagonal tiles: the only
@@ -1040,8 +1042,8 @@ __global__ void __launch_bounds__(256, 1) k_chol_i8(const __grid_constant__ Chol
       bar_expect(&s_full[st], oz::STAGE);
       // A: tile rows ra, ra + 1, all 8 digits (a single task's spare row is
       // loaded and ignored); B: tile row j
-      tma3d(dst, &M.qmapA, &s_full[st], 0, ra * TB, (k * 2 + kh) * 8);
-      tma3d(dst + oz::ST_A, &M.qmapB, &s_full[st], 0, j * TB, (k * 2 + kh) * 8);
+      tma3d(dst, &M.qmapA, &s_full[st], 0, ra * TB, (k * 2 + kh) * QD);
+      tma3d(dst + oz::ST_A, &M.qmapB, &s_full[st], 0, j * TB, (k * 2 + kh) * QD);
     }
     if (tr) tr[4] = t_dep;
     (void)t_ring;
@@ -1060,15 +1062,15 @@ __global__ void __launch_bounds__(256, 1) k_chol_i8(const __grid_constant__ Chol
       // accumulators are first touched by the a = 1 MMAs: only they may
       // overwrite (first stage)
 #pragma unroll
-      for (int a = 1; a <= 8; ++a) {
+      for (int a = 1; a <= QD; ++a) {
         const uint64_t A = ad + (((a - 1) * oz::DIG_A) >> 4);
 #pragma unroll
-        for (int b0 = 1; b0 <= 9 - a; b0 += 4) {
-          const int n = (10 - a - b0) < 4 ? (10 - a - b0) : 4;
+        for (int b0 = 1; b0 <= QD + 1 - a; b0 += 4) {
+          const int n = (QD + 2 - a - b0) < 4 ? (QD + 2 - a - b0) : 4;
           const uint64_t B = bd + (((b0 - 1) * oz::DIG_B) >> 4);
           const uint32_t acc = (u > 0 || a > 1) ? 1u : 0u;
           const uint32_t d = tmem + 64 * (a + b0 - 2);
-          if (a > 4)
+          if (QD + 1 - a <= 4)  // one MMA for this A digit: no collector
             oz::mma_i8<0>(d, A, B, oz::idesc(n), acc);
           else if (b0 == 1)
             oz::mma_i8<1>(d, A, B, oz::idesc(n), acc);
@@ -1108,7 +1110,7 @@ __global__ void __launch_bounds__(256, 1) k_chol_i8(const __grid_constant__ Chol
     for (int c = 0; c < 32; ++c) s[c] = 0.0;
     if (nchunk > 0) {
 #pragma unroll 1
-      for (int t = 7; t >= 0; --t) {
+      for (int t = QD - 1; t >= 0; --t) {
         int v[32];
         oz::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + 64 * t + 32 * h, v);
 #pragma unroll

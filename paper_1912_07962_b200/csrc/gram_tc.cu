@@ -284,9 +284,9 @@ bool tma_map_q(CUtensorMap* m, const int8_t* base, int qT, int box_rows) {
   if (!enc) return false;
   // dim0: 32 B of one digit (K = 32 int8), dim1: rows over all tile rows of a
   // column (qT * 64), dim2: (column, k half, digit) blocks
-  cuuint64_t dims[3] = {32, (cuuint64_t)qT * 64, (cuuint64_t)qT * 16};
+  cuuint64_t dims[3] = {32, (cuuint64_t)qT * 64, (cuuint64_t)qT * 2 * QD};
   cuuint64_t strides[2] = {32, (cuuint64_t)qT * 64 * 32};
-  cuuint32_t box[3] = {32, (cuuint32_t)box_rows, 8};
+  cuuint32_t box[3] = {32, (cuuint32_t)box_rows, (cuuint32_t)QD};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)base, dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,

@@ -138,12 +138,19 @@ size_t chol_smem_bytes();
 // factorization kernel: true = int8 tensor-core updates (default), false =
 // fp64 DMMA updates (SLIM_CHOL=dmma, kept for A/B measurements)
 bool chol_use_i8();
-// int8 updates: |P_t| <= (2 * 127 * 64 + 6 * 64^2) * 64 T < 2^31
+// signed 7-bit digits per factor entry in the int8 tensor-core updates
+// (k_chol_i8): QD digits keep 7 QD bits below each row's scale
+#ifndef SLIM_QD
+#define SLIM_QD 8
+#endif
+constexpr int QD = SLIM_QD;
+static_assert(QD >= 5 && QD <= 8, "digit count");
+// int8 updates: |P_t| <= (2 * 127 * 64 + (QD - 2) * 64^2) * 64 T < 2^31
 constexpr int CHOL_I8_TMAX = 800;
 // TMA views of a sliced factor buffer with qT tile rows per column (box
-// rows = 128 for the A operand, 64 for B; 8 digits per box)
+// rows = 128 for the A operand, 64 for B; QD digits per box)
 bool tma_map_q(CUtensorMap* m, const int8_t* base, int qT, int box_rows);
-// bytes of a sliced factor buffer
-inline size_t q_bytes(int qT) { return (size_t)qT * qT * 32768; }
+// bytes of a sliced factor buffer: [k][k half][digit][tile row][64 rows][32 B]
+inline size_t q_bytes(int qT) { return (size_t)qT * qT * 2 * QD * 64 * 32; }
 
 }  // namespace slim
