@@ -90,6 +90,10 @@ int slim_upload_dense(slim_ctx* ctx, const void* a_rowmajor, const double* b);
  * block, col/val hold rowptr[ell] entries, b_block has ell entries.      */
 int slim_upload_csr_block(slim_ctx* ctx, int64_t block, const int64_t* rowptr,
                           const int32_t* col, const void* val, const double* b_block);
+/* every block at once (block i + 1 = rowptrs[i], cols[i], vals[i]; b is the
+ * whole right-hand side): one call instead of n_blocks                    */
+int slim_upload_csr_blocks(slim_ctx* ctx, int64_t count, const int64_t* const* rowptrs,
+                           const int32_t* const* cols, const void* const* vals, const double* b);
 /* All CSR blocks at once: global rowptr (n_rows+1 entries, int64).       */
 int slim_upload_csr(slim_ctx* ctx, const int64_t* rowptr, const int32_t* col,
                     const void* val, const double* b);

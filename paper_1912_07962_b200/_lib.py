@@ -26,7 +26,7 @@ SLIM_METHOD_SLIMLS, SLIM_METHOD_SG = 0, 1
 # every symbol include/slimb200.h declares (checked by tests/test_capi_exports.py)
 EXPORTS = (
     "slim_create", "slim_destroy", "slim_last_error", "slim_abi_version",
-    "slim_upload_dense", "slim_upload_csr_block", "slim_upload_csr", "slim_finalize_operator",
+    "slim_upload_dense", "slim_upload_csr_block", "slim_upload_csr_blocks", "slim_upload_csr", "slim_finalize_operator",
     "slim_set_rhs", "slim_gen_apply", "slim_set_x", "slim_get_x", "slim_set_references",
     "slim_set_divergence_limit", "slim_run", "slim_set_host_streaming", "slim_nccl_unique_id", "slim_comm_init",
     "slim_local_group_create", "slim_local_group_destroy", "slim_comm_init_local", "slim_set_factor_round_robin", "slim_set_method",
@@ -60,6 +60,7 @@ _SIGS = {
     "slim_abi_version": (C.c_int, []),
     "slim_upload_dense": (C.c_int, [_P, _P, _DP]),
     "slim_upload_csr_block": (C.c_int, [_P, _I64, _I64P, _I32P, _P, _DP]),
+    "slim_upload_csr_blocks": (C.c_int, [_P, _I64, C.c_void_p, C.c_void_p, C.c_void_p, _DP]),
     "slim_upload_csr": (C.c_int, [_P, _I64P, _I32P, _P, _DP]),
     "slim_finalize_operator": (C.c_int, [_P]),
     "slim_set_rhs": (C.c_int, [_P, _DP]),

@@ -744,6 +744,17 @@ int slim_upload_csr(slim_ctx* c, const int64_t* rowptr, const int32_t* col, cons
   return SLIM_OK;
 }
 
+int slim_upload_csr_blocks(slim_ctx* c, int64_t count, const int64_t* const* rowptrs,
+                           const int32_t* const* cols, const void* const* vals, const double* b) {
+  if (!c || !rowptrs || !cols || !vals || !b) FAIL(c, SLIM_EINVAL, "null argument");
+  if (count != c->M) FAIL(c, SLIM_EINVAL, "expected %lld blocks, got %lld", (long long)c->M, (long long)count);
+  for (int64_t i = 0; i < count; ++i) {
+    const int rc = slim_upload_csr_block(c, i + 1, rowptrs[i], cols[i], vals[i], b + i * c->ell);
+    if (rc) return rc;
+  }
+  return SLIM_OK;
+}
+
 int slim_upload_csr_block(slim_ctx* c, int64_t block, const int64_t* rowptr, const int32_t* col,
                           const void* val, const double* b_block) {
   if (!c || !rowptr || !b_block) FAIL(c, SLIM_EINVAL, "null argument");

@@ -466,15 +466,20 @@ def device_operator(op, r: int, device: int = 0) -> DeviceOperator:
                              dtype=src.dtype, device=device)
         dop.call("slim_set_host_streaming", 1)
         refs = [b]
-        for i in range(1, src.n_blocks + 1):
+        nb = src.n_blocks
+        ptrs = np.empty((3, nb), dtype=np.uintp)
+        for i in range(1, nb + 1):
             ip, ix, d, _ = src.csr_block(i)
             ip = np.ascontiguousarray(ip, dtype=np.int64)
             ix = np.ascontiguousarray(ix, dtype=np.int32)
             d = np.ascontiguousarray(d, dtype=src.dtype)
-            bb = b[(i - 1) * ell:i * ell]
-            dop.call("slim_upload_csr_block", i, _lib.i64ptr(ip), _lib.i32ptr(ix), _lib.vptr(d),
-                     _lib.dptr(bb))
+            ptrs[0, i - 1] = ip.ctypes.data
+            ptrs[1, i - 1] = ix.ctypes.data
+            ptrs[2, i - 1] = d.ctypes.data
             refs.append((ip, ix, d))
+        # one registration call for all blocks (the host arrays stay alive in refs)
+        dop.call("slim_upload_csr_blocks", nb, C.c_void_p(ptrs[0].ctypes.data),
+                 C.c_void_p(ptrs[1].ctypes.data), C.c_void_p(ptrs[2].ctypes.data), _lib.dptr(b))
         dop.host_refs = refs
     else:
         if isinstance(src, SparseBlockOperator):
