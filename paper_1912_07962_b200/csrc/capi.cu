@@ -1433,15 +1433,9 @@ static int enqueue_x_chain(slim_ctx* c, const Window& W, int64_t k, int d, doubl
       launch_mtw_dense<double>(c->spart, nsplit, W, (const double*)c->A, c->n, n, c->wvec, c->ctl, s);
     else
       launch_mtw_dense<float>(c->spart, nsplit, W, (const float*)c->A, c->n, n, c->wvec, c->ctl, s);
-  } else {
-    if (c->vdt == SLIM_F64)
-      launch_mtw_csc<double>(c->spart, W, c->colptr, n, c->cscrow, (const double*)c->cscval,
-                             c->blkbase, c->wvec, c->ctl, s);
-    else
-      launch_mtw_csc<float>(c->spart, W, c->colptr, n, c->cscrow, (const float*)c->cscval,
-                            c->blkbase, c->wvec, c->ctl, s);
   }
-  CKLAUNCH(c);
+  const bool fused = c->layout == SLIM_CSR_PERBLOCK;  // M^T w inside the finish kernel
+  if (!fused) CKLAUNCH(c);
   FinishParams F{};
   F.x = c->x;
   F.s_parts = s_parts;
@@ -1459,7 +1453,17 @@ static int enqueue_x_chain(slim_ctx* c, const Window& W, int64_t k, int d, doubl
   F.ell = ell;
   F.split = c->comm ? 1 : 0;
   F.norms = c->norms;
-  launch_finish(F, s);
+  if (fused) {
+    if (c->vdt == SLIM_F64)
+      launch_mtw_finish_csc<double>(F, W, c->colptr, c->cscrow, (const double*)c->cscval, c->blkbase,
+                                    c->wvec, s);
+    else
+      launch_mtw_finish_csc<float>(F, W, c->colptr, c->cscrow, (const float*)c->cscval, c->blkbase,
+                                   c->wvec, s);
+    c->launches -= 1;  // one kernel instead of M^T w + finish
+  } else {
+    launch_finish(F, s);
+  }
   CKLAUNCH(c);
   if (c->comm) {
     // global ||x||^2 and ||x - ref||^2 over all column shards, then decide

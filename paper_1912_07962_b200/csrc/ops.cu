@@ -423,15 +423,11 @@ __global__ void __launch_bounds__(256) k_mtw_dense(double* __restrict__ part, Wi
 // block (the kernel was latency-bound at 3 chains x r + 1 blocks). The
 // accumulation order (block, then nonzero) is unchanged.
 template <typename T, int MTW_GROUP>
-__global__ void __launch_bounds__(256) k_mtw_csc(double* __restrict__ s_out, Window W,
-                                                 const int* __restrict__ colptr, int n,
-                                                 const int* __restrict__ cscrow,
-                                                 const T* __restrict__ cscval,
-                                                 const int64_t* __restrict__ blkbase,
-                                                 const double* __restrict__ w, const Ctl* ctl) {
-  if (ctl->diverged_at != 0) return;
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= n) return;
+__device__ __forceinline__ double mtw_csc_col(int c, const Window& W, const int* __restrict__ colptr,
+                                              int n, const int* __restrict__ cscrow,
+                                              const T* __restrict__ cscval,
+                                              const int64_t* __restrict__ blkbase,
+                                              const double* __restrict__ w) {
   const int ell = W.ell;
   double s = 0.0;
   for (int P0 = 0; P0 < W.nw; P0 += MTW_GROUP) {
@@ -469,25 +465,35 @@ __global__ void __launch_bounds__(256) k_mtw_csc(double* __restrict__ s_out, Win
       }
     }
   }
-  s_out[c] = s;
+  return s;
+}
+template <typename T, int MTW_GROUP>
+__global__ void __launch_bounds__(256) k_mtw_csc(double* __restrict__ s_out, Window W,
+                                                 const int* __restrict__ colptr, int n,
+                                                 const int* __restrict__ cscrow,
+                                                 const T* __restrict__ cscval,
+                                                 const int64_t* __restrict__ blkbase,
+                                                 const double* __restrict__ w, const Ctl* ctl) {
+  if (ctl->diverged_at != 0) return;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  s_out[c] = mtw_csc_col<T, MTW_GROUP>(c, W, colptr, n, cscrow, cscval, blkbase, w);
 }
 
 // ---------------------------------------------------------------------------
 // finish: x update, norms, divergence, history (last-block reduction)
 // ---------------------------------------------------------------------------
 
-__global__ void __launch_bounds__(256) k_finish(FinishParams F) {
+// x[c] -= alpha sn for this thread's column, then the norms, divergence and
+// history row by a last-block reduction (every thread of the grid calls it)
+__device__ __forceinline__ void finish_body(const FinishParams& F, int c, double sn) {
   Ctl* ctl = F.ctl;
-  if (ctl->diverged_at != 0) return;
   const int tid = threadIdx.x;
-  const int c = blockIdx.x * blockDim.x + tid;
   const int nq = 1 + F.nref;
   double loc[1 + MAX_REFS];
 #pragma unroll
   for (int q = 0; q < 1 + MAX_REFS; ++q) loc[q] = 0.0;
   if (c < F.n) {
-    double sn = 0.0;
-    for (int z = 0; z < F.nsplit; ++z) sn += F.s_parts[(int64_t)z * F.n + c];
     const double xn = F.x[c] - F.alpha * sn;
     F.x[c] = xn;
     loc[0] = xn * xn;
@@ -558,6 +564,30 @@ __global__ void __launch_bounds__(256) k_finish(FinishParams F) {
       for (int q = 0; q < F.nref; ++q) h[SLIM_HIST_FIXED_DEV + q] = sqrt(tot[1 + q]);
     }
   }
+}
+
+__global__ void __launch_bounds__(256) k_finish(FinishParams F) {
+  if (F.ctl->diverged_at != 0) return;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  double sn = 0.0;
+  if (c < F.n)
+    for (int z = 0; z < F.nsplit; ++z) sn += F.s_parts[(int64_t)z * F.n + c];
+  finish_body(F, c, sn);
+}
+
+// CSC M^T w fused with the finish: s stays in registers (bit-identical to
+// k_mtw_csc + k_finish: the same sums, and 0 + s = s)
+template <typename T>
+__global__ void __launch_bounds__(256) k_mtw_finish_csc(FinishParams F, Window W,
+                                                        const int* __restrict__ colptr,
+                                                        const int* __restrict__ cscrow,
+                                                        const T* __restrict__ cscval,
+                                                        const int64_t* __restrict__ blkbase,
+                                                        const double* __restrict__ w) {
+  if (F.ctl->diverged_at != 0) return;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const double sn = c < F.n ? mtw_csc_col<T, 3>(c, W, colptr, F.n, cscrow, cscval, blkbase, w) : 0.0;
+  finish_body(F, c, sn);
 }
 
 __global__ void k_stamp_start(Ctl* ctl) { ctl->t_start_ns = globaltimer_ns(); }
@@ -896,6 +926,18 @@ void launch_mtw_csc(double* s_out, const Window& W, const int* colptr, int n, co
 void launch_finish(const FinishParams& F, cudaStream_t s) {
   k_finish<<<cdiv(F.n, 256), 256, 0, s>>>(F);
 }
+template <typename T>
+void launch_mtw_finish_csc(const FinishParams& F, const Window& W, const int* colptr,
+                           const int* cscrow, const T* cscval, const int64_t* blkbase,
+                           const double* w, cudaStream_t s) {
+  k_mtw_finish_csc<T><<<cdiv(F.n, 256), 256, 0, s>>>(F, W, colptr, cscrow, cscval, blkbase, w);
+}
+template void launch_mtw_finish_csc<double>(const FinishParams&, const Window&, const int*,
+                                            const int*, const double*, const int64_t*,
+                                            const double*, cudaStream_t);
+template void launch_mtw_finish_csc<float>(const FinishParams&, const Window&, const int*,
+                                           const int*, const float*, const int64_t*,
+                                           const double*, cudaStream_t);
 int finish_grid(int n) { return (int)cdiv(n, 256); }
 // L2 flush by reading (the lines it leaves are clean, so the next kernel's
 // DRAM bandwidth is not shared with write-backs)

@@ -90,6 +90,11 @@ void launch_build_csc(int* colptr, int* cscrow, T* cscval, const int64_t* rowptr
                       const T* val, const int64_t* blkbase, int64_t m, int ell, int n,
                       int64_t nblocks, cudaStream_t s, int64_t blk0 = 0, int64_t nblk = -1);
 void launch_finish(const FinishParams& F, cudaStream_t s);
+// CSC M^T w and the finish in one kernel (s never leaves registers)
+template <typename T>
+void launch_mtw_finish_csc(const FinishParams& F, const Window& W, const int* colptr,
+                           const int* cscrow, const T* cscval, const int64_t* blkbase,
+                           const double* w, cudaStream_t s);
 void launch_gram_reduce(double* panel, const Window& W, const double* part, int nsplit,
                         cudaStream_t s);
 void launch_gram_diag_fp64(double* panel_diag, int64_t ld, const float* A, int ell, int n,
