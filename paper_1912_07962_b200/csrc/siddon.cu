@@ -209,6 +209,52 @@ __global__ void __launch_bounds__(256) k_siddon_fill(RayGeom G, const int64_t* _
   RayState R;
   ray_setup(G, row, R);
   const int64_t lo = rowptr[row], hi = rowptr[row + 1];
+  const int n = G.n;
+  if (DIM == 2 || R.d[2] == 0.0) {
+    // At most two varying axes (2D, or 3D with the ray in a z plane): the
+    // row is written straight into its sorted place -- mirrored when the
+    // outer axis runs backwards -- and each group of equal outer index is
+    // reversed as soon as it is complete (its entries are still in L2)
+    // when the inner axis runs backwards in the written order. The
+    // monotonicity that makes this the sorted order is checked per run.
+    const bool mirror = R.d[1] < 0.0;
+    const bool grev = (R.d[0] < 0.0) != mirror;
+    int64_t q = 0, gkey = -1, gstart = 0, last = 0;
+    int px = -1, py = -1, pz = -1;
+    bool bad = false;
+    trace<DIM>(R, n, [&](int64_t flat, double len) {
+      const int ix = (int)(flat % n), iy = (int)((flat / n) % n), iz = (int)(flat / ((int64_t)n * n));
+      if (px >= 0) {
+        bad |= R.d[0] > 0.0 ? ix < px : (R.d[0] < 0.0 ? ix > px : ix != px);
+        bad |= R.d[1] > 0.0 ? iy < py : (R.d[1] < 0.0 ? iy > py : iy != py);
+        bad |= iz != pz;
+      }
+      px = ix, py = iy, pz = iz;
+      const int64_t pos = mirror ? hi - 1 - q : lo + q;
+      const int64_t key = flat / n;
+      if (key != gkey) {
+        if (grev && gkey >= 0) {
+          if (mirror) reverse_range(col, val, last, gstart + 1);
+          else reverse_range(col, val, gstart, last + 1);
+        }
+        gkey = key;
+        gstart = pos;
+      }
+      if (pos >= lo && pos < hi) col[pos] = (int)flat, val[pos] = (T)len;
+      last = pos;
+      ++q;
+    });
+    if (q != hi - lo) {
+      atomicOr(err, 1);
+      return;
+    }
+    if (grev && gkey >= 0) {
+      if (mirror) reverse_range(col, val, last, gstart + 1);
+      else reverse_range(col, val, gstart, last + 1);
+    }
+    if (bad) atomicOr(err, 2);
+    return;
+  }
   int64_t e = lo;
   trace<DIM>(R, G.n, [&](int64_t flat, double len) {
     if (e < hi) col[e] = (int)flat, val[e] = (T)len;
@@ -218,8 +264,8 @@ __global__ void __launch_bounds__(256) k_siddon_fill(RayGeom G, const int64_t* _
     atomicOr(err, 1);
     return;
   }
-  // sort by flat index: the outermost axis first, then within its groups
-  const int n = G.n;
+  // general 3D direction: sort by flat index in passes, the outermost axis
+  // first, then within its groups
   int flip = 1;
   {
     const int a = DIM - 1;
