@@ -927,18 +927,19 @@ static void par_memcpy(char* dst, const char* src, size_t n) {
   }
   const size_t part = (n / NT + 63) & ~(size_t)63;
   std::thread th[NT - 1];
-  size_t done = part;  // bytes from 0 this thread copies (grows if a helper cannot start)
+  size_t rest = n;  // start of the range no helper took (copied here)
   for (int t = 1; t < NT; ++t) {
     const size_t o = part * t;
     if (o >= n) break;
     try {
       th[t - 1] = std::thread([=]() { memcpy(dst + o, src + o, std::min(part, n - o)); });
     } catch (...) {  // no thread available: copy the rest here (nothing may escape the C ABI)
-      done = n;
+      rest = o;
       break;
     }
   }
-  memcpy(dst, src, std::min(done, n));
+  memcpy(dst, src, std::min(part, n));
+  if (rest < n) memcpy(dst + rest, src + rest, n - rest);
   for (auto& t : th)
     if (t.joinable()) t.join();
 }
