@@ -473,3 +473,25 @@ def test_host_streaming_rejects_bad_column(slim, monkeypatch):
     with pytest.raises(ValueError, match="column index"):
         slim.run("slimls", op, slim.Sampler("cyclic", 6, 0), slim.Schedule("constant", 10.0),
                  epochs=1.0, r=1)
+
+
+def test_streaming_probe_keeps_solver_state(slim):
+    """slim_probe_stream (bench 'streaming') measures the operator-streaming
+    kernels on scratch only: a run after the probe continues bit-identically."""
+    import ctypes as C
+    from paper_1912_07962_b200 import _lib, problems
+    from paper_1912_07962_b200.linops import device_operator
+    prob = problems.tomo2d(grid=32, n_views=20, rays=46, seed=3)
+    op = prob.op
+    mk = lambda: slim.Sampler("random_cyclic", op.n_blocks, 2)
+    kw = dict(epochs=30 / op.n_blocks, r=3)
+    ref = slim.run("slimls", op, mk(), slim.Schedule("constant", 1000.0), **kw)
+    dop = device_operator(op, 3, 0)
+    us, nbytes = C.c_double(0), C.c_double(0)
+    for kid in (0, 1, 2):
+        dop.call("slim_probe_stream", kid, 4, C.byref(us), C.byref(nbytes))
+        assert us.value > 0 and nbytes.value > 0
+    again = slim.run("slimls", op, mk(), slim.Schedule("constant", 1000.0), **kw)
+    np.testing.assert_array_equal(again.x_final, ref.x_final)
+    with pytest.raises(ValueError):
+        dop.call("slim_probe_stream", 3, 4, C.byref(us), C.byref(nbytes))
