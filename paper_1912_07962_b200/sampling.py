@@ -1,10 +1,13 @@
-"""Block-index selection, bit-exact with the reference ``Sampler``.
+"""Block-index selection, bit-exact with the reference ``Sampler``
+(sampling.py:35-84).
 
-Same three schemes over 1-based block indices and the same Philox 4x64
-stream keyed by the seed (reference sampling.py:35-84), so an index trace
-is a pure function of (scheme, M, seed).  The B200 driver consumes the
-trace up front: :meth:`Sampler.indices` gives the whole run's sequence,
-which the device loop then walks without any host round trip.
+An index trace is a pure function of (scheme, M, seed): the three schemes
+draw 1-based block indices from the Philox 4x64 stream keyed by the seed,
+with the reference's draw sequence (one bounded draw per step for
+``uniform_iid``; one backward Fisher-Yates shuffle per epoch for
+``random_cyclic``; no draws for ``cyclic``). The B200 driver takes the whole
+run's trace up front (:meth:`Sampler.indices`) and the device loop walks it
+without host round trips.
 """
 
 from __future__ import annotations
@@ -14,51 +17,56 @@ import numpy as np
 SCHEMES = ("cyclic", "random_cyclic", "uniform_iid")
 
 
-def _fisher_yates(m: int, rng: np.random.Generator) -> np.ndarray:
-    """Backward shuffle of 1..m, one bounded draw per position (sampling.py:38-44)."""
-    perm = np.arange(1, m + 1, dtype=np.int64)
+def _shuffled(m: int, rng: np.random.Generator) -> np.ndarray:
+    """1..m permuted by a backward Fisher-Yates pass: position i (from m - 1
+    down to 1) swaps with a uniform draw from [0, i] (sampling.py:38-44)."""
+    order = np.arange(1, m + 1, dtype=np.int64)
     for i in range(m - 1, 0, -1):
         j = int(rng.integers(0, i + 1))
-        perm[i], perm[j] = perm[j], perm[i]
-    return perm
+        order[[i, j]] = order[[j, i]]
+    return order
 
 
 class Sampler:
-    """Stateful index source (sampling.py:47-84); single-threaded."""
+    """Stateful index source with the reference attributes (``scheme``,
+    ``n_blocks``, ``seed``, ``rng``, ``position``); single-threaded."""
 
     def __init__(self, scheme: str, n_blocks: int, seed: int = 0):
         if scheme not in SCHEMES:
             raise ValueError(f"unknown scheme {scheme!r}, want one of {SCHEMES}")
         if n_blocks < 1:
             raise ValueError("n_blocks must be >= 1")
-        self.scheme = scheme
-        self.n_blocks = int(n_blocks)
-        self.seed = int(seed)
+        self.scheme, self.n_blocks, self.seed = scheme, int(n_blocks), int(seed)
         self.rng = np.random.Generator(np.random.Philox(key=self.seed))
         self.position = 0
-        self._epoch_perm: np.ndarray | None = None
+        self._order = None  # the current epoch's permutation (random_cyclic)
+        self._draw = {"cyclic": self._draw_cyclic, "uniform_iid": self._draw_iid,
+                      "random_cyclic": self._draw_permuted}[scheme]
+
+    def _draw_cyclic(self) -> int:
+        return self.position % self.n_blocks + 1
+
+    def _draw_iid(self) -> int:
+        return int(self.rng.integers(1, self.n_blocks + 1))
+
+    def _draw_permuted(self) -> int:
+        slot = self.position % self.n_blocks
+        if slot == 0:  # a new epoch: a fresh permutation
+            self._order = _shuffled(self.n_blocks, self.rng)
+        return int(self._order[slot])
 
     def next_index(self) -> int:
-        m = self.n_blocks
-        if self.scheme == "cyclic":
-            idx = self.position % m + 1
-        elif self.scheme == "uniform_iid":
-            idx = int(self.rng.integers(1, m + 1))
-        else:
-            offset = self.position % m
-            if offset == 0:
-                self._epoch_perm = _fisher_yates(m, self.rng)
-            idx = int(self._epoch_perm[offset])
+        idx = self._draw()
         self.position += 1
         return idx
 
     def indices(self, count: int) -> np.ndarray:
-        """The next ``count`` indices (same sequence as repeated next_index)."""
-        if self.scheme == "cyclic":
+        """The next ``count`` indices, as ``count`` calls of next_index."""
+        if self.scheme == "cyclic":  # no draws: closed form
             out = (self.position + np.arange(count, dtype=np.int64)) % self.n_blocks + 1
             self.position += count
             return out
-        return np.array([self.next_index() for _ in range(count)], dtype=np.int64)
+        return np.fromiter((self.next_index() for _ in range(count)), dtype=np.int64, count=count)
 
     @property
     def epochs_completed(self) -> float:

@@ -24,13 +24,33 @@ from .linops import DeviceOperator, RowBlockOperator, SampleBlock, SparseBlockOp
 TOMO3D_MAX_N = 64  # reference guard for host-built 3D projectors (tomo.py:304-320)
 
 
+def _checked_views(mode: str, angles, directions):
+    """Validated view parameters of a geometry (same rules and messages as
+    tomo.py:153-178): 2D angles in (-90, 90] degrees, 3D unit directions."""
+    if mode == "parallel_2d":
+        if angles is None or len(angles) == 0:
+            raise ValueError("2D geometry needs at least one angle")
+        ang = np.asarray(angles, dtype=float)
+        if ((ang <= -90.0) | (ang > 90.0)).any():
+            raise ValueError("view angles must lie in (-90, 90] degrees")
+        return ang, directions
+    if mode == "parallel_3d":
+        if directions is None or len(directions) == 0:
+            raise ValueError("3D geometry needs at least one direction")
+        dirs = np.asarray(directions, dtype=float)
+        if dirs.ndim != 2 or dirs.shape[1] != 3:
+            raise ValueError("directions must be (n_views, 3)")
+        if (np.abs(np.sqrt((dirs * dirs).sum(axis=1)) - 1.0) > 1e-12).any():
+            raise ValueError("directions must be unit vectors (1e-12)")
+        return angles, dirs
+    raise ValueError(f"unknown geometry mode {mode!r}")
+
+
 @dataclass(frozen=True)
 class ProjectionGeometry:
-    """Parallel-beam acquisition description (tomo.py:139-182).
-
-    ``rays_per_view`` is the ray count for 2D views and the per-axis
-    detector side for 3D views (a 3D block has rays_per_view**2 rows).
-    """
+    """Parallel-beam acquisition (reference schema, tomo.py:139-182): 2D views
+    by angle, 3D views by direction; ``rays_per_view`` is the 2D ray count or
+    the 3D detector side (a 3D view then has rays_per_view**2 rows)."""
 
     mode: str
     angles: np.ndarray | None = None
@@ -39,45 +59,32 @@ class ProjectionGeometry:
     detector_spacing: float = 1.0
 
     def __post_init__(self):
-        if self.mode == "parallel_2d":
-            if self.angles is None or len(self.angles) == 0:
-                raise ValueError("2D geometry needs at least one angle")
-            ang = np.asarray(self.angles, dtype=float)
-            if np.any(ang <= -90.0) or np.any(ang > 90.0):
-                raise ValueError("view angles must lie in (-90, 90] degrees")
-            object.__setattr__(self, "angles", ang)
-        elif self.mode == "parallel_3d":
-            if self.directions is None or len(self.directions) == 0:
-                raise ValueError("3D geometry needs at least one direction")
-            dirs = np.asarray(self.directions, dtype=float)
-            if dirs.ndim != 2 or dirs.shape[1] != 3:
-                raise ValueError("directions must be (n_views, 3)")
-            norms = np.linalg.norm(dirs, axis=1)
-            if np.any(np.abs(norms - 1.0) > 1e-12):
-                raise ValueError("directions must be unit vectors (1e-12)")
-            object.__setattr__(self, "directions", dirs)
-        else:
-            raise ValueError(f"unknown geometry mode {self.mode!r}")
+        ang, dirs = _checked_views(self.mode, self.angles, self.directions)
+        object.__setattr__(self, "angles", ang)
+        object.__setattr__(self, "directions", dirs)
         if self.rays_per_view < 1:
             raise ValueError("rays_per_view must be >= 1")
-        if self.detector_spacing <= 0:
+        if not self.detector_spacing > 0:
             raise ValueError("detector_spacing must be > 0")
 
     @property
     def n_views(self) -> int:
-        return len(self.angles) if self.mode == "parallel_2d" else len(self.directions)
+        views = self.angles if self.mode == "parallel_2d" else self.directions
+        return len(views)
 
 
 def parallel_2d_geometry(angles_deg, rays_per_view: int,
                          detector_spacing: float = 1.0) -> ProjectionGeometry:
-    return ProjectionGeometry("parallel_2d", angles=np.asarray(angles_deg, dtype=float),
-                              rays_per_view=rays_per_view, detector_spacing=detector_spacing)
+    """Geometry of 2D views at ``angles_deg`` (tomo.py:185-193)."""
+    return ProjectionGeometry("parallel_2d", np.asarray(angles_deg, dtype=float), None,
+                              rays_per_view, detector_spacing)
 
 
 def parallel_3d_geometry(directions, detector_side: int,
                          detector_spacing: float = 1.0) -> ProjectionGeometry:
-    return ProjectionGeometry("parallel_3d", directions=np.asarray(directions, dtype=float),
-                              rays_per_view=detector_side, detector_spacing=detector_spacing)
+    """Geometry of 3D views along unit ``directions`` (tomo.py:196-204)."""
+    return ProjectionGeometry("parallel_3d", None, np.asarray(directions, dtype=float),
+                              detector_side, detector_spacing)
 
 
 def _host_view(geom: ProjectionGeometry, n: int, v: int):

@@ -103,3 +103,17 @@ def test_sparse_restatement_matches_reference(name):
                                atol=1e-10 * np.abs(c["x_final"]).max())
     np.testing.assert_allclose(traj.rel_errors["x_true"], c["rel"]["x_true"], rtol=1e-10)
     np.testing.assert_allclose(traj.residual_norms, c["residual_norms"], rtol=1e-10, equal_nan=True)
+
+
+def test_package_sampler_matches_reference_traces():
+    """The product's Sampler (next_index and the up-front indices() trace,
+    mixed) reproduces every reference trace bit for bit."""
+    from paper_1912_07962_b200.sampling import Sampler
+    d = gc.load("sampler.npz")
+    for key in d.files:
+        scheme, m, seed = key.split("/")
+        s = Sampler(scheme, int(m), int(seed))
+        n = len(d[key])
+        got = np.concatenate([s.indices(n // 2), [s.next_index() for _ in range(n - n // 2)]])
+        assert np.array_equal(got, d[key]), key
+        assert s.epochs_completed == n / int(m)
