@@ -362,13 +362,17 @@ def run_ours(args, world, rank, local, dist):
     i8ops = timing.get("cholesky_i8ops", 0.0) / max(1, timing["cholesky_count"])
     if i8ops > 0:
         # int8 tensor-core factorization: the tile updates are exact int32
-        # digit-pair products (36 per 64^3 update); POTRF/TRSM stay fp64
+        # digit-pair products (QD (QD + 1) / 2 per 64^3 update); POTRF/TRSM
+        # stay fp64
+        qd, dbits = timing["cholesky_digits"]
+        pairs = qd * (qd + 1) // 2
         ach_i8 = i8ops / (chol_ms * 1e-3) / 1e12
         roofline = {"bound": "tensor", "achieved": ach_i8, "peak": I8_PEAK_TOPS,
                     "unit": "TOPS (int8)", "frac": ach_i8 / I8_PEAK_TOPS, "traffic": traffic,
                     "kernel": f"k_chol_i8 (tile-DAG Cholesky, updates on tcgen05 kind::i8 with "
                               f"TMEM accumulators, {per_launch:g} systems of N={N} per launch)",
-                    "algorithmic_per_launch": f"{i8ops:.4g} int8 ops (36 digit-pair products x "
+                    "algorithmic_per_launch": f"{i8ops:.4g} int8 ops ({pairs} digit-pair products "
+                                              f"({qd} digits: 7-bit lead, {dbits}-bit rest) x "
                                               f"2*64^3 per 64x64x64 tile update; the launch "
                                               f"factors {flops_chol:.4g} fp64-equivalent flop)",
                     "peak_source": "int8 tcgen05 peak measured on this pool, M=128 N=256 "

@@ -193,8 +193,11 @@ int slim_block_residual(slim_ctx* ctx, int64_t block, const double* x, double* r
  * which = 5 returns instead the algorithmic fp64 flops of the profiled
  * factorization launches (the tiles they factor; (64 T)^3 / 3 for a
  * from-scratch system) in *ms_out and their count in *launches_out;
- * which = 6 the int8 tensor-core ops of their tile updates (36 digit-pair
- * products of 2 * 64^3 per 64x64x64 update; 0 with SLIM_CHOL=dmma).      */
+ * which = 6 the int8 tensor-core ops of their tile updates (QD (QD + 1) / 2
+ * digit-pair products of 2 * 64^3 per 64x64x64 update; 0 with
+ * SLIM_CHOL=dmma); which = 7 the digit layout of those updates: the digit
+ * count QD in *ms_out and the trailing-digit width in bits in
+ * *launches_out (compile-time SLIM_QD / SLIM_DBITS).                     */
 int slim_timing(slim_ctx* ctx, int32_t which, double* ms_out, int64_t* launches_out);
 int slim_set_profiling(slim_ctx* ctx, int32_t enable);
 /* time only steps k0..K of the next slim_run (which = 3 in slim_timing):

@@ -1271,7 +1271,12 @@ int slim_set_timing_start(slim_ctx* c, int64_t k0) {
 }
 
 int slim_timing(slim_ctx* c, int32_t which, double* ms, int64_t* launches) {
-  if (!c || which < 0 || which > 6) FAIL(c, SLIM_EINVAL, "bad argument");
+  if (!c || which < 0 || which > 7) FAIL(c, SLIM_EINVAL, "bad argument");
+  if (which == 7) {  // digit layout of the int8 factorization (compile time)
+    if (ms) *ms = (double)QD;
+    if (launches) *launches = DBITS;
+    return SLIM_OK;
+  }
   if (which == 6) {  // int8 tensor ops of the profiled factorization launches
     if (ms) *ms = chol_use_i8() ? c->chol_i8ops : 0.0;
     if (launches) *launches = c->t_n[1];

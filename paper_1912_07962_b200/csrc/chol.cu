@@ -902,7 +902,8 @@ __device__ __forceinline__ void slice_tile(const double* X, const int* rex, int 
   // I = rint(L 2^(7 QD - e)) = rint(v 2^(7 (QD - 1))): |I| < 127.5 2^(7 (QD - 1)),
   // exact in fp64 and int64; balanced base-128 digits peeled off from the
   // bottom in integer arithmetic, the remaining top digit in [-127, 127]
-  const double sc = oz::pow2(7 * QD - __ldcg(rex + r));
+  // (DBITS = 8: base-256 digits in [-128, 127], same argument)
+  const double sc = oz::pow2(7 + DBITS * (QD - 1) - __ldcg(rex + r));
   uint32_t w[QD][4];
 #pragma unroll
   for (int a = 0; a < QD; ++a)
@@ -913,8 +914,9 @@ __device__ __forceinline__ void slice_tile(const double* X, const int* rex, int 
     long long I = __double2ll_rn(X[r * TS + 16 * kq + cc] * sc);
 #pragma unroll
     for (int a = QD - 1; a >= 1; --a) {
-      const int d = (((int)I + 64) & 127) - 64;
-      I = (I - d) >> 7;
+      constexpr int H = 1 << (DBITS - 1);
+      const int d = (((int)I + H) & (2 * H - 1)) - H;
+      I = (I - d) >> DBITS;
       w[a][cc >> 2] |= ((uint32_t)d & 0xffu) << (8 * (cc & 3));
     }
     w[0][cc >> 2] |= ((uint32_t)(int)I & 0xffu) << (8 * (cc & 3));
@@ -1134,7 +1136,7 @@ __global__ void __launch_bounds__(256, 1) k_chol_i8(const __grid_constant__ Chol
         int v[32];
         oz::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + 64 * t + 32 * h, v);
 #pragma unroll
-        for (int c = 0; c < 32; ++c) s[c] = fma(s[c], 0.0078125, (double)v[c]);
+        for (int c = 0; c < 32; ++c) s[c] = fma(s[c], 1.0 / (1 << DBITS), (double)v[c]);
       }
     }
     if (sel == 0 || two) {

@@ -30,8 +30,8 @@ struct CholMat {
   double* Linv;         // T x 4096: inverses of the diagonal tiles (k_diag_inv)
   // int8 digit slices of L for the tensor-core updates (chol.cu, k_chol_i8),
   // by tile column: [k][k half][digit][tile row i < qT][64 rows][32 B], so the
-  // A operand of a task (tile rows i, i + 1, all 8 digits) is one 3D TMA box;
-  // qmapA boxes 128 rows x 8 digits, qmapB 64 rows x 8 digits (SWIZZLE_32B)
+  // A operand of a task (tile rows i, i + 1, all QD digits) is one 3D TMA box;
+  // qmapA boxes 128 rows x QD digits, qmapB 64 rows x QD digits (SWIZZLE_32B)
   int8_t* Q;
   CUtensorMap qmapA, qmapB;
   int qT;               // tile rows per column in Q (the buffer's Tmax)
@@ -138,15 +138,25 @@ size_t chol_smem_bytes();
 // factorization kernel: true = int8 tensor-core updates (default), false =
 // fp64 DMMA updates (SLIM_CHOL=dmma, kept for A/B measurements)
 bool chol_use_i8();
-// signed 7-bit digits per factor entry in the int8 tensor-core updates
-// (k_chol_i8): QD digits keep 7 QD bits below each row's scale
+// signed digits per factor entry in the int8 tensor-core updates
+// (k_chol_i8): a leading digit in [-127, 127] (7 bits) and QD - 1 balanced
+// digits of DBITS bits each, so 7 + DBITS (QD - 1) bits below each row's scale
 #ifndef SLIM_QD
-#define SLIM_QD 8
+#define SLIM_QD 7
+#endif
+#ifndef SLIM_DBITS
+#define SLIM_DBITS 8
 #endif
 constexpr int QD = SLIM_QD;
+constexpr int DBITS = SLIM_DBITS;
 static_assert(QD >= 5 && QD <= 8, "digit count");
-// int8 updates: |P_t| <= (2 * 127 * 64 + (QD - 2) * 64^2) * 64 T < 2^31
-constexpr int CHOL_I8_TMAX = 800;
+static_assert(DBITS == 7 || DBITS == 8, "digit width");
+// int8 updates: |P_t| <= (2 * 127 * H + (QD - 2) * H^2) * 64 T < 2^31 with
+// H = 2^(DBITS - 1) the largest trailing digit magnitude
+constexpr long long CHOL_I8_PAIRMAX =
+    (2LL * 127 * (1 << (DBITS - 1)) + (QD - 2) * (1LL << (2 * (DBITS - 1)))) * 64;
+constexpr int CHOL_I8_TMAX =
+    (int)(((1LL << 31) - 1) / CHOL_I8_PAIRMAX < 800 ? ((1LL << 31) - 1) / CHOL_I8_PAIRMAX : 800);
 // TMA views of a sliced factor buffer with qT tile rows per column (box
 // rows = 128 for the A operand, 64 for B; QD digits per box)
 bool tma_map_q(CUtensorMap* m, const int8_t* base, int qT, int box_rows);
