@@ -495,3 +495,21 @@ def test_streaming_probe_keeps_solver_state(slim):
     np.testing.assert_array_equal(again.x_final, ref.x_final)
     with pytest.raises(ValueError):
         dop.call("slim_probe_stream", 3, 4, C.byref(us), C.byref(nbytes))
+
+
+def test_factorization_digit_layout_reported(slim):
+    """slim_timing which = 7 reports the compile-time digit layout of k_chol_i8
+    (seven digits, 8-bit trailing width by default), and the int8 op count of
+    the profiled launches (which = 6) is the layout's digit pairs times the
+    tile-update flops: QD (QD + 1) / 2 products of 2 * 64^3 per update."""
+    c = gc.dense_case("dense_dual")
+    op = slim.DenseBlockOperator(c["A"], int(c["ell"]), c["b"])
+    timing = {"start_step": 1}
+    traj = slim.run("slimls", op, slim.Sampler("random_cyclic", op.n_blocks, 5),
+                    slim.Schedule("constant", 100.0), epochs=2.0, r=3, timing=timing)
+    assert traj.status == "ok"
+    qd, dbits = timing["cholesky_digits"]
+    assert (qd, dbits) == (7, 8)
+    if timing["cholesky_i8ops"] > 0:  # SLIM_CHOL=dmma reports 0
+        updates = timing["cholesky_i8ops"] / (qd * (qd + 1) // 2 * 2 * 64 ** 3)
+        assert updates == int(updates) and updates >= 1
