@@ -1,5 +1,9 @@
 #!/bin/bash
 # round-1 evidence after the 8-bit trailing digits (SLIM_QD=7 SLIM_DBITS=8):
+# (build the comparison library first, in the build container:
+#  SLIM_NVCC_EXTRA="-DSLIM_QD=8 -DSLIM_DBITS=7" python -m paper_1912_07962_b200.build &&
+#  mv paper_1912_07962_b200/libslimb200.so paper_1912_07962_b200/libslimb200_d7.so &&
+#  python -m paper_1912_07962_b200.build)
 # factorization accuracy vs the previous layout (libslimb200_d7.so), GPU suite,
 # smoke, full bench lines, reference arm, launch list, ncu of k_chol_i8
 mkdir -p gpurun_out
