@@ -1,28 +1,51 @@
-"""Benchmark: slimLS iterations/s on the BASELINE headline workload.
+"""Benchmark: slimLS iterations/s (and rows/s) on the BASELINE headline workload.
 
-Workload (BASELINE.json configs[1], the config the metric is quoted on):
-2D parallel-beam tomography, 256x256 image (n = 65,536), 180 views over
-[0, pi) x 362 rays, Siddon CSR fp64, 10-ellipse phantom, 1% noise, one
-block = one view (ell = 362), r = 10, lambda = 1e-3 (alpha = 1000),
-random_cyclic sampling.  A "step" is one slimLS iteration.
+Workload (default ``--config 3`` = BASELINE.json configs[2], the config the
+metric's 1/2/4/8-GPU series is quoted on): 2D parallel-beam tomography,
+1024x1024 image (n = 1,048,576), 720 views over [0, pi) x 1448 rays, Siddon
+CSR with fp32 values / int32 indices (961 M nonzeros, 7.7 GB), 10-ellipse
+phantom, 1% noise, one block = one view (ell = 1448), r = 8 (dual systems of
+N = 13,032), lambda = 1e-3 (alpha = 1000), random_cyclic sampling.  A "step"
+is one slimLS iteration.  ``--config 1..5`` selects the other BASELINE
+configs, ``--config 6`` the weak-scaling family (below).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-* warm-up: max(W, r + 1) untimed steps so the memory window is full when
-  the timed region starts (the same slim_run call continues into it);
-* value: K / device time of steps W'+1 .. W'+K (CUDA events on the
-  x-chain stream, all streams joined at the end), operator resident in
-  HBM; per-iteration working set (Gram ring 254 MB + two factor buffers
-  + CSR 180 MB) exceeds the 126 MB L2, so no flush is inserted;
-* e2e: the public ``run()`` on a fresh host-resident operator, timed by
-  wall clock including the operator upload and the history / x download;
-* cpu_baseline / --impl reference: the oracle port of the reference's
-  algorithm (dense fetch, vstack, full Gram, LAPACK Cholesky) on the
-  host cores, a bounded sample (window fill + 3 steady-state steps).
+Timing (ours):
+* warm-up: max(W, r + 1) untimed steps (rounded to whole factorization
+  batches) so the memory window is full when the timed region opens; the
+  same slim_run call continues into the K timed steps;
+* value: K / device time of those steps (CUDA events on the x-chain stream,
+  every stream joined at both ends), max over ranks; the operator is
+  resident in HBM; the per-iteration working set (Gram ring + factor
+  buffers + operator) exceeds the 126 MB L2, so no flush is inserted;
+* e2e: the public ``run()`` on a fresh host-resident operator (block
+  uploads streamed in first-use order, history and x downloaded), wall
+  clock; h2d bytes are the bytes the library actually copied;
+* roofline: the dominant kernel (k_chol_i8), int8 ops per launch / mean
+  launch time from CUDA events on its stream; traffic from the committed
+  ncu capture with the same launch shape.
 
-N > 1 (torchrun): replicas only -- every rank runs an independent
-replica (sampler seed base + rank, like the reference harness), timing
-is the max over ranks, value = all ranks' steps / that time.
+N GPUs: ``--gpus N`` without torchrun spawns N ranks itself (127.0.0.1);
+under torchrun each rank reads RANK / LOCAL_RANK / WORLD_SIZE.  N > 1 runs
+ONE column-sharded solve (``--shard columns``, NCCL over NVLink: the Gram
+panel, residual partials and norm partials are sum-allreduced per step) with
+the factorizations distributed round-robin over the ranks (``--factor
+round_robin``) -- strong scaling on the fixed configs[2].
+``--config 6`` is the weak-scaling family: configs[4]'s generator with
+n = 8192 P columns (8192 per GPU), m = 4,194,304, ell = 256, r = 20.
+``--shard replicas`` runs N independent solves instead.
+
+Reference arm (``--impl reference``, rank 0 only): the reference's own CPU
+implementation on the host cores, without this repo's library:
+* configs[0], [1], [4]: the unmodified ``slimsolve.run`` from
+  ``baseline/_ref`` (operators from the reference's own projector /
+  a generator subclass of its RowBlockOperator);
+* configs[2], [3]: the reference cannot densify these blocks (12-34 GB
+  each), so the oracle's sparse dual-form restatement of its step is timed,
+  labelled as such, on blocks built by the reference's projector;
+BLAS threads are swept over {1, 2, 4, all} on one full-window step each and
+the K timed steps run at the best count.
 """
 
 from __future__ import annotations
@@ -31,6 +54,7 @@ import argparse
 import gc
 import json
 import os
+import socket
 import subprocess
 import sys
 import time
@@ -39,32 +63,44 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+REF_PATH = os.path.join(ROOT, "baseline", "_ref")
 
 METRIC = "slim iterations/s and rows/s at 1/2/4/8 B200; HBM GB/s vs roofline"
+DEFAULT_CONFIG = 3
 
 # BASELINE.json configs (1-based here); lambda = 1 / alpha
 CONFIGS = {
     1: dict(workload="configs[0]: dense Gaussian LS 20,000 x 1,000 fp64, ell=100, r=5, "
-                     "lambda=1e-2, random_cyclic", r=5, alpha=100.0, scheme="random_cyclic",
-            dtype="f64"),
+                     "lambda=1e-2, random_cyclic", r=5, alpha=100.0, scheme="random_cyclic"),
     2: dict(workload="configs[1]: 2D parallel-beam tomography 256x256, 180 views x 362 rays, "
                      "Siddon CSR fp64, r=10, lambda=1e-3, random_cyclic", r=10, alpha=1000.0,
-            scheme="random_cyclic", dtype="f64"),
+            scheme="random_cyclic"),
     3: dict(workload="configs[2]: 2D tomography 1024x1024, 720 views x 1448 rays, Siddon CSR "
                      "fp32 values / int32 indices, r=8, lambda=1e-3, random_cyclic", r=8,
-            alpha=1000.0, scheme="random_cyclic", dtype="f32 values, f64 arithmetic"),
+            alpha=1000.0, scheme="random_cyclic"),
     4: dict(workload="configs[3]: 3D parallel-beam tomography 128^3, 180 directions x 128x128 "
                      "detector, 8 sub-blocks of 2048 rays per view, CSR fp32, r=5, lambda=1e-3, "
-                     "random_cyclic", r=5, alpha=1000.0, scheme="random_cyclic",
-            dtype="f32 values, f64 arithmetic"),
+                     "random_cyclic", r=5, alpha=1000.0, scheme="random_cyclic"),
     5: dict(workload="configs[4]: streaming dense LS n=65,536, m=4,194,304, splitmix64 rows "
                      "generated in-kernel (fp32), ell=256, r=20, lambda=1e-2, single pass",
-            r=20, alpha=100.0, scheme="cyclic", dtype="f32 values, f64 arithmetic"),
+            r=20, alpha=100.0, scheme="cyclic"),
+    6: dict(workload="weak-scaling family of configs[4]: splitmix64 rows generated in-kernel, "
+                     "n = 8192 x P columns (8192 per GPU), m=4,194,304, ell=256, r=20, "
+                     "lambda=1e-2, single pass", r=20, alpha=100.0, scheme="cyclic"),
 }
 SAMPLER_SEED = 7962
+# ||A x_true|| of the whole operator for the large tomography configs (host
+# projector, tools/bench_constants.py): the reference arm builds only the
+# views its sample touches and scales the 1% noise with these
+CLEAN_NORM = {3: 796647.3575867971, 4: 59051.36952100318}
+DTYPE = {1: "f64", 2: "f64", 3: "f32 values, f64 arithmetic", 4: "f32 values, f64 arithmetic",
+         5: "f32 values (generated), f64 arithmetic", 6: "f32 values (generated), f64 arithmetic"}
+DTYPE_NOTE = ("fp64 iterates, Gram and solves; the dual-system Cholesky's tile updates are fp64 "
+              "emulated exactly by int8 digit-slice products on tcgen05 (7 signed digits, 55 "
+              "bits below each row's scale), POTRF/TRSM in fp64 DMMA")
 
 
-def build_config(cfg_id, threads=None):
+def build_config(cfg_id, threads=None, world=1):
     """(op, b, x_true) of a BASELINE config at full size."""
     from paper_1912_07962_b200 import problems
 
@@ -78,8 +114,10 @@ def build_config(cfg_id, threads=None):
     elif cfg_id == 4:
         p = problems.tomo3d(grid=128, n_views=180, side=128, sub_rows=2048, seed=4,
                             threads=threads)
-    else:
+    elif cfg_id == 5:
         return problems.generated_dense()
+    else:
+        return problems.generated_dense(n=8192 * world)
     return p.op, p.b, p.x_true
 
 
@@ -109,6 +147,31 @@ I8_PEAK_TOPS = 4579.0
 I8_N64_CEIL_TOPS = 3056.0
 
 
+# ---------------------------------------------------------------------------
+# ranks
+# ---------------------------------------------------------------------------
+
+
+def _free_port() -> int:
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _spawn(n: int) -> int:
+    """--gpus N without torchrun: launch N ranks of this script (one per GPU);
+    rank 0's stdout is the bench line."""
+    port = _free_port()
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n),
+                   LOCAL_WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__), *sys.argv[1:]],
+                                      env=env, stdout=None if r == 0 else subprocess.DEVNULL))
+    rcs = [p.wait() for p in procs]
+    return max(rcs, key=abs)
+
+
 def _dist():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -116,6 +179,8 @@ def _dist():
     if world > 1:
         import torch.distributed as dist
 
+        # host plumbing (NCCL id broadcast, barriers, max-over-ranks timing);
+        # the data path's collectives are NCCL inside the library
         dist.init_process_group("gloo")
         return world, rank, local, dist
     return 1, 0, 0, None
@@ -188,8 +253,13 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+# ---------------------------------------------------------------------------
+# the reference's CPU implementation (reference arm and cpu_baseline)
+# ---------------------------------------------------------------------------
+
+
 def oracle_fetch(op, b):
-    """The oracle's fetch for the operator (reference arithmetic)."""
+    """The oracle's fetch for an operator of this package (test helper)."""
     from oracle import slimls_oracle as orc
     from paper_1912_07962_b200.linops import GeneratedBlockOperator, SparseBlockOperator
 
@@ -200,83 +270,298 @@ def oracle_fetch(op, b):
     return orc.dense_fetch(op.matrix, b, op.block_rows)
 
 
-def cpu_sample(cfg_id, op, b, r, alpha, scheme, seed, steady=3):
-    """The reference algorithm (oracle port) on the host: the window is filled
-    with r fetched blocks (untimed), then ``steady`` full-window steps are
-    timed, each including its block fetch as in the reference loop."""
-    from collections import deque
+def _reference_pkg():
+    if REF_PATH not in sys.path:
+        sys.path.insert(0, REF_PATH)
+    import slimsolve  # noqa: F401  (baseline/_ref: the unmodified reference install)
+    return slimsolve
 
-    from oracle import slimls_oracle as orc
 
-    idx = orc.sampler_indices(scheme, op.n_blocks, seed, r + steady)
-    n = op.n_cols
-    if cfg_id in (3, 4):
-        # dense fetch infeasible (12-34 GB per block): sparse dual-form restatement
-        import scipy.sparse as sp
+def _ref_tomo_blocks(cfg_id, needed):
+    """CSR blocks of a tomography config built by the reference's own
+    projector (tomo._view_block_2d / _view_block_3d) for the 1-based blocks
+    in ``needed``; others are empty placeholders the run never fetches.
+    Returns (blocks, x_true, b, n_views_built)."""
+    import scipy.sparse as sp
 
-        mats = [sp.csr_matrix((d.astype(float), ix, ip), shape=shp)
-                for ip, ix, d, shp in (op.csr_block(int(i)) for i in set(idx.tolist()))]
-        lookup = dict(zip(sorted(set(idx.tolist())), mats))
-        x = np.zeros(n)
-        window = deque(maxlen=r + 1)
-        for k in range(r):
-            window.append(lookup[int(idx[k])])
-        times = []
-        ell = op.block_rows
-        for k in range(r, r + steady):
-            i = int(idx[k])
-            t0 = time.perf_counter()
-            a = lookup[i]
-            window.append(a)
-            res = a @ x - b[(i - 1) * ell:i * ell]
-            mat = sp.vstack(list(window)).tocsr()
-            g = (mat @ mat.T).toarray() * alpha
-            g[np.diag_indices_from(g)] += 1.0
-            y = np.zeros(mat.shape[0])
-            y[-ell:] = res
-            import scipy.linalg
+    _reference_pkg()
+    from slimsolve import tomo as rtomo
 
-            w = scipy.linalg.solve(g, y, assume_a="pos")
-            x = x - alpha * (mat.T @ w)
-            times.append(time.perf_counter() - t0)
-        what = ("sparse dual-form restatement of the reference step (the reference's dense "
-                "block fetch needs 12-34 GB per block here)")
+    from paper_1912_07962_b200 import problems
+
+    if cfg_id in (2, 3):
+        grid, views, rays, seed = (256, 180, 362, 2) if cfg_id == 2 else (1024, 720, 1448, 3)
+        angles = problems.angles_0_pi(views)
+        x_true = problems.random_ellipses(grid, 10, seed)
+        ell, n = rays, grid * grid
+        blocks = []
+        for i in range(1, views + 1):
+            if i in needed:
+                blk = rtomo._view_block_2d(float(angles[i - 1]), grid, rays, 1.0).tocsr()
+                if cfg_id == 3:  # configs[2] stores fp32 values
+                    blk = sp.csr_matrix((blk.data.astype(np.float32).astype(np.float64),
+                                         blk.indices, blk.indptr), shape=blk.shape)
+                blocks.append(blk)
+            else:
+                blocks.append(sp.csr_matrix((ell, n)))
+        built = len(needed)
+    else:  # configs[3]: 3D, 8 sub-blocks of 2048 rays per view (seeded ray permutation)
+        dirs, ray_of_row = problems.tomo3d_geometry(180, 128, 2048, 4)
+        x_true = problems.random_ellipsoids(128, 20, 4)
+        side, sub = 128, 2048
+        rows, per = side * side, (side * side) // sub
+        ell, n = sub, 128 ** 3
+        blocks = [None] * (180 * per)
+        views = sorted({(i - 1) // per for i in needed})
+        for v in views:
+            full = rtomo._view_block_3d(dirs[v], 128, side, 1.0).tocsr()
+            perm = ray_of_row[v * rows:(v + 1) * rows]
+            for q in range(per):
+                sel = full[perm[q * sub:(q + 1) * sub]]
+                blocks[v * per + q] = sp.csr_matrix(
+                    (sel.data.astype(np.float32).astype(np.float64), sel.indices, sel.indptr),
+                    shape=sel.shape)
+        blocks = [blk if blk is not None else sp.csr_matrix((ell, n)) for blk in blocks]
+        built = len(views)
+    m = ell * len(blocks)
+    clean = np.zeros(m)
+    for i in needed:
+        clean[(i - 1) * ell:i * ell] = blocks[i - 1] @ x_true
+    if cfg_id == 2:
+        norm = float(np.linalg.norm(clean))  # every view was built
     else:
-        fetch = oracle_fetch(op, b)
-        st = orc._State(x=np.zeros(n), window=deque(maxlen=r + 1), div_limit_sq=np.inf)
-        for k in range(r):
-            st.window.append((int(idx[k]), fetch(int(idx[k]))[0]))
+        norm = CLEAN_NORM[cfg_id]
+        if norm is None:
+            raise SystemExit("bench.py: CLEAN_NORM missing (run tools/bench_constants.py)")
+    rng = np.random.Generator(np.random.Philox(key=problems_seed(cfg_id) + 1))
+    eps = rng.standard_normal(m)
+    eps *= 0.01 * norm / np.linalg.norm(eps)
+    return blocks, x_true, clean + eps, built
+
+
+def problems_seed(cfg_id):
+    return {2: 2, 3: 3, 4: 4}[cfg_id]
+
+
+class _Threads:
+    """BLAS thread count for the reference's NumPy/SciPy calls (threadpoolctl)."""
+
+    def __init__(self):
+        from threadpoolctl import threadpool_limits
+        self._limits = threadpool_limits
+        self._ctx = None
+
+    def set(self, n):
+        if self._ctx is not None:
+            self._ctx.unregister()
+        self._ctx = self._limits(limits=int(n))
+
+
+def _thread_counts():
+    allc = os.cpu_count() or 1
+    return sorted({c for c in (1, 2, 4, allc) if c <= allc})
+
+
+def _reference_sample(cfg_id, steps, warmup, sweep=True, budget_s=150.0):
+    """Time the reference's CPU implementation on a bounded sample of the
+    workload.  Returns a dict with the timed step count, per-step times, the
+    thread sweep and a description."""
+    cfg = CONFIGS[cfg_id]
+    r, alpha, scheme = cfg["r"], cfg["alpha"], cfg["scheme"]
+    pre = max(warmup, r + 1)  # window full before the timed steps
+    counts = _thread_counts() if sweep else []
+    nsweep = len(counts)
+    total = pre + nsweep + steps
+    _reference_pkg()
+    from slimsolve.sampling import Sampler as RefSampler
+
+    t_build = time.perf_counter()
+    threads = _Threads()
+    threads.set(os.cpu_count() or 1)
+    if cfg_id in (1, 5):
+        m_blocks = 200 if cfg_id == 1 else 16384
+    elif cfg_id == 2:
+        m_blocks = 180
+    elif cfg_id == 3:
+        m_blocks = 720
+    else:
+        m_blocks = 1440
+    idx = RefSampler(scheme, m_blocks, seed=SAMPLER_SEED).indices(total)
+    needed = set(int(i) for i in idx)
+    sweep_times = {}
+    if cfg_id in (3, 4):
+        from oracle import slimls_oracle as orc
+
+        blocks, xt, b, built = _ref_tomo_blocks(cfg_id, needed)
+        parts = [(blk.indptr, blk.indices, blk.data, blk.shape) for blk in blocks]
+        t_build = time.perf_counter() - t_build
         times = []
-        for k in range(r, r + steady):
-            i = int(idx[k])
-            t0 = time.perf_counter()
-            a, bb = fetch(i)
-            orc.slimls_step(st, i, a, bb, alpha)
-            times.append(time.perf_counter() - t0)
-        what = ("oracle restatement of the reference step (block fetch, vstack, full Gram, "
-                "LAPACK Cholesky solve)")
-    per_step = float(np.mean(times))
-    return {"value": 1.0 / per_step, "unit": "it/s", "cores": os.cpu_count(), "kind": "port",
-            "sample": f"{what}; window prefilled with {r} blocks (untimed), {steady} full-window "
-                      f"steps timed ({sum(times):.1f} s), BLAS threads = all {os.cpu_count()} "
-                      f"host cores"}
+        order = {pre + q + 1: c for q, c in enumerate(counts)}  # sweep step -> threads
+        first_timed = pre + nsweep + 1
+        best = [os.cpu_count() or 1]
+        t0 = [0.0]
+
+        class _Budget(Exception):
+            pass
+
+        def threads_at(k):
+            if (k - 1) in order:  # the sweep step that just finished
+                sweep_times[order[k - 1]] = times[-1]
+            if k in order:
+                threads.set(order[k])
+            elif k == first_timed:
+                if sweep_times:
+                    best[0] = min(sweep_times, key=sweep_times.get)
+                threads.set(best[0])
+                t0[0] = time.perf_counter()
+            elif k > first_timed + 1 and time.perf_counter() - t0[0] > budget_s:
+                raise _Budget()  # bounded sample: stop before step k
+
+        try:
+            orc.run_slimls_sparse(parts, b, idx, np.full(total, alpha), r=r,
+                                  references={"x_true": xt}, step_times=times,
+                                  threads_at=threads_at)
+        except _Budget:
+            pass
+        timed = times[first_timed - 1:]
+        what = (f"sparse dual-form restatement of the reference step (oracle/slimls_oracle.py "
+                f"run_slimls_sparse: full Gram recompute, LAPACK Cholesky solve), labelled: the "
+                f"reference's dense block fetch needs 12-34 GB per block here; blocks from the "
+                f"reference projector ({built} views built)")
+        kind = "port"
+    else:
+        from slimsolve.linops import DenseBlockOperator as RefDense
+        from slimsolve.linops import RowBlockOperator, SampleBlock
+        from slimsolve.linops import SparseBlockOperator as RefSparse
+        from slimsolve.solvers import Schedule as RefSchedule
+        from slimsolve.solvers import SolverState, run as ref_run, slimls_step
+
+        if cfg_id == 1:
+            from paper_1912_07962_b200 import problems
+            g = np.random.Generator(np.random.Philox(key=1912))
+            a = g.standard_normal((20000, 1000)) / np.sqrt(1000.0)
+            xt = g.standard_normal(1000)
+            clean = a @ xt
+            b = problems.scaled_noise(clean, 0.01, g)
+            op = RefDense(a, 100, b)
+            src = "dense operator (reference DenseBlockOperator)"
+        elif cfg_id == 2:
+            blocks, xt, b, built = _ref_tomo_blocks(2, set(range(1, 181)))
+            op = RefSparse(blocks, b)
+            src = "reference SparseBlockOperator from the reference projector (all 180 views)"
+        else:
+            from oracle import slimls_oracle as orc
+            n, ell, seed = 65536, 256, 1912
+            xt = np.random.Generator(np.random.Philox(key=seed)).standard_normal(n)
+            rows = total * ell  # cyclic single pass: blocks 1..total
+            clean = np.concatenate([orc.gen_rows(seed, s, ell, n) @ xt
+                                    for s in range(0, rows, ell)])
+            eps = np.random.Generator(np.random.Philox(key=seed + 1)).standard_normal(rows)
+            eps *= 0.005 * np.linalg.norm(clean) / np.linalg.norm(eps)
+            b_used = clean + eps
+
+            class GeneratedOperator(RowBlockOperator):
+                """Generator subclass of the reference's RowBlockOperator
+                (linops.py:75-100): block i generated on fetch."""
+
+                access_mode = "random_access"
+                n_rows, n_cols, block_rows, n_blocks = 4194304, n, ell, 16384
+
+                def has_rhs(self):
+                    return True
+
+                def fetch_block(self, i):
+                    self._check_index(i)
+                    s, e = self.row_range(i)
+                    return SampleBlock(i, orc.gen_rows(seed, s, ell, n), b_used[s:e])
+
+            op = GeneratedOperator()
+            src = ("generator RowBlockOperator subclass (splitmix64 rows evaluated in NumPy on "
+                   "fetch; b on the sampled rows)")
+        t_build = time.perf_counter() - t_build
+        # thread sweep: one full-window step per thread count through the
+        # reference's own slimls_step, after an untimed window fill
+        if counts:
+            st = SolverState.start(np.zeros(op.n_cols), RefSchedule("constant", alpha), r=r)
+            for k in range(pre):
+                slimls_step(st, op.fetch_block(int(idx[k])))
+            for q, c in enumerate(counts):
+                threads.set(c)
+                t0 = time.perf_counter()
+                slimls_step(st, op.fetch_block(int(idx[pre + q])))
+                sweep_times[c] = time.perf_counter() - t0
+            del st
+        best = [min(sweep_times, key=sweep_times.get) if sweep_times else (os.cpu_count() or 1)]
+        threads.set(best[0])
+        # the timed steps: the unmodified reference run() (pre + steps steps),
+        # per-step wall times from its own Trajectory (record_every = 1);
+        # bounded: fewer steps if the budget would be exceeded
+        per = min(sweep_times.values()) if sweep_times else None
+        k_run = steps
+        if per is not None and per * (pre + steps) > budget_s:
+            k_run = max(2, int(budget_s / per) - pre)
+        traj = ref_run("slimls", op, RefSampler(scheme, op.n_blocks, seed=SAMPLER_SEED),
+                       RefSchedule("constant", alpha), epochs=(pre + k_run) / op.n_blocks, r=r,
+                       references={"x_true": xt}, record_every=1)
+        timed = list(np.asarray(traj.wall_times)[1 + pre:])
+        what = f"unmodified slimsolve.run (baseline/_ref) on the {src}"
+        kind = "reference"
+    threads.set(os.cpu_count() or 1)
+    return {"timed": timed, "sweep": sweep_times, "best_threads": best[0], "prefill": pre,
+            "what": what, "kind": kind, "build_s": t_build}
+
+
+def _cpu_line(res, ell):
+    timed = res["timed"]
+    per = float(np.mean(timed)) if timed else float("nan")
+    sweep = {str(k): round(1.0 / v, 4) for k, v in sorted(res["sweep"].items())}
+    return {"value": 1.0 / per, "unit": "it/s", "cores": int(res["best_threads"]),
+            "kind": res["kind"], "rows_per_s": ell / per,
+            "sample": (f"{res['what']}; window filled with {res['prefill']} untimed steps, "
+                       f"{len(timed)} full-window steps timed ({sum(timed):.1f} s) at "
+                       f"{res['best_threads']} BLAS threads"
+                       + (f"; thread sweep (it/s by threads, one full-window step each): "
+                          f"{sweep}" if sweep else "")
+                       + f"; host has {os.cpu_count()} cores"),
+            "thread_sweep_it_per_s": sweep or None, "timed_steps": len(timed)}
 
 
 def run_reference(args, world, rank, dist):
     if rank != 0:
         return
-    cfg = CONFIGS[args.config]
-    op, b, _ = build_config(args.config)
-    cb = cpu_sample(args.config, op, b, cfg["r"], cfg["alpha"], cfg["scheme"], SAMPLER_SEED)
+    cfg_id = args.config
+    if cfg_id == 6:
+        cfg_id_ref = 5  # the family's P = 8 member is configs[4]; P = 1 has n = 8192
+    else:
+        cfg_id_ref = cfg_id
+    res = _reference_sample(cfg_id_ref, args.steps, args.warmup)
+    ell = {1: 100, 2: 362, 3: 1448, 4: 2048, 5: 256}[cfg_id_ref]
+    cb = _cpu_line(res, ell)
+    loaded = _native_loaded()
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "it/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 / cb["value"], "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": _config_dict(args.config, op, world),
-            "rows_per_s": cb["value"] * op.block_rows, "cpu_baseline": cb,
+            "n_gpus": world, "steps": len(res["timed"]), "steps_requested": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 / cb["value"], "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": CONFIGS[cfg_id_ref]["workload"], "reference": res["what"]},
+            "rows_per_s": cb["rows_per_s"], "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": "it/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+                    "d2h_bytes_per_step": 0},
+            "setup_s": round(res["build_s"], 1), "repo_native_loaded": loaded}
     print(json.dumps(line), flush=True)
+
+
+def _native_loaded():
+    try:
+        with open("/proc/self/maps") as fh:
+            return sorted({ln.split()[-1] for ln in fh if "libslimb200" in ln})
+    except OSError:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
 
 
 def _config_dict(cfg_id, op, world, sharded=False, factor="replicated"):
@@ -289,23 +574,78 @@ def _config_dict(cfg_id, op, world, sharded=False, factor="replicated"):
             "l2": "per-iteration working set > 126 MB L2 (no flush)"}
 
 
+def _roofline(timing, steps, N, cfg_id):
+    per_launch = steps / max(1, timing["cholesky_count"])
+    flops_chol = timing["cholesky_flops"] / max(1, timing["cholesky_count"])
+    chol_ms = timing["cholesky_ms"] / max(1, timing["cholesky_count"])
+    achieved = flops_chol / (chol_ms * 1e-3) / 1e12
+    agg = timing["cholesky_flops"] / (timing["window_ms"] * 1e-3) / 1e12
+    traffic, traffic_src = None, None
+    try:  # dram bytes per launch from the committed ncu --set full capture
+        with open(os.path.join(ROOT, "profiles", f"ncu_chol_cfg{cfg_id}.json")) as fh:
+            prof = json.load(fh)
+        traffic = prof["dram_bytes_per_launch"]
+        traffic_src = (f"profiles/ncu_chol_cfg{cfg_id}.json: {prof['systems_per_launch']} systems "
+                       f"per launch")
+    except (OSError, ValueError, KeyError):
+        pass
+    i8ops = timing.get("cholesky_i8ops", 0.0) / max(1, timing["cholesky_count"])
+    if i8ops > 0:
+        qd, dbits = timing["cholesky_digits"]
+        pairs = qd * (qd + 1) // 2
+        ach_i8 = i8ops / (chol_ms * 1e-3) / 1e12
+        return {"bound": "tensor", "achieved": ach_i8, "peak": I8_PEAK_TOPS,
+                "unit": "TOPS (int8)", "frac": ach_i8 / I8_PEAK_TOPS, "traffic": traffic,
+                "traffic_source": traffic_src,
+                "kernel": f"k_chol_i8 (tile-DAG Cholesky, updates on tcgen05 kind::i8 with "
+                          f"TMEM accumulators, {per_launch:g} systems of N={N} per launch)",
+                "algorithmic_per_launch": f"{i8ops:.4g} int8 ops ({pairs} digit-pair products "
+                                          f"({qd} digits: 7-bit lead, {dbits}-bit rest) x "
+                                          f"2*64^3 per 64x64x64 tile update; the launch "
+                                          f"factors {flops_chol:.4g} fp64-equivalent flop)",
+                "peak_source": "int8 tcgen05 peak measured on this pool, M=128 N=256 "
+                               "(tools/microbench/i8_rates.cu, profiles/i8_peak_r01.txt); "
+                               "MEASURED_PEAKS.json has no int8 entry (2 x its bf16 burst "
+                               "would be 3249 TOPS)",
+                "shape_ceiling_tops": I8_N64_CEIL_TOPS,
+                "fp64_equivalent_tflops": achieved,
+                "fp64_equivalent_frac_of_dmma_peak": achieved / FP64_PEAK_TFLOPS,
+                "aggregate_tflops_over_window": agg,
+                "avg_launch_ms": chol_ms, "launches": timing["cholesky_count"]}
+    return {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
+            "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+            "traffic_source": traffic_src,
+            "kernel": f"k_chol_tiles (fp64 DMMA tile-DAG Cholesky, {per_launch:g} systems "
+                      f"of N={N} interleaved per launch)",
+            "algorithmic_per_launch": f"{flops_chol:.4g} flop",
+            "peak_source": "FP64 DMMA peak measured on this pool "
+                           "(tools/microbench/fp64_rates.cu, profiles/fp64_peak_r01.txt)",
+            "aggregate_tflops_over_window": agg,
+            "avg_launch_ms": chol_ms, "launches": timing["cholesky_count"]}
+
+
 def run_ours(args, world, rank, local, dist):
     import paper_1912_07962_b200 as slim
 
     dev = local
-    cfg = CONFIGS[args.config]
-    op, b, xt = build_config(args.config)
+    cfg_id = args.config
+    cfg = CONFIGS[cfg_id]
+    sharded = world > 1 and args.shard == "columns"
+    if sharded:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines for the driver's log
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    op, b, xt = build_config(cfg_id, world=world)
     r, alpha, scheme = cfg["r"], cfg["alpha"], cfg["scheme"]
     ell, M = op.block_rows, op.n_blocks
-    seed = SAMPLER_SEED + rank
+    seed = SAMPLER_SEED + (0 if sharded else rank)
     N = (r + 1) * ell
     D = batch_size(N)
     wprime = -(-max(args.warmup, r + 1) // D) * D  # whole factorization batches
     total = wprime + args.steps
     if scheme == "cyclic" and total > M:
-        raise SystemExit(f"config {args.config}: {total} steps exceed one pass ({M} blocks)")
+        raise SystemExit(f"config {cfg_id}: {total} steps exceed one pass ({M} blocks)")
 
-    sharded = world > 1 and args.shard == "columns"
     if sharded:
         from paper_1912_07962_b200.parallel import NcclShard
 
@@ -313,7 +653,6 @@ def run_ours(args, world, rank, local, dist):
 
         torch.cuda.set_device(dev)
         shard = NcclShard.from_torch(op.n_cols, round_robin=args.factor == "round_robin")
-        seed = SAMPLER_SEED  # one solve: every shard walks the same index trace
     else:
         shard = None
 
@@ -342,60 +681,7 @@ def run_ours(args, world, rank, local, dist):
     t_win = _max_over_ranks(dist, timing["window_ms"] / 1e3)
     # replicas: every rank solves its own problem; columns: all ranks one solve
     value = (1 if sharded else world) * args.steps / t_win
-    # ---- roofline of the dominant kernel (batched tile Cholesky), per launch ----
-    # systems per batched launch; the algorithmic flops are those of the tiles
-    # the launches factor (a step recomputes only the tiles its new block
-    # reaches), counted by the library per launch
-    per_launch = args.steps / max(1, timing["cholesky_count"])
-    flops_chol = timing["cholesky_flops"] / max(1, timing["cholesky_count"])
-    chol_ms = timing["cholesky_ms"] / max(1, timing["cholesky_count"])
-    achieved = flops_chol / (chol_ms * 1e-3) / 1e12
-    agg = timing["cholesky_flops"] / (timing["window_ms"] * 1e-3) / 1e12
-    traffic = None
-    try:  # dram bytes per launch from the committed ncu --set full capture
-        with open(os.path.join(ROOT, "profiles", f"ncu_chol_cfg{args.config}.json")) as fh:
-            prof = json.load(fh)
-        if int(prof.get("systems_per_launch", 0)) == int(round(per_launch)):
-            traffic = prof["dram_bytes_per_launch"]
-    except (OSError, ValueError, KeyError):
-        pass
-    i8ops = timing.get("cholesky_i8ops", 0.0) / max(1, timing["cholesky_count"])
-    if i8ops > 0:
-        # int8 tensor-core factorization: the tile updates are exact int32
-        # digit-pair products (QD (QD + 1) / 2 per 64^3 update); POTRF/TRSM
-        # stay fp64
-        qd, dbits = timing["cholesky_digits"]
-        pairs = qd * (qd + 1) // 2
-        ach_i8 = i8ops / (chol_ms * 1e-3) / 1e12
-        roofline = {"bound": "tensor", "achieved": ach_i8, "peak": I8_PEAK_TOPS,
-                    "unit": "TOPS (int8)", "frac": ach_i8 / I8_PEAK_TOPS, "traffic": traffic,
-                    "kernel": f"k_chol_i8 (tile-DAG Cholesky, updates on tcgen05 kind::i8 with "
-                              f"TMEM accumulators, {per_launch:g} systems of N={N} per launch)",
-                    "algorithmic_per_launch": f"{i8ops:.4g} int8 ops ({pairs} digit-pair products "
-                                              f"({qd} digits: 7-bit lead, {dbits}-bit rest) x "
-                                              f"2*64^3 per 64x64x64 tile update; the launch "
-                                              f"factors {flops_chol:.4g} fp64-equivalent flop)",
-                    "peak_source": "int8 tcgen05 peak measured on this pool, M=128 N=256 "
-                                   "(tools/microbench/i8_rates.cu, profiles/i8_peak_r01.txt)",
-                    "shape_ceiling_tops": I8_N64_CEIL_TOPS,
-                    "frac_of_shape_ceiling": ach_i8 / I8_N64_CEIL_TOPS,
-                    "fp64_equivalent_tflops": achieved,
-                    "fp64_equivalent_frac_of_dmma_peak": achieved / FP64_PEAK_TFLOPS,
-                    "aggregate_tflops_over_window": agg,
-                    "avg_launch_ms": chol_ms, "launches": timing["cholesky_count"]}
-    else:
-        roofline = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
-                    "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
-                    "kernel": f"k_chol_tiles (fp64 DMMA tile-DAG Cholesky, {per_launch:g} systems "
-                              f"of N={N} interleaved per launch)",
-                    "algorithmic_per_launch": f"{flops_chol:.4g} flop (tiles factored, 2*64^3 per "
-                                              f"tile update; from scratch a system is N^3/3 = "
-                                              f"{N ** 3 / 3.0:.4g})",
-                    "peak_source": "FP64 DMMA peak measured on this pool "
-                                   "(tools/microbench/fp64_rates.cu, profiles/fp64_peak_r01.txt)",
-                    "aggregate_tflops_over_window": agg,
-                    "aggregate_frac": agg / FP64_PEAK_TFLOPS,
-                    "avg_launch_ms": chol_ms, "launches": timing["cholesky_count"]}
+    roofline = _roofline(timing, args.steps, N, cfg_id)
     # ---- operator-streaming kernels alone (K1, K5, CSR K2), cold L2 ----
     hbm_peak = float(_peaks().get("hbm_gbs", 0.0)) or 7700.0
     streaming = {"peak_gbs": hbm_peak,
@@ -411,57 +697,126 @@ def run_ours(args, world, rank, local, dist):
                            "frac": gbs / hbm_peak}
     # ---- e2e through the public API, host-resident fresh operator ----
     e2e = None
-    if not args.quick and not args.bare and not sharded:
-        op2, b2, _ = (op, b, xt) if args.config == 5 else build_config(args.config)
-        if args.config == 5:
-            op2 = op.with_rhs(b)  # fresh operator object: no cached device state
-        h2d = _operator_bytes(op2) + 2 * xt.nbytes + total * 16
-        walls = []
-        while True:  # short runs are repeated on fresh operators, median reported
-            gc.collect()  # the previous operator's context is released here, untimed
-            t0 = time.perf_counter()
-            tr2 = slim.run("slimls", op2, sampler(), slim.Schedule("constant", alpha),
-                           epochs=total / M, r=r, references={"x_true": xt}, record_every=1,
-                           device=dev)
-            walls.append(time.perf_counter() - t0)
-            if len(walls) == 5 or sum(walls) > 2.0:
-                break
-            op2 = op2.with_rhs(op2.rhs)  # same arrays, no cached device state
-        wall = float(np.median(walls))
-        print("e2e walls (s): " + " ".join(f"{w:.4f}" for w in walls), file=sys.stderr)
-        del op2
-        wall = _max_over_ranks(dist, wall)
-        d2h = (total + 1) * (5 + 1) * 8 + xt.nbytes
-        e2e = {"value": world * total / wall, "unit": "it/s",
-               "h2d_bytes_per_step": int(h2d / total), "d2h_bytes_per_step": int(d2h / total),
-               "what": f"public run() on a fresh host operator: operator upload (streamed "
-                       f"block by block in first-use order, + per-block CSC build for CSR) + "
-                       f"{total} steps + history/x download, wall clock, median of "
-                       f"{len(walls)} fresh operators"}
-        assert tr2.status == "ok"
+    if not args.quick and not args.bare:
+        e2e = _e2e_leg(slim, args, op, b, xt, r, alpha, total, M, sampler, dev, dist, shard,
+                       cfg_id, world)
     # ---- device projector: tomography operators traced in HBM ----
     projector = None
-    if args.config in (2, 3, 4) and not sharded and not args.bare:
+    if cfg_id in (2, 3, 4) and not sharded and not args.bare:
         projector = _projector_leg(args, dev, b, xt, r, alpha, scheme, total, M, sampler)
     if rank != 0:
         return
     cb = None
-    if world == 1 and not args.quick and not args.bare:
-        cb = cpu_sample(args.config, op, b, r, alpha, scheme, SAMPLER_SEED)
+    if world == 1 and not args.quick and not args.bare and cfg_id != 6:
+        # a bounded sample of the reference's CPU path on this host (the
+        # reference arm measures it in full: --impl reference)
+        res = _reference_sample(cfg_id, 2, 0, sweep=False, budget_s=30.0)
+        cb = _cpu_line(res, ell)
     line = {"metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_win / args.steps,
-            "higher_is_better": True, "scaling": "strong" if sharded else "weak",
-            "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": _config_dict(args.config, op, world, sharded, args.factor),
+            "higher_is_better": True,
+            "scaling": "weak" if (cfg_id == 6 or not sharded) else "strong",
+            "vs_baseline": None, "dtype": DTYPE[cfg_id], "dtype_note": DTYPE_NOTE,
+            "data": "synthetic (seeded; BASELINE.json shapes)",
+            "config": _config_dict(cfg_id, op, world, sharded, args.factor),
             "rows_per_s": value * ell, "roofline": roofline, "streaming": streaming,
             "cpu_baseline": cb, "e2e": e2e, "device_projector": projector,
             "gpu_launches": int(timing["launches"]), "clocks": clk.summary(),
             "kernel_ms_per_step": {
                 "gram": timing["gram_ms"] / max(1, timing["gram_count"]),
-                "cholesky": chol_ms,
+                "cholesky_launch": roofline["avg_launch_ms"],
                 "x_chain": timing["x_chain_ms"] / max(1, timing["x_chain_count"])},
             "final_rel_err_x_true": float(traj.rel_errors["x_true"][-1])}
     print(json.dumps(line), flush=True)
+
+
+def _fresh(op):
+    """The same host arrays behind a new operator object (no cached device state)."""
+    if hasattr(op, "with_rhs"):
+        return op.with_rhs(op.rhs)
+    return op
+
+
+def _e2e_leg(slim, args, op, b, xt, r, alpha, total, M, sampler, dev, dist, shard, cfg_id,
+             world):
+    """Public run() on a fresh host-resident operator: the block uploads
+    (streamed in first-use order; per-block CSC built on the device), the
+    steps, the history / x download; wall clock, median of repeats, max over
+    ranks.  Column shards: the host-side column slicing is problem setup and
+    done before the clock starts; the sliced operator's upload, the NCCL
+    communicator set-up and the steps are timed."""
+    import ctypes as C
+
+    generated = hasattr(op, "seed")
+    src_op, refs = op, {"x_true": xt}
+    if shard is not None and not generated:
+        from paper_1912_07962_b200.parallel import shard_operator
+        src_op = shard_operator(op, shard.col0, shard.col1)
+        refs = {"x_true": np.ascontiguousarray(xt[shard.col0:shard.col1])}
+    walls, h2d = [], []
+    for _ in range(5):
+        gc.collect()  # the previous operator's context is released here, untimed
+        op2 = _fresh(src_op)
+        sh2 = None
+        if shard is not None:
+            from paper_1912_07962_b200.parallel import NcclShard
+            sh2 = NcclShard.from_torch(op.n_cols, round_robin=getattr(shard, "round_robin", False))
+            if not generated:
+                sh2 = _PreSliced(sh2)
+        _barrier(dist)
+        t0 = time.perf_counter()
+        tr2 = slim.run("slimls", op2, sampler(), slim.Schedule("constant", alpha),
+                       epochs=total / M, r=r, references=refs, record_every=1, device=dev,
+                       shard=sh2)
+        walls.append(time.perf_counter() - t0)
+        assert tr2.status == "ok"
+        # operator bytes the library copied to HBM (sampled blocks, row pointers, b)
+        caches = op2.__dict__.get("_slim_shard_cache") or op2.__dict__.get("_slim_device_cache", {})
+        nbytes = 0.0
+        for dop in caches.values():
+            v, cnt = C.c_double(0), C.c_int64(0)
+            dop.call("slim_timing", 8, C.byref(v), C.byref(cnt))
+            nbytes += v.value
+        h2d.append(nbytes)
+        del op2, tr2, caches
+        if sum(walls) > 3.0 and len(walls) >= 2:
+            break
+    wall = _max_over_ranks(dist, float(np.median(walls)))
+    print("e2e walls (s): " + " ".join(f"{w:.4f}" for w in walls), file=sys.stderr)
+    n_loc = xt.shape[0] if shard is None else shard.col1 - shard.col0
+    vec_h2d = 8 * n_loc * 2 + 16 * total  # x0, x_true reference, index and alpha traces
+    d2h = (total + 1) * (5 + 1) * 8 + 8 * n_loc  # history rows + x_final
+    h2d_step = (float(np.median(h2d)) + vec_h2d) / total
+    return {"value": (1 if shard is not None else world) * total / wall, "unit": "it/s",
+            "h2d_bytes_per_step": int(h2d_step), "d2h_bytes_per_step": int(d2h / total),
+            "what": f"public run() on a fresh host operator: operator upload (streamed block by "
+                    f"block in first-use order, + per-block CSC build for CSR) + {total} steps "
+                    f"(warm-up included) + history/x download, wall clock, median of "
+                    f"{len(walls)} fresh operators; h2d = bytes the library copied (only the "
+                    f"sampled blocks) + x0/reference/index/alpha vectors"}
+
+
+class _PreSliced:
+    """Shard wrapper for an operator that is already this shard's column slice."""
+
+    def __init__(self, shard):
+        self._shard = shard
+        self.col0, self.col1 = 0, shard.col1 - shard.col0
+        self.rank, self.nranks = shard.rank, shard.nranks
+        self.round_robin = getattr(shard, "round_robin", False)
+
+    def device_operator(self, op, r, device):
+        from paper_1912_07962_b200.linops import device_operator
+        src = op.source if hasattr(op, "source") else op
+        cache = src.__dict__.setdefault("_slim_shard_cache", {})
+        key = (device, r)
+        dop = cache.get(key)
+        if dop is None:
+            dop = device_operator(op, r, device)
+            self._shard._attach(dop)
+            cache[key] = dop
+        dop.call("slim_set_factor_round_robin", 1 if self.round_robin else 0)
+        return dop
 
 
 def _projector_leg(args, dev, b, xt, r, alpha, scheme, total, M, sampler):
@@ -519,37 +874,29 @@ def _projector_leg(args, dev, b, xt, r, alpha, scheme, total, M, sampler):
     return out
 
 
-def _operator_bytes(op) -> int:
-    parts = getattr(op, "_parts", None)
-    if parts is not None:
-        return sum(p[0].nbytes + p[1].nbytes + p[2].nbytes for p in parts) + op.rhs.nbytes
-    a = getattr(op, "matrix", None)
-    if a is not None:
-        return a.nbytes + op.rhs.nbytes
-    return op.rhs.nbytes  # generated: only b crosses the bus
-
-
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=176,
-                    help="timed steps (default 176: with the warm-up batch one epoch of configs[1], the reference K = 180)")
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS),
-                    help="BASELINE config (1-based); 2 = configs[1], the metric's config")
-    ap.add_argument("--shard", default="replicas", choices=["replicas", "columns"],
-                    help="N > 1: independent replicas (default) or one column-sharded solve "
-                         "(NCCL allreduce of Gram panel / residual / norm partials per step)")
-    ap.add_argument("--factor", default="replicated", choices=["replicated", "round_robin"],
-                    help="--shard columns: every rank factors every system (replicated) or "
-                         "batch B is factored on rank B mod N only (SURVEY 8f.1)")
+    ap.add_argument("--config", type=int, default=DEFAULT_CONFIG, choices=sorted(CONFIGS),
+                    help="BASELINE config (1-based): 3 = configs[2], the metric's multi-GPU "
+                         "config (default); 6 = the weak-scaling family")
+    ap.add_argument("--shard", default="columns", choices=["replicas", "columns"],
+                    help="N > 1: one column-sharded solve (default; NCCL allreduce of Gram "
+                         "panel / residual / norm partials per step) or N independent replicas")
+    ap.add_argument("--factor", default="round_robin", choices=["replicated", "round_robin"],
+                    help="--shard columns: batch B is factored on rank B mod N only (default, "
+                         "SURVEY 8f.1) or every rank factors every system")
     ap.add_argument("--bare", action="store_true",
                     help="only the timed steps (no streaming probe, projector leg, e2e or CPU "
                          "legs): for ncu launch lists whose kernel shares are the step's")
     ap.add_argument("--quick", action="store_true",
                     help="skip the CPU baseline and the e2e leg (profiling runs)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_spawn(args.gpus))
     world, rank, local, dist = _dist()
     if args.impl == "reference":
         run_reference(args, world, rank, dist)

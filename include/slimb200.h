@@ -197,7 +197,10 @@ int slim_block_residual(slim_ctx* ctx, int64_t block, const double* x, double* r
  * digit-pair products of 2 * 64^3 per 64x64x64 update; 0 with
  * SLIM_CHOL=dmma); which = 7 the digit layout of those updates: the digit
  * count QD in *ms_out and the trailing-digit width in bits in
- * *launches_out (compile-time SLIM_QD / SLIM_DBITS).                     */
+ * *launches_out (compile-time SLIM_QD / SLIM_DBITS); which = 8 the operator
+ * bytes copied host -> device since the operator was registered (block
+ * values and columns, row pointers, b; host streaming counts only the
+ * blocks a run actually sampled) in *ms_out.                             */
 int slim_timing(slim_ctx* ctx, int32_t which, double* ms_out, int64_t* launches_out);
 int slim_set_profiling(slim_ctx* ctx, int32_t enable);
 /* time only steps k0..K of the next slim_run (which = 3 in slim_timing):

@@ -398,7 +398,10 @@ def gen_fetch(seed: int, n: int, ell: int, b: np.ndarray):
 
 
 def run_slimls_sparse(blocks, b, indices, alphas, *, r=0, x0=None, references=None,
-                      record_every=1):
+                      record_every=1, step_times=None, threads_at=None):
+    """``step_times`` (optional list) receives each step's wall time (the
+    bench's CPU legs); ``threads_at(k)`` (optional) is called before step k
+    to set the BLAS thread count (the reference arm's thread sweep)."""
     import scipy.sparse as sp
 
     mats = [sp.csr_matrix((np.asarray(d, dtype=float), ix, ip), shape=shp)
@@ -424,6 +427,9 @@ def run_slimls_sparse(blocks, b, indices, alphas, *, r=0, x0=None, references=No
 
     rec()
     for k in range(1, steps + 1):
+        if threads_at is not None:
+            threads_at(k)
+        t0 = time.perf_counter()
         idx = int(indices[k - 1])
         alpha = float(alphas[k - 1])
         a = mats[idx - 1]
@@ -451,6 +457,8 @@ def run_slimls_sparse(blocks, b, indices, alphas, *, r=0, x0=None, references=No
             s = alpha * (mat.T @ w)
         x = x - s
         ok = float(x @ x) <= limit * limit
+        if step_times is not None:
+            step_times.append(time.perf_counter() - t0)
         if not ok or k % record_every == 0 or k == steps:
             ks.append(k)
             resid.append(rn)

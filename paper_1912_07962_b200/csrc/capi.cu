@@ -224,6 +224,9 @@ struct slim_ctx {
   std::vector<const char*> hs_val;
   std::vector<char> resident;               // per block: copied to HBM
   cudaStream_t su = nullptr;
+  // host->device operator bytes (block values/columns, row pointers, b) since
+  // the operator was registered: the e2e leg's measured h2d traffic
+  std::atomic<int64_t> h2d_bytes{0};
   // column sharding: exchange of partial sums (nullptr = single context)
   Comm* comm = nullptr;
   double* zero_b = nullptr;  // ell zeros: ranks != 0 do not subtract b
@@ -233,6 +236,7 @@ struct slim_ctx {
   float* gring_hi = nullptr;  // 3xTF32 split of the ring for the tcgen05 Gram
   float* gring_lo = nullptr;
   bool use_tc = false;
+  bool use_i8 = true;  // int8 tensor-core factorization (else fp64 DMMA, chol_i8_for)
   uint64_t gen_seed = 0;
   int64_t gen_n_total = 0, col_offset = 0;
   // state
@@ -573,9 +577,9 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
   const int64_t Nmax = W * ell;
   c->Tmax = (int)((Nmax + TB - 1) / TB);
   const int64_t ntiles = (int64_t)c->Tmax * (c->Tmax + 1) / 2;
-  if (chol_use_i8() && c->Tmax > CHOL_I8_TMAX)  // int32 digit-product sums stay exact
-    FAIL(c, SLIM_EINVAL, "dual system of %lld rows exceeds the tensor-core factorization's limit "
-         "(%d rows)", (long long)Nmax, CHOL_I8_TMAX * TB);
+  // int32 digit-product sums stay exact up to CHOL_I8_TMAX tile rows; larger
+  // dual systems factor with the fp64 DMMA kernel
+  c->use_i8 = chol_i8_for(c->Tmax);
   {
     // the triangular-solve cluster keeps per-row vectors in shared memory
     int optin = 0;
@@ -609,8 +613,8 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
     const size_t ib = sizeof(double) * (size_t)c->Tmax * TB * TB;
     const size_t fb = ((sizeof(int) * (size_t)ntiles + 255) / 256) * 256;
     // int8 digit slices (same bytes as the fp64 tiles) + row exponents
-    const size_t qb = chol_use_i8() ? q_bytes(c->Tmax) : 0;
-    const size_t eb = chol_use_i8() ? ((sizeof(int) * (size_t)c->Tmax * TB + 1023) / 1024) * 1024 : 0;
+    const size_t qb = c->use_i8 ? q_bytes(c->Tmax) : 0;
+    const size_t eb = c->use_i8 ? ((sizeof(int) * (size_t)c->Tmax * TB + 1023) / 1024) * 1024 : 0;
     const size_t per = lb + db + ib + qb + eb;
     ALLOC(c, c->factor_slab, (per + fb) * 2 * c->D);
     char* base = (char*)c->factor_slab;
@@ -703,8 +707,10 @@ int slim_upload_dense(slim_ctx* c, const void* a, const double* b) {
     c->resident.assign(c->M, 0);
   } else {
     CK(c, cudaMemcpy(c->A, a, bytes, cudaMemcpyHostToDevice));
+    c->h2d_bytes += (int64_t)bytes;
   }
   CK(c, cudaMemcpy(c->b, b, sizeof(double) * c->m, cudaMemcpyHostToDevice));
+  c->h2d_bytes += (int64_t)(sizeof(double) * c->m);
   c->op_ready = true;
   return SLIM_OK;
 }
@@ -740,6 +746,8 @@ int slim_upload_csr(slim_ctx* c, const int64_t* rowptr, const int32_t* col, cons
     CK(c, cudaMemcpy(c->val, val, c->vsize * nnz, cudaMemcpyHostToDevice));
   }
   CK(c, cudaMemcpy(c->b, b, sizeof(double) * c->m, cudaMemcpyHostToDevice));
+  c->h2d_bytes += (int64_t)(sizeof(int64_t) * (c->m + 1) + (sizeof(int) + c->vsize) * nnz +
+                            sizeof(double) * c->m);
   c->op_ready = false;
   return SLIM_OK;
 }
@@ -880,6 +888,7 @@ static int size_streamed_csr(slim_ctx* c) {
   CK(c, cudaMemcpy(c->rowptr, rp.data(), sizeof(int64_t) * (c->m + 1), cudaMemcpyHostToDevice));
   CK(c, cudaMemcpy(c->blkbase, c->h_blkbase.data(), sizeof(int64_t) * (M + 1), cudaMemcpyHostToDevice));
   CK(c, cudaMemcpy(c->b, c->h_b.data(), sizeof(double) * c->m, cudaMemcpyHostToDevice));
+  c->h2d_bytes += (int64_t)(sizeof(int64_t) * (c->m + 1 + M + 1) + sizeof(double) * c->m);
   c->h_have.clear();
   c->h_b.clear();
   c->resident.assign(M, 0);
@@ -914,7 +923,15 @@ struct PinRing {
     return ok = true;
   }
 };
-static PinRing g_pin;
+// one ring per device: its events can only be recorded on that device's streams
+static std::mutex g_pin_mu;
+static std::map<int, PinRing*> g_pin;
+static PinRing& pin_ring(int dev) {
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  PinRing*& r = g_pin[dev];
+  if (!r) r = new PinRing();  // process lifetime (like a caching host allocator)
+  return *r;
+}
 
 // host memcpy into the pinned ring, split over 4 threads for large chunks
 // (one thread copies ~10 GB/s from pageable memory; the first batch's blocks
@@ -946,6 +963,10 @@ static void par_memcpy(char* dst, const char* src, size_t n) {
 
 // host -> device copy of `bytes` through the pinned ring (pageable fallback)
 static cudaError_t staged_copy(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  int dev = 0;
+  cudaError_t ed = cudaGetDevice(&dev);
+  if (ed != cudaSuccess) return ed;
+  PinRing& g_pin = pin_ring(dev);  // the caller's current device owns stream s
   std::lock_guard<std::mutex> lk(g_pin.m);
   if (!g_pin.init()) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
   const char* sp = static_cast<const char*>(src);
@@ -979,6 +1000,7 @@ static int copy_block(slim_ctx* c, int64_t bk, std::string& err, int64_t* launch
       err = "block upload failed";
       return SLIM_ECUDA;
     }
+    c->h2d_bytes += (int64_t)rb;
     return SLIM_OK;
   }
   const int64_t* r = c->hs_rowptr[bk];
@@ -1003,6 +1025,7 @@ static int copy_block(slim_ctx* c, int64_t bk, std::string& err, int64_t* launch
       err = "block upload failed";
       return SLIM_ECUDA;
     }
+    c->h2d_bytes += (int64_t)((sizeof(int) + c->vsize) * nb);
   }
   if (!build_csc) return SLIM_OK;  // the caller builds a whole batch's CSC at once
   if (c->vdt == SLIM_F64)
@@ -1087,6 +1110,7 @@ int slim_set_rhs(slim_ctx* c, const double* b) {
   if (!c || !b) FAIL(c, SLIM_EINVAL, "null argument");
   CK(c, cudaSetDevice(c->dev));
   CK(c, cudaMemcpy(c->b, b, sizeof(double) * c->m, cudaMemcpyHostToDevice));
+  c->h2d_bytes += (int64_t)(sizeof(double) * c->m);
   c->rhs_set = true;
   return SLIM_OK;
 }
@@ -1203,11 +1227,9 @@ int slim_nccl_unique_id(void* out128) {
 int slim_comm_init(slim_ctx* c, const void* uid, int32_t nranks, int32_t rank) {
   if (!c || !uid) FAIL(c, SLIM_EINVAL, "null argument");
   if (nranks < 1 || rank < 0 || rank >= nranks) FAIL(c, SLIM_EINVAL, "bad rank %d of %d", rank, nranks);
-  if (nranks == 1) {
-    delete c->comm;
-    c->comm = nullptr;
-    return SLIM_OK;
-  }
+  // a one-rank communicator is real too: every exchange goes through NCCL
+  // (in-place single-rank allreduces), which is how the tests exercise the
+  // NCCL path on one GPU
   std::string err;
   NcclApi* api = nccl_api(err);
   if (!api) FAIL(c, SLIM_ENCCL, "%s", err.c_str());
@@ -1271,14 +1293,19 @@ int slim_set_timing_start(slim_ctx* c, int64_t k0) {
 }
 
 int slim_timing(slim_ctx* c, int32_t which, double* ms, int64_t* launches) {
-  if (!c || which < 0 || which > 7) FAIL(c, SLIM_EINVAL, "bad argument");
+  if (!c || which < 0 || which > 8) FAIL(c, SLIM_EINVAL, "bad argument");
+  if (which == 8) {  // operator bytes copied host -> device so far (e2e accounting)
+    if (ms) *ms = (double)c->h2d_bytes.load();
+    if (launches) *launches = 0;
+    return SLIM_OK;
+  }
   if (which == 7) {  // digit layout of the int8 factorization (compile time)
     if (ms) *ms = (double)QD;
     if (launches) *launches = DBITS;
     return SLIM_OK;
   }
   if (which == 6) {  // int8 tensor ops of the profiled factorization launches
-    if (ms) *ms = chol_use_i8() ? c->chol_i8ops : 0.0;
+    if (ms) *ms = c->use_i8 ? c->chol_i8ops : 0.0;
     if (launches) *launches = c->t_n[1];
     return SLIM_OK;
   }
@@ -1610,6 +1637,7 @@ static int enqueue_chol_batch(slim_ctx* c, const Window* Ws, int nb, int set, co
   P.ell = (int)c->ell;
   P.S = c->S;
   P.W = (int)(c->r + 1);
+  P.i8 = c->use_i8 ? 1 : 0;
   P.prevL = prev >= 0 ? c->Lbuf[prev] : nullptr;
   P.prevDinv = prev >= 0 ? c->Dinv[prev] : nullptr;
   P.prevQ = prev >= 0 ? c->Qbuf[prev] : nullptr;
@@ -2101,9 +2129,7 @@ static int potrf_impl(int32_t device, const double* G, int64_t N, double* L_out,
   if (!G || !L_out || N < 1) FAIL((slim_ctx*)nullptr, SLIM_EINVAL, "bad argument");
   if (cudaSetDevice(device) != cudaSuccess) FAIL((slim_ctx*)nullptr, SLIM_ECUDA, "cudaSetDevice");
   const int T = (int)((N + TB - 1) / TB);
-  if (chol_use_i8() && T > CHOL_I8_TMAX)
-    FAIL((slim_ctx*)nullptr, SLIM_EINVAL, "N = %lld exceeds the tensor-core factorization's limit (%d)",
-         (long long)N, CHOL_I8_TMAX * TB);
+  const bool i8 = chol_i8_for(T);  // fp64 DMMA above CHOL_I8_TMAX tile rows
   const int64_t ntiles = (int64_t)T * (T + 1) / 2;
   double *dG = nullptr, *dL = nullptr, *dD = nullptr;
   int *flags = nullptr, *ticket = nullptr, *err = nullptr, *rx = nullptr;
@@ -2123,8 +2149,8 @@ static int potrf_impl(int32_t device, const double* G, int64_t N, double* L_out,
       cudaMalloc(&dD, sizeof(double) * T * 512) != cudaSuccess ||
       cudaMalloc(&flags, sizeof(int) * ntiles) != cudaSuccess ||
       cudaMalloc(&ticket, sizeof(int)) != cudaSuccess || cudaMalloc(&err, sizeof(int)) != cudaSuccess ||
-      cudaMalloc(&dQ, q_bytes(T)) != cudaSuccess ||
-      cudaMalloc(&rx, sizeof(int) * T * TB) != cudaSuccess) {
+      (i8 && cudaMalloc(&dQ, q_bytes(T)) != cudaSuccess) ||
+      (i8 && cudaMalloc(&rx, sizeof(int) * T * TB) != cudaSuccess)) {
     cleanup();
     FAIL((slim_ctx*)nullptr, SLIM_ENOMEM, "device allocation failed");
   }
@@ -2138,12 +2164,13 @@ static int potrf_impl(int32_t device, const double* G, int64_t N, double* L_out,
     FAIL((slim_ctx*)nullptr, SLIM_ECUDA, "TMA descriptor could not be encoded");
   }
   P.m[0].qT = T;
-  if (chol_use_i8() && (!tma_map_q(&P.m[0].qmapA, dQ, T, 128) || !tma_map_q(&P.m[0].qmapB, dQ, T, 64))) {
+  if (i8 && (!tma_map_q(&P.m[0].qmapA, dQ, T, 128) || !tma_map_q(&P.m[0].qmapB, dQ, T, 64))) {
     cleanup();
     FAIL((slim_ctx*)nullptr, SLIM_ECUDA, "TMA descriptor could not be encoded");
   }
-  P.m[0].Q = chol_use_i8() ? dQ : nullptr;
-  P.m[0].rexp = chol_use_i8() ? rx : nullptr;
+  P.i8 = i8 ? 1 : 0;
+  P.m[0].Q = i8 ? dQ : nullptr;
+  P.m[0].rexp = i8 ? rx : nullptr;
   P.m[0].L = dL;
   P.m[0].Dinv = dD;
   P.m[0].flags = flags;

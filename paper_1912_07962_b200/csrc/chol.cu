@@ -850,9 +850,10 @@ __device__ __forceinline__ uint64_t sw32_desc(uint32_t saddr) {
 // One MMA per (A digit a, run of up to four B digits b0 .. b0 + n - 1): the
 // B digits are stacked along N (64 rows each), and D starts at accumulator
 // t = a + b0 - 2, so the product with B digit b lands in TMEM column block
-// a + b - 2 -- its own accumulator.  12 MMAs (N up to 256) per stage instead
-// of 36 with N = 64 (which cap at 2/3 of the tensor peak); the two MMAs of
-// one A digit share it through the A-operand collector.
+// a + b - 2 -- its own accumulator.  With the default seven digits that is
+// 10 MMAs (N up to 256) per stage instead of 28 with N = 64 (which cap at 2/3
+// of the tensor peak); the MMAs of one A digit share it through the A-operand
+// collector.
 template <int COLL>  // 0 plain, 1 fill, 3 lastuse
 __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idsc,
                                        uint32_t acc) {
@@ -893,7 +894,8 @@ __device__ __forceinline__ double pow2(int e) {  // exact 2^e, |e| < 1000
 
 // digit slices of the 64x64 fp64 tile X (smem, stride TS) with row
 // exponents rex[0..63]: thread = (row, 16 consecutive k); v = L 2^(7 - e)
-// lies in (-127.5, 127.5), and d_a = rint(v), v <- (v - d_a) 128 is exact
+// lies in (-127.5, 127.5); the integer I = rint(v 2^(DBITS (QD - 1))) is cut
+// into a 7-bit leading digit and QD - 1 balanced DBITS-bit digits
 struct Digits {
   uint4 w[QD];  // digit a of the thread's 16 entries, one byte each
 };
@@ -1055,7 +1057,7 @@ __global__ void __launch_bounds__(256, 1) k_chol_i8(const __grid_constant__ Chol
       }
       uint8_t* dst = stage + st * oz::STAGE;
       bar_expect(&s_full[st], oz::STAGE);
-      // A: tile rows ra, ra + 1, all 8 digits (a single task's spare row is
+      // A: tile rows ra, ra + 1, all QD digits (a single task's spare row is
       // loaded and ignored); B: tile row j
 #if SLIM_OZ_HINT
       // A (this task's row pair) is streamed once; B (row j) is shared by
@@ -1107,7 +1109,7 @@ __global__ void __launch_bounds__(256, 1) k_chol_i8(const __grid_constant__ Chol
   }
   __syncwarp();
 
-  // ---------------- combine: X = G - 2^(e_r + e_c - 14) sum_t 2^(-7t) P_t ----------------
+  // ------- combine: X = G - 2^(e_r + e_c - 14) sum_t 2^(-DBITS t) P_t -------
   {
     if (nchunk > 0) {
       // idle warps poll with back-off: a tight try_wait loop of 250 threads
@@ -1194,6 +1196,8 @@ bool chol_use_i8() {
   return v == 1;
 }
 
+bool chol_i8_for(int T) { return chol_use_i8() && T <= CHOL_I8_TMAX; }
+
 size_t chol_smem_bytes() { return chol_use_i8() ? (size_t)oz::SMEM : (size_t)SMB_TOTAL; }
 
 // Ticket order.  A system's tasks are its fresh tiles (tile_fresh), grouped
@@ -1254,7 +1258,7 @@ void launch_chol(const CholParams& P, cudaStream_t s) {
     cudaFuncSetAttribute(k_chol_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)oz::SMEM);
     configured = true;
   }
-  if (chol_use_i8())
+  if (P.i8)
     k_chol_i8<<<P.ntasks, 256, oz::SMEM, s>>>(P);
   else
     k_chol_tiles<<<P.ntasks, 256, SMB_TOTAL, s>>>(P);

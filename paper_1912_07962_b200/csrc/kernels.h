@@ -59,6 +59,7 @@ struct CholParams {
   int64_t panel_stride;  // (r + 1) * ell * ell: one product block per window position
   int ell, S;
   int W;                 // window positions (r + 1)
+  int i8;                // 1: k_chol_i8 (int8 tensor-core updates), 0: k_chol_tiles (fp64 DMMA)
   // tiles a system shares with the previous batch's last system (step
   // k0 - 1) are copied from its factor buffer by k_assemble
   const double* prevL;
@@ -138,6 +139,9 @@ size_t chol_smem_bytes();
 // factorization kernel: true = int8 tensor-core updates (default), false =
 // fp64 DMMA updates (SLIM_CHOL=dmma, kept for A/B measurements)
 bool chol_use_i8();
+// kernel for a system of T tile rows: int8 unless disabled or T exceeds
+// CHOL_I8_TMAX (the exact int32 digit-product bound), then fp64 DMMA
+bool chol_i8_for(int T);
 // signed digits per factor entry in the int8 tensor-core updates
 // (k_chol_i8): a leading digit in [-127, 127] (7 bits) and QD - 1 balanced
 // digits of DBITS bits each, so 7 + DBITS (QD - 1) bits below each row's scale

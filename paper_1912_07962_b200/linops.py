@@ -446,6 +446,16 @@ def device_operator(op, r: int, device: int = 0) -> DeviceOperator:
         dop.call("slim_finalize_operator")
         cache[key] = dop
         return dop
+    if hasattr(src, "sparse_block") and not isinstance(src, SparseBlockOperator):
+        # a reference SparseBlockOperator (linops.py:209-299): take its CSR
+        # blocks as they are -- never its ``matrix`` property, which densifies
+        # the whole operator -- and upload them like our own sparse operator
+        mine = SparseBlockOperator([src.sparse_block(i) for i in range(1, src.n_blocks + 1)],
+                                   src.rhs)
+        dop = device_operator(mine, r, device)
+        dop.host_op = mine  # keeps the registered host arrays alive
+        cache[key] = dop
+        return dop
     # host streaming (default): the operator is registered by pointer and each
     # block is copied to HBM inside slim_run right before the batch that first
     # samples it, overlapped with the device work of earlier batches; the
@@ -485,10 +495,6 @@ def device_operator(op, r: int, device: int = 0) -> DeviceOperator:
         if isinstance(src, SparseBlockOperator):
             rowptr, col, val = src.global_csr()
             dtype = src.dtype
-        elif hasattr(src, "sparse_block"):  # reference SparseBlockOperator
-            tmp = SparseBlockOperator([src.sparse_block(i) for i in range(1, src.n_blocks + 1)])
-            rowptr, col, val = tmp.global_csr()
-            dtype = tmp.dtype
         else:  # generic random-access operator: densify once on the host
             blocks = [np.asarray(src.fetch_block(i).a_block, dtype=float)
                       for i in range(1, src.n_blocks + 1)]

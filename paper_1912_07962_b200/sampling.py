@@ -40,8 +40,6 @@ class Sampler:
         self.rng = np.random.Generator(np.random.Philox(key=self.seed))
         self.position = 0
         self._order = None  # the current epoch's permutation (random_cyclic)
-        self._draw = {"cyclic": self._draw_cyclic, "uniform_iid": self._draw_iid,
-                      "random_cyclic": self._draw_permuted}[scheme]
 
     def _draw_cyclic(self) -> int:
         return self.position % self.n_blocks + 1
@@ -54,6 +52,13 @@ class Sampler:
         if slot == 0:  # a new epoch: a fresh permutation
             self._order = _shuffled(self.n_blocks, self.rng)
         return int(self._order[slot])
+
+    def _draw(self) -> int:
+        if self.scheme == "cyclic":
+            return self._draw_cyclic()
+        if self.scheme == "uniform_iid":
+            return self._draw_iid()
+        return self._draw_permuted()
 
     def next_index(self) -> int:
         idx = self._draw()

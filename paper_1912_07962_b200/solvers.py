@@ -16,6 +16,7 @@ Everything else raises ``ValueError`` -- there is no CPU fallback.
 
 from __future__ import annotations
 
+import copy
 import ctypes as C
 from dataclasses import dataclass
 
@@ -128,6 +129,23 @@ def _validate(method, op, sampler, epochs, r, reg, lam, inner, record_every, sch
     return steps, schedule
 
 
+def _check_dual_alphas(method, inner, alphas):
+    """The reference's auto dispatch sends alpha_k > 1e8 to the n x n
+    ``direct_step`` (innersolve.py:356, 377-380; solvers.py:230-237): the dual
+    system I + alpha M M^T is then too ill-conditioned to trust.  The device
+    path solves only the dual form, so ``inner="auto"`` refuses such a
+    schedule instead of silently changing the route; ``inner="dual"`` (the
+    reference's explicit dual route) is honoured."""
+    if method == "sg" or inner != "auto" or alphas.size == 0:
+        return
+    k = int(np.argmax(alphas))
+    if alphas[k] > DUAL_MAX_ALPHA:
+        raise ValueError(
+            f"alpha_{k + 1} = {alphas[k]:g} > {DUAL_MAX_ALPHA:g}: the reference's auto dispatch "
+            "takes the direct (n x n normal-equation) route there, which is not on the B200 "
+            "path; pass inner='dual' to solve the dual system anyway")
+
+
 def run(method: str, op: RowBlockOperator, sampler, schedule: Schedule, *, epochs: float,
         r: int = 0, reg=None, lam: float = 0.0, olbfgs_memory: int = 10,
         x0: np.ndarray | None = None, references: dict | None = None, record_every: int = 1,
@@ -154,12 +172,17 @@ def run(method: str, op: RowBlockOperator, sampler, schedule: Schedule, *, epoch
     x0 = np.zeros(op.n_cols) if x0 is None else np.asarray(x0, dtype=float).reshape(-1)
     if x0.shape != (op.n_cols,):
         raise ValueError(f"x0 has shape {x0.shape}, expected ({op.n_cols},)")
-    idx = sampler.indices(steps) if steps else np.zeros(0, dtype=np.int64)
-    idx = np.ascontiguousarray(idx, dtype=np.int64)
     alphas = np.array([schedule.alpha_at(k) for k in range(1, steps + 1)], dtype=float)
     for k in range(steps):
         if not alphas[k] > 0:
             raise ValueError(f"schedule produced alpha_{k + 1} = {alphas[k]} <= 0")
+    _check_dual_alphas(method, inner, alphas)
+    # the whole trace is drawn up front; the sampler's state before the draws
+    # is kept so a diverged run leaves it where the reference's would be
+    # (solvers.py:560-570 draws one index per executed step)
+    sampler_before = copy.deepcopy(sampler) if steps else None
+    idx = sampler.indices(steps) if steps else np.zeros(0, dtype=np.int64)
+    idx = np.ascontiguousarray(idx, dtype=np.int64)
 
     references = references or {}
     ref_items = [(name, np.ascontiguousarray(np.asarray(v, dtype=float).reshape(-1)),
@@ -230,10 +253,21 @@ def run(method: str, op: RowBlockOperator, sampler, schedule: Schedule, *, epoch
                 timing["streaming"][name] = (us.value, nbytes.value)
     x_final = np.empty(x0.shape[0])
     dop.call("slim_get_x", _lib.dptr(x_final))
+    if status.value and sampler_before is not None:
+        _rewind_sampler(sampler, sampler_before, int(div_at.value))
     if stream_state is not None:
         op._next = stream_state + (int(div_at.value) if status.value else steps)
     return _trajectory(hist[: n_rows.value], iters, x0_full, ref_items, big_m, status.value,
                        div_at.value, x_final, store_iterates)
+
+
+def _rewind_sampler(sampler, before, consumed: int):
+    """Put ``sampler`` in the state of ``before`` advanced by ``consumed`` draws."""
+    state = copy.deepcopy(before.__dict__)
+    sampler.__dict__.clear()
+    sampler.__dict__.update(state)
+    if consumed:
+        sampler.indices(consumed)
 
 
 def _trajectory(rows, iters, x0, ref_items, big_m, status, div_at, x_final, store_iterates):

@@ -16,6 +16,20 @@ DENSE_CASES = ("scalar", "direct_route", "dense_dual", "cfg1_reduced", "ramp", "
 SG_CASES = ("sg_dense", "sg_ramp_r3", "sg_decay", "sg_diverge")
 
 
+def operator_digest(op) -> str:
+    """sha256 over a CSR operator's per-block arrays (relative rowptr, int32
+    columns, values): the full-run goldens record the exact operator bits."""
+    import hashlib
+
+    h = hashlib.sha256()
+    for i in range(1, op.n_blocks + 1):
+        ip, ix, d, _ = op.csr_block(i)
+        h.update(np.ascontiguousarray(ip - ip[0], dtype=np.int64).tobytes())
+        h.update(np.ascontiguousarray(ix[ip[0]:ip[-1]], dtype=np.int32).tobytes())
+        h.update(np.ascontiguousarray(d[ip[0]:ip[-1]]).tobytes())
+    return h.hexdigest()
+
+
 def load(name):
     return np.load(os.path.join(GOLDEN, name), allow_pickle=False)
 

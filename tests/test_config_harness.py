@@ -89,3 +89,22 @@ def test_slim_container_roundtrip(tmp_path):
         assert st.fetch_block(1).a_block.shape == (3, 5)
         with pytest.raises(StreamOrderError):
             st.fetch_block(3)
+
+
+def test_auto_dispatch_refuses_direct_route_alphas():
+    """alpha_k > 1e8 sends the reference's auto dispatch to the n x n direct
+    route (innersolve.py:356, 377-380); the device path raises ValueError
+    before touching the GPU instead of silently solving the dual form."""
+    import numpy as np
+    import pytest
+
+    import paper_1912_07962_b200 as slim
+
+    rng = np.random.default_rng(0)
+    op = slim.DenseBlockOperator(rng.standard_normal((40, 10)), 4, rng.standard_normal(40))
+    with pytest.raises(ValueError, match="direct"):
+        slim.run("slimls", op, slim.Sampler("cyclic", op.n_blocks, 0),
+                 slim.Schedule("constant", 2e8), epochs=1, r=2)
+    with pytest.raises(ValueError, match="direct"):  # a decaying schedule starting above 1e8
+        slim.run("slimls", op, slim.Sampler("cyclic", op.n_blocks, 0),
+                 slim.Schedule("decay", 4e8, decay_exponent=1.0), epochs=1, r=2)
