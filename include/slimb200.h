@@ -143,6 +143,17 @@ int slim_run(slim_ctx* ctx, const int64_t* block_idx, const double* alphas, int6
  * generated layout or sharded contexts.                                  */
 int slim_set_host_streaming(slim_ctx* ctx, int32_t enable);
 
+/* Single-pass .slim stream file as the operator (replaces the reference's
+ * FileStreamOperator.fetch_block, linops.py:374-415).  Layout: "SLIM1",
+ * then m, n, M, ell as little-endian uint64, then M records of ell*n fp64
+ * block rows followed by the block's ell fp64 rhs entries.  The header must
+ * match the (dense, fp64) context; the file stays open and slim_run reads
+ * each record once, when its block is first sampled, through the pinned
+ * ring straight into HBM -- no host copy of the matrix.  SLIM_EINVAL
+ * (ValueError) for a bad magic, an inconsistent header or a truncated
+ * record, with the reference's messages.  Implies host streaming.        */
+int slim_attach_stream_file(slim_ctx* ctx, const char* path);
+
 /* ---- column sharding -------------------------------------
  * Each rank's context holds the columns [col_offset, col_offset + n_cols)
  * of A (and the matching slice of x and of every reference).  Per step the

@@ -28,7 +28,7 @@ EXPORTS = (
     "slim_create", "slim_destroy", "slim_last_error", "slim_abi_version",
     "slim_upload_dense", "slim_upload_csr_block", "slim_upload_csr_blocks", "slim_upload_csr", "slim_finalize_operator",
     "slim_set_rhs", "slim_gen_apply", "slim_set_x", "slim_get_x", "slim_set_references",
-    "slim_set_divergence_limit", "slim_run", "slim_set_host_streaming", "slim_nccl_unique_id", "slim_comm_init",
+    "slim_set_divergence_limit", "slim_run", "slim_set_host_streaming", "slim_attach_stream_file", "slim_nccl_unique_id", "slim_comm_init",
     "slim_local_group_create", "slim_local_group_destroy", "slim_comm_init_local", "slim_set_factor_round_robin", "slim_set_method",
     "slim_dual_step", "slim_potrf", "slim_potrf_traced", "slim_block_residual", "slim_timing", "slim_set_profiling", "slim_set_timing_start", "slim_probe_stream",
     "slim_siddon2d_view", "slim_siddon3d_view",
@@ -71,6 +71,7 @@ _SIGS = {
     "slim_set_divergence_limit": (C.c_int, [_P, _D]),
     "slim_run": (C.c_int, [_P, _I64P, _DP, _I64, _I64, _DP, _I64P, _I32P, _I64P, _DP]),
     "slim_set_host_streaming": (C.c_int, [_P, _I32]),
+    "slim_attach_stream_file": (C.c_int, [_P, C.c_char_p]),
     "slim_comm_init": (C.c_int, [_P, _P, _I32, _I32]),
     "slim_nccl_unique_id": (C.c_int, [_P]),
     "slim_local_group_create": (C.c_void_p, [_I32]),

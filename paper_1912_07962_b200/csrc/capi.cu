@@ -16,7 +16,10 @@
 // overwritten while a factorization that reads it may still be running.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <fcntl.h>
 #include <nccl.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
@@ -219,6 +222,10 @@ struct slim_ctx {
   // samples it, overlapped with the factorizations of earlier batches
   bool streaming = false;
   const char* hs_dense = nullptr;           // dense rows
+  // .slim stream file (slim_attach_stream_file): records are read straight
+  // from the file into the pinned ring and DMAed to HBM, block by block
+  int sfd = -1;
+  int64_t s_head = 0, s_rec = 0;            // header bytes, bytes per record
   std::vector<const int64_t*> hs_rowptr;    // CSR: per block (ell + 1 entries, any base)
   std::vector<const int32_t*> hs_col;
   std::vector<const char*> hs_val;
@@ -688,6 +695,7 @@ void slim_destroy(slim_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->dev);
   cudaDeviceSynchronize();
+  if (c->sfd >= 0) close(c->sfd);
   free_all(c);
   delete c;
 }
@@ -711,6 +719,60 @@ int slim_upload_dense(slim_ctx* c, const void* a, const double* b) {
   }
   CK(c, cudaMemcpy(c->b, b, sizeof(double) * c->m, cudaMemcpyHostToDevice));
   c->h2d_bytes += (int64_t)(sizeof(double) * c->m);
+  c->op_ready = true;
+  return SLIM_OK;
+}
+
+// .slim container (reference linops.py:334-429): "SLIM1", then m, n, M, ell
+// as little-endian uint64, then M records of ell*n fp64 block entries and
+// ell fp64 rhs entries.  The context keeps the file open and slim_run reads
+// each record once, when its block is first sampled, straight into HBM.
+int slim_attach_stream_file(slim_ctx* c, const char* path) {
+  if (!c || !path) FAIL(c, SLIM_EINVAL, "null argument");
+  if (c->layout != SLIM_DENSE_ROWMAJOR || c->vdt != SLIM_F64)
+    FAIL(c, SLIM_EINVAL, "stream files hold fp64 dense rows: create a dense fp64 context");
+  if (c->comm) FAIL(c, SLIM_EINVAL, "stream files are single-context only");
+  const int fd = open(path, O_RDONLY | O_CLOEXEC);
+  if (fd < 0) FAIL(c, SLIM_EINVAL, "%s: cannot open", path);
+  unsigned char h[37];
+  if (pread(fd, h, sizeof h, 0) != (ssize_t)sizeof h) {
+    close(fd);
+    FAIL(c, SLIM_EINVAL, "%s: truncated header", path);
+  }
+  if (memcmp(h, "SLIM1", 5) != 0) {
+    close(fd);
+    FAIL(c, SLIM_EINVAL, "%s: bad magic, expected b'SLIM1'", path);
+  }
+  uint64_t v[4];
+  for (int q = 0; q < 4; ++q) {
+    v[q] = 0;
+    for (int t = 7; t >= 0; --t) v[q] = (v[q] << 8) | h[5 + 8 * q + t];
+  }
+  if (v[2] * v[3] != v[0]) {
+    close(fd);
+    FAIL(c, SLIM_EINVAL, "%s: header inconsistent, M*ell != m", path);
+  }
+  if ((int64_t)v[0] != c->m || (int64_t)v[1] != c->n || (int64_t)v[3] != c->ell) {
+    close(fd);
+    FAIL(c, SLIM_EINVAL, "%s: header (m=%llu, n=%llu, ell=%llu) does not match the context", path,
+         (unsigned long long)v[0], (unsigned long long)v[1], (unsigned long long)v[3]);
+  }
+  const int64_t rec = (c->ell * c->n + c->ell) * (int64_t)sizeof(double);
+  struct stat st;
+  if (fstat(fd, &st) != 0 || (int64_t)st.st_size < 37 + c->M * rec) {
+    const int64_t have = fstat(fd, &st) == 0 ? ((int64_t)st.st_size - 37) / rec : 0;
+    close(fd);
+    FAIL(c, SLIM_EINVAL, "%s: truncated record %lld", path, (long long)have + 1);
+  }
+  CK(c, cudaSetDevice(c->dev));
+  if (!c->A) ALLOC(c, c->A, (size_t)c->m * c->n * sizeof(double));
+  if (c->sfd >= 0) close(c->sfd);
+  c->sfd = fd;
+  c->s_head = 37;
+  c->s_rec = rec;
+  c->streaming = true;
+  c->hs_dense = nullptr;
+  c->resident.assign(c->M, 0);
   c->op_ready = true;
   return SLIM_OK;
 }
@@ -990,10 +1052,67 @@ static cudaError_t staged_copy(void* dst, const void* src, size_t bytes, cudaStr
   return cudaSuccess;
 }
 
+// file -> device copy of `bytes` at file offset `off` through the pinned ring:
+// pread fills a slot (no host buffer beyond the ring), the DMA drains it
+static cudaError_t staged_file_copy(void* dst, int fd, int64_t off, size_t bytes, cudaStream_t s,
+                                    std::string& err) {
+  int dev = 0;
+  cudaError_t ed = cudaGetDevice(&dev);
+  if (ed != cudaSuccess) return ed;
+  PinRing& ring = pin_ring(dev);
+  std::lock_guard<std::mutex> lk(ring.m);
+  if (!ring.init()) {
+    err = "pinned staging ring unavailable";
+    return cudaErrorMemoryAllocation;
+  }
+  char* dp = static_cast<char*>(dst);
+  while (bytes > 0) {
+    const size_t n = std::min(bytes, PinRing::SLOT);
+    const int q = ring.next;
+    ring.next = (q + 1) % PinRing::NSLOT;
+    if (ring.used[q]) {
+      cudaError_t e = cudaEventSynchronize(ring.ev[q]);
+      if (e != cudaSuccess) return e;
+    }
+    char* slot = ring.buf + (size_t)q * PinRing::SLOT;
+    size_t got = 0;
+    while (got < n) {
+      const ssize_t rd = pread(fd, slot + got, n - got, (off_t)(off + got));
+      if (rd <= 0) {
+        err = "read error or truncated record in the stream file";
+        return cudaErrorInvalidValue;
+      }
+      got += (size_t)rd;
+    }
+    cudaError_t e = cudaMemcpyAsync(dp, slot, n, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaEventRecord(ring.ev[q], s)) != cudaSuccess) return e;
+    ring.used[q] = true;
+    off += (int64_t)n, dp += n, bytes -= n;
+  }
+  return cudaSuccess;
+}
+
 // copy one row block (0-based) to HBM on su (+ its CSC build); thread-safe
 // with respect to the context's error string (the message goes to err)
 static int copy_block(slim_ctx* c, int64_t bk, std::string& err, int64_t* launches, bool build_csc = true) {
   char msg[160];
+  if (c->layout == SLIM_DENSE_ROWMAJOR && c->sfd >= 0) {
+    // .slim record bk: ell x n fp64 rows, then the block's ell rhs entries
+    const size_t rb = (size_t)c->ell * c->n * sizeof(double);
+    const int64_t off = c->s_head + bk * c->s_rec;
+    std::string e2;
+    if (staged_file_copy((char*)c->A + bk * rb, c->sfd, off, rb, c->su, e2) != cudaSuccess ||
+        staged_file_copy(c->b + bk * c->ell, c->sfd, off + (int64_t)rb, sizeof(double) * c->ell,
+                         c->su, e2) != cudaSuccess) {
+      snprintf(msg, sizeof msg, "stream file: block %lld: %s", (long long)bk + 1,
+               e2.empty() ? "upload failed" : e2.c_str());
+      err = msg;
+      return e2.empty() ? SLIM_ECUDA : SLIM_EINVAL;
+    }
+    c->h2d_bytes += (int64_t)(rb + sizeof(double) * c->ell);
+    return SLIM_OK;
+  }
   if (c->layout == SLIM_DENSE_ROWMAJOR) {
     const size_t rb = (size_t)c->ell * c->n * c->vsize;
     if (staged_copy((char*)c->A + bk * rb, c->hs_dense + bk * rb, rb, c->su) != cudaSuccess) {

@@ -1212,7 +1212,89 @@ size_t chol_smem_bytes() { return chol_use_i8() ? (size_t)oz::SMEM : (size_t)SMB
 // with an earlier system of the batch is produced by that system's task in
 // the same or an earlier group, so every dependency holds a smaller ticket
 // and spinning on it cannot deadlock.
-std::vector<int2> chol_task_map(const SysShape* sh, int nb, int W, int ell) {
+// Banded order (cols = C >= 2): the columns are taken C at a time.  Each
+// group first emits, column by column and system-minor, the tasks whose
+// rows reach no further than J + C + 1 (the diagonal chain: stand-alone,
+// first off-diagonal and pair tasks, as above); then the rest of the C
+// columns in bands of `band` tile rows, each band system by system, rows
+// ascending and, for one row pair, the C columns back to back.  Dual tasks
+// pair rows (i, i + 1) with i EVEN in every column, so the tasks of one row
+// pair in consecutive columns stream the same A panel (tile rows i, i + 1,
+// k = 0 ..) at the same time: the second read hits L2 instead of DRAM.  A
+// task whose first row is in the group's diagonal block goes to the head;
+// the others are keyed by their aligned row pair (last row | 1), so every
+// dependency (rows of the same or an earlier row pair in earlier columns,
+// the diagonal chain) holds a smaller ticket and spinning on it cannot
+// deadlock (checked for the configuration shapes by tools/taskmap_check.cu).
+static std::vector<int2> chol_task_map_banded(const SysShape* sh, int nb, int W, int ell, int C,
+                                              int band) {
+  int Tmax = 0;
+  for (int b = 0; b < nb; ++b) Tmax = std::max(Tmax, sh[b].T);
+  auto fresh = [&](int b, int i, int j) { return tile_fresh(sh[b].full, sh[b].pnew, W, ell, i, j); };
+  struct Task {
+    int first, last, code;
+  };
+  // tasks of column j of system b, in the diagonal-chain order of chol_task_map
+  auto column = [&](int b, int j, std::vector<Task>& out) {
+    out.clear();
+    const int T = sh[b].T;
+    if (j >= T) return;
+    if (!fresh(b, j, j) && j + 1 < T && fresh(b, j + 1, j))
+      out.push_back({j + 1, j + 1, ((j + 1) << 16) | j});
+    if (j + 2 < T && fresh(b, j + 2, j)) out.push_back({j + 2, j + 2, ((j + 2) << 16) | j});
+    if (j + 1 < T && fresh(b, j + 1, j + 1))
+      out.push_back({j + 1, std::min(j + 2, T - 1), ((j + 1) << 16) | (j + 1)});
+    for (int i = j + 3; i < T; ++i) {
+      if (!fresh(b, i, j)) continue;
+      if ((i & 1) == 0 && i + 1 < T && fresh(b, i + 1, j)) {
+        out.push_back({i, i + 1, (i << 16) | 0x8000 | j});
+        ++i;
+      } else {
+        out.push_back({i, i, (i << 16) | j});
+      }
+    }
+  };
+  std::vector<int2> out;
+  for (int b = 0; b < nb; ++b)
+    if (fresh(b, 0, 0)) out.push_back(make_int2(b, 0));
+  std::vector<Task> col;
+  struct Body {
+    int b, last, c, code;
+  };
+  std::vector<Body> body;
+  for (int J = 0; J < Tmax; J += C) {
+    const int Jend = std::min(J + C, Tmax), head = J + C + 1;
+    body.clear();
+    for (int c = J; c < Jend; ++c)
+      for (int b = 0; b < nb; ++b) {
+        column(b, c, col);
+        for (const Task& t : col) {
+          if (t.first <= head) out.push_back(make_int2(b, t.code));
+          else body.push_back({b, t.last | 1, c, t.code});  // keyed by its aligned row pair
+        }
+      }
+    // bands of `band` rows after the head; inside a band: system, row pair, column
+    std::stable_sort(body.begin(), body.end(), [&](const Body& x, const Body& y) {
+      const int bx = (x.last - head - 1) / band, by = (y.last - head - 1) / band;
+      if (bx != by) return bx < by;
+      if (x.b != y.b) return x.b < y.b;
+      if (x.last != y.last) return x.last < y.last;
+      return x.c < y.c;
+    });
+    for (const Body& t : body) out.push_back(make_int2(t.b, t.code));
+  }
+  return out;
+}
+
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+std::vector<int2> chol_task_map(const SysShape* sh, int nb, int W, int ell, int cols, int band) {
+  if (cols < 0) cols = env_int("SLIM_CHOL_COLS", CHOL_COLS_DEFAULT);
+  if (band < 0) band = env_int("SLIM_CHOL_BAND", CHOL_BAND_DEFAULT);
+  if (cols >= 2) return chol_task_map_banded(sh, nb, W, ell, cols, std::max(2, band));
   int Tmax = 0;
   for (int b = 0; b < nb; ++b) Tmax = std::max(Tmax, sh[b].T);
   std::vector<int2> out;

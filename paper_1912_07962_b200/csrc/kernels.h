@@ -124,7 +124,14 @@ void launch_chol(const CholParams& P, cudaStream_t s);
 // G tiles of every system of the batch into its factor buffer
 // (P.tile_base[b] = first CTA of system b, P.tile_base[nb] = total)
 void launch_assemble(const CholParams& P, cudaStream_t s);
-std::vector<int2> chol_task_map(const SysShape* sh, int nb, int W, int ell);
+// ticket order of one batched factorization launch; cols >= 2 selects the
+// banded order (C columns per group, `band` tile rows per band), cols < 2
+// the column-by-column order; -1 = SLIM_CHOL_COLS / SLIM_CHOL_BAND or the
+// defaults below
+constexpr int CHOL_COLS_DEFAULT = 1;
+constexpr int CHOL_BAND_DEFAULT = 32;
+std::vector<int2> chol_task_map(const SysShape* sh, int nb, int W, int ell, int cols = -1,
+                                int band = -1);
 // inverses of the diagonal tiles of every system of the batch (after launch_chol)
 void launch_diag_inv(const CholParams& P, cudaStream_t s);
 // one cluster of P.C CTAs (trsv_cluster_size(T))

@@ -420,15 +420,31 @@ def _dense_source(op):
     return None
 
 
+def _stream_file_path(src):
+    """Path of a single-pass .slim stream operator, else None."""
+    if getattr(src, "access_mode", None) != "single_pass":
+        return None
+    path = getattr(src, "device_path", None)
+    if path is None and type(src).__name__ == "FileStreamOperator":
+        path = getattr(src, "_path", None)  # the reference's class (linops.py:374-386)
+    return os.fspath(path) if path is not None else None
+
+
 def device_operator(op, r: int, device: int = 0) -> DeviceOperator:
     """Upload ``op`` (once per (device, r)) and return its device context."""
     src = op.source if isinstance(op, SinglePassAdapter) else getattr(op, "_op", op)
-    if hasattr(src, "consume_all") and src.access_mode == "single_pass":
-        # a file stream: one in-order pass into HBM, cached on the stream object
+    path = _stream_file_path(src)
+    if path is not None:
+        # a .slim stream (ours or the reference's FileStreamOperator): the
+        # library reads each record from the file into HBM when its block is
+        # first sampled; the matrix never passes through host memory
         cache = src.__dict__.setdefault("_slim_device_cache", {})
-        key = (int(device), int(r), "stream")
+        key = (int(device), int(r), "file", path)
         if key not in cache:
-            cache[key] = device_operator(src.consume_all(), r, device)
+            dop = DeviceOperator(n_rows=src.n_rows, n_cols=src.n_cols, ell=src.block_rows, r=r,
+                                 layout=_lib.SLIM_DENSE_ROWMAJOR, dtype=np.float64, device=device)
+            dop.call("slim_attach_stream_file", os.fsencode(path))
+            cache[key] = dop
         return cache[key]
     if hasattr(src, "device_context"):  # tomo.ProjectorOperator: traced on the device
         return src.device_context(r, device)

@@ -15,7 +15,8 @@
 
 using namespace slim;
 
-static int check(int r, int ell, int D, int nsteps, bool alpha_change_mid) {
+static int check(int r, int ell, int D, int nsteps, bool alpha_change_mid, int cols = 1,
+                 int band = 32) {
   const int W = r + 1;
   int bad = 0, batches = 0;
   long long tasks_total = 0, tiles_total = 0;
@@ -29,7 +30,7 @@ static int check(int r, int ell, int D, int nsteps, bool alpha_change_mid) {
       const bool full = (k == 1) || (alpha_change_mid && k == nsteps / 2);
       sh[b] = SysShape{T, (k - 1) % W, full ? 1 : 0};
     }
-    std::vector<int2> map = chol_task_map(sh.data(), nb, W, ell);
+    std::vector<int2> map = chol_task_map(sh.data(), nb, W, ell, cols, band);
     // producer ticket of each (system, tile); -1 = before the launch
     std::vector<std::map<long long, int>> prod(nb);
     auto key = [](int i, int j) { return ((long long)i << 20) | j; };
@@ -96,8 +97,8 @@ static int check(int r, int ell, int D, int nsteps, bool alpha_change_mid) {
     tasks_total += map.size();
     ++batches;
   }
-  printf("r=%2d ell=%4d D=%d steps=%3d alpha_change=%d: %d batches, %lld tasks for %lld tiles (%.2f)%s\n",
-         r, ell, D, nsteps, (int)alpha_change_mid, batches, tasks_total, tiles_total,
+  printf("r=%2d ell=%4d D=%d steps=%3d alpha_change=%d cols=%d band=%d: %d batches, %lld tasks for %lld tiles (%.2f)%s\n",
+         r, ell, D, nsteps, (int)alpha_change_mid, cols, band, batches, tasks_total, tiles_total,
          (double)tasks_total / (double)tiles_total, bad ? "  FAIL" : "");
   return bad;
 }
@@ -114,6 +115,20 @@ int main() {
   bad += check(0, 50, 8, 20, false);
   bad += check(31, 64, 8, 100, false);
   bad += check(2, 1, 3, 20, false);
+  bad += check(8, 1448, 4, 24, false);   // configs[2] at the run's batch size
+  // banded ticket orders (SLIM_CHOL_COLS / SLIM_CHOL_BAND)
+  for (int cols : {2, 3, 4})
+    for (int band : {2, 7, 16, 32}) {
+      bad += check(10, 362, 16, 48, false, cols, band);
+      bad += check(8, 1448, 4, 24, false, cols, band);
+      bad += check(5, 2048, 4, 20, false, cols, band);
+      bad += check(20, 256, 16, 64, false, cols, band);
+      bad += check(5, 100, 8, 40, true, cols, band);
+      bad += check(3, 7, 4, 30, false, cols, band);
+      bad += check(0, 50, 8, 20, false, cols, band);
+      bad += check(31, 64, 8, 100, false, cols, band);
+      bad += check(2, 1, 3, 20, false, cols, band);
+    }
   printf(bad ? "FAILED\n" : "all orders valid\n");
   return bad ? 1 : 0;
 }
