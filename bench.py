@@ -592,7 +592,7 @@ def _roofline(timing, steps, N, cfg_id):
     i8ops = timing.get("cholesky_i8ops", 0.0) / max(1, timing["cholesky_count"])
     if i8ops > 0:
         qd, dbits = timing["cholesky_digits"]
-        pairs = qd * (qd + 1) // 2
+        pairs, qx = timing["cholesky_pairs"]
         ach_i8 = i8ops / (chol_ms * 1e-3) / 1e12
         return {"bound": "tensor", "achieved": ach_i8, "peak": I8_PEAK_TOPS,
                 "unit": "TOPS (int8)", "frac": ach_i8 / I8_PEAK_TOPS, "traffic": traffic,
@@ -600,7 +600,7 @@ def _roofline(timing, steps, N, cfg_id):
                 "kernel": f"k_chol_i8 (tile-DAG Cholesky, updates on tcgen05 kind::i8 with "
                           f"TMEM accumulators, {per_launch:g} systems of N={N} per launch)",
                 "algorithmic_per_launch": f"{i8ops:.4g} int8 ops ({pairs} digit-pair products "
-                                          f"({qd} digits: 7-bit lead, {dbits}-bit rest) x "
+                                          f"({qd} digits: 7-bit lead, {dbits}-bit rest; pairs with a + b <= {qd + 1 + qx}) x "
                                           f"2*64^3 per 64x64x64 tile update; the launch "
                                           f"factors {flops_chol:.4g} fp64-equivalent flop)",
                 "peak_source": "int8 tcgen05 peak measured on this pool, M=128 N=256 "

@@ -211,7 +211,9 @@ int slim_block_residual(slim_ctx* ctx, int64_t block, const double* x, double* r
  * *launches_out (compile-time SLIM_QD / SLIM_DBITS); which = 8 the operator
  * bytes copied host -> device since the operator was registered (block
  * values and columns, row pointers, b; host streaming counts only the
- * blocks a run actually sampled) in *ms_out.                             */
+ * blocks a run actually sampled) in *ms_out; which = 9 the digit-pair
+ * products per 64^3 tile update in *ms_out and the extra pair order QX
+ * (compile-time SLIM_QX) in *launches_out.                               */
 int slim_timing(slim_ctx* ctx, int32_t which, double* ms_out, int64_t* launches_out);
 int slim_set_profiling(slim_ctx* ctx, int32_t enable);
 /* time only steps k0..K of the next slim_run (which = 3 in slim_timing):

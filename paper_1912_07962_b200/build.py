@@ -21,7 +21,10 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 OBJDIR = os.path.join(ROOT, "build", "obj")
-LIB = os.path.join(HERE, "libslimb200.so")
+# SLIM_BUILD_TAG=<tag>: an alternate build (e.g. another digit layout via
+# SLIM_NVCC_EXTRA) into libslimb200_<tag>.so, loaded with SLIM_LIB=<path>
+_TAG = os.environ.get("SLIM_BUILD_TAG", "")
+LIB = os.path.join(HERE, f"libslimb200_{_TAG}.so" if _TAG else "libslimb200.so")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -943,7 +943,7 @@ static int size_streamed_csr(slim_ctx* c) {
   ALLOC(c, c->rowptr, sizeof(int64_t) * (c->m + 1));
   ALLOC(c, c->col, sizeof(int) * (size_t)std::max<int64_t>(1, nnz));
   ALLOC(c, c->val, c->vsize * (size_t)std::max<int64_t>(1, nnz));
-  ALLOC(c, c->colptr, sizeof(int) * (size_t)M * (c->n + 1));
+  ALLOC(c, c->colptr, sizeof(int) * (size_t)M * csc_stride((int)c->n));
   ALLOC(c, c->cscrow, sizeof(int) * (size_t)std::max<int64_t>(1, nnz));
   ALLOC(c, c->cscval, c->vsize * (size_t)std::max<int64_t>(1, nnz));
   ALLOC(c, c->blkbase, sizeof(int64_t) * (M + 1));
@@ -1205,7 +1205,7 @@ int slim_finalize_operator(slim_ctx* c) {
   if (c->cscrow) cache_release(c->cscrow), c->cscrow = nullptr;
   if (c->cscval) cache_release(c->cscval), c->cscval = nullptr;
   if (c->blkbase) cache_release(c->blkbase), c->blkbase = nullptr;
-  ALLOC(c, c->colptr, sizeof(int) * (size_t)c->M * (c->n + 1));
+  ALLOC(c, c->colptr, sizeof(int) * (size_t)c->M * csc_stride((int)c->n));
   ALLOC(c, c->cscrow, sizeof(int) * (size_t)std::max<int64_t>(1, c->nnz));
   ALLOC(c, c->cscval, c->vsize * (size_t)std::max<int64_t>(1, c->nnz));
   ALLOC(c, c->blkbase, sizeof(int64_t) * (c->M + 1));
@@ -1412,7 +1412,12 @@ int slim_set_timing_start(slim_ctx* c, int64_t k0) {
 }
 
 int slim_timing(slim_ctx* c, int32_t which, double* ms, int64_t* launches) {
-  if (!c || which < 0 || which > 8) FAIL(c, SLIM_EINVAL, "bad argument");
+  if (!c || which < 0 || which > 9) FAIL(c, SLIM_EINVAL, "bad argument");
+  if (which == 9) {  // digit-pair products per tile update and the extra order QX
+    if (ms) *ms = (double)QPAIRS;
+    if (launches) *launches = QX;
+    return SLIM_OK;
+  }
   if (which == 8) {  // operator bytes copied host -> device so far (e2e accounting)
     if (ms) *ms = (double)c->h2d_bytes.load();
     if (launches) *launches = 0;
@@ -1529,7 +1534,7 @@ static int enqueue_gram(slim_ctx* c, const Window& W, int64_t k, int64_t real_bl
       c->launches += 2, launch_gram_dense<float>(panel, c->gpart, c->nsplit_gram, W, (const float*)c->A, c->n,
                                newblk * c->ell, (int)c->n, c->sg);
   } else {
-    const int* cpn = c->colptr + newblk * (c->n + 1);
+    const int* cpn = c->colptr + newblk * csc_stride((int)c->n);
     const int64_t base = c->h_blkbase[newblk];
     if (c->vdt == SLIM_F64)
       c->launches += 1, launch_gram_csr<double>(panel, W, c->rowptr, c->col, (const double*)c->val, cpn, c->cscrow,
@@ -1686,7 +1691,7 @@ static const slim_ctx::TaskMap* task_map(slim_ctx* c, const std::vector<SysShape
   const double t3 = (double)TB * TB * TB;
   // int8 tensor-core path: 36 digit-pair products of 2 * 64^3 ops per 64x64x64
   // tile update (k_chol_i8)
-  const double u8 = (double)(QD * (QD + 1) / 2) * 2.0 * t3;
+  const double u8 = (double)QPAIRS * 2.0 * t3;
   double flops = 0.0, i8ops = 0.0;
   for (const int2& e : h) {
     const int i = e.y >> 16, j = e.y & 0x7fff;
@@ -2483,7 +2488,7 @@ extern "C" int slim_probe_stream(slim_ctx* c, int32_t kernel, int32_t reps, doub
       if (csr) {
         bytes = 8.0 * N * ell + 4.0 * (n + 1) + blk_nnz(nb) * (4 + vb);
         for (int P = 0; P < nw; ++P) bytes += blk_nnz(W.blk[P]) * (4 + vb) + 8.0 * (ell + 1);
-        const int* cpn = c->colptr + nb * (c->n + 1);
+        const int* cpn = c->colptr + nb * csc_stride((int)c->n);
         if (vb == 8)
           launch_gram_csr<double>(panel, W, c->rowptr, c->col, (const double*)c->val, cpn, c->cscrow,
                                   (const double*)c->cscval, c->h_blkbase[nb], s);

@@ -854,10 +854,61 @@ __device__ __forceinline__ uint64_t sw32_desc(uint32_t saddr) {
 // 10 MMAs (N up to 256) per stage instead of 28 with N = 64 (which cap at 2/3
 // of the tensor peak); the MMAs of one A digit share it through the A-operand
 // collector.
-template <int COLL>  // 0 plain, 1 fill, 3 lastuse
+// The digit-pair MMAs of one stage: A digit a times the run of B digits
+// b0 .. b0 + n - 1 (n <= 4, stacked along N) into accumulators
+// t = a + b0 - 2 .. + n - 1.  One MMA carries one overwrite flag, so on the
+// first stage a run is split where it would reach both accumulators written
+// by an earlier MMA and fresh ones (with QX = 1 that is the run of a = 2
+// reaching t = QD, first written by (a = 2, b = QD)).  coll: the A-operand
+// collector (0 none, 1 fill, 2 use, 3 lastuse) across the MMAs of one A digit.
+struct MmaGroup {
+  int a, b0, n, coll;
+  bool first;  // overwrites its accumulators on the first stage
+};
+struct MmaTable {
+  MmaGroup g[32];
+  int count;
+};
+constexpr MmaTable make_groups() {
+  MmaTable t{};
+  bool written[8] = {};
+  int cnt = 0;
+  for (int a = 1; a <= QD; ++a) {
+    const int nbd = q_nb(a);
+    const int first = cnt;
+    for (int b0 = 1; b0 <= nbd;) {
+      int n = nbd + 1 - b0 < 4 ? nbd + 1 - b0 : 4;
+      const int t0 = a + b0 - 2;
+      for (int q = 1; q < n; ++q)
+        if (written[t0 + q] != written[t0]) {
+          n = q;
+          break;
+        }
+      t.g[cnt] = MmaGroup{a, b0, n, 2, !written[t0]};
+      for (int q = 0; q < n; ++q) written[t0 + q] = true;
+      ++cnt;
+      b0 += n;
+    }
+    if (cnt - first == 1) {
+      t.g[first].coll = 0;
+    } else {
+      t.g[first].coll = 1;
+      t.g[cnt - 1].coll = 3;
+    }
+  }
+  t.count = cnt;
+  return t;
+}
+constexpr int NMMA = make_groups().count;
+
+template <int COLL>  // 0 plain, 1 fill, 2 use, 3 lastuse
 __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idsc,
                                        uint32_t acc) {
-  if (COLL == 1)
+  if (COLL == 2)
+    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                 "tcgen05.mma.cta_group::1.kind::i8.collector::a::use [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+                 "l"(adesc), "l"(bdesc), "r"(idsc), "r"(acc) : "memory");
+  else if (COLL == 1)
     asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
                  "tcgen05.mma.cta_group::1.kind::i8.collector::a::fill [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
                  "l"(adesc), "l"(bdesc), "r"(idsc), "r"(acc) : "memory");
@@ -1085,22 +1136,22 @@ __global__ void __launch_bounds__(256, 1) k_chol_i8(const __grid_constant__ Chol
       const uint64_t ad = oz::sw32_desc(a0), bd = oz::sw32_desc(a0 + oz::ST_A);
       // accumulators are first touched by the a = 1 MMAs: only they may
       // overwrite (first stage)
+      constexpr oz::MmaTable groups = oz::make_groups();
 #pragma unroll
-      for (int a = 1; a <= QD; ++a) {
-        const uint64_t A = ad + (((a - 1) * oz::DIG_A) >> 4);
-#pragma unroll
-        for (int b0 = 1; b0 <= QD + 1 - a; b0 += 4) {
-          const int n = (QD + 2 - a - b0) < 4 ? (QD + 2 - a - b0) : 4;
-          const uint64_t B = bd + (((b0 - 1) * oz::DIG_B) >> 4);
-          const uint32_t acc = (u > 0 || a > 1) ? 1u : 0u;
-          const uint32_t d = tmem + 64 * (a + b0 - 2);
-          if (QD + 1 - a <= 4)  // one MMA for this A digit: no collector
-            oz::mma_i8<0>(d, A, B, oz::idesc(n), acc);
-          else if (b0 == 1)
-            oz::mma_i8<1>(d, A, B, oz::idesc(n), acc);
-          else
-            oz::mma_i8<3>(d, A, B, oz::idesc(n), acc);
-        }
+      for (int g = 0; g < oz::NMMA; ++g) {
+        const oz::MmaGroup m = groups.g[g];
+        const uint64_t A = ad + (((m.a - 1) * oz::DIG_A) >> 4);
+        const uint64_t B = bd + (((m.b0 - 1) * oz::DIG_B) >> 4);
+        const uint32_t acc = (u > 0 || !m.first) ? 1u : 0u;
+        const uint32_t d = tmem + 64 * (m.a + m.b0 - 2);
+        if (m.coll == 0)
+          oz::mma_i8<0>(d, A, B, oz::idesc(m.n), acc);
+        else if (m.coll == 1)
+          oz::mma_i8<1>(d, A, B, oz::idesc(m.n), acc);
+        else if (m.coll == 2)
+          oz::mma_i8<2>(d, A, B, oz::idesc(m.n), acc);
+        else
+          oz::mma_i8<3>(d, A, B, oz::idesc(m.n), acc);
       }
       oz::mma_commit(&s_empty[st]);
     }
@@ -1134,7 +1185,7 @@ __global__ void __launch_bounds__(256, 1) k_chol_i8(const __grid_constant__ Chol
     for (int c = 0; c < 32; ++c) s[c] = 0.0;
     if (nchunk > 0) {
 #pragma unroll 1
-      for (int t = QD - 1; t >= 0; --t) {
+      for (int t = QACC - 1; t >= 0; --t) {
         int v[32];
         oz::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + 64 * t + 32 * h, v);
 #pragma unroll

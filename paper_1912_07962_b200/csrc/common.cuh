@@ -16,6 +16,10 @@ constexpr int MAX_BATCH = 16;    // systems factored by one interleaved launch
 constexpr int MAX_REFS = 8;      // error references tracked on device
 
 // ---- DMMA: D(8x8) += A(8x4, row) * B(4x8, col), fp64, IEEE FMA semantics ----
+// per-block CSC column pointers: n + 1 entries padded to a multiple of 4, so
+// every block's array starts 16-byte aligned (int4 loads of 4 columns)
+__host__ __device__ __forceinline__ int64_t csc_stride(int n) { return ((int64_t)n + 4) & ~(int64_t)3; }
+
 __device__ __forceinline__ void dmma8x8x4(double (&d)[2], double a, double b) {
   asm volatile(
       "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"

@@ -158,10 +158,28 @@ bool chol_i8_for(int T);
 #ifndef SLIM_DBITS
 #define SLIM_DBITS 8
 #endif
+// SLIM_QX: digit-pair products are kept for a + b <= QD + 1 + QX.  QX = 0
+// drops the order a + b = QD + 2 (weight ~2^-53 of the row scales per k
+// term, and not random: the iterate error at configs[1] grew to 2.6e-10 of
+// the reference's after one epoch); QX = 1 (default) keeps it -- QD - 1 more
+// products into an eighth TMEM accumulator, 34 instead of 28 pairs in 12
+// instead of 10 MMAs per stage -- for 3% of the factorization's speed
+// (operand-bandwidth bound) and a 26x smaller one-epoch error (9.9e-12)
+#ifndef SLIM_QX
+#define SLIM_QX 1
+#endif
 constexpr int QD = SLIM_QD;
 constexpr int DBITS = SLIM_DBITS;
+constexpr int QX = SLIM_QX;
+constexpr int QACC = QD + QX;  // TMEM accumulators of 64 columns (t = a + b - 2)
 static_assert(QD >= 5 && QD <= 8, "digit count");
 static_assert(DBITS == 7 || DBITS == 8, "digit width");
+static_assert(QX >= 0 && QACC <= 8, "TMEM holds at most 8 accumulators of 64 columns");
+static_assert(QX <= 1, "one extra accumulator: its first writer is the MMA (a = 2, b = QD)");
+// B digits multiplied with A digit a (1-based) and the digit-pair count
+__host__ __device__ constexpr int q_nb(int a) { return QD < QD + 1 + QX - a ? QD : QD + 1 + QX - a; }
+__host__ __device__ constexpr int q_pairs(int a = 1) { return a > QD ? 0 : q_nb(a) + q_pairs(a + 1); }
+constexpr int QPAIRS = q_pairs();
 // int8 updates: |P_t| <= (2 * 127 * H + (QD - 2) * H^2) * 64 T < 2^31 with
 // H = 2^(DBITS - 1) the largest trailing digit magnitude
 constexpr long long CHOL_I8_PAIRMAX =

@@ -439,7 +439,7 @@ __device__ __forceinline__ double mtw_csc_col(int c, const Window& W, const int*
       base[q] = 0;
       if (P0 + q < W.nw) {
         const int bk = W.blk[P0 + q];
-        const int* cp = colptr + (int64_t)bk * (n + 1);
+        const int* cp = colptr + (int64_t)bk * csc_stride(n);
         lo[q] = __ldcs(cp + c);
         hi[q] = __ldcs(cp + c + 1);
         base[q] = __ldg(blkbase + bk);
@@ -486,10 +486,9 @@ __global__ void __launch_bounds__(256) k_mtw_csc(double* __restrict__ s_out, Win
 
 // x[c] -= alpha sn for this thread's column, then the norms, divergence and
 // history row by a last-block reduction (every thread of the grid calls it)
+__device__ __forceinline__ void finish_reduce(const FinishParams& F, const double (&loc)[1 + MAX_REFS]);
+
 __device__ __forceinline__ void finish_body(const FinishParams& F, int c, double sn) {
-  Ctl* ctl = F.ctl;
-  const int tid = threadIdx.x;
-  const int nq = 1 + F.nref;
   double loc[1 + MAX_REFS];
 #pragma unroll
   for (int q = 0; q < 1 + MAX_REFS; ++q) loc[q] = 0.0;
@@ -504,6 +503,41 @@ __device__ __forceinline__ void finish_body(const FinishParams& F, int c, double
         loc[1 + q] = d * d;
       }
   }
+  finish_reduce(F, loc);
+}
+
+// four consecutive columns c0 .. c0 + 3 per thread (n % 4 == 0): 16-byte
+// loads and stores of x and the references
+__device__ __forceinline__ void finish_body4(const FinishParams& F, int c0, const double (&sn)[4]) {
+  double loc[1 + MAX_REFS];
+#pragma unroll
+  for (int q = 0; q < 1 + MAX_REFS; ++q) loc[q] = 0.0;
+  if (c0 < F.n) {
+    double2* xp = reinterpret_cast<double2*>(F.x + c0);
+    const double2 xa = xp[0], xb = xp[1];
+    const double x0 = xa.x - F.alpha * sn[0], x1 = xa.y - F.alpha * sn[1];
+    const double x2 = xb.x - F.alpha * sn[2], x3 = xb.y - F.alpha * sn[3];
+    xp[0] = make_double2(x0, x1);
+    xp[1] = make_double2(x2, x3);
+    loc[0] = (x0 * x0 + x1 * x1) + (x2 * x2 + x3 * x3);
+#pragma unroll
+    for (int q = 0; q < MAX_REFS; ++q)
+      if (q < F.nref) {
+        const double2* rp = reinterpret_cast<const double2*>(F.refs[q] + c0);
+        const double2 ra = __ldg(rp), rb = __ldg(rp + 1);
+        const double d0 = x0 - ra.x, d1 = x1 - ra.y, d2 = x2 - rb.x, d3 = x3 - rb.y;
+        loc[1 + q] = (d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3);
+      }
+  }
+  finish_reduce(F, loc);
+}
+
+// per-thread partial norms -> block partials -> (last block) the totals,
+// divergence test and history row, in a fixed order (deterministic)
+__device__ __forceinline__ void finish_reduce(const FinishParams& F, const double (&loc)[1 + MAX_REFS]) {
+  Ctl* ctl = F.ctl;
+  const int tid = threadIdx.x;
+  const int nq = 1 + F.nref;
   __shared__ double red[8][1 + MAX_REFS];
   __shared__ bool s_last;
   const int warp = tid >> 5, lane = tid & 31;
@@ -590,6 +624,125 @@ __global__ void __launch_bounds__(256) k_mtw_finish_csc(FinishParams F, Window W
   finish_body(F, c, sn);
 }
 
+// Four columns per thread (c0 = 4 t, n % 4 == 0): one 16-byte load brings
+// a block's four column pointers (the CSC arrays are padded to 16-byte
+// aligned strides, csc_stride), the fifth comes from the next lane; the
+// first E entries of G blocks are loaded before any is used, then their w
+// gathers, so a thread keeps ~3 G E independent loads in flight instead of
+// one dependent chain per block.  Per column the sums run block by block,
+// entry by entry, like mtw_csc_col.
+template <typename T, int G, int E>
+__device__ __forceinline__ void mtw_csc_quad(int c0, bool valid, const Window& W,
+                                             const int* __restrict__ colptr, int n,
+                                             const int* __restrict__ cscrow,
+                                             const T* __restrict__ cscval,
+                                             const int64_t* __restrict__ blkbase,
+                                             const double* __restrict__ w, double (&s)[4]) {
+  const int64_t cps = csc_stride(n);
+  const int ell = W.ell, lane = threadIdx.x & 31;
+  for (int P0 = 0; P0 < W.nw; P0 += G) {
+    int4 q[G];
+    int hi[G];
+    int64_t base[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      q[g] = make_int4(0, 0, 0, 0);
+      base[g] = 0;
+      if (P0 + g < W.nw) {
+        const int bk = W.blk[P0 + g];
+        q[g] = __ldcs(reinterpret_cast<const int4*>(colptr + (int64_t)bk * cps + c0));
+        base[g] = __ldg(blkbase + bk);
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      int nx = __shfl_down_sync(0xffffffffu, q[g].x, 1);
+      if (lane == 31 && P0 + g < W.nw) nx = __ldcs(colptr + (int64_t)W.blk[P0 + g] * cps + c0 + 4);
+      hi[g] = valid ? nx : q[g].x;
+    }
+    T v[G][E];
+    int rw[G][E];
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int idx = q[g].x + e;
+        v[g][e] = T(0);
+        rw[g][e] = 0;
+        if (idx < hi[g]) {
+          v[g][e] = __ldcs(cscval + base[g] + idx);
+          rw[g][e] = __ldcs(cscrow + base[g] + idx);
+        }
+      }
+    double wv[G][E];
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        wv[g][e] = (q[g].x + e < hi[g]) ? __ldg(w + (P0 + g) * ell + rw[g][e]) : 0.0;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const double* wp = w + (P0 + g) * ell;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int idx = q[g].x + e;
+        if (idx < hi[g]) {
+          const int k = (idx >= q[g].y) + (idx >= q[g].z) + (idx >= q[g].w);
+          const double pv = to_f64(v[g][e]);
+          if (k == 0) s[0] = fma(pv, wv[g][e], s[0]);
+          else if (k == 1) s[1] = fma(pv, wv[g][e], s[1]);
+          else if (k == 2) s[2] = fma(pv, wv[g][e], s[2]);
+          else s[3] = fma(pv, wv[g][e], s[3]);
+        }
+      }
+      for (int idx = q[g].x + E; idx < hi[g]; ++idx) {  // long columns (rare)
+        const int k = (idx >= q[g].y) + (idx >= q[g].z) + (idx >= q[g].w);
+        const double pv = to_f64(__ldcs(cscval + base[g] + idx));
+        const double wx = wp[__ldcs(cscrow + base[g] + idx)];
+        if (k == 0) s[0] = fma(pv, wx, s[0]);
+        else if (k == 1) s[1] = fma(pv, wx, s[1]);
+        else if (k == 2) s[2] = fma(pv, wx, s[2]);
+        else s[3] = fma(pv, wx, s[3]);
+      }
+    }
+  }
+}
+constexpr int MTW4_G = 3, MTW4_E = 4;
+template <typename T>
+__global__ void __launch_bounds__(256) k_mtw_finish_csc4(FinishParams F, Window W,
+                                                         const int* __restrict__ colptr,
+                                                         const int* __restrict__ cscrow,
+                                                         const T* __restrict__ cscval,
+                                                         const int64_t* __restrict__ blkbase,
+                                                         const double* __restrict__ w) {
+  if (F.ctl->diverged_at != 0) return;
+  const int c0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+  const bool valid = c0 < F.n;
+  double s[4] = {0.0, 0.0, 0.0, 0.0};
+  mtw_csc_quad<T, MTW4_G, MTW4_E>(valid ? c0 : F.n, valid, W, colptr, F.n, cscrow, cscval, blkbase,
+                                  w, s);
+  finish_body4(F, c0, s);
+}
+template <typename T>
+__global__ void __launch_bounds__(256) k_mtw_csc4(double* __restrict__ s_out, Window W,
+                                                  const int* __restrict__ colptr, int n,
+                                                  const int* __restrict__ cscrow,
+                                                  const T* __restrict__ cscval,
+                                                  const int64_t* __restrict__ blkbase,
+                                                  const double* __restrict__ w, const Ctl* ctl) {
+  if (ctl->diverged_at != 0) return;
+  const int c0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+  const bool valid = c0 < n;
+  double s[4] = {0.0, 0.0, 0.0, 0.0};
+  mtw_csc_quad<T, MTW4_G, MTW4_E>(valid ? c0 : n, valid, W, colptr, n, cscrow, cscval, blkbase, w,
+                                  s);
+  if (valid) {
+    double2* o = reinterpret_cast<double2*>(s_out + c0);
+    o[0] = make_double2(s[0], s[1]);
+    o[1] = make_double2(s[2], s[3]);
+  }
+}
+
 __global__ void k_stamp_start(Ctl* ctl) { ctl->t_start_ns = globaltimer_ns(); }
 
 // sharded mode: divergence decision and history row from allreduced norms
@@ -644,7 +797,7 @@ __global__ void k_csc_count(int* __restrict__ colptr, const int64_t* __restrict_
   const int lane = threadIdx.x & 31;
   if (row >= m) return;
   const int64_t b = row / ell;
-  int* cp = colptr + b * (int64_t)(n + 1);
+  int* cp = colptr + b * csc_stride(n);
   for (int64_t e = rowptr[row] + lane; e < rowptr[row + 1]; e += 32) atomicAdd(cp + col[e] + 1, 1);
 }
 
@@ -652,7 +805,7 @@ __global__ void __launch_bounds__(256) k_csc_scan(int* __restrict__ colptr, int 
   using Scan = cub::BlockScan<int, 256>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int carry;
-  int* cp = colptr + (int64_t)blockIdx.x * (n + 1);
+  int* cp = colptr + (int64_t)blockIdx.x * csc_stride(n);
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
   for (int base = 1; base <= n; base += 256) {
@@ -678,7 +831,7 @@ __global__ void k_csc_fill(int* __restrict__ colptr, const int64_t* __restrict__
   if (row >= m) return;
   const int64_t b = row / ell;
   const int64_t base = rowptr[b * ell];
-  int* cp = colptr + b * (int64_t)(n + 1);
+  int* cp = colptr + b * csc_stride(n);
   const int rloc = (int)(row - b * ell);
   for (int64_t e = rowptr[row] + lane; e < rowptr[row + 1]; e += 32) {
     const int pos = atomicAdd(cp + col[e], 1);
@@ -689,7 +842,7 @@ __global__ void k_csc_fill(int* __restrict__ colptr, const int64_t* __restrict__
 
 // after the fill, cp[c] holds the end of column c; shift right by one
 __global__ void __launch_bounds__(256) k_csc_shift(int* __restrict__ colptr, int n) {
-  int* cp = colptr + (int64_t)blockIdx.x * (n + 1);
+  int* cp = colptr + (int64_t)blockIdx.x * csc_stride(n);
   for (int hi = n + 1; hi > 0; hi -= 256) {
     const int c = hi - 256 + (int)threadIdx.x;  // writes positions [hi-256, hi)
     int v = 0;
@@ -709,7 +862,7 @@ __global__ void k_csc_sort(const int* __restrict__ colptr, int* __restrict__ csc
   if (gid >= nblocks * n) return;
   const int64_t b = gid / n;
   const int c = (int)(gid - b * n);
-  const int* cp = colptr + b * (int64_t)(n + 1);
+  const int* cp = colptr + b * csc_stride(n);
   const int64_t base = blkbase[b];
   const int lo = cp[c], hi = cp[c + 1];
   for (int e = lo + 1; e < hi; ++e) {
@@ -736,7 +889,7 @@ __global__ void k_csc_count_list(int* __restrict__ colptr, const int64_t* __rest
   if (lr >= (int64_t)L.n * ell) return;
   const int64_t b = L.id[lr / ell];
   const int64_t row = b * ell + lr % ell;
-  int* cp = colptr + b * (int64_t)(n + 1);
+  int* cp = colptr + b * csc_stride(n);
   for (int64_t e = rowptr[row] + lane; e < rowptr[row + 1]; e += 32) atomicAdd(cp + col[e] + 1, 1);
 }
 template <typename T>
@@ -751,7 +904,7 @@ __global__ void k_csc_fill_list(int* __restrict__ colptr, const int64_t* __restr
   const int rloc = (int)(lr % ell);
   const int64_t row = b * ell + rloc;
   const int64_t base = rowptr[b * ell];
-  int* cp = colptr + b * (int64_t)(n + 1);
+  int* cp = colptr + b * csc_stride(n);
   for (int64_t e = rowptr[row] + lane; e < rowptr[row + 1]; e += 32) {
     const int pos = atomicAdd(cp + col[e], 1);
     cscrow[base + pos] = rloc;
@@ -762,7 +915,7 @@ __global__ void __launch_bounds__(256) k_csc_scan_list(int* __restrict__ colptr,
   using Scan = cub::BlockScan<int, 256>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int carry;
-  int* cp = colptr + L.id[blockIdx.x] * (int64_t)(n + 1);
+  int* cp = colptr + L.id[blockIdx.x] * csc_stride(n);
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
   for (int base = 1; base <= n; base += 256) {
@@ -778,7 +931,7 @@ __global__ void __launch_bounds__(256) k_csc_scan_list(int* __restrict__ colptr,
   }
 }
 __global__ void __launch_bounds__(256) k_csc_shift_list(int* __restrict__ colptr, BlkList L, int n) {
-  int* cp = colptr + L.id[blockIdx.x] * (int64_t)(n + 1);
+  int* cp = colptr + L.id[blockIdx.x] * csc_stride(n);
   for (int hi = n + 1; hi > 0; hi -= 256) {
     const int c = hi - 256 + (int)threadIdx.x;
     int v = 0;
@@ -797,7 +950,7 @@ __global__ void k_csc_sort_list(const int* __restrict__ colptr, int* __restrict_
   if (gid >= (int64_t)L.n * n) return;
   const int64_t b = L.id[gid / n];
   const int c = (int)(gid % n);
-  const int* cp = colptr + b * (int64_t)(n + 1);
+  const int* cp = colptr + b * csc_stride(n);
   const int64_t base = blkbase[b];
   const int lo = cp[c], hi = cp[c + 1];
   for (int e = lo + 1; e < hi; ++e) {
@@ -909,10 +1062,18 @@ void launch_mtw_dense(double* part, int nsplit, const Window& W, const T* A, int
     k_mtw_dense<T, 1><<<grid, 256, 0, s>>>(part, W, A, lda, n, w, rps, ctl);
   }
 }
+static bool mtw_quad(int n) {
+  static const bool on = !(getenv("SLIM_MTW_QUAD") && getenv("SLIM_MTW_QUAD")[0] == '0');
+  return on && n % 4 == 0;
+}
 template <typename T>
 void launch_mtw_csc(double* s_out, const Window& W, const int* colptr, int n, const int* cscrow,
                     const T* cscval, const int64_t* blkbase, const double* w, const Ctl* ctl,
                     cudaStream_t s) {
+  if (mtw_quad(n)) {
+    k_mtw_csc4<T><<<cdiv(n / 4, 256), 256, 0, s>>>(s_out, W, colptr, n, cscrow, cscval, blkbase, w, ctl);
+    return;
+  }
   static const int grp = getenv("SLIM_MTW_GROUP") ? atoi(getenv("SLIM_MTW_GROUP")) : 3;
   if (grp <= 1)
     k_mtw_csc<T, 1><<<cdiv(n, 256), 256, 0, s>>>(s_out, W, colptr, n, cscrow, cscval, blkbase, w, ctl);
@@ -930,7 +1091,10 @@ template <typename T>
 void launch_mtw_finish_csc(const FinishParams& F, const Window& W, const int* colptr,
                            const int* cscrow, const T* cscval, const int64_t* blkbase,
                            const double* w, cudaStream_t s) {
-  k_mtw_finish_csc<T><<<cdiv(F.n, 256), 256, 0, s>>>(F, W, colptr, cscrow, cscval, blkbase, w);
+  if (mtw_quad(F.n))
+    k_mtw_finish_csc4<T><<<cdiv(F.n / 4, 256), 256, 0, s>>>(F, W, colptr, cscrow, cscval, blkbase, w);
+  else
+    k_mtw_finish_csc<T><<<cdiv(F.n, 256), 256, 0, s>>>(F, W, colptr, cscrow, cscval, blkbase, w);
 }
 template void launch_mtw_finish_csc<double>(const FinishParams&, const Window&, const int*,
                                             const int*, const double*, const int64_t*,
@@ -970,9 +1134,9 @@ void launch_build_csc(int* colptr, int* cscrow, T* cscval, const int64_t* rowptr
                       int64_t nblocks, cudaStream_t s, int64_t blk0, int64_t nblk) {
   if (nblk < 0) nblk = nblocks - blk0;
   if (nblk <= 0) return;
-  int* cp = colptr + blk0 * (int64_t)(n + 1);
+  int* cp = colptr + blk0 * csc_stride(n);
   const int64_t row0 = blk0 * ell, row1 = (blk0 + nblk) * (int64_t)ell;
-  cudaMemsetAsync(cp, 0, sizeof(int) * (size_t)nblk * (n + 1), s);
+  cudaMemsetAsync(cp, 0, sizeof(int) * (size_t)nblk * csc_stride(n), s);
   k_csc_count<<<cdiv(row1 - row0, 8), 256, 0, s>>>(colptr, rowptr, col, row0, row1, ell, n);
   k_csc_scan<<<(unsigned)nblk, 256, 0, s>>>(cp, n);
   k_csc_fill<T><<<cdiv(row1 - row0, 8), 256, 0, s>>>(colptr, rowptr, col, val, cscrow, cscval, row0,
@@ -987,7 +1151,7 @@ void launch_build_csc_list(int* colptr, int* cscrow, T* cscval, const int64_t* r
                            cudaStream_t s) {
   if (L.n <= 0) return;
   for (int q = 0; q < L.n; ++q)
-    cudaMemsetAsync(colptr + (int64_t)L.id[q] * (n + 1), 0, sizeof(int) * (size_t)(n + 1), s);
+    cudaMemsetAsync(colptr + (int64_t)L.id[q] * csc_stride(n), 0, sizeof(int) * (size_t)(n + 1), s);
   const int64_t rows = (int64_t)L.n * ell;
   k_csc_count_list<T><<<cdiv(rows, 8), 256, 0, s>>>(colptr, rowptr, col, L, ell, n);
   k_csc_scan_list<<<(unsigned)L.n, 256, 0, s>>>(colptr, L, n);

@@ -241,6 +241,8 @@ def run(method: str, op: RowBlockOperator, sampler, schedule: Schedule, *, epoch
         timing["cholesky_i8ops"] = ms.value
         dop.call("slim_timing", 7, C.byref(ms), C.byref(cnt))
         timing["cholesky_digits"] = (int(ms.value), int(cnt.value))  # (count, trailing bits)
+        dop.call("slim_timing", 9, C.byref(ms), C.byref(cnt))
+        timing["cholesky_pairs"] = (int(ms.value), int(cnt.value))  # (pairs per update, QX)
         reps = int(timing.get("probe_reps", 0))
         if reps > 0:  # operator-streaming kernels alone, cold L2 (bench "streaming")
             timing["streaming"] = {}

@@ -13,6 +13,7 @@ from tests import golden_cases as gc
 pytestmark = pytest.mark.gpu
 
 RTOL64 = 1e-10
+QX_DEFAULT = 1  # kernels.h SLIM_QX
 
 
 @pytest.fixture(scope="module")
@@ -516,6 +517,11 @@ def test_factorization_digit_layout_reported(slim):
     want_qd = int(extra.split("SLIM_QD=")[1].split()[0]) if "SLIM_QD=" in extra else 7
     want_db = int(extra.split("SLIM_DBITS=")[1].split()[0]) if "SLIM_DBITS=" in extra else 8
     assert (qd, dbits) == (want_qd, want_db)
+    pairs, qx = timing["cholesky_pairs"]
+    want_qx = int(extra.split("SLIM_QX=")[1].split()[0]) if "SLIM_QX=" in extra else QX_DEFAULT
+    assert qx == want_qx
+    # digit pairs (a, b) in [1, qd]^2 with a + b <= qd + 1 + qx
+    assert pairs == sum(min(qd, qd + 1 + qx - a) for a in range(1, qd + 1))
     if timing["cholesky_i8ops"] > 0:  # SLIM_CHOL=dmma reports 0
-        updates = timing["cholesky_i8ops"] / (qd * (qd + 1) // 2 * 2 * 64 ** 3)
+        updates = timing["cholesky_i8ops"] / (pairs * 2 * 64 ** 3)
         assert updates == int(updates) and updates >= 1
