@@ -624,6 +624,8 @@ __global__ void __launch_bounds__(256) k_mtw_finish_csc(FinishParams F, Window W
   finish_body(F, c, sn);
 }
 
+constexpr int MTW_QUAD_DEFAULT = 0;  // measured below the column kernel so far
+
 // Four columns per thread (c0 = 4 t, n % 4 == 0): one 16-byte load brings
 // a block's four column pointers (the CSC arrays are padded to 16-byte
 // aligned strides, csc_stride), the fifth comes from the next lane; the
@@ -707,8 +709,7 @@ __device__ __forceinline__ void mtw_csc_quad(int c0, bool valid, const Window& W
     }
   }
 }
-constexpr int MTW4_G = 3, MTW4_E = 4;
-template <typename T>
+template <typename T, int MTW4_G, int MTW4_E>
 __global__ void __launch_bounds__(256) k_mtw_finish_csc4(FinishParams F, Window W,
                                                          const int* __restrict__ colptr,
                                                          const int* __restrict__ cscrow,
@@ -723,7 +724,7 @@ __global__ void __launch_bounds__(256) k_mtw_finish_csc4(FinishParams F, Window 
                                   w, s);
   finish_body4(F, c0, s);
 }
-template <typename T>
+template <typename T, int MTW4_G, int MTW4_E>
 __global__ void __launch_bounds__(256) k_mtw_csc4(double* __restrict__ s_out, Window W,
                                                   const int* __restrict__ colptr, int n,
                                                   const int* __restrict__ cscrow,
@@ -1062,16 +1063,27 @@ void launch_mtw_dense(double* part, int nsplit, const Window& W, const T* A, int
     k_mtw_dense<T, 1><<<grid, 256, 0, s>>>(part, W, A, lda, n, w, rps, ctl);
   }
 }
-static bool mtw_quad(int n) {
-  static const bool on = !(getenv("SLIM_MTW_QUAD") && getenv("SLIM_MTW_QUAD")[0] == '0');
-  return on && n % 4 == 0;
+// SLIM_MTW_QUAD: 0 = one column per thread (k_mtw_csc); 1..5 = four columns
+// per thread with (G blocks, E entries) prefetched: (3,4) (2,6) (1,8) (3,2) (2,4)
+static int mtw_quad(int n) {
+  static const int v = getenv("SLIM_MTW_QUAD") ? atoi(getenv("SLIM_MTW_QUAD")) : MTW_QUAD_DEFAULT;
+  return (n % 4 == 0) ? v : 0;
 }
+#define MTW4_DISPATCH(KERNEL, GRID, ...)                                   \
+  switch (mtw_quad(n_)) {                                                  \
+    case 1: KERNEL<T, 3, 4><<<GRID, 256, 0, s>>>(__VA_ARGS__); break;      \
+    case 2: KERNEL<T, 2, 6><<<GRID, 256, 0, s>>>(__VA_ARGS__); break;      \
+    case 3: KERNEL<T, 1, 8><<<GRID, 256, 0, s>>>(__VA_ARGS__); break;      \
+    case 4: KERNEL<T, 3, 2><<<GRID, 256, 0, s>>>(__VA_ARGS__); break;      \
+    default: KERNEL<T, 2, 4><<<GRID, 256, 0, s>>>(__VA_ARGS__); break;     \
+  }
 template <typename T>
 void launch_mtw_csc(double* s_out, const Window& W, const int* colptr, int n, const int* cscrow,
                     const T* cscval, const int64_t* blkbase, const double* w, const Ctl* ctl,
                     cudaStream_t s) {
   if (mtw_quad(n)) {
-    k_mtw_csc4<T><<<cdiv(n / 4, 256), 256, 0, s>>>(s_out, W, colptr, n, cscrow, cscval, blkbase, w, ctl);
+    const int n_ = n;
+    MTW4_DISPATCH(k_mtw_csc4, cdiv(n / 4, 256), s_out, W, colptr, n, cscrow, cscval, blkbase, w, ctl);
     return;
   }
   static const int grp = getenv("SLIM_MTW_GROUP") ? atoi(getenv("SLIM_MTW_GROUP")) : 3;
@@ -1091,9 +1103,10 @@ template <typename T>
 void launch_mtw_finish_csc(const FinishParams& F, const Window& W, const int* colptr,
                            const int* cscrow, const T* cscval, const int64_t* blkbase,
                            const double* w, cudaStream_t s) {
-  if (mtw_quad(F.n))
-    k_mtw_finish_csc4<T><<<cdiv(F.n / 4, 256), 256, 0, s>>>(F, W, colptr, cscrow, cscval, blkbase, w);
-  else
+  const int n_ = F.n;
+  if (mtw_quad(n_)) {
+    MTW4_DISPATCH(k_mtw_finish_csc4, cdiv(F.n / 4, 256), F, W, colptr, cscrow, cscval, blkbase, w);
+  } else
     k_mtw_finish_csc<T><<<cdiv(F.n, 256), 256, 0, s>>>(F, W, colptr, cscrow, cscval, blkbase, w);
 }
 template void launch_mtw_finish_csc<double>(const FinishParams&, const Window&, const int*,

@@ -14,6 +14,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
 from oracle import slimls_oracle as orc
 from paper_1912_07962_b200.parallel import column_ranges, shard_operator, slice_csr_columns
 
@@ -142,3 +144,26 @@ def test_shard_operator_dense_and_sparse():
     ssh = shard_operator(sop, 2, 9)
     for i in range(1, 4):
         assert np.allclose(ssh.fetch_block(i).a_block, sop.fetch_block(i).a_block[:, 2:9])
+
+
+def test_bench_spawns_ranks_for_gpus_n():
+    """bench.py --gpus 2 without torchrun launches two ranks itself (gloo host
+    plumbing on 127.0.0.1); the reference arm runs on rank 0 only and prints
+    exactly one JSON line with n_gpus = 2."""
+    import json
+    import subprocess
+    import sys
+
+    env = dict(os.environ)
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(k, None)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                          "--gpus", "2", "--config", "1", "--steps", "3", "--warmup", "1"],
+                         capture_output=True, text=True, env=env, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    rec = json.loads(lines[0])
+    assert rec["impl"] == "reference" and rec["n_gpus"] == 2 and rec["steps"] == 3
+    assert rec["repo_native_loaded"] == []  # the reference arm never loads libslimb200.so
+    assert rec["cpu_baseline"]["kind"] == "reference"
