@@ -581,14 +581,16 @@ def _roofline(timing, steps, N, cfg_id):
     achieved = flops_chol / (chol_ms * 1e-3) / 1e12
     agg = timing["cholesky_flops"] / (timing["window_ms"] * 1e-3) / 1e12
     traffic, traffic_src = None, None
-    try:  # dram bytes per launch from the committed ncu --set full capture
-        with open(os.path.join(ROOT, "profiles", f"ncu_chol_cfg{cfg_id}.json")) as fh:
-            prof = json.load(fh)
-        traffic = prof["dram_bytes_per_launch"]
-        traffic_src = (f"profiles/ncu_chol_cfg{cfg_id}.json: {prof['systems_per_launch']} systems "
-                       f"per launch")
-    except (OSError, ValueError, KeyError):
-        pass
+    for name in (f"ncu_chol_cfg{cfg_id}_r02.json", f"ncu_chol_cfg{cfg_id}.json"):
+        try:  # dram bytes per launch from the committed ncu --set full capture
+            with open(os.path.join(ROOT, "profiles", name)) as fh:
+                prof = json.load(fh)
+            traffic = prof["dram_bytes_per_launch"]
+            traffic_src = (f"profiles/{name}: {prof['systems_per_launch']} systems per launch, "
+                           f"{prof.get('gpu__time_duration.sum', '?')} under ncu")
+            break
+        except (OSError, ValueError, KeyError):
+            continue
     i8ops = timing.get("cholesky_i8ops", 0.0) / max(1, timing["cholesky_count"])
     if i8ops > 0:
         qd, dbits = timing["cholesky_digits"]
