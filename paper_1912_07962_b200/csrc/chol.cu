@@ -830,7 +830,14 @@ constexpr int STAGE = ST_A + ST_B;       // 6 QD KB: one k half of three tiles
 // third of each SM's shared memory to the x-chain kernels running beside
 // the factorization; measured +0.8% at configs[1] over four, equal at [2]
 constexpr int NST = SLIM_OZ_NST;
-constexpr int SMEM = NST * STAGE + 1024;
+// SLIM_OZ_EXTRAB=1 (experiment only): each stage loads its B box a second
+// time into a scratch area (correct results, +1/3 operand bytes) to measure
+// how the factorization's time depends on operand bytes
+#ifndef SLIM_OZ_EXTRAB
+#define SLIM_OZ_EXTRAB 0
+#endif
+constexpr int EXTRA = SLIM_OZ_EXTRAB ? NST * ST_B : 0;
+constexpr int SMEM = NST * STAGE + EXTRA + 1024;
 // work tiles over the drained stage ring
 constexpr int W_X = 0;                               // 128 x TS fp64
 constexpr int W_SG = W_X + 2 * TB * TS * 8;          // L_jj, 64 x TS fp64
@@ -1107,7 +1114,11 @@ __global__ void __launch_bounds__(256, 1) k_chol_i8(const __grid_constant__ Chol
         if (tr) t_dep += globaltimer_ns() - w1;
       }
       uint8_t* dst = stage + st * oz::STAGE;
-      bar_expect(&s_full[st], oz::STAGE);
+      bar_expect(&s_full[st], oz::STAGE + (SLIM_OZ_EXTRAB ? oz::ST_B : 0));
+#if SLIM_OZ_EXTRAB
+      tma3d(stage + oz::NST * oz::STAGE + st * oz::ST_B, &M.qmapB, &s_full[st], 0, j * TB,
+            (k * 2 + kh) * QD);
+#endif
       // A: tile rows ra, ra + 1, all QD digits (a single task's spare row is
       // loaded and ignored); B: tile row j
 #if SLIM_OZ_HINT

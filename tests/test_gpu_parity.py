@@ -370,6 +370,7 @@ def test_generated_tensor_core_gram(slim, tc, monkeypatch):
 
 
 def _sharded_vs_single(slim, op, xt, scheme, seed, alpha, r, K, P, round_robin=False):
+    from oracle import slimls_oracle as orc
     from paper_1912_07962_b200.parallel import LocalGroup
     M = op.n_blocks
     kw = dict(epochs=K / M, r=r, references={"x_true": xt})
@@ -378,6 +379,15 @@ def _sharded_vs_single(slim, op, xt, scheme, seed, alpha, r, K, P, round_robin=F
     group = LocalGroup(P, round_robin=round_robin)
     full, per = group.run("slimls", op, lambda: slim.Sampler(scheme, M, seed),
                           slim.Schedule("constant", alpha), **kw)
+    # the sharded run against the CPU oracle too (not only against the unsharded run)
+    import bench
+    idx = orc.sampler_indices(scheme, M, seed, K)
+    ref = orc.run_slimls(bench.oracle_fetch(op, op.rhs), M, op.n_cols, idx, np.full(K, alpha), r=r,
+                         references={"x_true": xt})
+    err_o = np.linalg.norm(full.x_final - ref.x_final) / np.linalg.norm(ref.x_final)
+    print(f"{P} shards{' round-robin' if round_robin else ''}: relative error vs oracle {err_o:.2e}")
+    assert err_o <= 1e-10, err_o
+    np.testing.assert_allclose(full.rel_errors["x_true"], ref.rel_errors["x_true"], rtol=1e-10)
     err = np.linalg.norm(full.x_final - single.x_final) / np.linalg.norm(single.x_final)
     assert err <= 1e-10, err
     np.testing.assert_allclose(full.rel_errors["x_true"], single.rel_errors["x_true"], rtol=1e-10)
