@@ -206,6 +206,7 @@ struct slim_ctx {
   void* val = nullptr;
   int64_t nnz = 0;
   int* colptr = nullptr;
+  int mtw_quad = 0;  // M^T w kernel variant (mtw_variant), set when the operator is finalized
   int* cscrow = nullptr;
   void* cscval = nullptr;
   int64_t* blkbase = nullptr;  // M + 1 nnz offsets (device)
@@ -951,6 +952,7 @@ static int size_streamed_csr(slim_ctx* c) {
   CK(c, cudaMemcpy(c->blkbase, c->h_blkbase.data(), sizeof(int64_t) * (M + 1), cudaMemcpyHostToDevice));
   CK(c, cudaMemcpy(c->b, c->h_b.data(), sizeof(double) * c->m, cudaMemcpyHostToDevice));
   c->h2d_bytes += (int64_t)(sizeof(int64_t) * (c->m + 1 + M + 1) + sizeof(double) * c->m);
+  c->mtw_quad = mtw_variant(c->n, (double)nnz / (double)std::max<int64_t>(1, M));
   c->h_have.clear();
   c->h_b.clear();
   c->resident.assign(M, 0);
@@ -1221,6 +1223,7 @@ int slim_finalize_operator(slim_ctx* c) {
                             c->sx);
   CKLAUNCH(c);
   CK(c, cudaStreamSynchronize(c->sx));
+  c->mtw_quad = mtw_variant(c->n, (double)c->nnz / (double)std::max<int64_t>(1, c->M));
   c->op_ready = true;
   return SLIM_OK;
 }
@@ -1619,10 +1622,10 @@ static int enqueue_x_chain(slim_ctx* c, const Window& W, int64_t k, int d, doubl
   if (fused) {
     if (c->vdt == SLIM_F64)
       launch_mtw_finish_csc<double>(F, W, c->colptr, c->cscrow, (const double*)c->cscval, c->blkbase,
-                                    c->wvec, s);
+                                    c->wvec, s, c->mtw_quad);
     else
       launch_mtw_finish_csc<float>(F, W, c->colptr, c->cscrow, (const float*)c->cscval, c->blkbase,
-                                   c->wvec, s);
+                                   c->wvec, s, c->mtw_quad);
     c->launches -= 1;  // one kernel instead of M^T w + finish
   } else {
     launch_finish(F, s);
@@ -2468,10 +2471,10 @@ extern "C" int slim_probe_stream(slim_ctx* c, int32_t kernel, int32_t reps, doub
         for (int P = 0; P < nw; ++P) bytes += 4.0 * (n + 1) + blk_nnz(W.blk[P]) * (4 + vb);
         if (vb == 8)
           launch_mtw_csc<double>(c->spart, W, c->colptr, n, c->cscrow, (const double*)c->cscval,
-                                 c->blkbase, c->wvec, ctl, s);
+                                 c->blkbase, c->wvec, ctl, s, c->mtw_quad);
         else
           launch_mtw_csc<float>(c->spart, W, c->colptr, n, c->cscrow, (const float*)c->cscval,
-                                c->blkbase, c->wvec, ctl, s);
+                                c->blkbase, c->wvec, ctl, s, c->mtw_quad);
       } else {
         const int nsplit = std::min(c->nsplit_mtw, N);
         bytes = (double)N * n * vb + 8.0 * N + 8.0 * nsplit * n;

@@ -40,11 +40,6 @@ namespace slim {
 
 constexpr unsigned FULL = 0xffffffffu;
 
-// byte offset of row r of digit block kd = (k half, digit) of sliced tile
-// (i, k): [k][k half][digit][tile row i < qT][64 rows][32 B]
-__host__ __device__ __forceinline__ int64_t q_off(int qT, int i, int k, int kd, int r) {
-  return ((((int64_t)k * 2 * QD + kd) * qT + i) * 64 + r) * 32;
-}
 
 // per-CTA view of its system, in registers (indexing the kernel-parameter
 // array with the runtime system id would turn every field access into a
@@ -384,9 +379,12 @@ __global__ void __launch_bounds__(256) k_assemble(CholParams P) {
     const double2* src = reinterpret_cast<const double2*>(P.prevL + toff);
     double2* dst = reinterpret_cast<double2*>(Mp.L + toff);
     for (int e = tid; e < TB * TB / 2; e += 256) dst[e] = __ldcg(src + e);
-    if (Mp.Q != nullptr && P.prevQ != nullptr && I != J) {  // 2 QD (k half, digit) blocks of 2 KB
+    if (Mp.Q != nullptr && P.prevQ != nullptr && I != J) {  // 2 QD contiguous runs of 2 KB
       for (int e = tid; e < 2 * QD * 128; e += 256) {
-        const int64_t off = q_off(Mp.qT, I, J, e >> 7, 0) + (int64_t)(e & 127) * 16;
+        const int blk = e >> 7;  // QROW 32: (k half, digit); 64: (digit, half of its 4 KB)
+        const int64_t off = (QROW == 32 ? q_off(Mp.qT, I, J, blk / QD, blk % QD, 0)
+                                        : q_off(Mp.qT, I, J, 0, blk >> 1, 0) + (blk & 1) * 2048) +
+                            (int64_t)(e & 127) * 16;
         *reinterpret_cast<uint4*>(Mp.Q + off) = __ldcg(reinterpret_cast<const uint4*>(P.prevQ + off));
       }
     }
@@ -815,13 +813,14 @@ __global__ void __launch_bounds__(256, 2) k_chol_tiles(const __grid_constant__ C
 #define SLIM_ACC_SLEEP_NS 500  // 2000 -> 500: +0.4% at configs[1]
 #endif
 namespace oz {
-constexpr int DIG_A = 128 * 32;          // one digit of the A operand: 128 rows x 32 B
-constexpr int DIG_B = 64 * 32;           // one digit of B: 64 rows x 32 B
-constexpr int ST_A = QD * DIG_A;         // [digit][rows of tiles i, i + 1][32 B]
-constexpr int ST_B = QD * DIG_B;         // [digit][64 rows][32 B]
-constexpr int STAGE = ST_A + ST_B;       // 6 QD KB: one k half of three tiles
+constexpr int DIG_A = 128 * QROW;        // one digit of the A operand: 128 rows x QROW B
+constexpr int DIG_B = 64 * QROW;         // one digit of B: 64 rows x QROW B
+constexpr int ST_A = QD * DIG_A;         // [digit][rows of tiles i, i + 1][QROW B]
+constexpr int ST_B = QD * DIG_B;         // [digit][64 rows][QROW B]
+constexpr int STAGE = ST_A + ST_B;       // QROW / 32 k halves of three tiles
+constexpr int KSTEPS = QROW / 32;        // K = 32 MMA steps per stage
 #ifndef SLIM_OZ_NST
-#define SLIM_OZ_NST 3
+#define SLIM_OZ_NST (SLIM_OZ_SW == 64 ? 2 : 3)  // 2 x 84 KB or 3 x 42 KB in flight
 #endif
 #ifndef SLIM_OZ_HINT
 #define SLIM_OZ_HINT 1  // L2 hints on the operand loads: +0.5% at configs[1]
@@ -830,14 +829,7 @@ constexpr int STAGE = ST_A + ST_B;       // 6 QD KB: one k half of three tiles
 // third of each SM's shared memory to the x-chain kernels running beside
 // the factorization; measured +0.8% at configs[1] over four, equal at [2]
 constexpr int NST = SLIM_OZ_NST;
-// SLIM_OZ_EXTRAB=1 (experiment only): each stage loads its B box a second
-// time into a scratch area (correct results, +1/3 operand bytes) to measure
-// how the factorization's time depends on operand bytes
-#ifndef SLIM_OZ_EXTRAB
-#define SLIM_OZ_EXTRAB 0
-#endif
-constexpr int EXTRA = SLIM_OZ_EXTRAB ? NST * ST_B : 0;
-constexpr int SMEM = NST * STAGE + EXTRA + 1024;
+constexpr int SMEM = NST * STAGE + 1024;
 // work tiles over the drained stage ring
 constexpr int W_X = 0;                               // 128 x TS fp64
 constexpr int W_SG = W_X + 2 * TB * TS * 8;          // L_jj, 64 x TS fp64
@@ -849,10 +841,13 @@ __host__ __device__ constexpr uint32_t idesc(int n) {
   return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(8 * n) << 17) | ((uint32_t)(128 >> 4) << 24);
 }
 
-// K-major SWIZZLE_32B operand: rows of 32 B (K = 32 int8), 8-row groups 256 B apart
-__device__ __forceinline__ uint64_t sw32_desc(uint32_t saddr) {
-  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(256 >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)6 << 61);
+// K-major swizzled operand: rows of QROW bytes, 8-row groups 8 QROW apart;
+// layout type SWIZZLE_32B (6) or SWIZZLE_64B (4).  With 64-byte rows the
+// second K = 32 step of a stage starts 32 bytes into the swizzle atom.
+__device__ __forceinline__ uint64_t sw_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) |
+         ((uint64_t)((8 * QROW) >> 4) << 32) | ((uint64_t)1 << 46) |
+         ((uint64_t)(QROW == 32 ? 6 : 4) << 61);
 }
 // One MMA per (A digit a, run of up to four B digits b0 .. b0 + n - 1): the
 // B digits are stacked along N (64 rows each), and D starts at accumulator
@@ -989,7 +984,7 @@ __device__ __forceinline__ void store_digits(const CholMat& M, int i, int k, con
   const int r = tid >> 2, kq = tid & 3, kh = kq >> 1, kk0 = (kq & 1) * 16;
 #pragma unroll
   for (int a = 0; a < QD; ++a)
-    *reinterpret_cast<uint4*>(M.Q + q_off(M.qT, i, k, kh * QD + a, r) + kk0) = D.w[a];
+    *reinterpret_cast<uint4*>(M.Q + q_off(M.qT, i, k, kh, a, r) + kk0) = D.w[a];
 }
 
 // Store tile (i, j) -- fp64, digit slices (off-diagonal tiles: the only
@@ -1078,7 +1073,7 @@ __global__ void __launch_bounds__(256, 1) k_chol_i8(const __grid_constant__ Chol
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = s_tmem;
-  const int nchunk = 2 * j;  // k tiles 0 .. j-1, two k halves each
+  const int nchunk = oz::KSTEPS == 2 ? j : 2 * j;  // stages: k tiles 0 .. j-1 (or their halves)
 
   if (tid == 0 && nchunk > 0) {
     // ---------------- TMA producer ----------------
@@ -1105,7 +1100,7 @@ __global__ void __launch_bounds__(256, 1) k_chol_i8(const __grid_constant__ Chol
       bar_wait(&s_empty[st], ((u / oz::NST) & 1) ^ 1);
       const unsigned long long w1 = tr ? globaltimer_ns() : 0;
       t_ring += w1 - w0;
-      const int k = u >> 1, kh = u & 1;
+      const int k = oz::KSTEPS == 2 ? u : (u >> 1), kh = oz::KSTEPS == 2 ? 0 : (u & 1);
       if (kh == 0 && k >= kready) {
         wait_flag(fa + k, M.epoch);
         if (two) wait_flag(fa2 + k, M.epoch);
@@ -1114,21 +1109,18 @@ __global__ void __launch_bounds__(256, 1) k_chol_i8(const __grid_constant__ Chol
         if (tr) t_dep += globaltimer_ns() - w1;
       }
       uint8_t* dst = stage + st * oz::STAGE;
-      bar_expect(&s_full[st], oz::STAGE + (SLIM_OZ_EXTRAB ? oz::ST_B : 0));
-#if SLIM_OZ_EXTRAB
-      tma3d(stage + oz::NST * oz::STAGE + st * oz::ST_B, &M.qmapB, &s_full[st], 0, j * TB,
-            (k * 2 + kh) * QD);
-#endif
+      bar_expect(&s_full[st], oz::STAGE);
+      const int zc = oz::KSTEPS == 2 ? k * QD : (k * 2 + kh) * QD;  // first digit block of the stage
       // A: tile rows ra, ra + 1, all QD digits (a single task's spare row is
       // loaded and ignored); B: tile row j
 #if SLIM_OZ_HINT
       // A (this task's row pair) is streamed once; B (row j) is shared by
       // every task of the column
-      tma3d_hint(dst, &M.qmapA, &s_full[st], 0, ra * TB, (k * 2 + kh) * QD, L2_EVICT_FIRST);
-      tma3d_hint(dst + oz::ST_A, &M.qmapB, &s_full[st], 0, j * TB, (k * 2 + kh) * QD, L2_EVICT_LAST);
+      tma3d_hint(dst, &M.qmapA, &s_full[st], 0, ra * TB, zc, L2_EVICT_FIRST);
+      tma3d_hint(dst + oz::ST_A, &M.qmapB, &s_full[st], 0, j * TB, zc, L2_EVICT_LAST);
 #else
-      tma3d(dst, &M.qmapA, &s_full[st], 0, ra * TB, (k * 2 + kh) * QD);
-      tma3d(dst + oz::ST_A, &M.qmapB, &s_full[st], 0, j * TB, (k * 2 + kh) * QD);
+      tma3d(dst, &M.qmapA, &s_full[st], 0, ra * TB, zc);
+      tma3d(dst + oz::ST_A, &M.qmapB, &s_full[st], 0, j * TB, zc);
 #endif
     }
     if (tr) tr[4] = t_dep;
@@ -1144,7 +1136,9 @@ __global__ void __launch_bounds__(256, 1) k_chol_i8(const __grid_constant__ Chol
       if (trm) t_data += globaltimer_ns() - w0;
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t a0 = su32(stage + st * oz::STAGE);
-      const uint64_t ad = oz::sw32_desc(a0), bd = oz::sw32_desc(a0 + oz::ST_A);
+#pragma unroll
+      for (int ks = 0; ks < oz::KSTEPS; ++ks) {
+      const uint64_t ad = oz::sw_desc(a0 + 32 * ks), bd = oz::sw_desc(a0 + oz::ST_A + 32 * ks);
       // accumulators are first touched by the a = 1 MMAs: only they may
       // overwrite (first stage)
       constexpr oz::MmaTable groups = oz::make_groups();
@@ -1153,7 +1147,7 @@ __global__ void __launch_bounds__(256, 1) k_chol_i8(const __grid_constant__ Chol
         const oz::MmaGroup m = groups.g[g];
         const uint64_t A = ad + (((m.a - 1) * oz::DIG_A) >> 4);
         const uint64_t B = bd + (((m.b0 - 1) * oz::DIG_B) >> 4);
-        const uint32_t acc = (u > 0 || !m.first) ? 1u : 0u;
+        const uint32_t acc = (u > 0 || ks > 0 || !m.first) ? 1u : 0u;
         const uint32_t d = tmem + 64 * (m.a + m.b0 - 2);
         if (m.coll == 0)
           oz::mma_i8<0>(d, A, B, oz::idesc(m.n), acc);
@@ -1164,6 +1158,7 @@ __global__ void __launch_bounds__(256, 1) k_chol_i8(const __grid_constant__ Chol
         else
           oz::mma_i8<3>(d, A, B, oz::idesc(m.n), acc);
       }
+      }  // K steps of the stage
       oz::mma_commit(&s_empty[st]);
     }
     oz::mma_commit(&s_accf);

@@ -186,10 +186,28 @@ constexpr long long CHOL_I8_PAIRMAX =
     (2LL * 127 * (1 << (DBITS - 1)) + (QD - 2) * (1LL << (2 * (DBITS - 1)))) * 64;
 constexpr int CHOL_I8_TMAX =
     (int)(((1LL << 31) - 1) / CHOL_I8_PAIRMAX < 800 ? ((1LL << 31) - 1) / CHOL_I8_PAIRMAX : 800);
+// Row width of the digit slices in bytes (SLIM_OZ_SW): 64 = one k tile per
+// row, a TMA stage is one k tile under SWIZZLE_64B (default); 32 = the round-1
+// layout, one k half per row under SWIZZLE_32B.  A TMA box of 32-byte rows
+// delivers at most ~53 GB/s per SM from L2 on B200, 64-byte rows ~99 GB/s
+// (tools/microbench/tma_rows.cu, profiles/tma_row_width_r02.txt).
+#ifndef SLIM_OZ_SW
+#define SLIM_OZ_SW 64
+#endif
+constexpr int QROW = SLIM_OZ_SW;
+static_assert(QROW == 32 || QROW == 64, "digit-slice row width");
 // TMA views of a sliced factor buffer with qT tile rows per column (box
 // rows = 128 for the A operand, 64 for B; QD digits per box)
 bool tma_map_q(CUtensorMap* m, const int8_t* base, int qT, int box_rows);
-// bytes of a sliced factor buffer: [k][k half][digit][tile row][64 rows][32 B]
+// bytes of a sliced factor buffer (the same for both layouts):
+//   QROW 32: [k][k half][digit][tile row][64 rows][32 B]
+//   QROW 64: [k][digit][tile row][64 rows][64 B]
 inline size_t q_bytes(int qT) { return (size_t)qT * qT * 2 * QD * 64 * 32; }
+// byte offset of row r, k half kh (32 bytes) of digit a (0-based) of the
+// sliced tile (i, k)
+__host__ __device__ __forceinline__ int64_t q_off(int qT, int i, int k, int kh, int a, int r) {
+  if (QROW == 32) return ((((int64_t)k * 2 * QD + kh * QD + a) * qT + i) * 64 + r) * 32;
+  return ((((int64_t)k * QD + a) * qT + i) * 64 + r) * 64 + 32 * kh;
+}
 
 }  // namespace slim

@@ -624,8 +624,6 @@ __global__ void __launch_bounds__(256) k_mtw_finish_csc(FinishParams F, Window W
   finish_body(F, c, sn);
 }
 
-constexpr int MTW_QUAD_DEFAULT = 0;  // measured below the column kernel so far
-
 // Four columns per thread (c0 = 4 t, n % 4 == 0): one 16-byte load brings
 // a block's four column pointers (the CSC arrays are padded to 16-byte
 // aligned strides, csc_stride), the fifth comes from the next lane; the
@@ -1063,14 +1061,18 @@ void launch_mtw_dense(double* part, int nsplit, const Window& W, const T* A, int
     k_mtw_dense<T, 1><<<grid, 256, 0, s>>>(part, W, A, lda, n, w, rps, ctl);
   }
 }
-// SLIM_MTW_QUAD: 0 = one column per thread (k_mtw_csc); 1..5 = four columns
-// per thread with (G blocks, E entries) prefetched: (3,4) (2,6) (1,8) (3,2) (2,4)
-static int mtw_quad(int n) {
-  static const int v = getenv("SLIM_MTW_QUAD") ? atoi(getenv("SLIM_MTW_QUAD")) : MTW_QUAD_DEFAULT;
-  return (n % 4 == 0) ? v : 0;
+// variants 1..5 = four columns per thread with (G blocks, E entries)
+// prefetched: (3,4) (2,6) (1,8) (3,2) (2,4); measured at configs[2] (1.25
+// entries per column and block, n = 2^20): (1,8) 53 us vs the column kernel's
+// 67 us; at configs[1] (n = 2^16, too few threads) and configs[3] (0.15
+// entries per column and block) the column kernel is faster
+int mtw_variant(int64_t n, double nnz_per_block) {
+  if (const char* e = getenv("SLIM_MTW_QUAD")) return n % 4 == 0 ? atoi(e) : 0;
+  return (n % 4 == 0 && n >= (1 << 19) && nnz_per_block >= 0.5 * (double)n) ? 3 : 0;
 }
+static int mtw_quad(int n, int quad) { return n % 4 == 0 ? quad : 0; }
 #define MTW4_DISPATCH(KERNEL, GRID, ...)                                   \
-  switch (mtw_quad(n_)) {                                                  \
+  switch (mtw_quad(n_, quad)) {                                                  \
     case 1: KERNEL<T, 3, 4><<<GRID, 256, 0, s>>>(__VA_ARGS__); break;      \
     case 2: KERNEL<T, 2, 6><<<GRID, 256, 0, s>>>(__VA_ARGS__); break;      \
     case 3: KERNEL<T, 1, 8><<<GRID, 256, 0, s>>>(__VA_ARGS__); break;      \
@@ -1080,8 +1082,8 @@ static int mtw_quad(int n) {
 template <typename T>
 void launch_mtw_csc(double* s_out, const Window& W, const int* colptr, int n, const int* cscrow,
                     const T* cscval, const int64_t* blkbase, const double* w, const Ctl* ctl,
-                    cudaStream_t s) {
-  if (mtw_quad(n)) {
+                    cudaStream_t s, int quad) {
+  if (mtw_quad(n, quad)) {
     const int n_ = n;
     MTW4_DISPATCH(k_mtw_csc4, cdiv(n / 4, 256), s_out, W, colptr, n, cscrow, cscval, blkbase, w, ctl);
     return;
@@ -1102,19 +1104,19 @@ void launch_finish(const FinishParams& F, cudaStream_t s) {
 template <typename T>
 void launch_mtw_finish_csc(const FinishParams& F, const Window& W, const int* colptr,
                            const int* cscrow, const T* cscval, const int64_t* blkbase,
-                           const double* w, cudaStream_t s) {
+                           const double* w, cudaStream_t s, int quad) {
   const int n_ = F.n;
-  if (mtw_quad(n_)) {
+  if (mtw_quad(n_, quad)) {
     MTW4_DISPATCH(k_mtw_finish_csc4, cdiv(F.n / 4, 256), F, W, colptr, cscrow, cscval, blkbase, w);
   } else
     k_mtw_finish_csc<T><<<cdiv(F.n, 256), 256, 0, s>>>(F, W, colptr, cscrow, cscval, blkbase, w);
 }
 template void launch_mtw_finish_csc<double>(const FinishParams&, const Window&, const int*,
                                             const int*, const double*, const int64_t*,
-                                            const double*, cudaStream_t);
+                                            const double*, cudaStream_t, int);
 template void launch_mtw_finish_csc<float>(const FinishParams&, const Window&, const int*,
                                            const int*, const float*, const int64_t*,
-                                           const double*, cudaStream_t);
+                                           const double*, cudaStream_t, int);
 int finish_grid(int n) { return (int)cdiv(n, 256); }
 // L2 flush by reading (the lines it leaves are clean, so the next kernel's
 // DRAM bandwidth is not shared with write-backs)
@@ -1187,7 +1189,7 @@ void launch_build_csc_list(int* colptr, int* cscrow, T* cscval, const int64_t* r
   template void launch_mtw_dense<T>(double*, int, const Window&, const T*, int64_t, int,          \
                                     const double*, const Ctl*, cudaStream_t);                    \
   template void launch_mtw_csc<T>(double*, const Window&, const int*, int, const int*, const T*,  \
-                                  const int64_t*, const double*, const Ctl*, cudaStream_t);      \
+                                  const int64_t*, const double*, const Ctl*, cudaStream_t, int); \
   template void launch_build_csc<T>(int*, int*, T*, const int64_t*, const int*, const T*,         \
                                     const int64_t*, int64_t, int, int, int64_t, cudaStream_t,     \
                                     int64_t, int64_t);                                            \

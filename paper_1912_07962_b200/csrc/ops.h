@@ -75,7 +75,12 @@ void launch_mtw_dense(double* part, int nsplit, const Window& W, const T* A, int
 template <typename T>
 void launch_mtw_csc(double* s_out, const Window& W, const int* colptr, int n, const int* cscrow,
                     const T* cscval, const int64_t* blkbase, const double* w, const Ctl* ctl,
-                    cudaStream_t s);
+                    cudaStream_t s, int quad = 0);
+// M^T w kernel variant for a CSR operator: 0 = one column per thread, 3 =
+// four columns per thread with eight entries per block prefetched (dense
+// enough columns, n large enough to fill the GPU at n / 4 threads);
+// SLIM_MTW_QUAD=<v> overrides
+int mtw_variant(int64_t n, double nnz_per_block);
 // block list for the batched per-block CSC build of a streamed batch
 struct BlkList {
   int n;
@@ -94,7 +99,7 @@ void launch_finish(const FinishParams& F, cudaStream_t s);
 template <typename T>
 void launch_mtw_finish_csc(const FinishParams& F, const Window& W, const int* colptr,
                            const int* cscrow, const T* cscval, const int64_t* blkbase,
-                           const double* w, cudaStream_t s);
+                           const double* w, cudaStream_t s, int quad = 0);
 void launch_gram_reduce(double* panel, const Window& W, const double* part, int nsplit,
                         cudaStream_t s);
 void launch_gram_diag_fp64(double* panel_diag, int64_t ld, const float* A, int ell, int n,
