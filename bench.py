@@ -100,20 +100,26 @@ DTYPE_NOTE = ("fp64 iterates, Gram and solves; the dual-system Cholesky's tile u
               "bits below each row's scale), POTRF/TRSM in fp64 DMMA")
 
 
-def build_config(cfg_id, threads=None, world=1):
-    """(op, b, x_true) of a BASELINE config at full size."""
+TOMO_N = {2: 256 ** 2, 3: 1024 ** 2, 4: 128 ** 3}
+
+
+def build_config(cfg_id, threads=None, world=1, col_range=None):
+    """(op, b, x_true) of a BASELINE config at full size; for the tomography
+    configs ``col_range`` keeps only that column shard of the operator (built
+    view by view: a rank never holds the whole 7.7 GB of configs[2])."""
     from paper_1912_07962_b200 import problems
 
     if cfg_id == 1:
         return problems.gaussian_dense()
     if cfg_id == 2:
-        p = problems.tomo2d(grid=256, n_views=180, rays=362, seed=2, threads=threads)
+        p = problems.tomo2d(grid=256, n_views=180, rays=362, seed=2, threads=threads,
+                            col_range=col_range)
     elif cfg_id == 3:
         p = problems.tomo2d(grid=1024, n_views=720, rays=1448, seed=3, dtype=np.float32,
-                            threads=threads)
+                            threads=threads, col_range=col_range)
     elif cfg_id == 4:
         p = problems.tomo3d(grid=128, n_views=180, side=128, sub_rows=2048, seed=4,
-                            threads=threads)
+                            threads=threads, col_range=col_range)
     elif cfg_id == 5:
         return problems.generated_dense()
     else:
@@ -637,7 +643,14 @@ def run_ours(args, world, rank, local, dist):
         os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines for the driver's log
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
-    op, b, xt = build_config(cfg_id, world=world)
+    presliced = sharded and cfg_id in TOMO_N
+    if presliced:
+        from paper_1912_07962_b200.parallel import column_ranges
+        c0, c1 = column_ranges(TOMO_N[cfg_id], world)[rank]
+        op, b, xt_full = build_config(cfg_id, world=world, col_range=(c0, c1))
+        xt = np.ascontiguousarray(xt_full[c0:c1])
+    else:
+        op, b, xt = build_config(cfg_id, world=world)
     r, alpha, scheme = cfg["r"], cfg["alpha"], cfg["scheme"]
     ell, M = op.block_rows, op.n_blocks
     seed = SAMPLER_SEED + (0 if sharded else rank)
@@ -654,7 +667,10 @@ def run_ours(args, world, rank, local, dist):
         import torch
 
         torch.cuda.set_device(dev)
-        shard = NcclShard.from_torch(op.n_cols, round_robin=args.factor == "round_robin")
+        n_full = TOMO_N[cfg_id] if presliced else op.n_cols
+        shard = NcclShard.from_torch(n_full, round_robin=args.factor == "round_robin")
+        if presliced:
+            shard = _PreSliced(shard, n_full)  # the operator holds this rank's columns only
     else:
         shard = None
 
@@ -728,7 +744,8 @@ def run_ours(args, world, rank, local, dist):
                 "gram": timing["gram_ms"] / max(1, timing["gram_count"]),
                 "cholesky_launch": roofline["avg_launch_ms"],
                 "x_chain": timing["x_chain_ms"] / max(1, timing["x_chain_count"])},
-            "final_rel_err_x_true": float(traj.rel_errors["x_true"][-1])}
+            # (a pre-sliced shard normalises by its local ||x_true||: not reported)
+            "final_rel_err_x_true": None if presliced else float(traj.rel_errors["x_true"][-1])}
     print(json.dumps(line), flush=True)
 
 
@@ -751,7 +768,8 @@ def _e2e_leg(slim, args, op, b, xt, r, alpha, total, M, sampler, dev, dist, shar
 
     generated = hasattr(op, "seed")
     src_op, refs = op, {"x_true": xt}
-    if shard is not None and not generated:
+    presliced = isinstance(shard, _PreSliced)
+    if shard is not None and not generated and not presliced:
         from paper_1912_07962_b200.parallel import shard_operator
         src_op = shard_operator(op, shard.col0, shard.col1)
         refs = {"x_true": np.ascontiguousarray(xt[shard.col0:shard.col1])}
@@ -762,9 +780,10 @@ def _e2e_leg(slim, args, op, b, xt, r, alpha, total, M, sampler, dev, dist, shar
         sh2 = None
         if shard is not None:
             from paper_1912_07962_b200.parallel import NcclShard
-            sh2 = NcclShard.from_torch(op.n_cols, round_robin=getattr(shard, "round_robin", False))
+            n_full = shard.n_full if presliced else op.n_cols
+            sh2 = NcclShard.from_torch(n_full, round_robin=getattr(shard, "round_robin", False))
             if not generated:
-                sh2 = _PreSliced(sh2)
+                sh2 = _PreSliced(sh2, n_full)
         _barrier(dist)
         t0 = time.perf_counter()
         tr2 = slim.run("slimls", op2, sampler(), slim.Schedule("constant", alpha),
@@ -801,8 +820,9 @@ def _e2e_leg(slim, args, op, b, xt, r, alpha, total, M, sampler, dev, dist, shar
 class _PreSliced:
     """Shard wrapper for an operator that is already this shard's column slice."""
 
-    def __init__(self, shard):
+    def __init__(self, shard, n_full=None):
         self._shard = shard
+        self.n_full = n_full  # columns of the whole problem
         self.col0, self.col1 = 0, shard.col1 - shard.col0
         self.rank, self.nranks = shard.rank, shard.nranks
         self.round_robin = getattr(shard, "round_robin", False)

@@ -162,6 +162,25 @@ def _finish_tomo(parts, x_true, noise, seed, dtype):
     return TomoProblem(op, b, x_true)
 
 
+def _finish_tomo_columns(view_fn, items, split_fn, x_true, noise, seed, dtype, c0, c1,
+                         threads=None, chunk=32):
+    """Column shard [c0, c1) of a tomography operator, built view by view so a
+    rank never holds the whole operator: each view's rows are projected on
+    x_true (the same clean data and noise as the unsharded problem, so b is
+    bit-identical) and only the shard's columns are kept."""
+    from .parallel import slice_csr_columns
+
+    blocks, clean = [], []
+    for v0 in range(0, len(items), chunk):
+        for part in _pmap(view_fn, items[v0:v0 + chunk], threads):
+            for ip, ix, d, shp in split_fn(v0, part):
+                d = d.astype(dtype)
+                clean.append(_csr_matvec(ip, ix, d.astype(np.float64), x_true))
+                blocks.append(slice_csr_columns(ip, ix, d, shp, c0, c1))
+    b = scaled_noise(np.concatenate(clean), noise, _rng(seed + 1))
+    return TomoProblem(SparseBlockOperator(blocks, b, dtype=dtype), b, x_true)
+
+
 def _csr_matvec(indptr, indices, data, x):
     import scipy.sparse as sp
 
@@ -170,11 +189,16 @@ def _csr_matvec(indptr, indices, data, x):
 
 
 def tomo2d(grid=256, n_views=180, rays=362, ellipses=10, seed=2, noise=0.01,
-           dtype=np.float64, threads=None) -> TomoProblem:
-    """configs[1] / configs[2]: one block per view, ell = rays."""
+           dtype=np.float64, threads=None, col_range=None) -> TomoProblem:
+    """configs[1] / configs[2]: one block per view, ell = rays.  ``col_range``
+    = (c0, c1): only that column shard is kept (b and x_true stay whole)."""
     angles = angles_0_pi(n_views)
-    parts = _pmap(lambda a: siddon2d_block(a, grid, rays), list(angles), threads)
     x_true = random_ellipses(grid, ellipses, seed)
+    view = lambda a: siddon2d_block(a, grid, rays)  # noqa: E731
+    if col_range is not None:
+        return _finish_tomo_columns(view, list(angles), lambda v0, part: [part], x_true, noise,
+                                    seed, dtype, *col_range, threads=threads)
+    parts = _pmap(view, list(angles), threads)
     return _finish_tomo(parts, x_true, noise, seed, dtype)
 
 
@@ -207,29 +231,55 @@ def projector_config(cfg_id: int):
     raise ValueError(f"config {cfg_id} is not a tomography config")
 
 
+def _split_view_3d(part, perm, sub_rows):
+    """One 3D view's rows in the seeded order, cut into sub_rows-row blocks."""
+    ip, ix, d, (nr, nc) = part
+    counts = np.diff(ip)[perm]
+    starts = ip[:-1][perm]
+    out = []
+    for s in range(0, nr, sub_rows):
+        sel_c = counts[s:s + sub_rows]
+        sel_s = starts[s:s + sub_rows]
+        nip = np.zeros(sub_rows + 1, dtype=np.int64)
+        np.cumsum(sel_c, out=nip[1:])
+        gather = np.concatenate([np.arange(a, a + c) for a, c in zip(sel_s, sel_c)]) \
+            if sel_c.sum() else np.zeros(0, dtype=np.int64)
+        out.append((nip, ix[gather], d[gather], (sub_rows, nc)))
+    return out
+
+
 def tomo3d(grid=128, n_views=180, side=128, sub_rows=2048, ellipsoids=20, seed=4,
-           noise=0.01, dtype=np.float32, threads=None) -> TomoProblem:
+           noise=0.01, dtype=np.float32, threads=None, col_range=None) -> TomoProblem:
     """configs[3]: directions in the xy-plane over [0, pi); each view's
     side^2 rays split into side^2 / sub_rows contiguous blocks after a
-    seeded per-view row permutation (uniform partition, linops.py:64-72)."""
+    seeded per-view row permutation (uniform partition, linops.py:64-72).
+    ``col_range`` = (c0, c1): only that column shard is kept."""
     dirs, ray_of_row = tomo3d_geometry(n_views, side, sub_rows, seed)
-    parts = _pmap(lambda d: siddon3d_block(d, grid, side), list(dirs), threads)
-    blocks = []
     rows = side * side
-    for v, (ip, ix, d, (nr, nc)) in enumerate(parts):
-        perm = ray_of_row[v * rows:(v + 1) * rows]
-        counts = np.diff(ip)[perm]
-        starts = ip[:-1][perm]
-        for s in range(0, nr, sub_rows):
-            sel_c = counts[s:s + sub_rows]
-            sel_s = starts[s:s + sub_rows]
-            nip = np.zeros(sub_rows + 1, dtype=np.int64)
-            np.cumsum(sel_c, out=nip[1:])
-            gather = np.concatenate([np.arange(a, a + c) for a, c in zip(sel_s, sel_c)]) \
-                if sel_c.sum() else np.zeros(0, dtype=np.int64)
-            blocks.append((nip, ix[gather], d[gather], (sub_rows, nc)))
     x_true = random_ellipsoids(grid, ellipsoids, seed)
+    view = lambda d: siddon3d_block(d, grid, side)  # noqa: E731
+    if col_range is not None:
+        return _finish_tomo_columns(view, list(dirs), _Counter3d(ray_of_row, rows, sub_rows),
+                                    x_true, noise, seed, dtype, *col_range, threads=threads)
+    parts = _pmap(view, list(dirs), threads)
+    blocks = []
+    for v, part in enumerate(parts):
+        blocks += _split_view_3d(part, ray_of_row[v * rows:(v + 1) * rows], sub_rows)
     return _finish_tomo(blocks, x_true, noise, seed, dtype)
+
+
+class _Counter3d:
+    """split_fn for the view-by-view builder: views arrive in order, so the
+    view index is a running count."""
+
+    def __init__(self, ray_of_row, rows, sub_rows):
+        self.ray_of_row, self.rows, self.sub_rows, self.v = ray_of_row, rows, sub_rows, 0
+
+    def __call__(self, v0, part):
+        v = self.v
+        self.v += 1
+        return _split_view_3d(part, self.ray_of_row[v * self.rows:(v + 1) * self.rows],
+                              self.sub_rows)
 
 
 # ---------------------------------------------------------------------------
