@@ -682,6 +682,11 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
     int parts = gs;
     if (c->use_tc) parts = std::max<int>(parts, (int)(c->n / gram_tc_kchunk(c->n, 1)));
     ALLOC(c, c->gpart, sizeof(double) * (size_t)parts * Nmax * ell);
+  } else {
+    // CSR Gram: per-column records + row exponents of the newest block (fixed-point
+    // k_gram_csr_fx); SLIM_GRAM_LUT=0 keeps the fp64 pointer-chasing kernel for A/B
+    const char* env = getenv("SLIM_GRAM_LUT");
+    if (!(env && env[0] == '0')) ALLOC(c, c->gpart, gram_lut_bytes((int)c->n, (int)ell));
   }
   ALLOC(c, c->spart, sizeof(double) * (size_t)c->nsplit_mtw * c->n);
   ALLOC(c, c->fpart, sizeof(double) * (size_t)finish_grid((int)c->n) * (1 + MAX_REFS));
@@ -1540,11 +1545,12 @@ static int enqueue_gram(slim_ctx* c, const Window& W, int64_t k, int64_t real_bl
     const int* cpn = c->colptr + newblk * csc_stride((int)c->n);
     const int64_t base = c->h_blkbase[newblk];
     if (c->vdt == SLIM_F64)
-      c->launches += 1, launch_gram_csr<double>(panel, W, c->rowptr, c->col, (const double*)c->val, cpn, c->cscrow,
-                              (const double*)c->cscval, base, c->sg);
+      launch_gram_csr<double>(panel, W, c->rowptr, c->col, (const double*)c->val, cpn, c->cscrow,
+                              (const double*)c->cscval, base, c->sg, c->gpart, (int)c->n);
     else
-      c->launches += 1, launch_gram_csr<float>(panel, W, c->rowptr, c->col, (const float*)c->val, cpn, c->cscrow,
-                             (const float*)c->cscval, base, c->sg);
+      launch_gram_csr<float>(panel, W, c->rowptr, c->col, (const float*)c->val, cpn, c->cscrow,
+                             (const float*)c->cscval, base, c->sg, c->gpart, (int)c->n);
+    c->launches += c->gpart ? 3 : 1;
   }
   (void)k;
   CKLAUNCH(c);
@@ -2494,10 +2500,10 @@ extern "C" int slim_probe_stream(slim_ctx* c, int32_t kernel, int32_t reps, doub
         const int* cpn = c->colptr + nb * csc_stride((int)c->n);
         if (vb == 8)
           launch_gram_csr<double>(panel, W, c->rowptr, c->col, (const double*)c->val, cpn, c->cscrow,
-                                  (const double*)c->cscval, c->h_blkbase[nb], s);
+                                  (const double*)c->cscval, c->h_blkbase[nb], s, c->gpart, n);
         else
           launch_gram_csr<float>(panel, W, c->rowptr, c->col, (const float*)c->val, cpn, c->cscrow,
-                                 (const float*)c->cscval, c->h_blkbase[nb], s);
+                                 (const float*)c->cscval, c->h_blkbase[nb], s, c->gpart, n);
       } else {
         bytes = (double)N * n * vb + 8.0 * N * ell * (1 + c->nsplit_gram);
         if (vb == 8)

@@ -185,9 +185,15 @@ __global__ void __launch_bounds__(256) k_gen_apply(double* __restrict__ out, uin
   if (lane == 0) out[row] = s;
 }
 
-// one CTA (RES_THREADS) per row, four independent nonzeros in flight per
-// thread; partial sums added in a fixed order (deterministic)
+// one CTA (RES_THREADS) per row, four interleaved partial sums per thread
+// added in a fixed order (deterministic).  Rows of up to RES_PRE * RES_THREADS
+// nonzeros (every ray of the tomography configs) load ALL their (column,
+// value) pairs first and then gather x for all of them, so a row costs three
+// dependent memory latencies (row pointer, entries, x) instead of two per
+// group of four; the sums are formed in exactly the order of the loop below,
+// which longer rows still take.
 constexpr int RES_THREADS = 128;
+constexpr int RES_PRE = 12;
 template <typename T>
 __global__ void __launch_bounds__(RES_THREADS) k_residual_csr(double* r, const int64_t* __restrict__ rowptr,
                                                       const int* __restrict__ col,
@@ -196,23 +202,53 @@ __global__ void __launch_bounds__(RES_THREADS) k_residual_csr(double* r, const i
                                                       const double* __restrict__ x,
                                                       const double* __restrict__ b,
                                                       const Ctl* ctl) {
-  if (ctl->diverged_at != 0) return;
   const int row = blockIdx.x, tid = threadIdx.x;
   const int64_t lo = rowptr[row0 + row], hi = rowptr[row0 + row + 1];
+  const double bv = b[brow0 + row];
+  if (ctl->diverged_at != 0) return;
   constexpr int S = RES_THREADS;
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-  int64_t e = lo + tid;
-  for (; e + 3 * S < hi; e += 4 * S) {
-    const int k0 = __ldcs(col + e), k1 = __ldcs(col + e + S), k2 = __ldcs(col + e + 2 * S),
-              k3 = __ldcs(col + e + 3 * S);
-    const double v0 = to_f64(__ldcs(val + e)), v1 = to_f64(__ldcs(val + e + S)),
-                 v2 = to_f64(__ldcs(val + e + 2 * S)), v3 = to_f64(__ldcs(val + e + 3 * S));
-    s0 = fma(v0, __ldg(x + k0), s0);
-    s1 = fma(v1, __ldg(x + k1), s1);
-    s2 = fma(v2, __ldg(x + k2), s2);
-    s3 = fma(v3, __ldg(x + k3), s3);
+  if (hi - lo <= (int64_t)RES_PRE * S) {
+    const int64_t e0 = lo + tid;
+    int k[RES_PRE];
+    T v[RES_PRE];
+    double xv[RES_PRE];
+#pragma unroll
+    for (int u = 0; u < RES_PRE; ++u) {
+      const bool ok = e0 + u * S < hi;
+      k[u] = ok ? __ldcs(col + e0 + u * S) : 0;
+      v[u] = ok ? __ldcs(val + e0 + u * S) : T(0);
+    }
+#pragma unroll
+    for (int u = 0; u < RES_PRE; ++u) xv[u] = (e0 + u * S < hi) ? __ldg(x + k[u]) : 0.0;
+    // whole groups of four go to s0..s3, the remaining entries to s0
+    int done = 0;
+#pragma unroll
+    for (int g = 0; g < RES_PRE / 4; ++g)
+      if (done == 4 * g && e0 + (4 * g + 3) * S < hi) {
+        s0 = fma(to_f64(v[4 * g]), xv[4 * g], s0);
+        s1 = fma(to_f64(v[4 * g + 1]), xv[4 * g + 1], s1);
+        s2 = fma(to_f64(v[4 * g + 2]), xv[4 * g + 2], s2);
+        s3 = fma(to_f64(v[4 * g + 3]), xv[4 * g + 3], s3);
+        done = 4 * g + 4;
+      }
+#pragma unroll
+    for (int u = 0; u < RES_PRE; ++u)
+      if (u >= done && e0 + u * S < hi) s0 = fma(to_f64(v[u]), xv[u], s0);
+  } else {
+    int64_t e = lo + tid;
+    for (; e + 3 * S < hi; e += 4 * S) {
+      const int k0 = __ldcs(col + e), k1 = __ldcs(col + e + S), k2 = __ldcs(col + e + 2 * S),
+                k3 = __ldcs(col + e + 3 * S);
+      const double v0 = to_f64(__ldcs(val + e)), v1 = to_f64(__ldcs(val + e + S)),
+                   v2 = to_f64(__ldcs(val + e + 2 * S)), v3 = to_f64(__ldcs(val + e + 3 * S));
+      s0 = fma(v0, __ldg(x + k0), s0);
+      s1 = fma(v1, __ldg(x + k1), s1);
+      s2 = fma(v2, __ldg(x + k2), s2);
+      s3 = fma(v3, __ldg(x + k3), s3);
+    }
+    for (; e < hi; e += S) s0 = fma(to_f64(val[e]), x[col[e]], s0);
   }
-  for (; e < hi; e += S) s0 = fma(to_f64(val[e]), x[col[e]], s0);
   const double sv = warp_sum((s0 + s1) + (s2 + s3));
   __shared__ double ws[S / 32];
   if ((tid & 31) == 0) ws[tid >> 5] = sv;
@@ -221,7 +257,7 @@ __global__ void __launch_bounds__(RES_THREADS) k_residual_csr(double* r, const i
     double t = 0.0;
 #pragma unroll
     for (int w = 0; w < S / 32; ++w) t += ws[w];
-    r[row] = t - b[brow0 + row];
+    r[row] = t - bv;
   }
 }
 
@@ -304,6 +340,302 @@ __global__ void __launch_bounds__(128) k_gram_csr(double* __restrict__ panel, Wi
   double* out = panel + ((int64_t)P * ell + a) * ell;  // panels are indexed by window position
   for (int j = threadIdx.x; j < ell; j += 128)
     out[j] = (gacc[j] + gacc[ell + j]) + (gacc[2 * ell + j] + gacc[3 * ell + j]);
+}
+
+// ---------------------------------------------------------------------------
+// CSR Gram, round 2: per-column records + exact fixed-point accumulation.
+//
+// ncu of k_gram_csr: 10 warp instructions per nonzero, warps stalled on the
+// match_any / shuffle / shared-memory chain that keeps the sums in a fixed
+// order (short scoreboard 4.3, wait 2.5 per issue), not on memory.  Two
+// changes:
+//
+// * k_gram_lut packs every column of the new block into ONE record (entry
+//   count, the rows of its first two entries in 16 bits each, their values),
+//   so a nonzero of a window row costs one gather instead of the chain
+//   column pointer -> row index / value.  Ray geometry never has more than
+//   two entries per column and view; longer columns fall back to the CSC
+//   arrays for the entries past the second.
+//
+// * Products are accumulated as 64-bit integers.  With 2^ea >= 2 ||A_P[a]||_2
+//   (computed by the CTA from the row it just loaded) and 2^ej >= 2 ||A_k[j]||_2
+//   (k_gram_rowexp; the record values are pre-scaled by 2^-ej, exactly), every
+//   partial sum of a panel entry is below 2^60 quanta of 2^(ea + ej - 62) by
+//   Cauchy-Schwarz.  Integer addition is associative, so the result does not
+//   depend on the order in which threads add -- no grouping, no per-warp
+//   copies of the row -- and it is deterministic like the rest of the path.
+//   Each product is rounded once to 2^-62 of ||a|| ||b||, below the
+//   gamma_n |a|.|b| error bound of an fp64 dot product of the same rows.
+// ---------------------------------------------------------------------------
+template <typename T>
+struct GramRec;
+template <>
+struct __align__(16) GramRec<float> {
+  int cnt;
+  unsigned j01;  // row of entry 0 | row of entry 1 << 16
+  float v0, v1;  // values scaled by 2^-e(row)
+};
+template <>
+struct __align__(32) GramRec<double> {
+  int cnt;
+  unsigned j01;
+  double v0, v1;
+  double pad;
+};
+__device__ __forceinline__ float scale_pow2(float v, int e) { return ldexpf(v, e); }
+__device__ __forceinline__ double scale_pow2(double v, int e) { return ldexp(v, e); }
+// exponent e with 2^e >= 2 sqrt(ss) (0 for an empty row): with b = floor(log2 ss) from
+// the exponent field, sqrt(ss) < 2^ceil((b + 1) / 2)
+__device__ __forceinline__ int norm_exp(double ss) {
+  if (!(ss > 0.0)) return 0;
+  const int bexp = (__double2hiint(ss) >> 20) & 0x7ff;
+  const int b = bexp ? bexp - 1023 : ilogb(ss);  // subnormal sums take the slow path
+  return ((b + 2) >> 1) + 1;
+}
+
+// one warp per row of the new block: rowexp[j] = norm_exp(||A_k[j]||^2)
+template <typename T>
+__global__ void __launch_bounds__(256) k_gram_rowexp(int* __restrict__ rowexp,
+                                                     const int64_t* __restrict__ rowptr,
+                                                     const T* __restrict__ val, int64_t row0,
+                                                     int ell) {
+  const int j = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (j >= ell) return;
+  const int64_t lo = rowptr[row0 + j], hi = rowptr[row0 + j + 1];
+  double ss = 0.0;
+  for (int64_t e = lo + lane; e < hi; e += 32) {
+    const double v = to_f64(__ldg(val + e));
+    ss = fma(v, v, ss);
+  }
+  ss = warp_sum(ss);
+  if (lane == 0) rowexp[j] = norm_exp(ss);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_gram_lut(GramRec<T>* __restrict__ lut,
+                                                  const int* __restrict__ rowexp,
+                                                  const int* __restrict__ colptr_new,
+                                                  const int* __restrict__ cscrow,
+                                                  const T* __restrict__ cscval, int64_t base_new,
+                                                  int n) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const int cs = colptr_new[c], cnt = colptr_new[c + 1] - cs;
+  GramRec<T> rec{};
+  rec.cnt = cnt;
+  if (cnt > 0) {
+    const int j = cscrow[base_new + cs];
+    rec.j01 = (unsigned)j;
+    rec.v0 = scale_pow2(cscval[base_new + cs], -rowexp[j]);
+  }
+  if (cnt > 1) {
+    const int j = cscrow[base_new + cs + 1];
+    rec.j01 |= (unsigned)j << 16;
+    rec.v1 = scale_pow2(cscval[base_new + cs + 1], -rowexp[j]);
+  }
+  lut[c] = rec;
+}
+
+__device__ __forceinline__ GramRec<float> ld_rec(const GramRec<float>* p) {
+  const int4 q = __ldg(reinterpret_cast<const int4*>(p));
+  GramRec<float> r;
+  r.cnt = q.x;
+  r.j01 = (unsigned)q.y;
+  r.v0 = __int_as_float(q.z);
+  r.v1 = __int_as_float(q.w);
+  return r;
+}
+__device__ __forceinline__ GramRec<double> ld_rec(const GramRec<double>* p) {
+  const int4 a = __ldg(reinterpret_cast<const int4*>(p));
+  const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+  GramRec<double> r;
+  r.cnt = a.x;
+  r.j01 = (unsigned)a.y;
+  r.v0 = __hiloint2double(a.w, a.z);
+  r.v1 = b.x;
+  return r;
+}
+
+constexpr int GFX_THREADS = 256;
+constexpr int GFX_K = 6;  // nonzeros per thread and chunk (rows of <= 1536 nonzeros: one chunk)
+
+// acc[j] += d for a 64-bit two's-complement d, with the accumulator held as
+// two 32-bit words: shared memory has native 32-bit integer atomics only
+// (a 64-bit atomicAdd compiles to a compare-and-swap spin loop, ~70 shared
+// memory wavefronts per warp-level add under ncu).  The low word's add returns
+// the old value, which tells THIS add's carry; carries are added to the high
+// word with the addend's own high part.  The total is sum(d) mod 2^64 in any
+// order of arrival.
+__device__ __forceinline__ void fx_add(unsigned* lo, unsigned* hi, int j, long long d) {
+  const unsigned dl = (unsigned)(unsigned long long)d, dh = (unsigned)((unsigned long long)d >> 32);
+  const unsigned old = atomicAdd(lo + j, dl);
+  const unsigned carry = (old + dl < old) ? 1u : 0u;
+  if (dh + carry != 0u) atomicAdd(hi + j, dh + carry);
+}
+
+// 2^e as a double for any e in the normal range (callers keep it there)
+__device__ __forceinline__ double pow2_double(int e) { return __hiloint2double((1023 + e) << 20, 0); }
+__device__ __forceinline__ double pow2_any(int e) {
+  return (e > -1000 && e < 1000) ? pow2_double(e) : ldexp(1.0, e);
+}
+
+// Persistent CTAs, each taking window rows blockIdx.x, + gridDim.x, ...; acc[j]
+// (64-bit integers as two words) in shared memory.  A thread takes GFX_K
+// ADJACENT nonzeros of the row: neighbours along a ray meet the same ray of
+// the new view, so their products are first merged in registers (integer
+// adds, any grouping gives the same total) and roughly half the shared-memory
+// atomics go away.  While a row is processed, the row pointer of the CTA's
+// next row is fetched and its (column, value) lines are prefetched into L2.
+template <typename T>
+__global__ void __launch_bounds__(GFX_THREADS, 4) k_gram_csr_fx(double* __restrict__ panel, Window W,
+                                                                const int64_t* __restrict__ rowptr,
+                                                                const int* __restrict__ col,
+                                                                const T* __restrict__ val,
+                                                                const GramRec<T>* __restrict__ lut,
+                                                                const int* __restrict__ rowexp,
+                                                                const int* __restrict__ colptr_new,
+                                                                const int* __restrict__ cscrow,
+                                                                const T* __restrict__ cscval,
+                                                                int64_t base_new) {
+  extern __shared__ __align__(16) unsigned facc[];
+  __shared__ double red[2][GFX_THREADS / 32];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ell = W.ell, nrows = W.nw * ell;
+  unsigned* flo = facc;
+  unsigned* fhi = facc + ell;
+  constexpr int S = GFX_THREADS, CH = GFX_K * GFX_THREADS;
+  auto global_row = [&](int r) {
+    const int P = r / ell;
+    return (int64_t)W.blk[P] * ell + (r - P * ell);
+  };
+  int r = blockIdx.x;
+  if (r >= nrows) return;
+  int64_t rlo, rhi;
+  {
+    const int64_t g = global_row(r);
+    rlo = rowptr[g];
+    rhi = rowptr[g + 1];
+  }
+  for (int it = 0; r < nrows; r += gridDim.x, ++it) {
+    // next row of this CTA: row pointer now, its lines into L2
+    const int rn = r + gridDim.x;
+    int64_t nlo = 0, nhi = 0;
+    if (rn < nrows) {
+      const int64_t g = global_row(rn);
+      nlo = rowptr[g];
+      nhi = rowptr[g + 1];
+    }
+    int cc[GFX_K];
+    T vv[GFX_K];
+    {
+      const int64_t e0 = rlo + (int64_t)tid * GFX_K;
+#pragma unroll
+      for (int u = 0; u < GFX_K; ++u) {
+        cc[u] = -1;
+        vv[u] = T(0);
+        if (e0 + u < rhi) {
+          cc[u] = __ldcs(col + e0 + u);
+          vv[u] = __ldcs(val + e0 + u);
+        }
+      }
+    }
+    {  // 2 ell words, 16 bytes at a time (ell even is the common case)
+      uint4* z = reinterpret_cast<uint4*>(facc);
+      const int n4 = (2 * ell) >> 2;
+      for (int j = tid; j < n4; j += S) z[j] = make_uint4(0u, 0u, 0u, 0u);
+      for (int j = 4 * n4 + tid; j < 2 * ell; j += S) facc[j] = 0u;
+    }
+    if (rn < nrows) {
+      // 128-byte lines of col[nlo, nhi) and val[nlo, nhi)
+      const char* c0 = reinterpret_cast<const char*>(col + nlo);
+      const char* c1 = reinterpret_cast<const char*>(col + nhi);
+      for (const char* p = c0 + (size_t)tid * 128; p < c1; p += (size_t)S * 128)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+      const char* v0 = reinterpret_cast<const char*>(val + nlo);
+      const char* v1 = reinterpret_cast<const char*>(val + nhi);
+      for (const char* p = v0 + (size_t)tid * 128; p < v1; p += (size_t)S * 128)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+    }
+    // ||row||^2 in a fixed order: per thread, warp shuffle tree, warps in order
+    double ss = 0.0;
+#pragma unroll
+    for (int u = 0; u < GFX_K; ++u) ss = fma(to_f64(vv[u]), to_f64(vv[u]), ss);
+    for (int64_t e = rlo + CH + tid; e < rhi; e += S) {
+      const double v = to_f64(__ldg(val + e));
+      ss = fma(v, v, ss);
+    }
+    ss = warp_sum(ss);
+    if (lane == 0) red[it & 1][warp] = ss;
+    __syncthreads();  // also: acc zeroed, and the previous row's output loop is done
+    double tot = 0.0;
+#pragma unroll
+    for (int w = 0; w < S / 32; ++w) tot += red[it & 1][w];
+    const int ea = norm_exp(tot);
+    const double scale = pow2_any(62 - ea);
+    for (int64_t base = rlo; base < rhi; base += CH) {
+      if (base != rlo) {
+        const int64_t e0 = base + (int64_t)tid * GFX_K;
+#pragma unroll
+        for (int u = 0; u < GFX_K; ++u) {
+          cc[u] = -1;
+          vv[u] = T(0);
+          if (e0 + u < rhi) {
+            cc[u] = __ldcs(col + e0 + u);
+            vv[u] = __ldcs(val + e0 + u);
+          }
+        }
+      }
+      GramRec<T> rec[GFX_K];
+#pragma unroll
+      for (int u = 0; u < GFX_K; ++u) {
+        rec[u].cnt = 0;
+        if (cc[u] >= 0) rec[u] = ld_rec(lut + cc[u]);
+      }
+      // entries 0 and 1 of each column: runs of equal rows merged in registers
+#pragma unroll
+      for (int sl = 0; sl < 2; ++sl) {
+        int curj = -1;
+        long long cur = 0;
+#pragma unroll
+        for (int u = 0; u < GFX_K; ++u)
+          if (rec[u].cnt > sl) {
+            const int j = sl == 0 ? (int)(rec[u].j01 & 0xffffu) : (int)(rec[u].j01 >> 16);
+            const double uv = to_f64(sl == 0 ? rec[u].v0 : rec[u].v1);
+            const long long d = __double2ll_rn(to_f64(vv[u]) * scale * uv);
+            if (j == curj) {
+              cur += d;
+            } else {
+              if (curj >= 0) fx_add(flo, fhi, curj, cur);
+              curj = j;
+              cur = d;
+            }
+          }
+        if (curj >= 0) fx_add(flo, fhi, curj, cur);
+      }
+#pragma unroll
+      for (int u = 0; u < GFX_K; ++u)
+        if (rec[u].cnt > 2) {  // a column with more than two entries: the CSC arrays
+          const int64_t q0 = base_new + colptr_new[cc[u]];
+          for (int t = 2; t < rec[u].cnt; ++t) {
+            const int j = cscrow[q0 + t];
+            const double uv = ldexp(to_f64(cscval[q0 + t]), -rowexp[j]);
+            fx_add(flo, fhi, j, __double2ll_rn(to_f64(vv[u]) * scale * uv));
+          }
+        }
+    }
+    __syncthreads();
+    const int P = r / ell;
+    double* out = panel + ((int64_t)P * ell + (r - P * ell)) * ell;  // indexed by window position
+    for (int j = tid; j < ell; j += S) {
+      // (int)hi 2^32 + lo, rounded once: the correctly rounded 64-bit integer
+      const double qd = fma((double)(int)fhi[j], 4294967296.0, (double)flo[j]);
+      const int e = ea + __ldg(rowexp + j) - 62;
+      out[j] = (e > -1000 && e < 1000) ? qd * pow2_double(e) : ldexp(qd, e);
+    }
+    __syncthreads();  // acc is zeroed again at the top
+    rlo = nlo;
+    rhi = nhi;
+  }
 }
 
 // Dense: DMMA tile GEMM, 64 window rows x 64 new rows per CTA, split-K over
@@ -742,6 +1074,191 @@ __global__ void __launch_bounds__(256) k_mtw_csc4(double* __restrict__ s_out, Wi
   }
 }
 
+// ---------------------------------------------------------------------------
+// M^T w with warp-staged, asynchronously prefetched entries (round 2, variant 6).
+//
+// ncu of the four-column kernel: 2.5 TB/s with the warps waiting on their own
+// loads (long scoreboard) -- every byte in flight needs a destination
+// register, and a lane walks its ~5 entries per block one dependent gather
+// at a time.  Here a warp owns 128 consecutive columns (four per lane).  Per
+// window block it reads their column pointers with one 16-byte load per lane.
+// The warp's entries of that block are CONTIGUOUS in the block's CSC, so they
+// are copied entry-parallel straight into shared memory with cp.async, two
+// blocks ahead of the one being summed (the bytes in flight sit in shared
+// memory, not registers).  When a block's entries have landed the lanes
+// gather w[row] entry-parallel (neighbouring entries hit neighbouring rows)
+// and each lane sums its four columns out of shared memory: two unrolled
+// entries per column and a loop for longer ones.  A range longer than MS_CAP
+// entries takes the direct global path for that block (warp-uniform).  Per
+// column the sums still run block by block and entry by entry with the same
+// fma chain, so s is bit-identical to the other variants.
+// ---------------------------------------------------------------------------
+constexpr int MS_CAP = 192;  // staged entries per warp and block
+constexpr int MS_EPL = MS_CAP / 32;
+constexpr int MS_NB = 3;     // entry buffers per warp (prefetch distance 2)
+template <typename T>
+constexpr size_t mtw_stage_smem() {
+  return (size_t)8 * MS_CAP * (sizeof(double) + MS_NB * (sizeof(int) + sizeof(T)));
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+               "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+               "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_val(float* smem, const float* gmem) { cp_async4(smem, gmem); }
+__device__ __forceinline__ void cp_async_val(double* smem, const double* gmem) { cp_async8(smem, gmem); }
+
+// column pointers of one block for this lane's four columns
+struct MtwCols {
+  int4 q;
+  int nx;        // lane 31: the pointer after its last column
+  int64_t base;  // first entry of the block in cscrow / cscval
+};
+
+template <typename T>
+__device__ __forceinline__ void mtw_csc_stage(int c0, bool valid, const Window& W,
+                                              const int* __restrict__ colptr, int n,
+                                              const int* __restrict__ cscrow,
+                                              const T* __restrict__ cscval,
+                                              const int64_t* __restrict__ blkbase,
+                                              const double* __restrict__ w, double (&s)[4]) {
+  extern __shared__ __align__(16) unsigned char ms_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned full = 0xffffffffu;
+  double* sw = reinterpret_cast<double*>(ms_raw) + warp * MS_CAP;
+  T* svalb = reinterpret_cast<T*>(ms_raw + 8 * MS_CAP * sizeof(double)) + warp * MS_NB * MS_CAP;
+  int* srowb = reinterpret_cast<int*>(ms_raw + 8 * MS_CAP * (sizeof(double) + MS_NB * sizeof(T))) +
+               warp * MS_NB * MS_CAP;
+  const int64_t cps = csc_stride(n);
+  const int ell = W.ell, nw = W.nw;
+  auto load_cols = [&](int P) {
+    MtwCols m;
+    m.q = make_int4(0, 0, 0, 0);
+    m.nx = 0;
+    m.base = 0;
+    if (P < nw) {
+      const int bk = W.blk[P];
+      m.q = __ldcs(reinterpret_cast<const int4*>(colptr + (int64_t)bk * cps + c0));
+      if (lane == 31) m.nx = __ldcs(colptr + (int64_t)bk * cps + c0 + (valid ? 4 : 0));
+      m.base = __ldg(blkbase + bk);
+    }
+    return m;
+  };
+  // this lane's end pointer, the warp's first entry and entry count
+  auto range = [&](const MtwCols& m, int& hi, int& s0, int& cnt) {
+    hi = __shfl_down_sync(full, m.q.x, 1);
+    if (lane == 31) hi = m.nx;
+    if (!valid) hi = m.q.x;
+    s0 = __shfl_sync(full, m.q.x, 0);
+    cnt = __shfl_sync(full, hi, 31) - s0;
+  };
+  // start copying block P's entries into buffer P % MS_NB (one group per call)
+  auto prefetch = [&](int P, const MtwCols& m) {
+    if (P < nw) {
+      int hi, s0, cnt;
+      range(m, hi, s0, cnt);
+      if (cnt > 0 && cnt <= MS_CAP) {
+        int* sr = srowb + (P % MS_NB) * MS_CAP;
+        T* sv = svalb + (P % MS_NB) * MS_CAP;
+#pragma unroll
+        for (int i = 0; i < MS_EPL; ++i) {
+          const int idx = lane + 32 * i;
+          if (idx < cnt) {
+            cp_async4(sr + idx, cscrow + m.base + s0 + idx);
+            cp_async_val(sv + idx, cscval + m.base + s0 + idx);
+          }
+        }
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  MtwCols m0 = load_cols(0), m1 = load_cols(1), m2 = load_cols(2);
+  prefetch(0, m0);
+  prefetch(1, m1);
+  for (int P = 0; P < nw; ++P) {
+    const MtwCols m3 = load_cols(P + 3);
+    prefetch(P + 2, m2);
+    asm volatile("cp.async.wait_group 2;" ::: "memory");
+    __syncwarp();
+    int hi, s0, cnt;
+    range(m0, hi, s0, cnt);
+    const int4 q = m0.q;
+    const double* wp = w + (int64_t)P * ell;
+    if (cnt > 0 && cnt <= MS_CAP) {
+      const int* sr = srowb + (P % MS_NB) * MS_CAP;
+      const T* sv = svalb + (P % MS_NB) * MS_CAP;
+      int rw[MS_EPL];
+#pragma unroll
+      for (int i = 0; i < MS_EPL; ++i) rw[i] = (lane + 32 * i < cnt) ? sr[lane + 32 * i] : -1;
+      double wv[MS_EPL];
+#pragma unroll
+      for (int i = 0; i < MS_EPL; ++i) wv[i] = rw[i] >= 0 ? __ldg(wp + rw[i]) : 0.0;
+#pragma unroll
+      for (int i = 0; i < MS_EPL; ++i)
+        if (rw[i] >= 0) sw[lane + 32 * i] = wv[i];
+      __syncwarp();
+      const int st[5] = {q.x - s0, q.y - s0, q.z - s0, q.w - s0, hi - s0};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int a = st[k], b = st[k + 1];
+        if (a < b) s[k] = fma(to_f64(sv[a]), sw[a], s[k]);
+        if (a + 1 < b) s[k] = fma(to_f64(sv[a + 1]), sw[a + 1], s[k]);
+        for (int idx = a + 2; idx < b; ++idx) s[k] = fma(to_f64(sv[idx]), sw[idx], s[k]);
+      }
+      __syncwarp();  // sw and this entry buffer are rewritten by later blocks
+    } else if (cnt > 0) {
+      for (int idx = q.x; idx < hi; ++idx) {
+        const int k = (idx >= q.y) + (idx >= q.z) + (idx >= q.w);
+        const double pv = to_f64(__ldcs(cscval + m0.base + idx));
+        const double wx = wp[__ldcs(cscrow + m0.base + idx)];
+        if (k == 0) s[0] = fma(pv, wx, s[0]);
+        else if (k == 1) s[1] = fma(pv, wx, s[1]);
+        else if (k == 2) s[2] = fma(pv, wx, s[2]);
+        else s[3] = fma(pv, wx, s[3]);
+      }
+    }
+    m0 = m1;
+    m1 = m2;
+    m2 = m3;
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+template <typename T>
+__global__ void __launch_bounds__(256) k_mtw_finish_stage(FinishParams F, Window W,
+                                                          const int* __restrict__ colptr,
+                                                          const int* __restrict__ cscrow,
+                                                          const T* __restrict__ cscval,
+                                                          const int64_t* __restrict__ blkbase,
+                                                          const double* __restrict__ w) {
+  if (F.ctl->diverged_at != 0) return;
+  const int c0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+  const bool valid = c0 < F.n;
+  double s[4] = {0.0, 0.0, 0.0, 0.0};
+  mtw_csc_stage<T>(valid ? c0 : F.n, valid, W, colptr, F.n, cscrow, cscval, blkbase, w, s);
+  finish_body4(F, c0, s);
+}
+template <typename T>
+__global__ void __launch_bounds__(256) k_mtw_stage(double* __restrict__ s_out, Window W,
+                                                   const int* __restrict__ colptr, int n,
+                                                   const int* __restrict__ cscrow,
+                                                   const T* __restrict__ cscval,
+                                                   const int64_t* __restrict__ blkbase,
+                                                   const double* __restrict__ w, const Ctl* ctl) {
+  if (ctl->diverged_at != 0) return;
+  const int c0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+  const bool valid = c0 < n;
+  double s[4] = {0.0, 0.0, 0.0, 0.0};
+  mtw_csc_stage<T>(valid ? c0 : n, valid, W, colptr, n, cscrow, cscval, blkbase, w, s);
+  if (valid) {
+    double2* o = reinterpret_cast<double2*>(s_out + c0);
+    o[0] = make_double2(s[0], s[1]);
+    o[1] = make_double2(s[2], s[3]);
+  }
+}
+
 __global__ void k_stamp_start(Ctl* ctl) { ctl->t_start_ns = globaltimer_ns(); }
 
 // sharded mode: divergence decision and history row from allreduced norms
@@ -1001,10 +1518,35 @@ void launch_residual_csr(double* r, const int64_t* rowptr, const int* col, const
                          const Ctl* ctl, cudaStream_t s) {
   k_residual_csr<T><<<ell, RES_THREADS, 0, s>>>(r, rowptr, col, val, row0, brow0, ell, x, b, ctl);
 }
+// scratch of the fixed-point CSR Gram: n column records + ell row exponents
+size_t gram_lut_bytes(int n, int ell) {
+  return (size_t)n * sizeof(GramRec<double>) + (size_t)ell * sizeof(int);
+}
 template <typename T>
 void launch_gram_csr(double* panel, const Window& W, const int64_t* rowptr, const int* col,
                      const T* val, const int* colptr_new, const int* cscrow, const T* cscval,
-                     int64_t base_new, cudaStream_t s) {
+                     int64_t base_new, cudaStream_t s, void* lut, int n) {
+  const unsigned grid = (unsigned)((int64_t)W.nw * W.ell);
+  const size_t fx_smem = (size_t)W.ell * 2 * sizeof(unsigned);
+  if (lut && W.ell <= 65536 && fx_smem <= 200 * 1024) {  // rows of the new block packed in 16 bits
+    if (fx_smem > 48 * 1024) {
+      static bool configured = false;
+      if (!configured) {
+        cudaFuncSetAttribute(k_gram_csr_fx<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        configured = true;
+      }
+    }
+    GramRec<T>* L = reinterpret_cast<GramRec<T>*>(lut);
+    int* rowexp = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(lut) +
+                                         (size_t)n * sizeof(GramRec<double>));
+    const int64_t newrow0 = (int64_t)W.blk[W.newp] * W.ell;
+    k_gram_rowexp<T><<<cdiv(W.ell, 8), 256, 0, s>>>(rowexp, rowptr, val, newrow0, W.ell);
+    k_gram_lut<T><<<cdiv(n, 256), 256, 0, s>>>(L, rowexp, colptr_new, cscrow, cscval, base_new, n);
+    const unsigned pgrid = std::min<unsigned>(grid, 148u * 4u);  // persistent: 4 CTAs per SM
+    k_gram_csr_fx<T><<<pgrid, GFX_THREADS, fx_smem, s>>>(panel, W, rowptr, col, val, L, rowexp,
+                                                         colptr_new, cscrow, cscval, base_new);
+    return;
+  }
   const size_t smem = (size_t)4 * W.ell * sizeof(double);
   if (smem > 48 * 1024) {
     static bool configured = false;  // one ell per process in practice; idempotent anyway
@@ -1013,8 +1555,8 @@ void launch_gram_csr(double* panel, const Window& W, const int64_t* rowptr, cons
       configured = true;
     }
   }
-  k_gram_csr<T><<<(unsigned)((int64_t)W.nw * W.ell), 128, smem, s>>>(
-      panel, W, rowptr, col, val, colptr_new, cscrow, cscval, base_new);
+  k_gram_csr<T><<<grid, 128, smem, s>>>(panel, W, rowptr, col, val, colptr_new, cscrow, cscval,
+                                        base_new);
 }
 template <typename T>
 void launch_gram_dense(double* panel, double* part, int nsplit, const Window& W, const T* A,
@@ -1062,15 +1604,28 @@ void launch_mtw_dense(double* part, int nsplit, const Window& W, const T* A, int
   }
 }
 // variants 1..5 = four columns per thread with (G blocks, E entries)
-// prefetched: (3,4) (2,6) (1,8) (3,2) (2,4); measured at configs[2] (1.25
-// entries per column and block, n = 2^20): (1,8) 53 us vs the column kernel's
-// 67 us; at configs[1] (n = 2^16, too few threads) and configs[3] (0.15
-// entries per column and block) the column kernel is faster
+// prefetched: (3,4) (2,6) (1,8) (3,2) (2,4); 6 = warp-staged entries with
+// cp.async prefetch (k_mtw_stage).  Cold-L2 probe, round 2: configs[2] (1.25
+// entries per column and block, n = 2^20) column kernel 67 us, (1,8) 53 us,
+// staged 47 us; configs[3] (0.15 entries per column and block, n = 2^21)
+// column kernel 45 us, staged 41 us; configs[1] (n = 2^16: n / 4 threads do
+// not fill the GPU) column kernel 20 us = staged
 int mtw_variant(int64_t n, double nnz_per_block) {
   if (const char* e = getenv("SLIM_MTW_QUAD")) return n % 4 == 0 ? atoi(e) : 0;
-  return (n % 4 == 0 && n >= (1 << 19) && nnz_per_block >= 0.5 * (double)n) ? 3 : 0;
+  (void)nnz_per_block;
+  return (n % 4 == 0 && n >= (1 << 19)) ? 6 : 0;
 }
 static int mtw_quad(int n, int quad) { return n % 4 == 0 ? quad : 0; }
+template <typename T>
+static void mtw_stage_configure() {
+  static bool done = false;
+  if (done) return;
+  cudaFuncSetAttribute(k_mtw_stage<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)mtw_stage_smem<T>());
+  cudaFuncSetAttribute(k_mtw_finish_stage<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)mtw_stage_smem<T>());
+  done = true;
+}
 #define MTW4_DISPATCH(KERNEL, GRID, ...)                                   \
   switch (mtw_quad(n_, quad)) {                                                  \
     case 1: KERNEL<T, 3, 4><<<GRID, 256, 0, s>>>(__VA_ARGS__); break;      \
@@ -1083,6 +1638,12 @@ template <typename T>
 void launch_mtw_csc(double* s_out, const Window& W, const int* colptr, int n, const int* cscrow,
                     const T* cscval, const int64_t* blkbase, const double* w, const Ctl* ctl,
                     cudaStream_t s, int quad) {
+  if (mtw_quad(n, quad) == 6) {
+    mtw_stage_configure<T>();
+    k_mtw_stage<T><<<cdiv(n / 4, 256), 256, mtw_stage_smem<T>(), s>>>(s_out, W, colptr, n, cscrow,
+                                                                      cscval, blkbase, w, ctl);
+    return;
+  }
   if (mtw_quad(n, quad)) {
     const int n_ = n;
     MTW4_DISPATCH(k_mtw_csc4, cdiv(n / 4, 256), s_out, W, colptr, n, cscrow, cscval, blkbase, w, ctl);
@@ -1106,7 +1667,11 @@ void launch_mtw_finish_csc(const FinishParams& F, const Window& W, const int* co
                            const int* cscrow, const T* cscval, const int64_t* blkbase,
                            const double* w, cudaStream_t s, int quad) {
   const int n_ = F.n;
-  if (mtw_quad(n_, quad)) {
+  if (mtw_quad(n_, quad) == 6) {
+    mtw_stage_configure<T>();
+    k_mtw_finish_stage<T><<<cdiv(F.n / 4, 256), 256, mtw_stage_smem<T>(), s>>>(F, W, colptr, cscrow,
+                                                                              cscval, blkbase, w);
+  } else if (mtw_quad(n_, quad)) {
     MTW4_DISPATCH(k_mtw_finish_csc4, cdiv(F.n / 4, 256), F, W, colptr, cscrow, cscval, blkbase, w);
   } else
     k_mtw_finish_csc<T><<<cdiv(F.n, 256), 256, 0, s>>>(F, W, colptr, cscrow, cscval, blkbase, w);
@@ -1183,7 +1748,8 @@ void launch_build_csc_list(int* colptr, int* cscrow, T* cscval, const int64_t* r
                                        int64_t, int, const double*, const double*, const Ctl*,   \
                                        cudaStream_t);                                            \
   template void launch_gram_csr<T>(double*, const Window&, const int64_t*, const int*, const T*,  \
-                                   const int*, const int*, const T*, int64_t, cudaStream_t);      \
+                                   const int*, const int*, const T*, int64_t, cudaStream_t,       \
+                                   void*, int);                                                  \
   template void launch_gram_dense<T>(double*, double*, int, const Window&, const T*, int64_t,     \
                                      int64_t, int, cudaStream_t);                                \
   template void launch_mtw_dense<T>(double*, int, const Window&, const T*, int64_t, int,          \

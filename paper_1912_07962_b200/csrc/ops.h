@@ -62,10 +62,15 @@ template <typename T>
 void launch_residual_csr(double* r, const int64_t* rowptr, const int* col, const T* val,
                          int64_t row0, int64_t brow0, int ell, const double* x, const double* b,
                          const Ctl* ctl, cudaStream_t s);
+// `lut`: scratch of gram_lut_bytes(n, ell) for the per-column records and row
+// exponents of the new block (k_gram_rowexp + k_gram_lut + k_gram_csr_fx:
+// one gather per nonzero, exact fixed-point sums); nullptr runs the
+// pointer-chasing fp64 k_gram_csr.
+size_t gram_lut_bytes(int n, int ell);
 template <typename T>
 void launch_gram_csr(double* panel, const Window& W, const int64_t* rowptr, const int* col,
                      const T* val, const int* colptr_new, const int* cscrow, const T* cscval,
-                     int64_t base_new, cudaStream_t s);
+                     int64_t base_new, cudaStream_t s, void* lut, int n);
 template <typename T>
 void launch_gram_dense(double* panel, double* part, int nsplit, const Window& W, const T* A,
                        int64_t lda, int64_t newrow0, int n, cudaStream_t s);
