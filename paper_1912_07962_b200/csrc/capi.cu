@@ -207,6 +207,7 @@ struct slim_ctx {
   int64_t nnz = 0;
   int* colptr = nullptr;
   int mtw_quad = 0;  // M^T w kernel variant (mtw_variant), set when the operator is finalized
+  bool gram_fx = false;  // CSR Gram: fixed-point record kernel (gram_csr_variant), set with mtw_quad
   int* cscrow = nullptr;
   void* cscval = nullptr;
   int64_t* blkbase = nullptr;  // M + 1 nnz offsets (device)
@@ -683,10 +684,9 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
     if (c->use_tc) parts = std::max<int>(parts, (int)(c->n / gram_tc_kchunk(c->n, 1)));
     ALLOC(c, c->gpart, sizeof(double) * (size_t)parts * Nmax * ell);
   } else {
-    // CSR Gram: per-column records + row exponents of the newest block (fixed-point
-    // k_gram_csr_fx); SLIM_GRAM_LUT=0 keeps the fp64 pointer-chasing kernel for A/B
-    const char* env = getenv("SLIM_GRAM_LUT");
-    if (!(env && env[0] == '0')) ALLOC(c, c->gpart, gram_lut_bytes((int)c->n, (int)ell));
+    // CSR Gram: per-column records + row exponents of the newest block for the
+    // fixed-point k_gram_csr_fx (chosen per operator: gram_csr_variant)
+    ALLOC(c, c->gpart, gram_lut_bytes((int)c->n, (int)ell));
   }
   ALLOC(c, c->spart, sizeof(double) * (size_t)c->nsplit_mtw * c->n);
   ALLOC(c, c->fpart, sizeof(double) * (size_t)finish_grid((int)c->n) * (1 + MAX_REFS));
@@ -958,6 +958,7 @@ static int size_streamed_csr(slim_ctx* c) {
   CK(c, cudaMemcpy(c->b, c->h_b.data(), sizeof(double) * c->m, cudaMemcpyHostToDevice));
   c->h2d_bytes += (int64_t)(sizeof(int64_t) * (c->m + 1 + M + 1) + sizeof(double) * c->m);
   c->mtw_quad = mtw_variant(c->n, (double)nnz / (double)std::max<int64_t>(1, M));
+  c->gram_fx = c->gpart && gram_csr_variant((double)nnz / (double)std::max<int64_t>(1, M));
   c->h_have.clear();
   c->h_b.clear();
   c->resident.assign(M, 0);
@@ -1004,30 +1005,73 @@ static PinRing& pin_ring(int dev) {
 
 // host memcpy into the pinned ring, split over 4 threads for large chunks
 // (one thread copies ~10 GB/s from pageable memory; the first batch's blocks
-// are on the critical path of a fresh run)
-static void par_memcpy(char* dst, const char* src, size_t n) {
-  constexpr int NT = 4;
-  if (n < ((size_t)1 << 20)) {
-    memcpy(dst, src, n);
-    return;
+// are on the critical path of a fresh run).  The three helpers are started
+// once per process and sleep on a condition variable: creating threads per
+// chunk cost ~4 ms each time while another thread of the process was busy
+// (one scheduler tick before a new thread first ran; round 2 trace).
+class CopyPool {
+ public:
+  static constexpr int NH = 3;
+  // copies [src, src + n) to dst; returns false if the helpers could not be started
+  bool copy(char* dst, const char* src, size_t n) {
+    std::lock_guard<std::mutex> one(call_);  // one copy at a time (rings of two devices may call)
+    std::unique_lock<std::mutex> lk(m_);
+    if (!started_ && !start()) return false;
+    const size_t part = (n / (NH + 1) + 63) & ~(size_t)63;
+    pending_ = 0;
+    for (int t = 0; t < NH; ++t) {
+      const size_t o = part * (t + 1);
+      job_[t] = Job{nullptr, nullptr, 0};
+      if (o < n) job_[t] = Job{dst + o, src + o, std::min(part, n - o)}, ++pending_;
+    }
+    ++gen_;
+    lk.unlock();
+    cv_.notify_all();
+    memcpy(dst, src, std::min(part, n));
+    lk.lock();
+    done_.wait(lk, [&] { return pending_ == 0; });
+    return true;
   }
-  const size_t part = (n / NT + 63) & ~(size_t)63;
-  std::thread th[NT - 1];
-  size_t rest = n;  // start of the range no helper took (copied here)
-  for (int t = 1; t < NT; ++t) {
-    const size_t o = part * t;
-    if (o >= n) break;
+
+ private:
+  struct Job {
+    char* d;
+    const char* s;
+    size_t n;
+  };
+  bool start() {
     try {
-      th[t - 1] = std::thread([=]() { memcpy(dst + o, src + o, std::min(part, n - o)); });
-    } catch (...) {  // no thread available: copy the rest here (nothing may escape the C ABI)
-      rest = o;
-      break;
+      for (int t = 0; t < NH; ++t) std::thread([this, t] { loop(t); }).detach();
+    } catch (...) {
+      return false;  // helpers already started keep sleeping; the caller copies alone
+    }
+    started_ = true;
+    return true;
+  }
+  void loop(int t) {
+    uint64_t seen = 0;
+    std::unique_lock<std::mutex> lk(m_);
+    for (;;) {
+      cv_.wait(lk, [&] { return gen_ != seen; });
+      seen = gen_;
+      const Job j = job_[t];
+      if (!j.n) continue;
+      lk.unlock();
+      memcpy(j.d, j.s, j.n);
+      lk.lock();
+      if (--pending_ == 0) done_.notify_one();
     }
   }
-  memcpy(dst, src, std::min(part, n));
-  if (rest < n) memcpy(dst + rest, src + rest, n - rest);
-  for (auto& t : th)
-    if (t.joinable()) t.join();
+  std::mutex call_, m_;
+  std::condition_variable cv_, done_;
+  Job job_[NH]{};
+  uint64_t gen_ = 0;
+  int pending_ = 0;
+  bool started_ = false;
+};
+static void par_memcpy(char* dst, const char* src, size_t n) {
+  static CopyPool* pool = new CopyPool();  // process lifetime, like the ring
+  if (n < ((size_t)1 << 20) || !pool->copy(dst, src, n)) memcpy(dst, src, n);
 }
 
 // host -> device copy of `bytes` through the pinned ring (pageable fallback)
@@ -1229,6 +1273,7 @@ int slim_finalize_operator(slim_ctx* c) {
   CKLAUNCH(c);
   CK(c, cudaStreamSynchronize(c->sx));
   c->mtw_quad = mtw_variant(c->n, (double)c->nnz / (double)std::max<int64_t>(1, c->M));
+  c->gram_fx = c->gpart && gram_csr_variant((double)c->nnz / (double)std::max<int64_t>(1, c->M));
   c->op_ready = true;
   return SLIM_OK;
 }
@@ -1546,11 +1591,11 @@ static int enqueue_gram(slim_ctx* c, const Window& W, int64_t k, int64_t real_bl
     const int64_t base = c->h_blkbase[newblk];
     if (c->vdt == SLIM_F64)
       launch_gram_csr<double>(panel, W, c->rowptr, c->col, (const double*)c->val, cpn, c->cscrow,
-                              (const double*)c->cscval, base, c->sg, c->gpart, (int)c->n);
+                              (const double*)c->cscval, base, c->sg, c->gram_fx ? c->gpart : nullptr, (int)c->n);
     else
       launch_gram_csr<float>(panel, W, c->rowptr, c->col, (const float*)c->val, cpn, c->cscrow,
-                             (const float*)c->cscval, base, c->sg, c->gpart, (int)c->n);
-    c->launches += c->gpart ? 3 : 1;
+                             (const float*)c->cscval, base, c->sg, c->gram_fx ? c->gpart : nullptr, (int)c->n);
+    c->launches += c->gram_fx ? 3 : 1;
   }
   (void)k;
   CKLAUNCH(c);
@@ -1825,6 +1870,20 @@ struct Uploader {
   std::vector<std::vector<int64_t>> blocks;  // per batch: first-use blocks
   std::vector<cudaEvent_t> ev;               // per batch: copies enqueued (nullptr: none)
   std::atomic<int64_t> done{0};              // batches whose uploads are enqueued
+  std::mutex mu;
+  std::condition_variable cv;                // signalled on every change of `done`
+  void set_done(int64_t v) {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      done.store(v, std::memory_order_release);
+    }
+    cv.notify_all();
+  }
+  // blocks (no spinning: a busy waiter delayed the copy helpers) until batch B is enqueued
+  void wait_batch(int64_t B) {
+    std::unique_lock<std::mutex> lk(mu);
+    cv.wait(lk, [&] { return done.load(std::memory_order_acquire) > B; });
+  }
   int rc = SLIM_OK;
   std::string msg;
   int64_t launches = 0;
@@ -1885,6 +1944,7 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
     return used.back();
   };
 
+  const auto host_t0 = std::chrono::steady_clock::now();
   launch_stamp_start(c->ctl, c->sx);
   CKLAUNCH(c);
   const int64_t k0 = std::min<int64_t>(std::max<int64_t>(c->timing_k0, 1), std::max<int64_t>(K, 1));
@@ -1921,15 +1981,20 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
     }
     up.active = true;
     up.th = std::thread([c, &up, nbatch]() {
+      const bool trace_up = getenv("SLIM_TRACE_RUN") != nullptr;
       cudaSetDevice(c->dev);
       for (int64_t B = 0; B < nbatch; ++B) {
         const bool csr = c->layout == SLIM_CSR_PERBLOCK;
         BlkList L{};
         for (int64_t bk : up.blocks[B]) {
+          const auto tb0 = std::chrono::steady_clock::now();
           const int rc = copy_block(c, bk, up.msg, &up.launches, !csr);
+          if (trace_up)
+            fprintf(stderr, "    uploader: batch %lld block %lld copy_block %.2f ms\n", (long long)B, (long long)bk,
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tb0).count());
           if (rc) {
             up.rc = rc;
-            up.done.store(nbatch + 1, std::memory_order_release);
+            up.set_done(nbatch + 1);
             return;
           }
           c->resident[bk] = 1;
@@ -1947,13 +2012,32 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
         if (up.ev[B] && cudaEventRecord(up.ev[B], c->su) != cudaSuccess) {
           up.rc = SLIM_ECUDA;
           up.msg = "upload event record failed";
-          up.done.store(nbatch + 1, std::memory_order_release);
+          up.set_done(nbatch + 1);
           return;
         }
-        up.done.store(B + 1, std::memory_order_release);
+        up.set_done(B + 1);
       }
     });
   }
+  // SLIM_TRACE_RUN=1: device timeline of the run's batches on stderr (Gram
+  // panels, factorization and x-chain of every batch, ms since the run's start)
+  const bool trace_run = getenv("SLIM_TRACE_RUN") != nullptr;
+  std::vector<cudaEvent_t> tev;
+  cudaEvent_t t_base = nullptr;
+  auto tmark = [&](cudaStream_t st) {
+    if (!trace_run) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    tev.push_back(e);
+  };
+  if (trace_run) {
+    cudaEventCreate(&t_base);
+    cudaEventRecord(t_base, c->sx);
+    cudaStreamWaitEvent(c->sg, t_base, 0);
+    cudaStreamWaitEvent(c->sf, t_base, 0);
+  }
+  std::vector<double> host_enq;
   for (int64_t B = 0; B < nbatch && !stop; ++B) {
     const int64_t kb0 = B * D + 1;
     const int nb = (int)std::min<int64_t>(D, K - kb0 + 1);
@@ -1977,7 +2061,7 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
     // worker thread (below); wait until it has enqueued them, then order the
     // batch's Gram panels and x-chain after the copies
     if (up.active) {
-      while (up.done.load(std::memory_order_acquire) <= B) std::this_thread::yield();
+      up.wait_batch(B);
       if (up.rc) {
         up.join();
         FAIL(c, up.rc, "%s", up.msg.c_str());
@@ -1994,6 +2078,12 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
       CK(c, cudaStreamWaitEvent(c->sg, c->ev_x[(B - 2) % NEV], 0));
     ProfPair pg{};
     const bool prof_b = c->prof && kb0 >= k0;
+    auto hmark = [&]() {
+      if (trace_run)
+        host_enq.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host_t0).count());
+    };
+    hmark();
+    tmark(c->sg);
     if (prof_b) pg = take(c->prof_gram, pgr), cudaEventRecord(pg.a, c->sg);
     for (int b = 0; b < nb; ++b) {
       if (c->sgm) {  // sg: no Gram panel; a generated block is still generated
@@ -2011,6 +2101,7 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
       if (rc) return rc;
     }
     if (prof_b) cudaEventRecord(pg.b, c->sg);
+    tmark(c->sg);
     CK(c, cudaEventRecord(c->ev_g[B % NEV], c->sg));
     // ---- batched factorization (sf): buffer set reused from batch B - 2
     const bool rr = c->rr && c->comm && c->comm->nranks > 1;
@@ -2020,6 +2111,8 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
     if (B >= 2) CK(c, cudaStreamWaitEvent(c->sf, c->ev_x[(B - 2) % NEV], 0));
     if (B >= 1 && c->serial) CK(c, cudaStreamWaitEvent(c->sf, c->ev_x[(B - 1) % NEV], 0));
     ProfPair pc{};
+    hmark();
+    tmark(c->sf);
     if (prof_b) pc = take(c->prof_chol, pch), cudaEventRecord(pc.a, c->sf);
     {
       double fl = 0.0, i8 = 0.0;
@@ -2031,8 +2124,12 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
       if (prof_b) c->chol_flops += fl, c->chol_i8ops += i8;
     }
     if (prof_b) cudaEventRecord(pc.b, c->sf);
+    tmark(c->sf);
     CK(c, cudaEventRecord(c->ev_f[B % NEV], c->sf));
+    } else if (trace_run) {
+      hmark(), tmark(c->sf), tmark(c->sf);
     }
+    hmark();
     // ---- x-chain (sx), one step at a time
     for (int b = 0; b < nb; ++b) {
       const int64_t k = kb0 + b;
@@ -2064,6 +2161,7 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
       }
 
     }
+    tmark(c->sx);
     CK(c, cudaEventRecord(c->ev_x[B % NEV], c->sx));
     // cheap divergence poll: stop enqueueing once the device reported it
     if ((B & 7) == 7 && !c->comm) {  // shards must enqueue identical exchange sequences
@@ -2087,6 +2185,21 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
   c->epoch_base += K + 1;
   c->timing_k0 = 1;
   CK(c, cudaDeviceSynchronize());
+  if (trace_run) {
+    const double host_end =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host_t0).count();
+    fprintf(stderr, "slim_run trace: %lld steps, D = %d, host enqueue + sync %.2f ms\n", (long long)K, D, host_end);
+    for (size_t B = 0; 5 * B + 4 < tev.size(); ++B) {
+      float t[5];
+      for (int q = 0; q < 5; ++q) cudaEventElapsedTime(&t[q], t_base, tev[5 * B + q]);
+      fprintf(stderr, "  batch %2zu: host: uploads ready %8.2f, gram enqueued %8.2f, factor enqueued %8.2f | gram %8.2f - %8.2f | factor %8.2f - %8.2f | x-chain end %8.2f\n",
+              B, 3 * B + 2 < host_enq.size() ? host_enq[3 * B] : -1.0,
+              3 * B + 2 < host_enq.size() ? host_enq[3 * B + 1] : -1.0,
+              3 * B + 2 < host_enq.size() ? host_enq[3 * B + 2] : -1.0, t[0], t[1], t[2], t[3], t[4]);
+    }
+    for (auto e : tev) cudaEventDestroy(e);
+    cudaEventDestroy(t_base);
+  }
   Ctl hc{};
   CK(c, cudaMemcpy(&hc, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
   int herr = 0;
@@ -2500,10 +2613,12 @@ extern "C" int slim_probe_stream(slim_ctx* c, int32_t kernel, int32_t reps, doub
         const int* cpn = c->colptr + nb * csc_stride((int)c->n);
         if (vb == 8)
           launch_gram_csr<double>(panel, W, c->rowptr, c->col, (const double*)c->val, cpn, c->cscrow,
-                                  (const double*)c->cscval, c->h_blkbase[nb], s, c->gpart, n);
+                                  (const double*)c->cscval, c->h_blkbase[nb], s,
+                                  c->gram_fx ? c->gpart : nullptr, n);
         else
           launch_gram_csr<float>(panel, W, c->rowptr, c->col, (const float*)c->val, cpn, c->cscrow,
-                                 (const float*)c->cscval, c->h_blkbase[nb], s, c->gpart, n);
+                                 (const float*)c->cscval, c->h_blkbase[nb], s,
+                                 c->gram_fx ? c->gpart : nullptr, n);
       } else {
         bytes = (double)N * n * vb + 8.0 * N * ell * (1 + c->nsplit_gram);
         if (vb == 8)

@@ -1518,6 +1518,15 @@ void launch_residual_csr(double* r, const int64_t* rowptr, const int* col, const
                          const Ctl* ctl, cudaStream_t s) {
   k_residual_csr<T><<<ell, RES_THREADS, 0, s>>>(r, rowptr, col, val, row0, brow0, ell, x, b, ctl);
 }
+// CSR Gram kernel per operator: the fixed-point record kernel pays off once a
+// block has enough nonzeros to amortise its two small preparation kernels
+// (cold-L2 probe: configs[2], 1.3 M nonzeros per block: 195 vs 543 us;
+// configs[3], 450 k: 126 vs 129 us; configs[1], 131 k: 56 vs 34 us);
+// SLIM_GRAM_LUT=1/0 overrides
+bool gram_csr_variant(double nnz_per_block) {
+  if (const char* e = getenv("SLIM_GRAM_LUT")) return e[0] != '0';
+  return nnz_per_block >= (double)(1 << 18);
+}
 // scratch of the fixed-point CSR Gram: n column records + ell row exponents
 size_t gram_lut_bytes(int n, int ell) {
   return (size_t)n * sizeof(GramRec<double>) + (size_t)ell * sizeof(int);

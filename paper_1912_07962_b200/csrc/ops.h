@@ -67,6 +67,7 @@ void launch_residual_csr(double* r, const int64_t* rowptr, const int* col, const
 // one gather per nonzero, exact fixed-point sums); nullptr runs the
 // pointer-chasing fp64 k_gram_csr.
 size_t gram_lut_bytes(int n, int ell);
+bool gram_csr_variant(double nnz_per_block);  // true: k_gram_csr_fx
 template <typename T>
 void launch_gram_csr(double* panel, const Window& W, const int64_t* rowptr, const int* col,
                      const T* val, const int* colptr_new, const int* cscrow, const T* cscval,
