@@ -50,7 +50,12 @@ def _digest(path, flags):
     with open(os.path.join(INCLUDE, "slimb200.h"), "rb") as fh:
         h.update(fh.read())
     with open(path, "rb") as fh:
-        h.update(fh.read())
+        text = fh.read()
+    h.update(text)
+    for name in sorted(os.listdir(CSRC)):  # a source that includes another .cu (chol_q6.cu)
+        if name.endswith(".cu") and f'#include "{name}"'.encode() in text:
+            with open(os.path.join(CSRC, name), "rb") as fh:
+                h.update(fh.read())
     return h.hexdigest()[:16]
 
 

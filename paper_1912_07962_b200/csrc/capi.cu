@@ -246,6 +246,10 @@ struct slim_ctx {
   float* gring_lo = nullptr;
   bool use_tc = false;
   bool use_i8 = true;  // int8 tensor-core factorization (else fp64 DMMA, chol_i8_for)
+  // digit layout of the int8 factorization (kernels.h CholVariant) and whether w
+  // gets one step of iterative refinement (the six-digit layout needs it)
+  const CholVariant* cv = &chol_table;
+  bool refine = false;
   uint64_t gen_seed = 0;
   int64_t gen_n_total = 0, col_offset = 0;
   // state
@@ -297,6 +301,8 @@ struct slim_ctx {
   int nsplit_mtw = 1;
   double* fpart = nullptr;
   double* gpart = nullptr;
+  double* refpart = nullptr;  // refinement: (r + 1) x Tmax TB partial sums of G w
+  double* refres = nullptr;   // ... residual y - G w and the correction dw (2 x Tmax TB)
   int nsplit_gram = 1;
   double* hist = nullptr;
   int64_t hist_rows_cap = 0;
@@ -454,7 +460,7 @@ static void free_all(slim_ctx* c) {
   cudaDeviceSynchronize();  // no pending work may touch recycled blocks
   void* ptrs[] = {c->gring_hi, c->gring_lo, c->zero_b, c->norms, c->gring, c->A, c->b, c->rowptr, c->col, c->val, c->colptr, c->cscrow, c->cscval,
                   c->blkbase, c->x, c->ctl, c->panels, c->tickets, c->tflags, c->errflag,
-                  c->rvec, c->tvec, c->wvec, c->spart, c->fpart, c->gpart, c->hist, c->iters_dev};
+                  c->rvec, c->tvec, c->wvec, c->spart, c->fpart, c->gpart, c->refpart, c->refres, c->hist, c->iters_dev};
   for (void* p : ptrs) cache_free(p);
   for (int q = 0; q < MAX_REFS; ++q) cache_free(c->refs[q]);
   cache_free(c->factor_slab);
@@ -590,6 +596,18 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
   // dual systems factor with the fp64 DMMA kernel
   c->use_i8 = chol_i8_for(c->Tmax);
   {
+    // Large dual systems (the D = 4 batch class: configs[2], configs[3]) are bound
+    // by the factorization stream and their x-chain has room: six digits
+    // (21 instead of 34 digit-pair products, 6/7 of the operand bytes) plus one
+    // refinement step of w against the fp64 Gram ring.  Smaller systems keep
+    // seven digits and no refinement (their x-chain is as long as their
+    // factorizations).  SLIM_REFINE=0/1 overrides.
+    bool refine = c->use_i8 && Nmax > 6144;
+    if (const char* env = getenv("SLIM_REFINE")) refine = c->use_i8 && env[0] != '0';
+    c->refine = refine;
+    c->cv = refine ? &q6::chol_table : &chol_table;
+  }
+  {
     // the triangular-solve cluster keeps per-row vectors in shared memory
     int optin = 0;
     CK(c, cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->dev));
@@ -622,7 +640,7 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
     const size_t ib = sizeof(double) * (size_t)c->Tmax * TB * TB;
     const size_t fb = ((sizeof(int) * (size_t)ntiles + 255) / 256) * 256;
     // int8 digit slices (same bytes as the fp64 tiles) + row exponents
-    const size_t qb = c->use_i8 ? q_bytes(c->Tmax) : 0;
+    const size_t qb = c->use_i8 ? c->cv->q_bytes(c->Tmax) : 0;
     const size_t eb = c->use_i8 ? ((sizeof(int) * (size_t)c->Tmax * TB + 1023) / 1024) * 1024 : 0;
     const size_t per = lb + db + ib + qb + eb;
     ALLOC(c, c->factor_slab, (per + fb) * 2 * c->D);
@@ -638,8 +656,8 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
         FAIL(c, SLIM_ECUDA, "TMA descriptor for the factor buffer could not be encoded");
       c->Qbuf[q] = qb ? (int8_t*)(base + per * q + lb + db + ib) : nullptr;
       c->rexp[q] = eb ? (int*)(base + per * q + lb + db + ib + qb) : nullptr;
-      if (qb && (!tma_map_q(&c->QmapA[q], c->Qbuf[q], c->Tmax, 128) ||
-                 !tma_map_q(&c->QmapB[q], c->Qbuf[q], c->Tmax, 64)))
+      if (qb && (!tma_map_q(&c->QmapA[q], c->Qbuf[q], c->Tmax, 128, c->cv->qd) ||
+                 !tma_map_q(&c->QmapB[q], c->Qbuf[q], c->Tmax, 64, c->cv->qd)))
         FAIL(c, SLIM_ECUDA, "TMA descriptor for the sliced factor buffer could not be encoded");
     }
   }
@@ -660,6 +678,10 @@ int slim_create(slim_ctx** out, const slim_desc* d) {
   }
   ALLOC(c, c->tvec, sizeof(double) * c->Tmax * TB);
   ALLOC(c, c->wvec, sizeof(double) * c->Tmax * TB);
+  if (c->refine) {
+    ALLOC(c, c->refpart, sizeof(double) * (size_t)W * c->Tmax * TB);
+    ALLOC(c, c->refres, sizeof(double) * 2 * (size_t)c->Tmax * TB);
+  }
   // M^T w: split the window rows over CTAs when n alone cannot fill the GPU
   if (c->layout == SLIM_GEN_SPLITMIX64) {
     ALLOC(c, c->gring, sizeof(float) * (size_t)c->S * ell * c->n);
@@ -1467,8 +1489,8 @@ int slim_set_timing_start(slim_ctx* c, int64_t k0) {
 int slim_timing(slim_ctx* c, int32_t which, double* ms, int64_t* launches) {
   if (!c || which < 0 || which > 9) FAIL(c, SLIM_EINVAL, "bad argument");
   if (which == 9) {  // digit-pair products per tile update and the extra order QX
-    if (ms) *ms = (double)QPAIRS;
-    if (launches) *launches = QX;
+    if (ms) *ms = (double)c->cv->pairs;
+    if (launches) *launches = c->cv->qx;
     return SLIM_OK;
   }
   if (which == 8) {  // operator bytes copied host -> device so far (e2e accounting)
@@ -1477,8 +1499,8 @@ int slim_timing(slim_ctx* c, int32_t which, double* ms, int64_t* launches) {
     return SLIM_OK;
   }
   if (which == 7) {  // digit layout of the int8 factorization (compile time)
-    if (ms) *ms = (double)QD;
-    if (launches) *launches = DBITS;
+    if (ms) *ms = (double)c->cv->qd;
+    if (launches) *launches = c->cv->dbits;
     return SLIM_OK;
   }
   if (which == 6) {  // int8 tensor ops of the profiled factorization launches
@@ -1632,6 +1654,37 @@ static int enqueue_x_chain(slim_ctx* c, const Window& W, int64_t k, int d, doubl
   }
   CK(c, launch_trsv(T, s));
   CKLAUNCH(c);
+  if (c->refine) {
+    // one step of iterative refinement: w += G^{-1} (y - G w), G from the fp64
+    // Gram ring (the six-digit factors carry ~2^-45 relative error)
+    GramApplyParams G{};
+    G.panels = c->panels;
+    G.panel_stride = c->panel_stride;
+    G.ell = ell;
+    G.nw = W.nw;
+    G.newp = W.newp;
+    G.npad = T.T * TB;
+    for (int P = 0; P < W.nw; ++P) G.slot[P] = W.slot[P], G.age[P] = W.age[P];
+    G.alpha = alpha;
+    G.w = c->wvec;
+    G.r = c->rvec;
+    G.part = c->refpart;
+    G.ldp = (int64_t)c->Tmax * TB;
+    G.res = c->refres;
+    G.ctl = c->ctl;
+    launch_gram_apply(G, s);
+    CKLAUNCH(c);
+    TrsvParams T2 = T;
+    T2.rstart = 0;
+    T2.rend = T.T * TB;
+    T2.i0 = 0;
+    T2.r = c->refres;
+    T2.w = c->refres + (int64_t)c->Tmax * TB;
+    CK(c, launch_trsv(T2, s));
+    launch_add_inplace(c->wvec, T2.w, N, c->ctl, s);
+    CKLAUNCH(c);
+    c->launches += 4;
+  }
   }
   if (c->rr && c->comm && !c->sgm) {
     int rc = comm_allreduce(c, c->wvec, (size_t)N, s);
@@ -1745,7 +1798,7 @@ static const slim_ctx::TaskMap* task_map(slim_ctx* c, const std::vector<SysShape
   const double t3 = (double)TB * TB * TB;
   // int8 tensor-core path: 36 digit-pair products of 2 * 64^3 ops per 64x64x64
   // tile update (k_chol_i8)
-  const double u8 = (double)QPAIRS * 2.0 * t3;
+  const double u8 = (double)c->cv->pairs * 2.0 * t3;
   double flops = 0.0, i8ops = 0.0;
   for (const int2& e : h) {
     const int i = e.y >> 16, j = e.y & 0x7fff;
@@ -1821,7 +1874,7 @@ static int enqueue_chol_batch(slim_ctx* c, const Window* Ws, int nb, int set, co
   P.prevQ = prev >= 0 ? c->Qbuf[prev] : nullptr;
   P.tile_base[0] = 0;
   for (int b = 0; b < nb; ++b) P.tile_base[b + 1] = P.tile_base[b] + sh[b].T * (sh[b].T + 1) / 2;
-  launch_assemble(P, c->sf);
+  c->cv->launch_assemble(P, c->sf);
   c->launches += 1;
   CKLAUNCH(c);
   if (P.ntasks > 0) {
@@ -1837,7 +1890,7 @@ static int enqueue_chol_batch(slim_ctx* c, const Window* Ws, int nb, int set, co
       CK(c, cudaMemsetAsync(dtr, 0, sizeof(unsigned long long) * 8 * (size_t)P.ntasks, c->sf));
       P.trace = dtr;
     }
-    launch_chol(P, c->sf);
+    c->cv->launch_chol(P, c->sf);
     c->launches += 1;
     CKLAUNCH(c);
     if (dtr) {
@@ -2074,7 +2127,8 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
     // ---- Gram panels (sg): the ring slots they overwrite were last read by
     // the factorization (and, for generated blocks, the x-chain) of batch B - 2
     if (B >= 2) CK(c, cudaStreamWaitEvent(c->sg, c->ev_f[(B - 2) % NEV], 0));
-    if (B >= 2 && c->layout == SLIM_GEN_SPLITMIX64)
+    // (the refinement reads the ring on the x-chain: same rule as the generated blocks)
+    if (B >= 2 && (c->layout == SLIM_GEN_SPLITMIX64 || c->refine))
       CK(c, cudaStreamWaitEvent(c->sg, c->ev_x[(B - 2) % NEV], 0));
     ProfPair pg{};
     const bool prof_b = c->prof && kb0 >= k0;
@@ -2410,7 +2464,7 @@ static int potrf_impl(int32_t device, const double* G, int64_t N, double* L_out,
     FAIL((slim_ctx*)nullptr, SLIM_ECUDA, "TMA descriptor could not be encoded");
   }
   P.m[0].qT = T;
-  if (i8 && (!tma_map_q(&P.m[0].qmapA, dQ, T, 128) || !tma_map_q(&P.m[0].qmapB, dQ, T, 64))) {
+  if (i8 && (!tma_map_q(&P.m[0].qmapA, dQ, T, 128, QD) || !tma_map_q(&P.m[0].qmapB, dQ, T, 64, QD))) {
     cleanup();
     FAIL((slim_ctx*)nullptr, SLIM_ECUDA, "TMA descriptor could not be encoded");
   }

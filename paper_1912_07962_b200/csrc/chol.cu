@@ -37,6 +37,9 @@
 #include "kernels.h"
 
 namespace slim {
+#ifdef SLIM_CHOL_VARIANT
+namespace SLIM_CHOL_VARIANT {  // a second digit layout (chol_q6.cu)
+#endif
 
 constexpr unsigned FULL = 0xffffffffu;
 
@@ -1403,4 +1406,11 @@ void launch_chol(const CholParams& P, cudaStream_t s) {
     k_chol_tiles<<<P.ntasks, 256, SMB_TOTAL, s>>>(P);
 }
 
+static size_t table_q_bytes(int qT) { return q_bytes(qT); }
+extern const CholVariant chol_table = {QD,           QX,      DBITS, QPAIRS, CHOL_I8_TMAX, &table_q_bytes,
+                                       &launch_assemble, &launch_chol};
+
+#ifdef SLIM_CHOL_VARIANT
+}  // namespace SLIM_CHOL_VARIANT
+#endif
 }  // namespace slim

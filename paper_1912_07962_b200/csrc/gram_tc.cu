@@ -279,15 +279,15 @@ bool tma_map_f64_sw128(CUtensorMap* m, const double* base, int64_t rows, int64_t
   return r == CUDA_SUCCESS;
 }
 
-bool tma_map_q(CUtensorMap* m, const int8_t* base, int qT, int box_rows) {
+bool tma_map_q(CUtensorMap* m, const int8_t* base, int qT, int box_rows, int qd) {
   auto enc = get_encode();
   if (!enc) return false;
   // dim0: QROW bytes of one digit (K = QROW int8), dim1: rows over all tile
   // rows of a column (qT * 64), dim2: (column[, k half], digit) blocks
-  const cuuint64_t zblocks = (cuuint64_t)qT * (64 / QROW) * QD;
+  const cuuint64_t zblocks = (cuuint64_t)qT * (64 / QROW) * qd;
   cuuint64_t dims[3] = {(cuuint64_t)QROW, (cuuint64_t)qT * 64, zblocks};
   cuuint64_t strides[2] = {(cuuint64_t)QROW, (cuuint64_t)qT * 64 * QROW};
-  cuuint32_t box[3] = {(cuuint32_t)QROW, (cuuint32_t)box_rows, (cuuint32_t)QD};
+  cuuint32_t box[3] = {(cuuint32_t)QROW, (cuuint32_t)box_rows, (cuuint32_t)qd};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)base, dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE,

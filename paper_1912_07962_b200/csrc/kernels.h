@@ -139,8 +139,23 @@ cudaError_t launch_trsv(const TrsvParams& P, cudaStream_t s);
 int trsv_cluster_size(int T);
 size_t trsv_smem_bytes(int T, int C, int rs = 3);
 
-__global__ void k_chol_tiles(const __grid_constant__ CholParams P);
-__global__ void k_chol_i8(const __grid_constant__ CholParams P);
+
+// chol.cu is compiled once per digit layout of the int8 factorization (the
+// digit count shapes the TMA boxes, the MMA table and the TMEM accumulators at
+// compile time): the default layout in namespace slim, and through
+// chol_q6.cu a six-digit layout in namespace slim::q6 whose factors are
+// corrected by one step of iterative refinement on the x-chain (capi.cu picks
+// one per context).  A translation unit describes itself in `chol_table`.
+struct CholVariant {
+  int qd, qx, dbits, pairs, tmax;  // digits, extra pair order, digit bits, digit pairs, tile-row limit
+  size_t (*q_bytes)(int qT);
+  void (*launch_assemble)(const CholParams&, cudaStream_t);
+  void (*launch_chol)(const CholParams&, cudaStream_t);
+};
+extern const CholVariant chol_table;
+namespace q6 {
+extern const CholVariant chol_table;
+}
 
 size_t chol_smem_bytes();
 // factorization kernel: true = int8 tensor-core updates (default), false =
@@ -177,8 +192,8 @@ static_assert(DBITS == 7 || DBITS == 8, "digit width");
 static_assert(QX >= 0 && QACC <= 8, "TMEM holds at most 8 accumulators of 64 columns");
 static_assert(QX <= 1, "one extra accumulator: its first writer is the MMA (a = 2, b = QD)");
 // B digits multiplied with A digit a (1-based) and the digit-pair count
-__host__ __device__ constexpr int q_nb(int a) { return QD < QD + 1 + QX - a ? QD : QD + 1 + QX - a; }
-__host__ __device__ constexpr int q_pairs(int a = 1) { return a > QD ? 0 : q_nb(a) + q_pairs(a + 1); }
+static __host__ __device__ constexpr int q_nb(int a) { return QD < QD + 1 + QX - a ? QD : QD + 1 + QX - a; }
+static __host__ __device__ constexpr int q_pairs(int a = 1) { return a > QD ? 0 : q_nb(a) + q_pairs(a + 1); }
 constexpr int QPAIRS = q_pairs();
 // int8 updates: |P_t| <= (2 * 127 * H + (QD - 2) * H^2) * 64 T < 2^31 with
 // H = 2^(DBITS - 1) the largest trailing digit magnitude
@@ -198,14 +213,14 @@ constexpr int QROW = SLIM_OZ_SW;
 static_assert(QROW == 32 || QROW == 64, "digit-slice row width");
 // TMA views of a sliced factor buffer with qT tile rows per column (box
 // rows = 128 for the A operand, 64 for B; QD digits per box)
-bool tma_map_q(CUtensorMap* m, const int8_t* base, int qT, int box_rows);
+bool tma_map_q(CUtensorMap* m, const int8_t* base, int qT, int box_rows, int qd);
 // bytes of a sliced factor buffer (the same for both layouts):
 //   QROW 32: [k][k half][digit][tile row][64 rows][32 B]
 //   QROW 64: [k][digit][tile row][64 rows][64 B]
-inline size_t q_bytes(int qT) { return (size_t)qT * qT * 2 * QD * 64 * 32; }
+static inline size_t q_bytes(int qT, int qd = QD) { return (size_t)qT * qT * 2 * qd * 64 * 32; }
 // byte offset of row r, k half kh (32 bytes) of digit a (0-based) of the
 // sliced tile (i, k)
-__host__ __device__ __forceinline__ int64_t q_off(int qT, int i, int k, int kh, int a, int r) {
+static __host__ __device__ __forceinline__ int64_t q_off(int qT, int i, int k, int kh, int a, int r) {
   if (QROW == 32) return ((((int64_t)k * 2 * QD + kh * QD + a) * qT + i) * 64 + r) * 32;
   return ((((int64_t)k * QD + a) * qT + i) * 64 + r) * 64 + 32 * kh;
 }

@@ -1259,6 +1259,98 @@ __global__ void __launch_bounds__(256) k_mtw_stage(double* __restrict__ s_out, W
   }
 }
 
+// ---------------------------------------------------------------------------
+// Iterative refinement of w against the fp64 Gram ring (contexts whose
+// factorization keeps six digits, chol_q6.cu): res = y - G w with
+// G = I + alpha (ring) in slot order and y = r on the new block's rows.
+// The ring holds the product of two window blocks in the panel of the newer
+// one, at the older one's window position (see k_assemble), so for the rows
+// of block X the columns of an older-or-equal block Y are read down the
+// columns of X's own panel (threads along the rows of X: coalesced) and the
+// columns of a newer block Y along the rows of Y's panel (a warp per row).
+// One CTA per (64 rows of X, Y); the partial sums over Y are added in a fixed
+// order by k_gram_apply_finish.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_gram_apply(GramApplyParams G) {
+  if (G.ctl->diverged_at != 0) return;
+  __shared__ double red[4][64];
+  const int X = blockIdx.y, Y = blockIdx.z, a0 = blockIdx.x * 64;
+  const int ell = G.ell, tid = threadIdx.x;
+  const double* wy = G.w + (int64_t)Y * ell;
+  double* out = G.part + (int64_t)Y * G.ldp + (int64_t)X * ell;
+  if (G.age[Y] >= G.age[X]) {
+    // G(X a, Y c) = pan_X[(Y ell + c) ell + a]: threads along a, four groups of rows c
+    const double* pan = G.panels + (int64_t)G.slot[X] * G.panel_stride + (int64_t)Y * ell * ell;
+    const int ag = tid & 63, cg = tid >> 6, a = a0 + ag;
+    double s0 = 0.0, s1 = 0.0;
+    if (a < ell) {
+      int cidx = cg;
+      for (; cidx + 4 < ell; cidx += 8) {
+        s0 = fma(__ldcs(pan + (int64_t)cidx * ell + a), wy[cidx], s0);
+        s1 = fma(__ldcs(pan + (int64_t)(cidx + 4) * ell + a), wy[cidx + 4], s1);
+      }
+      if (cidx < ell) s0 = fma(__ldcs(pan + (int64_t)cidx * ell + a), wy[cidx], s0);
+    }
+    red[cg][ag] = s0 + s1;
+    __syncthreads();
+    if (tid < 64 && a0 + tid < ell)
+      out[a0 + tid] = (red[0][tid] + red[1][tid]) + (red[2][tid] + red[3][tid]);
+  } else {
+    // G(X a, Y c) = pan_Y[(X ell + a) ell + c]: a warp per row a, lanes along c
+    const double* pan = G.panels + (int64_t)G.slot[Y] * G.panel_stride + (int64_t)X * ell * ell;
+    const int warp = tid >> 5, lane = tid & 31;
+    for (int q = warp; q < 64; q += 8) {
+      const int a = a0 + q;
+      if (a >= ell) break;
+      const double* row = pan + (int64_t)a * ell;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int cidx = lane;
+      for (; cidx + 96 < ell; cidx += 128) {
+        s0 = fma(__ldcs(row + cidx), wy[cidx], s0);
+        s1 = fma(__ldcs(row + cidx + 32), wy[cidx + 32], s1);
+        s2 = fma(__ldcs(row + cidx + 64), wy[cidx + 64], s2);
+        s3 = fma(__ldcs(row + cidx + 96), wy[cidx + 96], s3);
+      }
+      for (; cidx < ell; cidx += 32) s0 = fma(__ldcs(row + cidx), wy[cidx], s0);
+      const double sv = warp_sum((s0 + s1) + (s2 + s3));
+      if (lane == 0) out[a] = sv;
+    }
+  }
+}
+
+// res[p] = y[p] - (w[p] + alpha sum_Y part[Y][p]) for p < N, 0 on the padding rows
+__global__ void __launch_bounds__(256) k_gram_apply_finish(GramApplyParams G) {
+  if (G.ctl->diverged_at != 0) return;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= G.npad) return;
+  const int N = G.nw * G.ell;
+  double v = 0.0;
+  if (p < N) {
+    double sum = 0.0;
+    for (int Y = 0; Y < G.nw; ++Y) sum += G.part[(int64_t)Y * G.ldp + p];
+    const int q = p - G.newp * G.ell;
+    const double y = (q >= 0 && q < G.ell) ? G.r[q] : 0.0;
+    v = y - fma(G.alpha, sum, G.w[p]);
+  }
+  G.res[p] = v;
+}
+
+__global__ void __launch_bounds__(256) k_add_inplace(double* __restrict__ w, const double* __restrict__ dw,
+                                                     int count, const Ctl* ctl) {
+  if (ctl->diverged_at != 0) return;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < count) w[p] += dw[p];
+}
+
+void launch_gram_apply(const GramApplyParams& G, cudaStream_t s) {
+  dim3 grid((unsigned)((G.ell + 63) / 64), G.nw, G.nw);
+  k_gram_apply<<<grid, 256, 0, s>>>(G);
+  k_gram_apply_finish<<<(unsigned)((G.npad + 255) / 256), 256, 0, s>>>(G);
+}
+void launch_add_inplace(double* w, const double* dw, int count, const Ctl* ctl, cudaStream_t s) {
+  k_add_inplace<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(w, dw, count, ctl);
+}
+
 __global__ void k_stamp_start(Ctl* ctl) { ctl->t_start_ns = globaltimer_ns(); }
 
 // sharded mode: divergence decision and history row from allreduced norms

@@ -111,6 +111,23 @@ void launch_gram_reduce(double* panel, const Window& W, const double* part, int 
 void launch_gram_diag_fp64(double* panel_diag, int64_t ld, const float* A, int ell, int n,
                            RowSplit rs, cudaStream_t s);
 int finish_grid(int n);
+// res = y - (I + alpha ring) w in slot order (iterative refinement of w); part:
+// nw x ldp partial sums, res: npad entries (the solve's padded length)
+struct GramApplyParams {
+  const double* panels;
+  int64_t panel_stride;
+  int ell, nw, newp, npad;
+  int slot[MAX_WINDOW], age[MAX_WINDOW];
+  double alpha;
+  const double* w;   // current solution (nw ell)
+  const double* r;   // residual of the new block (ell): y = r on its rows
+  double* part;
+  int64_t ldp;
+  double* res;
+  const Ctl* ctl;
+};
+void launch_gram_apply(const GramApplyParams& G, cudaStream_t s);
+void launch_add_inplace(double* w, const double* dw, int count, const Ctl* ctl, cudaStream_t s);
 void launch_stamp_start(Ctl* ctl, cudaStream_t s);
 void launch_flush_read(const void* buf, size_t bytes, unsigned* sink, cudaStream_t s);
 

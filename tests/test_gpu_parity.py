@@ -215,6 +215,78 @@ def test_config2_reduced_vs_oracle(slim):
     _tomo_vs_oracle(slim, prob, K=30, r=10, alpha=1000.0, seed=11, rtol=RTOL64)
 
 
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_refined_six_digit_factorization_vs_oracle(slim, monkeypatch, dtype):
+    """The six-digit int8 factorization with one refinement step of w against
+    the fp64 Gram ring (the default for dual systems above 6144 rows; forced
+    here with SLIM_REFINE=1 on the kappa ~ 1e6 reduced tomography) holds the
+    fp64 bar, is bit-identical run to run, and reports its layout."""
+    from oracle import slimls_oracle as orc
+    from paper_1912_07962_b200 import problems
+    monkeypatch.setenv("SLIM_REFINE", "1")
+    prob = problems.tomo2d(grid=64, n_views=45, rays=90, seed=2, dtype=dtype)
+    op, K, r, alpha, seed = prob.op, 30, 10, 1000.0, 11
+    runs = []
+    for _ in range(2):
+        timing = {"start_step": 1}
+        fresh = op.with_rhs(op.rhs)
+        runs.append(slim.run("slimls", fresh, slim.Sampler("random_cyclic", op.n_blocks, seed),
+                             slim.Schedule("constant", alpha), epochs=K / op.n_blocks, r=r,
+                             references={"x_true": prob.x_true}, timing=timing))
+        assert timing["cholesky_digits"][0] == 6 and timing["cholesky_pairs"] == (21, 0)
+    np.testing.assert_array_equal(runs[0].x_final, runs[1].x_final)
+    idx = orc.sampler_indices("random_cyclic", op.n_blocks, seed, K)
+    fetch = orc.csr_fetch([op.csr_block(i) for i in range(1, op.n_blocks + 1)], prob.b)
+    ref = _oracle_run(fetch, op.n_blocks, op.n_cols, idx, alpha, r, {"x_true": prob.x_true})
+    err = np.linalg.norm(runs[0].x_final - ref.x_final) / np.linalg.norm(ref.x_final)
+    print(f"six digits + refinement ({np.dtype(dtype).name} values): relative iterate error vs oracle {err:.2e}")
+    assert err <= RTOL64, err
+    np.testing.assert_allclose(runs[0].residual_norms, ref.residual_norms, rtol=RTOL64, equal_nan=True)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_fixed_point_csr_gram_general_sparse(slim, monkeypatch, dtype):
+    """The record / fixed-point CSR Gram kernel (k_gram_rowexp + k_gram_lut +
+    k_gram_csr_fx; chosen from 2^18 nonzeros per block, forced here) on a
+    general sparse operator: signed entries, ~6 entries per column and block
+    (the path past the two packed entries), row scales spread over 10^-3 .. 10^3,
+    an empty row and an empty column.  Same bar as the fp64 kernel, and the
+    two kernels' iterates agree far inside it."""
+    import scipy.sparse as sp
+    from oracle import slimls_oracle as orc
+    g = np.random.Generator(np.random.Philox(key=77))
+    n, ell, nb, r, alpha, K = 384, 48, 12, 4, 50.0, 30
+    blocks = []
+    for _ in range(nb):
+        a = sp.random(ell, n, density=0.12, random_state=g, data_rvs=g.standard_normal, format="csr")
+        a = sp.diags(10.0 ** g.uniform(-3, 3, ell)) @ a
+        a = a.tolil()
+        a[5, :] = 0.0          # an empty row
+        a[:, 17] = 0.0         # an empty column
+        a = a.tocsr()
+        a.sort_indices()
+        blocks.append(a.astype(dtype))
+    xt = g.standard_normal(n)
+    b = np.concatenate([blk.astype(float) @ xt for blk in blocks])
+    b = b + 1e-3 * np.abs(b).mean() * g.standard_normal(b.shape)
+    xs = {}
+    for lut in ("1", "0"):
+        monkeypatch.setenv("SLIM_GRAM_LUT", lut)
+        op = slim.SparseBlockOperator(blocks, b)
+        xs[lut] = slim.run("slimls", op, slim.Sampler("random_cyclic", nb, 4),
+                           slim.Schedule("constant", alpha), epochs=K / nb, r=r)
+    parts = [(blk.indptr, blk.indices, blk.data, blk.shape) for blk in blocks]
+    idx = orc.sampler_indices("random_cyclic", nb, 4, K)
+    ref = _oracle_run(orc.csr_fetch(parts, b), nb, n, idx, alpha, r, {})
+    nrm = np.linalg.norm(ref.x_final)
+    err = {k: np.linalg.norm(v.x_final - ref.x_final) / nrm for k, v in xs.items()}
+    diff = np.linalg.norm(xs["1"].x_final - xs["0"].x_final) / nrm
+    print(f"general sparse ({np.dtype(dtype).name}): fixed-point Gram vs oracle {err['1']:.2e}, "
+          f"fp64 Gram vs oracle {err['0']:.2e}, the two kernels differ by {diff:.2e}")
+    assert err["1"] <= RTOL64 and err["0"] <= RTOL64
+    np.testing.assert_allclose(xs["1"].residual_norms, ref.residual_norms, rtol=RTOL64, equal_nan=True)
+
+
 def test_fp32_tomo_reduced_vs_oracle(slim):
     """configs[2] style: fp32 values / int32 indices, fp64 accumulation (1e-4 bar;
     the oracle sees the same fp32-rounded values)."""
