@@ -62,6 +62,10 @@ enum slim_method {
 
 typedef struct slim_ctx slim_ctx;
 
+/* slim_desc.flags: factor the dual systems with the fp64 DMMA kernel instead of
+ * the int8 digit-slice kernel (like SLIM_CHOL=dmma, per context).         */
+#define SLIM_FLAG_FP64_FACTOR 1
+
 typedef struct slim_desc {
   int64_t n_rows;      /* m                                                */
   int64_t n_cols;      /* n (columns owned by this context)                */
@@ -70,7 +74,7 @@ typedef struct slim_desc {
   int32_t value_dtype; /* enum slim_dtype                                  */
   int32_t layout;      /* enum slim_layout                                 */
   int32_t device;      /* CUDA device ordinal                              */
-  int32_t flags;       /* reserved, 0                                      */
+  int32_t flags;       /* 0, or SLIM_FLAG_* bits                           */
   uint64_t gen_seed;   /* SLIM_GEN_SPLITMIX64 only                         */
   int64_t gen_n_total; /* generator row length (global n) for GEN layout   */
   int64_t col_offset;  /* first global column of this context's shard      */

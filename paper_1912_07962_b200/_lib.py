@@ -22,6 +22,7 @@ SLIM_F64, SLIM_F32 = 0, 1
 SLIM_DENSE_ROWMAJOR, SLIM_CSR_PERBLOCK, SLIM_GEN_SPLITMIX64 = 0, 1, 2
 SLIM_HIST_FIXED = 5
 SLIM_METHOD_SLIMLS, SLIM_METHOD_SG = 0, 1
+SLIM_FLAG_FP64_FACTOR = 1
 
 # every symbol include/slimb200.h declares (checked by tests/test_capi_exports.py)
 EXPORTS = (

@@ -9,4 +9,13 @@
 #define SLIM_QD 6
 #define SLIM_QX 0
 #define SLIM_CHOL_VARIANT q6
+// Six digits make a TMA stage 72 KB, so a THREE-stage operand ring fits an SM
+// (217 KB; seven digits: 3 x 84 KB does not).  Measured with two stages:
+// configs[2] 145.3 it/s, configs[3] 158.2; with three: 154.1 and 171.6, same
+// bits (profiles/chol_q6_stages_r02.txt) -- the operand bytes in flight per SM
+// were what held the two-stage kernel.  SLIM_Q6_NST=2 rebuilds the two-stage ring.
+#ifndef SLIM_Q6_NST
+#define SLIM_Q6_NST 3
+#endif
+#define SLIM_OZ_NST SLIM_Q6_NST
 #include "chol.cu"

@@ -219,6 +219,15 @@ __global__ void __launch_bounds__(RES_THREADS) k_residual_csr(double* r, const i
       k[u] = ok ? __ldcs(col + e0 + u * S) : 0;
       v[u] = ok ? __ldcs(val + e0 + u * S) : T(0);
     }
+#ifdef SLIM_BOUNDS
+#pragma unroll
+    for (int u = 0; u < RES_PRE; ++u)
+      if ((unsigned)k[u] > 0x3fffffu) {
+        printf("SLIM_BOUNDS k_residual_csr: row %d (global %lld) entry %lld col %d\n", row,
+               (long long)(row0 + row), (long long)(e0 + u * S), k[u]);
+        k[u] = 0;
+      }
+#endif
 #pragma unroll
     for (int u = 0; u < RES_PRE; ++u) xv[u] = (e0 + u * S < hi) ? __ldg(x + k[u]) : 0.0;
     // whole groups of four go to s0..s3, the remaining entries to s0
@@ -301,10 +310,22 @@ __global__ void __launch_bounds__(128) k_gram_csr(double* __restrict__ panel, Wi
     int cs = 0, cnt = 0;
     double v = 0.0;
     if (e < hi) {
-      const int c = col[e];
+      int c = col[e];
+#ifdef SLIM_BOUNDS
+      if ((unsigned)c > 0x3fffffu) {
+        printf("SLIM_BOUNDS k_gram_csr: window row %d entry %lld col %d\n", grow_w, (long long)e, c);
+        c = 0;
+      }
+#endif
       v = to_f64(val[e]);
       cs = colptr_new[c];
       cnt = colptr_new[c + 1] - cs;
+#ifdef SLIM_BOUNDS
+      if (cs < 0 || cnt < 0 || cnt > ell) {
+        printf("SLIM_BOUNDS k_gram_csr: new block column %d range [%d, +%d)\n", c, cs, cnt);
+        cnt = 0;
+      }
+#endif
     }
     int maxcnt = cnt;
 #pragma unroll
@@ -775,6 +796,13 @@ __device__ __forceinline__ double mtw_csc_col(int c, const Window& W, const int*
         lo[q] = __ldcs(cp + c);
         hi[q] = __ldcs(cp + c + 1);
         base[q] = __ldg(blkbase + bk);
+#ifdef SLIM_BOUNDS
+        if (lo[q] < 0 || hi[q] < lo[q] || hi[q] - lo[q] > ell) {
+          printf("SLIM_BOUNDS mtw_csc_col: block %d (position %d) column %d range [%d, %d)\n", bk, P0 + q,
+                 c, lo[q], hi[q]);
+          hi[q] = lo[q] = 0;
+        }
+#endif
       }
     }
     double v[MTW_GROUP], wv[MTW_GROUP];
@@ -784,6 +812,14 @@ __device__ __forceinline__ double mtw_csc_col(int c, const Window& W, const int*
       if (lo[q] < hi[q]) {
         const int64_t e = base[q] + lo[q];
         v[q] = to_f64(__ldcs(cscval + e));
+#ifdef SLIM_BOUNDS
+        if ((unsigned)__ldcs(cscrow + e) >= (unsigned)ell) {
+          printf("SLIM_BOUNDS mtw_csc_col: block at position %d column %d entry %lld row %d\n", P0 + q, c,
+                 (long long)e, __ldcs(cscrow + e));
+          lo[q] = hi[q] = 0;
+          continue;
+        }
+#endif
         wv[q] = __ldg(w + (P0 + q) * ell + __ldcs(cscrow + e));
       }
     }

@@ -370,6 +370,10 @@ class GeneratedBlockOperator(RowBlockOperator):
 class DeviceOperator:
     """Owns one C-ABI context holding the operator in HBM."""
 
+    # slim_desc.flags of the contexts created next (parallel.LocalShard sets
+    # SLIM_FLAG_FP64_FACTOR for in-process groups of three or more shards)
+    default_flags = 0
+
     def __init__(self, *, n_rows, n_cols, ell, r, layout, dtype, device=0, gen_seed=0,
                  gen_n_total=0, col_offset=0):
         L = _lib.lib()
@@ -378,6 +382,7 @@ class DeviceOperator:
         d.value_dtype = _lib.SLIM_F32 if np.dtype(dtype) == np.float32 else _lib.SLIM_F64
         d.layout = layout
         d.device = int(device)
+        d.flags = int(DeviceOperator.default_flags)
         d.gen_seed = int(gen_seed)
         d.gen_n_total = int(gen_n_total)
         d.col_offset = int(col_offset)
