@@ -95,9 +95,11 @@ SAMPLER_SEED = 7962
 CLEAN_NORM = {3: 796647.3575867971, 4: 59051.36952100318}
 DTYPE = {1: "f64", 2: "f64", 3: "f32 values, f64 arithmetic", 4: "f32 values, f64 arithmetic",
          5: "f32 values (generated), f64 arithmetic", 6: "f32 values (generated), f64 arithmetic"}
-DTYPE_NOTE = ("fp64 iterates, Gram and solves; the dual-system Cholesky's tile updates are fp64 "
-              "emulated exactly by int8 digit-slice products on tcgen05 (7 signed digits, 55 "
-              "bits below each row's scale), POTRF/TRSM in fp64 DMMA")
+DTYPE_NOTE = ("fp64 iterates, Gram and solves (the CSR Gram of large blocks as exact 64-bit "
+              "fixed-point sums, 62 bits below ||a|| ||b||); the dual-system Cholesky's tile "
+              "updates are fp64 emulated by int8 digit-slice products on tcgen05 -- 7 signed "
+              "digits (55 bits below each row's scale) for N <= 6144, 6 digits (47 bits) plus one "
+              "refinement step of w against the fp64 Gram ring above -- POTRF/TRSM in fp64 DMMA")
 
 
 TOMO_N = {2: 256 ** 2, 3: 1024 ** 2, 4: 128 ** 3}
@@ -586,16 +588,31 @@ def _roofline(timing, steps, N, cfg_id):
     chol_ms = timing["cholesky_ms"] / max(1, timing["cholesky_count"])
     achieved = flops_chol / (chol_ms * 1e-3) / 1e12
     agg = timing["cholesky_flops"] / (timing["window_ms"] * 1e-3) / 1e12
-    traffic, traffic_src = None, None
-    for name in (f"ncu_chol_cfg{cfg_id}_r02.json", f"ncu_chol_cfg{cfg_id}.json"):
-        try:  # dram bytes per launch from the committed ncu --set full capture
+    traffic, traffic_src, ncu_ctx = None, None, None
+    qd_run = timing.get("cholesky_digits", (0, 0))[0]
+    # dram bytes per launch from the committed ncu --set full capture of the SAME
+    # kernel variant (digit count) and launch shape
+    for name in (f"ncu_chol_cfg{cfg_id}_q{qd_run}_r02.json",
+                 f"ncu_chol_cfg{cfg_id}_r02.json" if qd_run == 7 else "",
+                 f"ncu_chol_cfg{cfg_id}.json" if qd_run == 7 else ""):
+        if not name:
+            continue
+        try:
             with open(os.path.join(ROOT, "profiles", name)) as fh:
                 prof = json.load(fh)
             traffic = prof["dram_bytes_per_launch"]
             traffic_src = (f"profiles/{name}: {prof['systems_per_launch']} systems per launch, "
                            f"{prof.get('gpu__time_duration.sum', '?')} under ncu")
+            ms = float(str(prof.get("gpu__time_duration.sum", "0")).split()[0])
+            pipe = str(prof.get("sm__ops_path_tensor_op_utcimma_src_int8_sparsity_off.avg."
+                                "pct_of_peak_sustained_elapsed", "")).split()
+            if ms > 0:
+                ncu_ctx = {"launch_ms_alone": ms, "dram_gbs": traffic / (ms * 1e-3) / 1e9,
+                           "dram_frac_of_hbm_peak": traffic / (ms * 1e-3) / 1e9 /
+                           (float(_peaks().get("hbm_gbs", 0.0)) or 7700.0),
+                           "int8_pipe_busy_pct": float(pipe[0]) if pipe else None}
             break
-        except (OSError, ValueError, KeyError):
+        except (OSError, ValueError, KeyError, IndexError):
             continue
     i8ops = timing.get("cholesky_i8ops", 0.0) / max(1, timing["cholesky_count"])
     if i8ops > 0:
@@ -616,6 +633,12 @@ def _roofline(timing, steps, N, cfg_id):
                                "MEASURED_PEAKS.json has no int8 entry (2 x its bf16 burst "
                                "would be 3249 TOPS)",
                 "shape_ceiling_tops": I8_N64_CEIL_TOPS,
+                "ncu": ncu_ctx,
+                "note": ("the kernel is bound by operand delivery from HBM/L2, not by the int8 "
+                         "pipe (ncu: see 'ncu'); six digits do 21/34 of the seven-digit layout's "
+                         "int8 ops per tile update for the same factor, so 'achieved' counts "
+                         "fewer ops per launch while the fp64-equivalent rate rises")
+                if qd_run == 6 else None,
                 "fp64_equivalent_tflops": achieved,
                 "fp64_equivalent_frac_of_dmma_peak": achieved / FP64_PEAK_TFLOPS,
                 "aggregate_tflops_over_window": agg,
