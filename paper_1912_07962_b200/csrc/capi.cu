@@ -1667,7 +1667,7 @@ static int enqueue_x_chain(slim_ctx* c, const Window& W, int64_t k, int d, doubl
   T.ctl = c->ctl;
   T.C = c->trsv_C > 0 ? std::min(c->trsv_C, T.T) : trsv_cluster_size(T.T);
   {
-    static const int rs = getenv("SLIM_TRSV_RING") ? std::max(1, std::min(3, atoi(getenv("SLIM_TRSV_RING")))) : 3;
+    static const int rs = getenv("SLIM_TRSV_RING") ? std::max(1, std::min(4, atoi(getenv("SLIM_TRSV_RING")))) : 3;
     T.rs = rs;
   }
   CK(c, launch_trsv(T, s));

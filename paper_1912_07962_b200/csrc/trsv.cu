@@ -98,7 +98,7 @@ __device__ __forceinline__ void gemvT_smem(double* out, const double* M, const d
   __syncthreads();
 }
 // ---- bulk-copy ring of the non-critical tiles ----
-constexpr int RS_MAX = 3;  // 32 KB slots (P.rs in use)
+constexpr int RS_MAX = 4;  // 32 KB slots (P.rs in use)
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(n));
 }
