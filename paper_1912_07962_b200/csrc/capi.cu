@@ -1818,8 +1818,8 @@ static const slim_ctx::TaskMap* task_map(slim_ctx* c, const std::vector<SysShape
   if (it != c->maps.end()) return &it->second;
   std::vector<int2> h = chol_task_map(sh.data(), (int)sh.size(), (int)(c->r + 1), (int)c->ell);
   const double t3 = (double)TB * TB * TB;
-  // int8 tensor-core path: 36 digit-pair products of 2 * 64^3 ops per 64x64x64
-  // tile update (k_chol_i8)
+  // int8 tensor-core path: the context's digit-pair products (CholVariant::pairs)
+  // of 2 * 64^3 ops per 64x64x64 tile update (k_chol_i8)
   const double u8 = (double)c->cv->pairs * 2.0 * t3;
   double flops = 0.0, i8ops = 0.0;
   for (const int2& e : h) {

@@ -787,30 +787,31 @@ __global__ void __launch_bounds__(256, 2) k_chol_tiles(const __grid_constant__ C
 //
 // The left-looking update C = G_ij - sum_k L_ik L_jk^T dominates the
 // factorization (all but O(T^2) of its flops).  tcgen05 has no fp64 kind, so
-// the update is computed EXACTLY in integer arithmetic from digit slices:
-// every entry of L row p is written as
-//     L_pk = 2^(e_p - 7) sum_{a=1..8} d_a 2^(-7 (a-1)),
-// d_1 in [-127, 127], d_a in [-64, 64] for a > 1, with 2^(e_p) >= 1.004
+// the update is computed in integer arithmetic from digit slices: every
+// entry of L row p is written with QD signed digits (kernels.h: SLIM_QD, 7 in
+// this translation unit by default, 6 in chol_q6.cu), a 7-bit leading digit
+// and balanced DBITS = 8-bit digits after it,
+//     L_pk = 2^(e_p - 7) sum_{a=1..QD} d_a 2^(-8 (a-1)),
+// d_1 in [-127, 127], d_a in [-128, 127] for a > 1, with 2^(e_p) >= 1.004
 // sqrt(G_pp) >= 1.004 |L_pk| (row scales known before the factorization
-// starts, k_assemble), so the representation error is below 2^-57 2^(e_p).
-// (QD = SLIM_QD digits in general, kernels.h; 8 is the default and the only
-// count that keeps the products fp64-class)
+// starts, k_assemble): 7 + 8 (QD - 1) bits below each row's scale.
 // Then
-//     sum_k L_ik L_jk = 2^(e_i + e_j - 14) sum_{t=0..7} 2^(-7 t) P_t,
+//     sum_k L_ik L_jk = 2^(e_i + e_j - 14) sum_t 2^(-8 t) P_t,
 //     P_t = sum_{a + b = t + 2} D_a(i) D_b(j)^T        (int32, exact)
-// where the 36 digit products with a + b <= 9 are kept; the dropped ones
-// weigh < 2^-56 of sqrt(G_ii G_jj) per k, the size of fp64 rounding (the
-// Cholesky backward-error bound is componentwise in sqrt(G_ii G_jj), so this
-// row scaling is the natural one).  Each P_t is one TMEM accumulator
-// (M = 128 rows of two output tiles x N = 64: 8 x 64 = all 512 columns), the
-// int32 sums are exact (|P_t| <= (2 * 127 * 64 + 6 * 64^2) 64 T < 2^31 for
-// T <= 800, checked at context creation), and
-// the eight are combined in fp64 once per task.  POTRF, TRSM and the 8x8
-// inverses stay in fp64 (DMMA), on O(T^2) tiles.
+// where the digit products with a + b <= QD + 1 + QX are kept (34 pairs for
+// QD = 7, QX = 1; 21 for QD = 6, QX = 0, whose truncation the x-chain's
+// refinement step removes).  The Cholesky backward-error bound
+// is componentwise in sqrt(G_ii G_jj), so this row scaling is the natural one.
+// Each P_t is one TMEM accumulator (M = 128 rows of two output tiles x N = 64;
+// QACC = QD + QX of them, at most 8 x 64 = all 512 columns), the int32 sums
+// are exact for T <= CHOL_I8_TMAX tile rows (checked at context creation), and
+// the accumulators are combined in fp64 once per task.  POTRF, TRSM and the
+// 8x8 inverses stay in fp64 (DMMA), on O(T^2) tiles.
 //
-// A sliced tile (32 KB, the size of its fp64 tile) is stored as
-// [k half h][digit quad dq][row][4 digits x 32 k] so that one K = 32 MMA
-// step of a digit pair is one 32-byte column of a SWIZZLE_128B row.
+// A sliced tile (QD x 4 KB) is stored by tile column in 64-byte rows,
+// [k][digit][tile row][64 rows][64 B] (q_off, kernels.h), so a task's A operand
+// (tile rows i, i + 1, all digits of one k tile) is one 3D TMA box under
+// SWIZZLE_64B and its B operand (tile row j) another.
 // ===========================================================================
 #ifndef SLIM_ACC_SLEEP_NS
 #define SLIM_ACC_SLEEP_NS 500  // 2000 -> 500: +0.4% at configs[1]
@@ -1024,10 +1025,11 @@ __device__ void store_publish_i8(const CholParams& P, int b, int i, int j, const
 
 // One task per CTA (same ticket map as k_chol_tiles): output rows ra (and
 // ra + 1 for pair / dual tasks) of tile column j.  Warp 0 lane 0 streams the
-// digit slices of L_(ra, k), L_(ra+1, k), L_(j, k) for k < j through a 4-stage
-// TMA ring (48 KB per k half); warp 1 lane 0 issues the 36 digit-pair MMAs
-// per stage into the eight TMEM accumulators; then all eight warps combine
-// the accumulators with G in fp64 and finish the tiles (POTRF / TRSM, DMMA).
+// digit slices of L_(ra, k), L_(ra+1, k), L_(j, k) for k < j through an
+// NST-stage TMA ring (one k tile per stage: 2 x 84 KB with seven digits, 3 x 72 KB
+// with six); warp 1 lane 0 issues the stage's digit-pair MMAs (make_groups) into
+// the QACC TMEM accumulators; then all eight warps combine the accumulators
+// with G in fp64 and finish the tiles (POTRF / TRSM, DMMA).
 __global__ void __launch_bounds__(256, 1) k_chol_i8(const __grid_constant__ CholParams P) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* base = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
