@@ -494,6 +494,20 @@ def test_sharded_round_robin_tomography(slim, P):
                        round_robin=True)
 
 
+@pytest.mark.parametrize("round_robin", [False, True])
+def test_sharded_tomography_with_refinement(slim, monkeypatch, round_robin):
+    """Column shards with the six-digit factorization and its refinement step
+    forced (SLIM_REFINE=1; the default for dual systems above 6144 rows): the
+    refinement reads the allreduced Gram ring on the x-chain of the rank that
+    solves the step, replicated or round-robin."""
+    from paper_1912_07962_b200 import problems
+    monkeypatch.setenv("SLIM_REFINE", "1")
+    prob = problems.tomo2d(grid=48, n_views=30, rays=68, seed=6)
+    op = prob.op.with_rhs(prob.op.rhs)  # fresh contexts: the variant is chosen at creation
+    _sharded_vs_single(slim, op, prob.x_true, "random_cyclic", 5, 1000.0, 6, 40, 2,
+                       round_robin=round_robin)
+
+
 def test_sharded_round_robin_dense(slim):
     c = gc.dense_case("dense_dual")
     op = slim.DenseBlockOperator(c["A"], 20, c["b"])
