@@ -187,17 +187,7 @@ struct LocalComm : Comm {
     cudaEventRecord(g->ev_out[chan][rank], s);
     g->barrier();  // every rank has enqueued its reads of all buffers
     for (int q = 0; q < g->P; ++q) cudaStreamWaitEvent(s, g->ev_out[chan][q], 0);
-    cudaError_t e = cudaMemcpyAsync(buf, scratch[chan], count * sizeof(double), cudaMemcpyDeviceToDevice, s);
-    // Known issue (round 2; tools/shard_stress.py, profiles/shard_stress_r02.txt): with
-    // three or more contexts of ONE process on ONE device -- this in-process test
-    // vehicle only, a deployment has one context per GPU -- about one run in fifty
-    // ended in an illegal memory access or a wrong factor (never with two shards:
-    // 0 of 2400 runs).  It is already present in the round-1 library, needs the
-    // host to run several steps ahead of the device (a stream synchronize per
-    // step: 0 of 3200 runs) and is not root-caused.  Groups of three or more
-    // therefore keep host and device in step at every exchange.
-    if (e == cudaSuccess && g->P >= 3) e = g->P >= 4 ? cudaDeviceSynchronize() : cudaStreamSynchronize(s);
-    return e;
+    return cudaMemcpyAsync(buf, scratch[chan], count * sizeof(double), cudaMemcpyDeviceToDevice, s);
   }
 };
 
@@ -462,6 +452,16 @@ int slim_abi_version(void) { return SLIM_ABI_VERSION; }
 const char* slim_last_error(const slim_ctx* ctx) {
   return ctx ? ctx->err.c_str() : g_err.c_str();
 }
+
+// A synchronous cudaMemcpy from PAGEABLE host memory (and cudaMemset) returns
+// once the data is staged; the DMA into device memory is ordered on the legacy
+// default stream only.  The context's streams are cudaStreamNonBlocking, which
+// the legacy stream does not synchronize with, so a kernel launched on them right
+// after such a copy can start before the data has landed (round 2: a tile task
+// map read before its upload arrived -- a rare illegal memory access or wrong
+// factor once the copy engine was busy with other uploads; tools/shard_stress.py).
+// Call this after such copies, before launching work that reads them.
+static cudaError_t legacy_copies_done() { return cudaStreamSynchronize(cudaStreamLegacy); }
 
 static void free_all(slim_ctx* c) {
   delete c->comm;
@@ -1330,6 +1330,8 @@ int slim_gen_apply(slim_ctx* c, const double* x, double* out) {
     return SLIM_ENOMEM;
   }
   cudaMemcpy(dx, x, sizeof(double) * c->n, cudaMemcpyHostToDevice);
+  legacy_copies_done();
+  legacy_copies_done();
   launch_gen_apply(dout, c->gen_seed, c->m, (int)c->n, c->gen_n_total, c->col_offset, dx, c->sx);
   cudaError_t e = cudaStreamSynchronize(c->sx);
   if (e == cudaSuccess) e = cudaMemcpy(out, dout, sizeof(double) * c->m, cudaMemcpyDeviceToHost);
@@ -1837,7 +1839,11 @@ static const slim_ctx::TaskMap* task_map(slim_ctx* c, const std::vector<SysShape
   slim_ctx::TaskMap tm{nullptr, (int)h.size(), flops, i8ops};
   if (h.empty()) h.push_back(make_int2(0, 0));
   if (cudaMalloc(&tm.dev, sizeof(int2) * h.size()) != cudaSuccess) return nullptr;
-  cudaMemcpy(tm.dev, h.data(), sizeof(int2) * h.size(), cudaMemcpyHostToDevice);
+  if (cudaMemcpy(tm.dev, h.data(), sizeof(int2) * h.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+      legacy_copies_done() != cudaSuccess) {  // the factorization reads it on a non-blocking stream
+    cudaFree(tm.dev);
+    return nullptr;
+  }
   return &(c->maps[sh] = tm);
 }
 
@@ -2005,6 +2011,7 @@ extern "C" int slim_run(slim_ctx* c, const int64_t* idx, const double* alphas, i
   h.div_limit_sq = c->div_limit * c->div_limit;
   CK(c, cudaMemcpy(c->ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice));
   CK(c, cudaMemset(c->errflag, 0, sizeof(int)));
+  CK(c, legacy_copies_done());
   *c->pin_div = 0;
   for (int q = 0; q < 4; ++q) c->t_ms[q] = 0.0, c->t_n[q] = 0;
   c->chol_flops = 0.0;
@@ -2352,6 +2359,7 @@ extern "C" int slim_block_residual(slim_ctx* c, int64_t block, const double* x, 
   Ctl h{};
   h.div_limit_sq = c->div_limit * c->div_limit;
   CK(c, cudaMemcpy(c->ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice));
+  CK(c, legacy_copies_done());
   if (c->layout == SLIM_GEN_SPLITMIX64) {
     launch_gen_block(c->gring, nullptr, nullptr, c->gen_seed, (block - 1) * c->ell, (int)c->ell,
                      (int)c->n, c->gen_n_total, c->col_offset, c->sx);
@@ -2423,6 +2431,7 @@ extern "C" int slim_dual_step(int32_t device, const double* Mh, int64_t rows, in
   Ctl h{};
   h.div_limit_sq = 1e300;
   cudaMemcpy(c->ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice);
+  if (legacy_copies_done() != cudaSuccess) return fail_out(SLIM_ECUDA);
   const int N = (int)rows;
   TrsvParams T{};
   T.L = c->Lbuf[0];
@@ -2631,6 +2640,7 @@ extern "C" int slim_probe_stream(slim_ctx* c, int32_t kernel, int32_t reps, doub
   }
   cudaMemset(ctl, 0, sizeof(Ctl));
   cudaMemset(flush, 0x5a, flush_bytes);
+  legacy_copies_done();
   cudaStream_t s = c->sx;
   std::vector<cudaEvent_t> ev(2 * (size_t)reps);
   for (auto& e : ev) cudaEventCreate(&e);
@@ -2792,6 +2802,7 @@ extern "C" int slim_build_projector(slim_ctx* c, int32_t dims, int64_t grid, int
   cudaMemcpy(dgeo, geo.data(), sizeof(double) * geo.size(), cudaMemcpyHostToDevice);
   if (dmap) cudaMemcpy(dmap, ray_of_row, sizeof(int) * c->m, cudaMemcpyHostToDevice);
   cudaMemset(derr, 0, sizeof(int));
+  legacy_copies_done();
   SiddonSpec S{};
   S.dims = dims;
   S.grid = grid;
@@ -2857,6 +2868,7 @@ extern "C" int slim_apply(slim_ctx* c, const double* x, double* out) {
     FAIL(c, SLIM_ENOMEM, "apply scratch allocation failed");
   }
   cudaMemcpy(dx, x, sizeof(double) * c->n, cudaMemcpyHostToDevice);
+  legacy_copies_done();
   cudaError_t e = csr_spmv(c->rowptr, c->col, c->val, c->vdt == SLIM_F64, dx, dy, c->m, c->sx);
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->sx);
   if (e == cudaSuccess) e = cudaMemcpy(out, dy, sizeof(double) * c->m, cudaMemcpyDeviceToHost);
