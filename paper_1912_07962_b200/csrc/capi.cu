@@ -1264,6 +1264,7 @@ static int ensure_blocks(slim_ctx* c, const int64_t* blks, int cnt, int* copied 
 int slim_finalize_operator(slim_ctx* c) {
   if (!c) FAIL(c, SLIM_EINVAL, "null argument");
   CK(c, cudaSetDevice(c->dev));
+  CK(c, legacy_copies_done());  // the uploaded arrays feed the CSC build on a context stream
   if (c->layout == SLIM_DENSE_ROWMAJOR) {
     if (!c->A) FAIL(c, SLIM_ESTATE, "no dense operator uploaded");
     c->op_ready = true;
@@ -1839,8 +1840,11 @@ static const slim_ctx::TaskMap* task_map(slim_ctx* c, const std::vector<SysShape
   slim_ctx::TaskMap tm{nullptr, (int)h.size(), flops, i8ops};
   if (h.empty()) h.push_back(make_int2(0, 0));
   if (cudaMalloc(&tm.dev, sizeof(int2) * h.size()) != cudaSuccess) return nullptr;
-  if (cudaMemcpy(tm.dev, h.data(), sizeof(int2) * h.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
-      legacy_copies_done() != cudaSuccess) {  // the factorization reads it on a non-blocking stream
+  // ordered on the factorization stream, the only reader (a synchronous cudaMemcpy
+  // is ordered on the legacy stream, which sf does not wait for: legacy_copies_done;
+  // the pageable source is staged before the call returns)
+  if (cudaMemcpyAsync(tm.dev, h.data(), sizeof(int2) * h.size(), cudaMemcpyHostToDevice, c->sf) !=
+      cudaSuccess) {
     cudaFree(tm.dev);
     return nullptr;
   }
