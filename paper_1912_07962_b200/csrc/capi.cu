@@ -1103,7 +1103,9 @@ class CopyPool {
 };
 static void par_memcpy(char* dst, const char* src, size_t n) {
   static CopyPool* pool = new CopyPool();  // process lifetime, like the ring
-  if (n < ((size_t)1 << 20) || !pool->copy(dst, src, n)) memcpy(dst, src, n);
+  // SLIM_COPY_HELPERS=0: plain memcpy (A/B of the staging copy)
+  static const bool helpers = !(getenv("SLIM_COPY_HELPERS") && getenv("SLIM_COPY_HELPERS")[0] == '0');
+  if (!helpers || n < ((size_t)1 << 20) || !pool->copy(dst, src, n)) memcpy(dst, src, n);
 }
 
 // host -> device copy of `bytes` through the pinned ring (pageable fallback)
